@@ -1,0 +1,194 @@
+/* tlb.h — C ABI of the B200-native (sm_100a) hot path that sits underneath the
+ * `tla` layout algebra of arXiv 2603.02298.
+ *
+ * The reference (/root/reference/proj/include/tla) has no FFI: everything is
+ * inline C++ called directly. The drop-in boundary is therefore the set of C++
+ * signatures in namespace tla (kept source-compatible by
+ * paper_2603_02298_b200/include/tla/) plus THIS C ABI, the
+ * new layer those signatures dispatch to when a tensor lives in device memory.
+ * Each entry point names the reference function it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Device pointers are BORROWED: never freed,
+ *    never retained after the call returns (the reference shares storage by
+ *    shared_ptr, tensor.hpp:29; ownership stays with the caller here too).
+ *  - Every call returns a tlb_status. The text of the last failure on the
+ *    calling thread is available from tlb_last_error(). Status values map
+ *    one-to-one onto the reference's exception types (common.hpp:13-97).
+ *  - All pre-flight checks (sizes, bounds of the whole offset image, overflow
+ *    range proofs) run on the host BEFORE any launch, so a failing call writes
+ *    nothing. (The reference writes partially before a mid-copy bounds_error;
+ *    documented difference.)
+ *  - `stream` is a cudaStream_t passed as void*. Calls are asynchronous with
+ *    respect to the host unless stated otherwise. Thread-safe; the only global
+ *    state is a mutex-guarded per-device cache of TMA tensor maps.
+ *  - There is no CPU fallback. Without a CUDA device every compute entry point
+ *    returns TLB_ERR_CUDA.
+ */
+#ifndef TLB_H_
+#define TLB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLB_ABI_VERSION 1
+#define TLB_MAX_MODES 16
+
+typedef enum tlb_status {
+    TLB_OK = 0,
+    TLB_ERR_CONTRACT = 1,    /* tla::contract_error   (tensor.hpp:93,197,216,222) */
+    TLB_ERR_BOUNDS = 2,      /* tla::bounds_error     (tensor.hpp:101)            */
+    TLB_ERR_STRUCTURAL = 3,  /* tla::structural_error (layout.hpp:57)             */
+    TLB_ERR_SEMIMODULE = 4,  /* tla::semimodule_error (tensor.hpp:59)             */
+    TLB_ERR_OVERFLOW = 5,    /* tla::overflow_error   (common.hpp:101,107)        */
+    TLB_ERR_CUDA = 6,        /* CUDA runtime / driver failure, or no device       */
+    TLB_ERR_UNSUPPORTED = 7, /* valid request this build has no kernel for        */
+    TLB_ERR_INDEX = 8        /* tla::index_error                                  */
+} tlb_status;
+
+/* Stride semimodule of a leaf (stride.hpp:16). */
+typedef enum tlb_kind { TLB_KIND_INT = 0, TLB_KIND_BASIS = 1, TLB_KIND_XOR = 2 } tlb_kind;
+
+/* One flat leaf of a layout, as produced by tla::flat_modes (layout.hpp:111):
+ * Int: stride; Xor: mask (f<mask>); Basis: scale on `axis` (a*e<axis>). */
+typedef struct tlb_mode {
+    int64_t extent;
+    int64_t stride;
+    int32_t kind; /* tlb_kind */
+    int32_t axis; /* Basis only */
+} tlb_mode;
+
+/* Device-ready layout: the lowering of a host-computed tla::Layout into flat
+ * evaluator parameters. POD, passed by value into kernels. Filled by
+ * tlb_layout_lower(); treat as opaque apart from the documented fields. */
+typedef struct tlb_layout_desc {
+    int32_t n_modes;            /* flat leaves, extent-1 leaves kept (they matter for the
+                                   extended domain: the LAST leaf is unbounded)          */
+    int32_t kind;               /* tlb_kind of the whole layout (stride_kind, stride.hpp:158) */
+    int32_t n_top;              /* top-level modes (rank); 1 for a flat request          */
+    int32_t flags;              /* TLB_LF_*                                             */
+    int64_t size;               /* product of extents (size, int_tuple.hpp:67)          */
+    int64_t cosize;             /* 1 + max offset; Int kind, non-negative strides; else -1 (cosize, layout.hpp:277) */
+    int64_t min_offset;         /* min over the domain [0,size) (negative strides allowed) */
+    int64_t max_offset;         /* max over the domain [0,size); Xor: OR-bound of all masks */
+    int32_t top_start[TLB_MAX_MODES + 1]; /* leaf index where top-level mode t starts; [n_top] = n_modes */
+    int64_t extent[TLB_MAX_MODES];
+    int64_t stride[TLB_MAX_MODES];
+    uint64_t magic[TLB_MAX_MODES]; /* fast division by extent for 0 <= i < 2^63, see tlb_lower.cpp */
+    uint8_t shift[TLB_MAX_MODES];
+    uint8_t log2e[TLB_MAX_MODES];  /* log2(extent) when a power of two, else 0xff          */
+} tlb_layout_desc;
+
+#define TLB_LF_ALL_POW2 1  /* every extent is a power of two                     */
+#define TLB_LF_HAS_NEG 2   /* some Int stride is negative                        */
+#define TLB_LF_INJECTIVE 4 /* proven injective on [0,size) by the sorted-stride test */
+
+/* A tensor = accessor o layout (tensor.hpp:111). */
+typedef enum tlb_accessor {
+    TLB_ACC_BUFFER = 0,  /* Accessor::buffer   (tensor.hpp:29): data + origin, bounds-checked against capacity */
+    TLB_ACC_COUNTING = 1 /* Accessor::counting (tensor.hpp:22): deref returns the position; read-only, 8-byte  */
+} tlb_accessor;
+
+typedef struct tlb_tensor {
+    const tlb_layout_desc* layout;
+    void* data;        /* device pointer to element 0 of the buffer (BORROWED); NULL for counting */
+    int64_t origin;    /* accessor position before the layout offset is applied (elements)       */
+    int64_t capacity;  /* buffer length in elements (bounds: 0 <= pos < capacity)                */
+    int32_t elem_bytes;/* 1, 2, 4, 8 or 16                                                        */
+    int32_t accessor;  /* tlb_accessor                                                            */
+} tlb_tensor;
+
+/* ---- library ---------------------------------------------------------- */
+int tlb_abi_version(void);
+const char* tlb_last_error(void);
+/* Number of kernels this library has launched on the calling process (for bench.py's gpu_launches). */
+uint64_t tlb_launch_count(void);
+/* Name of the plan the last tlb_copy/tlb_gemm_* call on this thread selected ("contig", "tiled", "tiled_tma", "gather", "ordered", "umma_2sm", ...). */
+const char* tlb_last_plan(void);
+
+/* ---- (1) lowering: host layout -> device evaluator parameters --------- */
+/* Replaces the per-element call chain Tensor::operator() -> layout_eval -> eval_rec ->
+ * idx2crd/eval_leaf (tensor.hpp:119, layout.hpp:49-74) with a one-time flattening
+ * (flat_modes, layout.hpp:111; oracle::detail::collect, oracle.hpp:22). */
+int tlb_layout_lower(const tlb_mode* modes, int n_modes, tlb_layout_desc* out);
+/* Same, keeping the top-level mode boundaries: top_leaves[t] = number of flat leaves in
+ * top-level mode t (sum = n_modes). Needed by gemm (rank-2, modes addressed by 1-D coordinates). */
+int tlb_layout_lower_ranked(const tlb_mode* modes, int n_modes, const int32_t* top_leaves, int n_top,
+                            tlb_layout_desc* out);
+
+/* ---- (2) bulk layout evaluation (config C5) --------------------------- */
+/* d_out[k] = L(i0 + k), k < n: tla::eval_int (layout.hpp:74) / oracle::oracle_eval_int
+ * (oracle.hpp:71) over a range, extended domain allowed (last leaf unbounded). int64 out.
+ * Xor layouts write the mask value. Basis layouts -> TLB_ERR_SEMIMODULE (use tlb_eval_axes_range). */
+int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64_t* d_out, void* stream);
+/* d_out[k*n_modes + r] = r-th natural-coordinate leaf of i0 + k: tla::idx2crd (int_tuple.hpp:129). */
+int tlb_idx2crd_range(const tlb_layout_desc* shape, uint64_t i0, uint64_t n, int64_t* d_out, void* stream);
+/* d_out[k] = crd2idx(d_crd[k*n_modes ..], shape): tla::crd2idx (int_tuple.hpp:148) on natural coordinates. */
+int tlb_crd2idx_range(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out, void* stream);
+/* Counts k in [k0, k0+n) with L(R(k)) != k into *d_mismatch (uint64, device, accumulated with atomicAdd;
+ * caller zeroes it): the defining property of tla::right_inverse (algebra.hpp:474) checked in bulk. */
+int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uint64_t k0, uint64_t n,
+                         unsigned long long* d_mismatch, void* stream);
+/* Counts i in [i0, i0+n) with A(B(i)) != R(i): the pointwise definition of tla::compose that
+ * detail::verify_distributed (algebra.hpp:211) re-checks on the host in O(size(B)). */
+int tlb_compose_check_range(const tlb_layout_desc* A, const tlb_layout_desc* B, const tlb_layout_desc* R,
+                            uint64_t i0, uint64_t n, unsigned long long* d_mismatch, void* stream);
+/* Per-axis evaluation of a Basis (coordinate) layout: d_out[k*n_axes + a] (layout_eval_axes, layout.hpp:103). */
+int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t i0, uint64_t n,
+                        int64_t* d_out, void* stream);
+
+/* ---- (3) layout-driven copy (configs C1, C3) -------------------------- */
+/* tla::copy(src, dst) (tensor.hpp:195-199): for i in [i_begin, i_end) ascending,
+ * dst(i) = src(i). Pass i_begin = 0, i_end = UINT64_MAX for the whole domain. Last-writer-wins
+ * order is preserved for non-injective destinations. Sizes must agree (contract_error).
+ * The planner picks contiguous / tiled (swizzled smem staging, optionally TMA-fed) / gather kernels. */
+int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, void* stream);
+/* Planner knobs for tlb_copy on the calling thread: force one path (testing / profiling).
+ * 0 = auto, 1 = gather only, 2 = tiled (LDG-fed), 3 = tiled TMA-fed. Returns the previous value. */
+int tlb_copy_set_path(int path);
+
+/* ---- (4) TMA tensor maps derived from divided layouts ------------------ */
+/* Builds the CUtensorMap (128 opaque bytes, 64-byte aligned) for loading one tile of
+ * zipped_divide(parent, tiler) (algebra.hpp:595): `parent` is the full Int-kind layout,
+ * `tile` the tile mode of the divide (its flat leaves select boxDim / elementStrides),
+ * both from tlb_layout_lower. swizzle: 0 none, 1 32B, 2 64B, 3 128B (= Swizzle<3,4,3> on byte
+ * offsets = the reference layout (128,8):(f1,f144) per 1 KiB, stride.hpp:142). */
+int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const tlb_layout_desc* tile, int elem_bytes,
+                               int swizzle, void* d_base, void* out_tensormap_128B);
+
+/* ---- (5) tiled GEMM (configs C2, C4) ----------------------------------- */
+/* tla::gemm(A, B, C) (tensor.hpp:214-233): C(m,n) += sum_k A(m,k) * B(n,k), all rank 2.
+ * bf16 x bf16 -> fp32, accumulator starts from C. tile_begin/tile_end select a range of
+ * output tiles (row-major over (m_tile, n_tile) of the 256x256 / 128x256 tiling; pass 0 and
+ * UINT32_MAX for all) so 1/2/4/8 GPUs can shard one problem by tile-coordinate ranges.
+ * K-major A and B with M-contiguous or N-contiguous C run on tcgen05 (TMA -> swizzled smem ->
+ * UMMA -> TMEM); every other layout family (NT, BLIS strides, GETT folded modes, Xor) runs on the
+ * layout-evaluating SIMT kernel. A.elem_bytes = B.elem_bytes = 2, C.elem_bytes = 4. */
+int tlb_gemm_bf16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin,
+                  uint32_t tile_end, void* stream);
+/* Batched: `batch` problems, operand b at data + b * batch_stride (elements); batches
+ * [batch_begin, batch_end) are executed (tile-range sharding at batch granularity, config C4). */
+int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_batch_stride,
+                          int64_t b_batch_stride, int64_t c_batch_stride, int32_t batch_begin,
+                          int32_t batch_end, void* stream);
+/* The reference's own value type: int64 cells, wrapping detected as overflow_error
+ * (checked_add/checked_mul, common.hpp:99-109) through *d_status (int32 on device, caller zeroes;
+ * set to TLB_ERR_OVERFLOW). All elem_bytes = 8. Any layouts. */
+int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream);
+/* Planner knob for tlb_gemm_bf16: 0 auto, 1 SIMT only, 2 tcgen05 cta_group::1, 3 tcgen05 cta_group::2. */
+int tlb_gemm_set_path(int path);
+
+/* ---- host-buffer convenience (the reference-facing call, used for e2e) -- */
+/* Same contracts with HOST pointers in the tlb_tensor.data fields: stages through device memory
+ * the library allocates per call, copies in, runs, copies the destination back, synchronises. */
+int tlb_copy_host(const tlb_tensor* src, const tlb_tensor* dst);
+int tlb_gemm_bf16_host(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLB_H_ */

@@ -1,0 +1,273 @@
+// Bulk layout evaluation on device (BASELINE config C5): index maps L(i), natural
+// coordinates, crd2idx and the right-inverse / composition identities, all bit-exact int64.
+//
+// Every kernel here is write-bound (8 B or more stored per evaluation, nothing read), so the
+// design rule is: one 16-byte coalesced store per thread per step, a grid of a few waves of
+// 148 SMs running a grid-stride loop, and a peel that costs a shift/mask per power-of-two
+// leaf (magic multiply otherwise) so the integer pipe stays far below the HBM write time.
+#include "tlb_internal.h"
+
+namespace tlb {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void st_cs_v2(int64_t* p, int64_t a, int64_t b) {
+    // streaming 16-byte store: the map is written once and not re-read by this kernel
+    asm volatile("st.global.cs.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+// out[k] = L(i0 + k). Pairs of consecutive k share one 16-byte store when `out` is 16-byte aligned.
+template <bool kPairs>
+__global__ void __launch_bounds__(kThreads) eval_range_kernel(const __grid_constant__ tlb_layout_desc L,
+                                                              uint64_t i0, uint64_t n, int64_t* __restrict__ out) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (kPairs) {
+        const uint64_t pairs = n >> 1;
+        for (uint64_t p = t; p < pairs; p += stride) {
+            const uint64_t k = p << 1;
+            st_cs_v2(out + k, dev_eval(L, i0 + k), dev_eval(L, i0 + k + 1));
+        }
+        if (t == 0 && (n & 1)) out[n - 1] = dev_eval(L, i0 + n - 1);
+    } else {
+        for (uint64_t k = t; k < n; k += stride) out[k] = dev_eval(L, i0 + k);
+    }
+}
+
+// out[k*nm + r] = natural coordinate leaf r of i0+k (idx2crd, int_tuple.hpp:129).
+__global__ void __launch_bounds__(kThreads) idx2crd_kernel(const __grid_constant__ tlb_layout_desc S, uint64_t i0,
+                                                           uint64_t n, int64_t* __restrict__ out) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const int nm = S.n_modes;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        uint64_t i = i0 + k;
+        int64_t* o = out + k * nm;
+        for (int r = 0; r < nm; ++r) {
+            if (r + 1 < nm) {
+                const uint64_t q = dev_div(S, r, i);
+                o[r] = static_cast<int64_t>(i - q * static_cast<uint64_t>(S.extent[r]));
+                i = q;
+            } else {
+                o[r] = static_cast<int64_t>(i);
+            }
+        }
+    }
+}
+
+// out[k] = sum_r crd[k*nm + r] * prod_{q<r} extent[q]  (crd2idx, int_tuple.hpp:148).
+__global__ void __launch_bounds__(kThreads) crd2idx_kernel(const __grid_constant__ tlb_layout_desc S,
+                                                           const int64_t* __restrict__ crd, uint64_t n,
+                                                           int64_t* __restrict__ out) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const int nm = S.n_modes;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const int64_t* c = crd + k * nm;
+        int64_t idx = 0, scale = 1;
+        for (int r = 0; r < nm; ++r) {
+            idx += c[r] * scale;
+            scale *= S.extent[r];
+        }
+        out[k] = idx;
+    }
+}
+
+__device__ __forceinline__ void block_count(unsigned long long bad, unsigned long long* d_mismatch) {
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    __shared__ unsigned long long warp_bad[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) warp_bad[threadIdx.x >> 5] = bad;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kThreads / 32; ++w) s += warp_bad[w];
+        if (s) atomicAdd(d_mismatch, s);
+    }
+}
+
+// Counts k with L(R(k)) != k.
+__global__ void __launch_bounds__(kThreads) rinv_check_kernel(const __grid_constant__ tlb_layout_desc L,
+                                                              const __grid_constant__ tlb_layout_desc R, uint64_t k0,
+                                                              uint64_t n, unsigned long long* d_mismatch) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    unsigned long long bad = 0;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const uint64_t k = k0 + j;
+        const int64_t rk = dev_eval(R, k);
+        const int64_t back = rk < 0 ? -1 : dev_eval(L, static_cast<uint64_t>(rk));
+        bad += (back != static_cast<int64_t>(k));
+    }
+    block_count(bad, d_mismatch);
+}
+
+// Counts i with A(B(i)) != Rr(i).
+__global__ void __launch_bounds__(kThreads) compose_check_kernel(const __grid_constant__ tlb_layout_desc A,
+                                                                 const __grid_constant__ tlb_layout_desc B,
+                                                                 const __grid_constant__ tlb_layout_desc Rr,
+                                                                 uint64_t i0, uint64_t n,
+                                                                 unsigned long long* d_mismatch) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    unsigned long long bad = 0;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const uint64_t i = i0 + j;
+        const int64_t b = dev_eval(B, i);
+        const int64_t want = b < 0 ? INT64_MIN : dev_eval(A, static_cast<uint64_t>(b));
+        bad += (want != dev_eval(Rr, i));
+    }
+    block_count(bad, d_mismatch);
+}
+
+struct AxesModes {
+    int32_t n_modes;
+    int32_t n_axes;
+    int64_t extent[TLB_MAX_MODES];
+    int64_t scale[TLB_MAX_MODES];
+    int32_t axis[TLB_MAX_MODES]; // -1 for Int(0) leaves
+};
+
+// Per-axis offsets of a coordinate (Basis) layout (layout_eval_axes, layout.hpp:103).
+__global__ void __launch_bounds__(kThreads) eval_axes_kernel(const __grid_constant__ AxesModes M, uint64_t i0,
+                                                             uint64_t n, int64_t* __restrict__ out) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        uint64_t i = i0 + k;
+        int64_t* o = out + k * M.n_axes;
+        for (int a = 0; a < M.n_axes; ++a) o[a] = 0;
+        for (int r = 0; r < M.n_modes; ++r) {
+            uint64_t c;
+            if (r + 1 < M.n_modes) {
+                const uint64_t e = static_cast<uint64_t>(M.extent[r]);
+                c = i % e;
+                i /= e;
+            } else {
+                c = i;
+            }
+            if (M.axis[r] >= 0) o[M.axis[r]] += static_cast<int64_t>(c) * M.scale[r];
+        }
+    }
+}
+
+int grid_for(uint64_t work_items) {
+    // a few resident waves of 148 SMs x (2048/kThreads) CTAs, never more CTAs than work
+    const uint64_t per_wave = static_cast<uint64_t>(sm_count()) * (2048 / kThreads);
+    uint64_t blocks = (work_items + kThreads - 1) / kThreads;
+    blocks = std::min<uint64_t>(blocks, per_wave * 4);
+    return static_cast<int>(std::max<uint64_t>(blocks, 1));
+}
+
+int check_int_or_xor(const tlb_layout_desc* L, const char* who) {
+    if (!L) return fail(TLB_ERR_CONTRACT, std::string(who) + ": null layout");
+    if (L->kind == TLB_KIND_BASIS) return fail(TLB_ERR_SEMIMODULE, "not an integer stride");
+    return TLB_OK;
+}
+
+} // namespace
+} // namespace tlb
+
+using namespace tlb;
+
+extern "C" {
+
+int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64_t* d_out, void* stream) {
+    TLB_TRY(check_int_or_xor(layout, "tlb_eval_range"));
+    if (n == 0) return TLB_OK;
+    if (!d_out) return fail(TLB_ERR_CONTRACT, "tlb_eval_range: null output");
+    if (i0 + n < i0 || (i0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
+    TLB_TRY(require_device());
+    TLB_TRY(overflow_preflight(*layout, 0, i0 + n - 1));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool pairs = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && n >= 2;
+    if (pairs) eval_range_kernel<true><<<grid_for(n >> 1), kThreads, 0, s>>>(*layout, i0, n, d_out);
+    else eval_range_kernel<false><<<grid_for(n), kThreads, 0, s>>>(*layout, i0, n, d_out);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    return TLB_OK;
+}
+
+int tlb_idx2crd_range(const tlb_layout_desc* shape, uint64_t i0, uint64_t n, int64_t* d_out, void* stream) {
+    if (!shape) return fail(TLB_ERR_CONTRACT, "tlb_idx2crd_range: null shape");
+    if (n == 0) return TLB_OK;
+    if (!d_out) return fail(TLB_ERR_CONTRACT, "tlb_idx2crd_range: null output");
+    if (i0 + n < i0 || (i0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
+    TLB_TRY(require_device());
+    idx2crd_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*shape, i0, n, d_out);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    return TLB_OK;
+}
+
+int tlb_crd2idx_range(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out, void* stream) {
+    if (!shape) return fail(TLB_ERR_CONTRACT, "tlb_crd2idx_range: null shape");
+    if (n == 0) return TLB_OK;
+    if (!d_crd || !d_out) return fail(TLB_ERR_CONTRACT, "tlb_crd2idx_range: null buffer");
+    TLB_TRY(require_device());
+    crd2idx_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*shape, d_crd, n, d_out);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    return TLB_OK;
+}
+
+int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uint64_t k0, uint64_t n,
+                         unsigned long long* d_mismatch, void* stream) {
+    TLB_TRY(check_int_or_xor(L, "tlb_rinv_check_range"));
+    TLB_TRY(check_int_or_xor(R, "tlb_rinv_check_range"));
+    if (n == 0) return TLB_OK;
+    if (!d_mismatch) return fail(TLB_ERR_CONTRACT, "tlb_rinv_check_range: null counter");
+    if (k0 + n < k0 || (k0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
+    TLB_TRY(require_device());
+    TLB_TRY(overflow_preflight(*R, 0, k0 + n - 1));
+    if (R->max_offset >= 0) TLB_TRY(overflow_preflight(*L, 0, static_cast<uint64_t>(R->max_offset)));
+    rinv_check_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*L, *R, k0, n, d_mismatch);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    return TLB_OK;
+}
+
+int tlb_compose_check_range(const tlb_layout_desc* A, const tlb_layout_desc* B, const tlb_layout_desc* R,
+                            uint64_t i0, uint64_t n, unsigned long long* d_mismatch, void* stream) {
+    TLB_TRY(check_int_or_xor(A, "tlb_compose_check_range"));
+    TLB_TRY(check_int_or_xor(B, "tlb_compose_check_range"));
+    TLB_TRY(check_int_or_xor(R, "tlb_compose_check_range"));
+    if (B->kind != TLB_KIND_INT) return fail(TLB_ERR_SEMIMODULE, "xor strides are not admissible on the right of composition");
+    if (n == 0) return TLB_OK;
+    if (!d_mismatch) return fail(TLB_ERR_CONTRACT, "tlb_compose_check_range: null counter");
+    if (i0 + n < i0 || (i0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
+    TLB_TRY(require_device());
+    TLB_TRY(overflow_preflight(*B, 0, i0 + n - 1));
+    TLB_TRY(overflow_preflight(*R, 0, i0 + n - 1));
+    if (B->max_offset >= 0) TLB_TRY(overflow_preflight(*A, 0, static_cast<uint64_t>(B->max_offset)));
+    compose_check_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*A, *B, *R, i0, n, d_mismatch);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    return TLB_OK;
+}
+
+int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t i0, uint64_t n, int64_t* d_out,
+                        void* stream) {
+    if (!modes || n_modes < 1 || n_modes > TLB_MAX_MODES) return fail(TLB_ERR_CONTRACT, "tlb_eval_axes_range: bad modes");
+    if (n_axes < 1 || n_axes > TLB_MAX_MODES) return fail(TLB_ERR_CONTRACT, "tlb_eval_axes_range: bad axis count");
+    AxesModes M{};
+    M.n_modes = n_modes;
+    M.n_axes = n_axes;
+    for (int r = 0; r < n_modes; ++r) {
+        if (modes[r].extent < 1) return fail(TLB_ERR_STRUCTURAL, "shape leaves must be positive");
+        M.extent[r] = modes[r].extent;
+        if (modes[r].kind == TLB_KIND_BASIS) {
+            if (modes[r].axis < 0 || modes[r].axis >= n_axes) return fail(TLB_ERR_CONTRACT, "basis axis out of range");
+            M.axis[r] = modes[r].axis;
+            M.scale[r] = modes[r].stride;
+        } else if (modes[r].kind == TLB_KIND_INT && modes[r].stride == 0) {
+            M.axis[r] = -1;
+        } else {
+            return fail(TLB_ERR_SEMIMODULE, "per-axis evaluation requires coordinate strides");
+        }
+    }
+    if (n == 0) return TLB_OK;
+    if (!d_out) return fail(TLB_ERR_CONTRACT, "tlb_eval_axes_range: null output");
+    TLB_TRY(require_device());
+    eval_axes_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(M, i0, n, d_out);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    return TLB_OK;
+}
+
+} // extern "C"

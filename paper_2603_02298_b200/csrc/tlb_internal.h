@@ -1,0 +1,130 @@
+// Internal declarations shared by the translation units of libtlb.so.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "tlb.h"
+
+namespace tlb {
+
+// ---- error plumbing ---------------------------------------------------------
+int fail(int status, const std::string& msg);   // records tlb_last_error(), returns status
+int cuda_fail(cudaError_t e, const char* what); // TLB_ERR_CUDA with the runtime's message
+void set_plan(const char* name);                // records tlb_last_plan()
+void count_launch(uint64_t n = 1);              // bumps tlb_launch_count()
+
+#define TLB_CUDA(expr)                                              \
+    do {                                                            \
+        cudaError_t e__ = (expr);                                   \
+        if (e__ != cudaSuccess) return ::tlb::cuda_fail(e__, #expr); \
+    } while (0)
+
+#define TLB_TRY(expr)                \
+    do {                             \
+        int s__ = (expr);            \
+        if (s__ != TLB_OK) return s__; \
+    } while (0)
+
+// One device is required; there is no CPU fallback anywhere in this library.
+int require_device();
+int sm_count();
+
+// ---- host helpers over descriptors -------------------------------------------
+// Exact min/max of origin (+|^) L(i) over i in [0, size): used by the bounds pre-flight.
+struct Span {
+    int64_t lo, hi;
+};
+int position_span(const tlb_layout_desc& L, int64_t origin, Span* out);
+// Conservative proof that no checked_add/checked_mul of the reference (common.hpp:99-109)
+// can overflow while evaluating L on [0, max_index].
+int overflow_preflight(const tlb_layout_desc& L, int64_t origin, uint64_t max_index);
+bool provably_injective(const tlb_layout_desc& L);
+
+// ---- TMA tensor maps (driver entry point resolved at run time; no libcuda link) ----
+struct TmaDesc {
+    alignas(64) unsigned char bytes[128];
+};
+enum TmaSwizzle { TMA_SW_NONE = 0, TMA_SW_32 = 1, TMA_SW_64 = 2, TMA_SW_128 = 3 };
+// dtype_bytes: 1,2,4,8 (16 is encoded as 4 x u32 with scaled dims by the caller).
+int tma_encode(TmaDesc* out, int dtype_bytes, bool is_bf16, int rank, void* base, const uint64_t* dims,
+               const uint64_t* strides_bytes /* rank-1 entries, dims 1.. */, const uint32_t* box,
+               int swizzle, int l2_promotion_bytes);
+
+} // namespace tlb
+
+// ---- device-side layout evaluator ----------------------------------------------
+// The flat peel of oracle::oracle_eval (oracle.hpp:58-69) == layout_eval on an integral
+// coordinate (layout.hpp:66-71): c_r = i mod e_r, i /= e_r, last leaf unbounded; Int leaves
+// contribute c*d (eval_leaf stride.hpp:138), Xor leaves the XOR of mask<<bit over the set bits
+// of c (stride.hpp:142-151), which is the carry-less product clmul(c, mask).
+#ifdef __CUDACC__
+namespace tlb {
+
+__device__ __forceinline__ uint64_t dev_div(const tlb_layout_desc& L, int r, uint64_t i) {
+    const unsigned l2 = L.log2e[r];
+    if (l2 != 0xffu) return i >> l2;
+    return __umul64hi(i, L.magic[r]) >> L.shift[r];
+}
+
+__device__ __forceinline__ int64_t dev_clmul(uint64_t c, uint64_t mask) {
+    uint64_t acc = 0;
+    while (mask) {
+        const int b = __ffsll(static_cast<long long>(mask)) - 1;
+        acc ^= c << b;
+        mask &= mask - 1;
+    }
+    return static_cast<int64_t>(acc);
+}
+
+// Offset of integral coordinate i (extended domain allowed).
+__device__ __forceinline__ int64_t dev_eval(const tlb_layout_desc& L, uint64_t i) {
+    int64_t acc = 0;
+    const int n = L.n_modes;
+    const bool is_xor = L.kind == TLB_KIND_XOR;
+    for (int r = 0; r < n; ++r) {
+        uint64_t c;
+        if (r + 1 < n) {
+            const uint64_t q = dev_div(L, r, i);
+            c = i - q * static_cast<uint64_t>(L.extent[r]);
+            i = q;
+        } else {
+            c = i;
+        }
+        if (is_xor) acc ^= dev_clmul(c, static_cast<uint64_t>(L.stride[r]));
+        else acc += static_cast<int64_t>(c) * L.stride[r];
+    }
+    return acc;
+}
+
+// Offset of a 1-D coordinate inside top-level mode t only (gemm addresses each of the two
+// top-level modes by one integer, tensor.hpp:203 + layout.hpp:54).
+__device__ __forceinline__ int64_t dev_eval_top(const tlb_layout_desc& L, int t, uint64_t i) {
+    int64_t acc = 0;
+    const int lo = L.top_start[t], hi = L.top_start[t + 1];
+    const bool is_xor = L.kind == TLB_KIND_XOR;
+    for (int r = lo; r < hi; ++r) {
+        uint64_t c;
+        if (r + 1 < hi) {
+            const uint64_t q = dev_div(L, r, i);
+            c = i - q * static_cast<uint64_t>(L.extent[r]);
+            i = q;
+        } else {
+            c = i;
+        }
+        if (is_xor) acc ^= dev_clmul(c, static_cast<uint64_t>(L.stride[r]));
+        else acc += static_cast<int64_t>(c) * L.stride[r];
+    }
+    return acc;
+}
+
+// Accessor::offset (tensor.hpp:48-60): Int adds, Xor XORs into the absolute position.
+__device__ __forceinline__ int64_t dev_position(const tlb_layout_desc& L, int64_t origin, int64_t off) {
+    return L.kind == TLB_KIND_XOR ? (origin ^ off) : (origin + off);
+}
+
+} // namespace tlb
+#endif
