@@ -1,0 +1,699 @@
+// Layout-driven copy: tla::copy(src, dst) (tensor.hpp:195-199) on device.
+//
+//   for i in [0, size) ascending:  dst(i) = src(i)
+//
+// Four kernels, chosen by a host planner that works on the COMMON REFINEMENT of the two
+// layouts (every refined mode has one extent, one source stride, one destination stride):
+//
+//   vec     one refined mode is contiguous on both sides: 16-byte (or narrower) vectors along
+//           it, one joint peel per vector.                                  [memcpy, row permutes]
+//   tiled   the source-contiguous run A and the destination-contiguous run B are different
+//           modes (transpose / permute): a CTA stages a (|B| rows x 128 B of A) tile in shared
+//           memory with the 128-byte XOR swizzle (Swizzle<3,4,3> on byte offsets, i.e. the
+//           reference layout (128,8):(f1,f144) per 1 KiB, stride.hpp:142), so that BOTH the
+//           global loads along A and the global stores along B are full 128-bit, fully
+//           coalesced accesses and every shared-memory access is a conflict-free 128-bit one.
+//           The V x V element blocks are transposed in registers in between.   [configs C1, C3]
+//   gather  anything else (Xor strides, non-refinable shapes, misalignment, counting source):
+//           one element per thread through the device evaluator. Always correct, never fast.
+//   ordered non-injective destinations: last writer wins in ascending i (tensor.hpp:198), kept
+//           by a two-pass winner election (atomicMax of i per destination cell).
+//
+// All contract / bounds / overflow checks happen on the host before any launch.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "tlb_internal.h"
+
+namespace tlb {
+namespace {
+
+thread_local int g_copy_path = 0; // 0 auto, 1 gather, 2 tiled (LDG), 3 tiled TMA
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------------------
+template <int BYTES> struct Cell;
+template <> struct Cell<1> { using type = uint8_t; };
+template <> struct Cell<2> { using type = uint16_t; };
+template <> struct Cell<4> { using type = uint32_t; };
+template <> struct Cell<8> { using type = uint64_t; };
+template <> struct Cell<16> { using type = uint4; };
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void stg_stream(void* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// gather: dst(i) = src(i), one element per thread, both layouts through the evaluator
+// ---------------------------------------------------------------------------------------
+template <int EB>
+__global__ void __launch_bounds__(kThreads)
+gather_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__ tlb_layout_desc D,
+              const void* __restrict__ src, void* __restrict__ dst, int64_t s_origin, int64_t d_origin, uint64_t i0,
+              uint64_t n, int counting) {
+    using T = typename Cell<EB>::type;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint64_t i = i0 + k;
+        const int64_t sp = dev_position(S, s_origin, dev_eval(S, i));
+        const int64_t dp = dev_position(D, d_origin, dev_eval(D, i));
+        if constexpr (EB == 8) {
+            if (counting) {
+                static_cast<uint64_t*>(dst)[dp] = static_cast<uint64_t>(sp); // Accessor::deref of a counting accessor
+                continue;
+            }
+        }
+        static_cast<T*>(dst)[dp] = static_cast<const T*>(src)[sp];
+    }
+}
+
+// ordered pass 1: winner[dp - lo] = max(i + 1) over the i that store to dp
+__global__ void __launch_bounds__(kThreads)
+winner_kernel(const __grid_constant__ tlb_layout_desc D, int64_t d_origin, int64_t lo, uint64_t i0, uint64_t n,
+              unsigned long long* __restrict__ winner) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint64_t i = i0 + k;
+        const int64_t dp = dev_position(D, d_origin, dev_eval(D, i));
+        atomicMax(winner + (dp - lo), static_cast<unsigned long long>(i + 1));
+    }
+}
+
+// ordered pass 2: only the last writer of each destination cell stores
+template <int EB>
+__global__ void __launch_bounds__(kThreads)
+ordered_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__ tlb_layout_desc D,
+               const void* __restrict__ src, void* __restrict__ dst, int64_t s_origin, int64_t d_origin, int64_t lo,
+               uint64_t i0, uint64_t n, int counting, const unsigned long long* __restrict__ winner) {
+    using T = typename Cell<EB>::type;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint64_t i = i0 + k;
+        const int64_t dp = dev_position(D, d_origin, dev_eval(D, i));
+        if (winner[dp - lo] != i + 1) continue;
+        const int64_t sp = dev_position(S, s_origin, dev_eval(S, i));
+        if constexpr (EB == 8) {
+            if (counting) {
+                static_cast<uint64_t*>(dst)[dp] = static_cast<uint64_t>(sp);
+                continue;
+            }
+        }
+        static_cast<T*>(dst)[dp] = static_cast<const T*>(src)[sp];
+    }
+}
+
+// exact min/max position of an Xor-kind tensor over [i0, i0+n) (used when the OR-bound is too loose)
+__global__ void __launch_bounds__(kThreads)
+span_kernel(const __grid_constant__ tlb_layout_desc L, int64_t origin, uint64_t i0, uint64_t n,
+            long long* __restrict__ lohi) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    long long lo = INT64_MAX, hi = INT64_MIN;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const long long p = dev_position(L, origin, dev_eval(L, i0 + k));
+        lo = p < lo ? p : lo;
+        hi = p > hi ? p : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(lohi, lo);
+        atomicMax(lohi + 1, hi);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// vec: one refined mode contiguous on both sides. J's mode 0 is that mode, counted in vectors.
+// ---------------------------------------------------------------------------------------
+template <int VB>
+__global__ void __launch_bounds__(kThreads)
+vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, char* __restrict__ dst, int eb,
+           uint64_t n_vec) {
+    using T = typename Cell<VB>::type;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n_vec; v += stride) {
+        int64_t so, dof;
+        dev_joint(J, v, &so, &dof); // offsets in elements
+        if constexpr (VB == 16) {
+            stg_stream(dst + dof * eb, ldg_stream(src + so * eb));
+        } else {
+            *reinterpret_cast<T*>(dst + dof * eb) = *reinterpret_cast<const T*>(src + so * eb);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// tiled: swizzled shared-memory staging between a source-contiguous run A and a
+// destination-contiguous run B.
+// ---------------------------------------------------------------------------------------
+constexpr int kMaxPieces = 6;
+
+struct TileParams {
+    JointDesc rest;         // tile index -> base offsets (elements) on both sides
+    int32_t nA, nB;         // pieces of the two runs
+    int64_t eA[kMaxPieces]; // A pieces: extents (product = La) ...
+    int64_t dA[kMaxPieces]; // ... and DESTINATION strides (the source stride chain is 1, e0, e0*e1, ...)
+    int64_t eB[kMaxPieces]; // B pieces: extents (product = Lb) ...
+    int64_t sB[kMaxPieces]; // ... and SOURCE strides
+    int32_t La, Lb;         // elements; La * EB = 128 bytes (one swizzle row), Lb rows
+    uint64_t n_tiles;
+};
+
+// byte offset of 16-byte chunk `c` of row `r` in the staged tile: 128 B rows, chunk index XORed
+// with the row index mod 8 == Swizzle<3,4,3> on the byte offset r*128 + c*16.
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return (r << 7) | ((c ^ (r & 7u)) << 4); }
+
+template <int EB, int LB>
+__global__ void __launch_bounds__(kThreads)
+tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src, char* __restrict__ dst) {
+    using T = typename Cell<EB>::type;
+    constexpr int V = 16 / EB;                         // elements per 16-byte vector
+    constexpr int LOGV = (V == 2) ? 1 : (V == 4) ? 2 : 3;
+    constexpr int NR = 3 - LOGV;                       // row bits a lane octet contributes
+    constexpr int CW = 8 >> NR;                        // chunks a warp-tile spans (V)
+    constexpr int LA = 128 / EB;                       // elements of A per row
+    __shared__ __align__(1024) unsigned char tile[LB * 128];
+    __shared__ int64_t s_offB[LB];                     // source offset of row b
+    __shared__ int64_t s_offA[LA];                     // destination offset of column a
+
+    int64_t base_s, base_d;
+    dev_joint(P.rest, blockIdx.x, &base_s, &base_d);
+
+    for (int t = threadIdx.x; t < LB + LA; t += kThreads) {
+        const bool isB = t < LB;
+        uint32_t i = isB ? t : t - LB;
+        const int np = isB ? P.nB : P.nA;
+        int64_t acc = 0;
+        for (int p = 0; p < np; ++p) {
+            const uint32_t e = static_cast<uint32_t>(isB ? P.eB[p] : P.eA[p]);
+            const uint32_t c = (p + 1 < np) ? i % e : i;
+            i /= e;
+            acc += static_cast<int64_t>(c) * (isB ? P.sB[p] : P.dA[p]);
+        }
+        if (isB) s_offB[t] = acc;
+        else s_offA[t - LB] = acc;
+    }
+    __syncthreads();
+
+    // phase 1: 128-bit loads along A (8 lanes = one 128 B line), swizzled 128-bit stores
+    constexpr int NVEC = LB * 8;
+    constexpr int PER = (NVEC + kThreads - 1) / kThreads;
+    uint4 stage[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (NVEC % kThreads == 0 || v < NVEC) {
+            const int c = v & 7, b = v >> 3;
+            stage[u] = ldg_stream(src + (base_s + s_offB[b] + c * V) * EB);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (NVEC % kThreads == 0 || v < NVEC) {
+            const int c = v & 7, b = v >> 3;
+            *reinterpret_cast<uint4*>(tile + swz(b, c)) = stage[u];
+        }
+    }
+    __syncthreads();
+
+    // phase 2: each lane owns V x V element blocks; conflict-free 128-bit smem reads,
+    // register transpose, 128-bit stores along B (lanes sharing a chunk cover 32 consecutive b).
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 7, p = lane >> 3;
+    const int bb = (q & ((1 << NR) - 1)) | (p << NR);
+    const int cl = q >> NR;
+    constexpr int GROUPS = 1 << NR;                    // warp-tiles per 128 B of A
+    constexpr int NWT = GROUPS * (LB / 32);
+    for (int wt = warp; wt < NWT; wt += kThreads / 32) {
+        const int c = (wt % GROUPS) * CW + cl;
+        const int r0 = (wt / GROUPS) * 32 + bb * V;
+        union { uint4 v; T e[V]; } in[V], out;
+#pragma unroll
+        for (int j = 0; j < V; ++j) in[j].v = *reinterpret_cast<const uint4*>(tile + swz(r0 + j, c));
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
+            stg_stream(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// host planner
+// ---------------------------------------------------------------------------------------
+struct JM {
+    int64_t e, ss, ds;
+};
+
+bool mul_ok(int64_t a, int64_t b, int64_t* r) { return !__builtin_mul_overflow(a, b, r); }
+
+// Common refinement of the two flat extent lists (both are mixed-radix splittings of the same
+// integral domain). Fails when some pair of radices is not nested (e.g. 6 against 4).
+bool refine_modes(const tlb_layout_desc& S, const tlb_layout_desc& D, std::vector<JM>* out) {
+    int i = 0, j = 0;
+    int64_t rs = S.extent[0], rd = D.extent[0], fs = 1, fd = 1;
+    int guard = 0;
+    while (i < S.n_modes || j < D.n_modes) {
+        if (++guard > 4 * TLB_MAX_MODES) return false;
+        const int64_t es = i < S.n_modes ? rs : 1, ed = j < D.n_modes ? rd : 1;
+        const int64_t g = std::min(es, ed);
+        if (std::max(es, ed) % g != 0) return false;
+        JM m{g, 0, 0};
+        if (i < S.n_modes && !mul_ok(S.stride[i], fs, &m.ss)) return false;
+        if (j < D.n_modes && !mul_ok(D.stride[j], fd, &m.ds)) return false;
+        if (g > 1) {
+            if (i >= S.n_modes || j >= D.n_modes) return false; // sizes differ (checked earlier)
+            out->push_back(m);
+        }
+        if (i < S.n_modes) {
+            rs /= g;
+            fs *= g;
+            if (rs == 1) {
+                ++i;
+                fs = 1;
+                if (i < S.n_modes) rs = S.extent[i];
+            }
+        }
+        if (j < D.n_modes) {
+            rd /= g;
+            fd *= g;
+            if (rd == 1) {
+                ++j;
+                fd = 1;
+                if (j < D.n_modes) rd = D.extent[j];
+            }
+        }
+    }
+    return true;
+}
+
+void joint_coalesce(std::vector<JM>* m) {
+    std::vector<JM> r;
+    for (const JM& x : *m) {
+        if (x.e == 1) continue;
+        if (!r.empty()) {
+            JM& b = r.back();
+            int64_t ns, nd;
+            if (mul_ok(b.ss, b.e, &ns) && mul_ok(b.ds, b.e, &nd) && ns == x.ss && nd == x.ds) {
+                b.e *= x.e;
+                continue;
+            }
+        }
+        r.push_back(x);
+    }
+    *m = r;
+}
+
+int launch_grid(uint64_t work_items, int threads, int waves) {
+    const uint64_t per_wave = static_cast<uint64_t>(sm_count()) * (2048 / threads);
+    uint64_t blocks = (work_items + threads - 1) / threads;
+    blocks = std::min<uint64_t>(blocks, per_wave * waves);
+    return static_cast<int>(std::max<uint64_t>(blocks, 1));
+}
+
+int fill_joint(const std::vector<JM>& m, JointDesc* J) {
+    std::memset(J, 0, sizeof(*J));
+    if (m.size() > TLB_MAX_MODES) return fail(TLB_ERR_UNSUPPORTED, "too many refined modes");
+    J->n = static_cast<int>(m.size());
+    for (size_t r = 0; r < m.size(); ++r) joint_set_mode(J, static_cast<int>(r), m[r].e, m[r].ss, m[r].ds);
+    if (J->n == 0) {
+        J->n = 1;
+        joint_set_mode(J, 0, 1, 0, 0);
+    }
+    return TLB_OK;
+}
+
+// Takes a run of total length L (elements) along the stride chain of one side, starting at the
+// mode whose stride on that side is 1. Pieces are split off `modes` (partial modes leave their
+// outer part behind). `src_side` selects which stride forms the chain.
+bool take_run(std::vector<JM>* modes, bool src_side, int64_t L, std::vector<JM>* pieces) {
+    int64_t want = L, next = 1;
+    while (want > 1) {
+        int hit = -1;
+        for (size_t r = 0; r < modes->size(); ++r)
+            if ((src_side ? (*modes)[r].ss : (*modes)[r].ds) == next && (*modes)[r].e > 1) {
+                hit = static_cast<int>(r);
+                break;
+            }
+        if (hit < 0) return false;
+        JM& m = (*modes)[hit];
+        if (m.e >= want) {
+            if (m.e % want != 0) return false;
+            pieces->push_back({want, m.ss, m.ds});
+            m.e /= want;
+            m.ss *= want;
+            m.ds *= want;
+            want = 1;
+        } else {
+            if (want % m.e != 0) return false;
+            pieces->push_back(m);
+            want /= m.e;
+            next *= m.e;
+            m.e = 1;
+        }
+    }
+    return true;
+}
+
+struct CopyCall {
+    const tlb_tensor* src;
+    const tlb_tensor* dst;
+    uint64_t i0, n;
+    cudaStream_t stream;
+};
+
+int launch_gather(const CopyCall& c) {
+    const tlb_layout_desc& S = *c.src->layout;
+    const tlb_layout_desc& D = *c.dst->layout;
+    const int counting = c.src->accessor == TLB_ACC_COUNTING;
+    const int grid = launch_grid(c.n, kThreads, 8);
+#define TLB_GATHER(EB)                                                                                        \
+    gather_kernel<EB><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
+                                                       c.i0, c.n, counting)
+    switch (c.dst->elem_bytes) {
+    case 1: TLB_GATHER(1); break;
+    case 2: TLB_GATHER(2); break;
+    case 4: TLB_GATHER(4); break;
+    case 8: TLB_GATHER(8); break;
+    default: TLB_GATHER(16); break;
+    }
+#undef TLB_GATHER
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    set_plan("gather");
+    return TLB_OK;
+}
+
+int launch_ordered(const CopyCall& c, Span dspan) {
+    const tlb_layout_desc& S = *c.src->layout;
+    const tlb_layout_desc& D = *c.dst->layout;
+    const int counting = c.src->accessor == TLB_ACC_COUNTING;
+    const uint64_t cells = static_cast<uint64_t>(dspan.hi - dspan.lo) + 1;
+    unsigned long long* winner = nullptr;
+    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&winner), cells * sizeof(unsigned long long), c.stream));
+    TLB_CUDA(cudaMemsetAsync(winner, 0, cells * sizeof(unsigned long long), c.stream));
+    const int grid = launch_grid(c.n, kThreads, 8);
+    winner_kernel<<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, winner);
+#define TLB_ORDERED(EB)                                                                                         \
+    ordered_kernel<EB><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
+                                                        dspan.lo, c.i0, c.n, counting, winner)
+    switch (c.dst->elem_bytes) {
+    case 1: TLB_ORDERED(1); break;
+    case 2: TLB_ORDERED(2); break;
+    case 4: TLB_ORDERED(4); break;
+    case 8: TLB_ORDERED(8); break;
+    default: TLB_ORDERED(16); break;
+    }
+#undef TLB_ORDERED
+    count_launch(2);
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(winner, c.stream);
+    TLB_CUDA(e);
+    set_plan("ordered");
+    return TLB_OK;
+}
+
+bool aligned_to(const void* p, int64_t origin, int eb, int bytes) {
+    return ((reinterpret_cast<uintptr_t>(p) + static_cast<uintptr_t>(origin) * eb) % bytes) == 0;
+}
+
+// Tries the vec and tiled plans. Returns TLB_OK with *done = true when a kernel was launched.
+int try_planned(const CopyCall& c, bool* done) {
+    *done = false;
+    const tlb_tensor& s = *c.src;
+    const tlb_tensor& d = *c.dst;
+    const tlb_layout_desc& S = *s.layout;
+    const tlb_layout_desc& D = *d.layout;
+    const int eb = d.elem_bytes;
+    if (S.kind != TLB_KIND_INT || D.kind != TLB_KIND_INT || s.accessor != TLB_ACC_BUFFER) return TLB_OK;
+    std::vector<JM> modes;
+    if (!refine_modes(S, D, &modes)) return TLB_OK;
+    joint_coalesce(&modes);
+    if (modes.empty()) return TLB_OK; // single element: gather
+    // Restrict to [i0, i0+n): the range must select whole slices of the outermost refined mode.
+    int64_t base_s = s.origin, base_d = d.origin;
+    if (c.n != static_cast<uint64_t>(S.size)) {
+        JM& last = modes.back();
+        const uint64_t prefix = static_cast<uint64_t>(S.size / last.e);
+        if (c.i0 % prefix != 0 || c.n % prefix != 0) return TLB_OK;
+        const int64_t c0 = static_cast<int64_t>(c.i0 / prefix);
+        base_s += c0 * last.ss;
+        base_d += c0 * last.ds;
+        last.e = static_cast<int64_t>(c.n / prefix);
+        if (last.e == 1) modes.pop_back();
+        if (modes.empty()) return TLB_OK;
+    }
+    int ia = -1, ib = -1;
+    for (size_t r = 0; r < modes.size(); ++r) {
+        if (modes[r].ss == 1 && ia < 0) ia = static_cast<int>(r);
+        if (modes[r].ds == 1 && ib < 0) ib = static_cast<int>(r);
+    }
+    if (ia < 0 || ib < 0) return TLB_OK;
+    const char* sp = static_cast<const char*>(s.data);
+    char* dp = static_cast<char*>(d.data);
+
+    if (ia == ib && g_copy_path != 2 && g_copy_path != 3) {
+        // ---- vec plan: widest power-of-two vector that divides the run and every other stride
+        int vb = 16;
+        auto fits = [&](int bytes) {
+            if (bytes < eb) return false;
+            const int64_t v = bytes / eb;
+            if (modes[ia].e % v != 0) return false;
+            for (size_t r = 0; r < modes.size(); ++r)
+                if (static_cast<int>(r) != ia && (modes[r].ss % v != 0 || modes[r].ds % v != 0)) return false;
+            return aligned_to(sp, base_s, eb, bytes) && aligned_to(dp, base_d, eb, bytes);
+        };
+        while (vb > eb && !fits(vb)) vb >>= 1;
+        if (eb == 16) vb = fits(16) ? 16 : 0;
+        if (vb < eb || vb == 1 || !fits(vb)) return TLB_OK;
+        const int64_t v = vb / eb;
+        std::vector<JM> order;
+        order.push_back({modes[ia].e / v, v, v});
+        std::vector<JM> rest;
+        for (size_t r = 0; r < modes.size(); ++r)
+            if (static_cast<int>(r) != ia) rest.push_back(modes[r]);
+        std::stable_sort(rest.begin(), rest.end(), [](const JM& a, const JM& b) {
+            return std::min(std::llabs(a.ss), std::llabs(a.ds)) < std::min(std::llabs(b.ss), std::llabs(b.ds));
+        });
+        order.insert(order.end(), rest.begin(), rest.end());
+        JointDesc J;
+        TLB_TRY(fill_joint(order, &J));
+        const uint64_t n_vec = c.n / static_cast<uint64_t>(v);
+        const int grid = launch_grid(n_vec, kThreads, 8);
+        const char* sb = sp + base_s * eb;
+        char* db = dp + base_d * eb;
+        switch (vb) {
+        case 2: vec_kernel<2><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
+        case 4: vec_kernel<4><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
+        case 8: vec_kernel<8><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
+        default: vec_kernel<16><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
+        }
+        count_launch();
+        TLB_CUDA(cudaGetLastError());
+        set_plan("vec");
+        *done = true;
+        return TLB_OK;
+    }
+    if (ia == ib) return TLB_OK;
+
+    // ---- tiled plan
+    if (eb != 2 && eb != 4 && eb != 8) return TLB_OK;
+    const int64_t V = 16 / eb, La = 128 / eb;
+    for (const JM& m : modes)
+        if (m.ss < 0 || m.ds < 0) return TLB_OK;
+    if (!aligned_to(sp, base_s, eb, 16) || !aligned_to(dp, base_d, eb, 16)) return TLB_OK;
+    static const int64_t kLb[] = {128, 64, 32};
+    for (int64_t Lb : kLb) {
+        std::vector<JM> work = modes, A, B;
+        if (!take_run(&work, true, La, &A)) break; // the A run does not depend on Lb
+        if (!take_run(&work, false, Lb, &B)) continue;
+        if (A.size() > kMaxPieces || B.size() > kMaxPieces) continue;
+        bool ok = true;
+        for (const JM& m : A) ok = ok && (m.ds % V == 0);
+        for (const JM& m : B) ok = ok && (m.ss % V == 0);
+        std::vector<JM> rest;
+        for (const JM& m : work)
+            if (m.e > 1) {
+                ok = ok && (m.ss % V == 0) && (m.ds % V == 0);
+                rest.push_back(m);
+            }
+        if (!ok) continue;
+        // B must be contiguous on the destination (row b -> +b) and A on the source: by construction.
+        TileParams P;
+        std::memset(&P, 0, sizeof(P));
+        // neighbouring CTAs should touch neighbouring memory: order the rest modes by locality
+        std::stable_sort(rest.begin(), rest.end(), [](const JM& a, const JM& b) {
+            return std::min(a.ss, a.ds) < std::min(b.ss, b.ds);
+        });
+        TLB_TRY(fill_joint(rest, &P.rest));
+        P.nA = static_cast<int>(A.size());
+        P.nB = static_cast<int>(B.size());
+        for (size_t r = 0; r < A.size(); ++r) { P.eA[r] = A[r].e; P.dA[r] = A[r].ds; }
+        for (size_t r = 0; r < B.size(); ++r) { P.eB[r] = B[r].e; P.sB[r] = B[r].ss; }
+        P.La = static_cast<int>(La);
+        P.Lb = static_cast<int>(Lb);
+        uint64_t tiles = 1;
+        for (const JM& m : rest) tiles *= static_cast<uint64_t>(m.e);
+        P.n_tiles = tiles;
+        if (tiles > 0x7fffffffull) return TLB_OK;
+        const char* sb = sp + base_s * eb;
+        char* db = dp + base_d * eb;
+        const unsigned grid = static_cast<unsigned>(tiles);
+#define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
+        if (eb == 4) {
+            if (Lb == 128) TLB_TILED(4, 128); else if (Lb == 64) TLB_TILED(4, 64); else TLB_TILED(4, 32);
+        } else if (eb == 8) {
+            if (Lb == 128) TLB_TILED(8, 128); else if (Lb == 64) TLB_TILED(8, 64); else TLB_TILED(8, 32);
+        } else {
+            if (Lb == 128) TLB_TILED(2, 128); else if (Lb == 64) TLB_TILED(2, 64); else TLB_TILED(2, 32);
+        }
+#undef TLB_TILED
+        count_launch();
+        TLB_CUDA(cudaGetLastError());
+        set_plan("tiled");
+        *done = true;
+        return TLB_OK;
+    }
+    return TLB_OK;
+}
+
+} // namespace
+
+// Exact span of positions for the bounds pre-flight (tensor.hpp:99): Int kind by interval
+// arithmetic over the modes (exact on the full domain, outer-mode-restricted on a sub-range),
+// Xor kind by the OR-bound with an exact device scan when that bound does not fit.
+int bounds_preflight(const tlb_tensor& t, uint64_t i0, uint64_t n, const char* who, cudaStream_t stream, Span* out) {
+    const tlb_layout_desc& L = *t.layout;
+    Span sp{0, 0};
+    if (L.kind == TLB_KIND_INT) {
+        __int128 lo = t.origin, hi = t.origin;
+        uint64_t prefix = 1;
+        for (int r = 0; r < L.n_modes; ++r) {
+            int64_t c_lo = 0, c_hi = L.extent[r] - 1;
+            if (r + 1 == L.n_modes) {
+                c_lo = static_cast<int64_t>(i0 / prefix);
+                c_hi = static_cast<int64_t>((i0 + n - 1) / prefix);
+            }
+            const __int128 a = static_cast<__int128>(c_lo) * L.stride[r], b = static_cast<__int128>(c_hi) * L.stride[r];
+            lo += a < b ? a : b;
+            hi += a < b ? b : a;
+            prefix *= static_cast<uint64_t>(L.extent[r]);
+        }
+        if (lo < INT64_MIN || hi > INT64_MAX) return fail(TLB_ERR_OVERFLOW, "integer overflow in addition");
+        sp.lo = static_cast<int64_t>(lo);
+        sp.hi = static_cast<int64_t>(hi);
+        // a sub-range narrower than the outermost mode's stride may be over-approximated; verify exactly
+        if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && n != static_cast<uint64_t>(L.size)) {
+            long long h[2] = {INT64_MAX, INT64_MIN};
+            long long* d = nullptr;
+            TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), stream));
+            TLB_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+            span_kernel<<<launch_grid(n, kThreads, 8), kThreads, 0, stream>>>(L, t.origin, i0, n, d);
+            count_launch();
+            TLB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+            TLB_CUDA(cudaStreamSynchronize(stream));
+            cudaFreeAsync(d, stream);
+            sp.lo = h[0];
+            sp.hi = h[1];
+        }
+    } else {
+        TLB_TRY(position_span(L, t.origin, &sp));
+        if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && t.origin >= 0) {
+            long long h[2] = {INT64_MAX, INT64_MIN};
+            long long* d = nullptr;
+            TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), stream));
+            TLB_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+            span_kernel<<<launch_grid(n, kThreads, 8), kThreads, 0, stream>>>(L, t.origin, i0, n, d);
+            count_launch();
+            TLB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+            TLB_CUDA(cudaStreamSynchronize(stream));
+            cudaFreeAsync(d, stream);
+            sp.lo = h[0];
+            sp.hi = h[1];
+        }
+    }
+    if (t.accessor == TLB_ACC_BUFFER && (sp.lo < 0 || sp.hi >= t.capacity))
+        return fail(TLB_ERR_BOUNDS, std::string("buffer access out of bounds (") + who + ")");
+    *out = sp;
+    return TLB_OK;
+}
+
+int check_tensor(const tlb_tensor* t, const char* who, bool writable) {
+    if (!t || !t->layout) return fail(TLB_ERR_CONTRACT, std::string(who) + ": null tensor");
+    if (t->layout->kind == TLB_KIND_BASIS)
+        return fail(TLB_ERR_SEMIMODULE, "integer accessor cannot take a coordinate offset");
+    if (t->accessor != TLB_ACC_BUFFER && t->accessor != TLB_ACC_COUNTING)
+        return fail(TLB_ERR_CONTRACT, std::string(who) + ": unknown accessor");
+    if (writable && t->accessor != TLB_ACC_BUFFER) return fail(TLB_ERR_CONTRACT, "only buffer accessors are writable");
+    if (t->accessor == TLB_ACC_BUFFER) {
+        if (!t->data) return fail(TLB_ERR_CONTRACT, "buffer accessor requires storage");
+        if (t->capacity < 0) return fail(TLB_ERR_CONTRACT, std::string(who) + ": negative capacity");
+    }
+    const int eb = t->elem_bytes;
+    if (eb != 1 && eb != 2 && eb != 4 && eb != 8 && eb != 16)
+        return fail(TLB_ERR_UNSUPPORTED, std::string(who) + ": element size must be 1, 2, 4, 8 or 16 bytes");
+    return TLB_OK;
+}
+
+int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, cudaStream_t stream) {
+    TLB_TRY(check_tensor(src, "tlb_copy source", false));
+    TLB_TRY(check_tensor(dst, "tlb_copy destination", true));
+    const tlb_layout_desc& S = *src->layout;
+    const tlb_layout_desc& D = *dst->layout;
+    if (S.size != D.size) return fail(TLB_ERR_CONTRACT, "copy requires equal sizes");
+    if (src->elem_bytes != dst->elem_bytes) return fail(TLB_ERR_CONTRACT, "tlb_copy: element sizes differ");
+    if (src->accessor == TLB_ACC_COUNTING && dst->elem_bytes != 8)
+        return fail(TLB_ERR_CONTRACT, "tlb_copy: a counting source produces 8-byte cells");
+    const uint64_t size = static_cast<uint64_t>(S.size);
+    if (i_end > size) i_end = size;
+    if (i_begin >= i_end) return TLB_OK;
+    TLB_TRY(require_device());
+    CopyCall c{src, dst, i_begin, i_end - i_begin, stream};
+    TLB_TRY(overflow_preflight(S, src->origin, i_end - 1));
+    TLB_TRY(overflow_preflight(D, dst->origin, i_end - 1));
+    Span sspan, dspan;
+    TLB_TRY(bounds_preflight(*src, c.i0, c.n, "source", stream, &sspan));
+    TLB_TRY(bounds_preflight(*dst, c.i0, c.n, "destination", stream, &dspan));
+    if (!(D.flags & TLB_LF_INJECTIVE)) return launch_ordered(c, dspan);
+    if (g_copy_path != 1) {
+        bool done = false;
+        TLB_TRY(try_planned(c, &done));
+        if (done) return TLB_OK;
+        if (g_copy_path == 2 || g_copy_path == 3)
+            return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the forced tiled path does not apply to these layouts");
+    }
+    return launch_gather(c);
+}
+
+} // namespace tlb
+
+extern "C" {
+
+int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, void* stream) {
+    return tlb::copy_impl(src, dst, i_begin, i_end, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_copy_set_path(int path) {
+    const int prev = tlb::g_copy_path;
+    if (path >= 0 && path <= 3) tlb::g_copy_path = path;
+    return prev;
+}
+
+} // extern "C"

@@ -1,0 +1,290 @@
+// tla::gemm(A, B, C) (tensor.hpp:214-233): contract checks, plan selection, and the
+// layout-evaluating SIMT kernels that serve every layout family the tcgen05 path does not
+// (NT, NTT, BLIS strides, GETT folded modes, Xor strides) as well as the reference's own
+// checked-int64 value type.
+//
+//   C(m,n) += sum_k A(m,k) * B(n,k)     all tensors rank 2, modes addressed by 1-D coordinates
+//
+// The SIMT kernels keep the reference's summation order (k ascending, accumulator starts
+// from C), so for bf16 they are bit-exact against the sequential fp32 restatement
+// (bf16 x bf16 is exact in fp32, hence fma(a, b, acc) == acc + a*b).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include <cuda_bf16.h>
+
+#include "tlb_internal.h"
+#include "tlb_gemm.h"
+
+namespace tlb {
+namespace {
+
+thread_local int g_gemm_path = 0; // 0 auto, 1 SIMT, 2 tcgen05 cta_group::1, 3 tcgen05 cta_group::2
+
+constexpr int kThreads = 256;
+
+struct SimtArgs {
+    int64_t a_origin, b_origin, c_origin;
+    int64_t a_bs, b_bs, c_bs; // batch strides (elements)
+    int64_t M, N, K;
+    TileGrid grid;
+    uint32_t tile_begin, tile_end; // global tile ids (batch-major)
+    int32_t batch_begin, batch_end;
+};
+
+__device__ __forceinline__ int64_t combine(int kind, int64_t a, int64_t b) { return kind == TLB_KIND_XOR ? (a ^ b) : (a + b); }
+
+template <bool kI64>
+__global__ void __launch_bounds__(kThreads)
+gemm_simt_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_constant__ tlb_layout_desc LB,
+                 const __grid_constant__ tlb_layout_desc LC, const void* __restrict__ A, const void* __restrict__ B,
+                 void* C, const __grid_constant__ SimtArgs p, int* d_status) {
+    const uint64_t per_batch = static_cast<uint64_t>(p.M) * static_cast<uint64_t>(p.N);
+    const uint64_t total = per_batch * static_cast<uint64_t>(p.batch_end - p.batch_begin);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint32_t tpb = tiles_per_batch(p.grid);
+    for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        const int64_t batch = p.batch_begin + static_cast<int64_t>(idx / per_batch);
+        const uint64_t e = idx % per_batch;
+        const int64_t m = static_cast<int64_t>(e % static_cast<uint64_t>(p.M));
+        const int64_t n = static_cast<int64_t>(e / static_cast<uint64_t>(p.M));
+        const uint64_t tile = static_cast<uint64_t>(batch) * tpb + tile_of(p.grid, m, n);
+        if (tile < p.tile_begin || tile >= p.tile_end) continue;
+        const int64_t a_m = dev_eval_top(LA, 0, m), b_n = dev_eval_top(LB, 0, n);
+        const int64_t cp = dev_position(LC, p.c_origin, combine(LC.kind, dev_eval_top(LC, 0, m), dev_eval_top(LC, 1, n))) +
+                           batch * p.c_bs;
+        if constexpr (kI64) {
+            const int64_t* a = static_cast<const int64_t*>(A) + batch * p.a_bs;
+            const int64_t* b = static_cast<const int64_t*>(B) + batch * p.b_bs;
+            int64_t* c = static_cast<int64_t*>(C);
+            int64_t acc = c[cp];
+            bool ovf = false;
+            for (int64_t k = 0; k < p.K; ++k) {
+                const int64_t x = a[dev_position(LA, p.a_origin, combine(LA.kind, a_m, dev_eval_top(LA, 1, k)))];
+                const int64_t y = b[dev_position(LB, p.b_origin, combine(LB.kind, b_n, dev_eval_top(LB, 1, k)))];
+                // checked_mul / checked_add (common.hpp:99-109)
+                const int64_t lo = static_cast<int64_t>(static_cast<uint64_t>(x) * static_cast<uint64_t>(y));
+                const int64_t hi = __mul64hi(x, y);
+                if (hi != (lo >> 63)) { ovf = true; break; }
+                const int64_t s = static_cast<int64_t>(static_cast<uint64_t>(acc) + static_cast<uint64_t>(lo));
+                if (((acc ^ s) & (lo ^ s)) < 0) { ovf = true; break; }
+                acc = s;
+            }
+            if (ovf) {
+                if (d_status) atomicExch(d_status, TLB_ERR_OVERFLOW);
+            } else {
+                c[cp] = acc;
+            }
+        } else {
+            const __nv_bfloat16* a = static_cast<const __nv_bfloat16*>(A) + batch * p.a_bs;
+            const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(B) + batch * p.b_bs;
+            float* c = static_cast<float*>(C);
+            float acc = c[cp];
+            for (int64_t k = 0; k < p.K; ++k) {
+                const float x = __bfloat162float(a[dev_position(LA, p.a_origin, combine(LA.kind, a_m, dev_eval_top(LA, 1, k)))]);
+                const float y = __bfloat162float(b[dev_position(LB, p.b_origin, combine(LB.kind, b_n, dev_eval_top(LB, 1, k)))]);
+                acc = __fmaf_rn(x, y, acc);
+            }
+            c[cp] = acc;
+        }
+    }
+}
+
+int64_t top_size(const tlb_layout_desc& L, int t) {
+    int64_t s = 1;
+    for (int r = L.top_start[t]; r < L.top_start[t + 1]; ++r) s *= L.extent[r];
+    return s;
+}
+
+// A top-level mode as one (extent, stride) pair, if its leaves coalesce to that.
+bool single_stride(const tlb_layout_desc& L, int t, int64_t* extent, int64_t* stride) {
+    int64_t e = 1, s = 0;
+    bool have = false;
+    for (int r = L.top_start[t]; r < L.top_start[t + 1]; ++r) {
+        if (L.extent[r] == 1) continue;
+        if (!have) {
+            e = L.extent[r];
+            s = L.stride[r];
+            have = true;
+        } else if (L.stride[r] == s * e) {
+            e *= L.extent[r];
+        } else {
+            return false;
+        }
+    }
+    *extent = e;
+    *stride = have ? s : 0;
+    return true;
+}
+
+struct GemmDims {
+    int64_t M, N, K;
+};
+
+int check_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int ab_bytes, int c_bytes, GemmDims* d) {
+    TLB_TRY(check_tensor(A, "tlb_gemm A", false));
+    TLB_TRY(check_tensor(B, "tlb_gemm B", false));
+    TLB_TRY(check_tensor(C, "tlb_gemm C", true));
+    if (A->accessor != TLB_ACC_BUFFER || B->accessor != TLB_ACC_BUFFER)
+        return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: operands must be buffer tensors");
+    if (A->layout->n_top != 2 || B->layout->n_top != 2 || C->layout->n_top != 2)
+        return fail(TLB_ERR_CONTRACT, "gemm requires rank-2 tensors");
+    d->M = top_size(*A->layout, 0);
+    d->N = top_size(*B->layout, 0);
+    d->K = top_size(*A->layout, 1);
+    if (d->M != top_size(*C->layout, 0) || d->N != top_size(*C->layout, 1) || d->K != top_size(*B->layout, 1))
+        return fail(TLB_ERR_CONTRACT, "gemm mode extents do not agree");
+    if (A->elem_bytes != ab_bytes || B->elem_bytes != ab_bytes || C->elem_bytes != c_bytes)
+        return fail(TLB_ERR_CONTRACT, "tlb_gemm: element sizes do not match the entry point");
+    return TLB_OK;
+}
+
+// Batched bounds: every batch must stay inside the buffer.
+int gemm_bounds(const tlb_tensor& t, int64_t bs, int b0, int b1, const char* who, cudaStream_t stream) {
+    tlb_tensor lo = t, hi = t;
+    lo.origin = t.origin + bs * b0;
+    hi.origin = t.origin + bs * (b1 - 1);
+    Span sp;
+    const uint64_t n = static_cast<uint64_t>(t.layout->size);
+    TLB_TRY(overflow_preflight(*t.layout, hi.origin, n - 1));
+    TLB_TRY(bounds_preflight(lo, 0, n, who, stream, &sp));
+    if (b1 - 1 != b0) TLB_TRY(bounds_preflight(hi, 0, n, who, stream, &sp));
+    return TLB_OK;
+}
+
+int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool i64, int64_t a_bs, int64_t b_bs,
+             int64_t c_bs, int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, int* d_status,
+             cudaStream_t stream) {
+    GemmDims d;
+    TLB_TRY(check_gemm(A, B, C, i64 ? 8 : 2, i64 ? 8 : 4, &d));
+    if (batch_begin < 0 || batch_end < batch_begin) return fail(TLB_ERR_CONTRACT, "tlb_gemm: bad batch range");
+    if (batch_end == batch_begin) return TLB_OK;
+    if (d.M >= (1ll << 31) || d.N >= (1ll << 31) || d.K >= (1ll << 31))
+        return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: extents must be below 2^31");
+    TLB_TRY(require_device());
+    TLB_TRY(gemm_bounds(*A, a_bs, batch_begin, batch_end, "A", stream));
+    TLB_TRY(gemm_bounds(*B, b_bs, batch_begin, batch_end, "B", stream));
+    TLB_TRY(gemm_bounds(*C, c_bs, batch_begin, batch_end, "C", stream));
+    TileGrid grid{static_cast<uint32_t>((d.M + 255) / 256), static_cast<uint32_t>((d.N + 255) / 256)};
+    const uint64_t tpb = tiles_per_batch(grid);
+    if (tpb * static_cast<uint64_t>(batch_end) > 0xffffffffull) return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: too many tiles");
+    // Global tile range: the caller's range applies inside [batch_begin, batch_end).
+    uint64_t t0 = static_cast<uint64_t>(batch_begin) * tpb, t1 = static_cast<uint64_t>(batch_end) * tpb;
+    if (tile_begin != 0 || tile_end != UINT32_MAX) {
+        t0 = std::max<uint64_t>(t0, tile_begin);
+        t1 = std::min<uint64_t>(t1, tile_end);
+        if (t0 >= t1) return TLB_OK;
+    }
+
+    // ---- tcgen05 plan: K-major A and B, single-stride C modes, TMA-legal strides
+    if (!i64 && g_gemm_path != 1) {
+        int64_t eM, lda, eK, ska, eN, ldb, eKb, skb, eCm, csm, eCn, csn;
+        const bool flat = A->layout->kind == TLB_KIND_INT && B->layout->kind == TLB_KIND_INT &&
+                          C->layout->kind == TLB_KIND_INT && single_stride(*A->layout, 0, &eM, &lda) &&
+                          single_stride(*A->layout, 1, &eK, &ska) && single_stride(*B->layout, 0, &eN, &ldb) &&
+                          single_stride(*B->layout, 1, &eKb, &skb) && single_stride(*C->layout, 0, &eCm, &csm) &&
+                          single_stride(*C->layout, 1, &eCn, &csn);
+        const bool batched = batch_end - batch_begin > 1 || batch_begin > 0;
+        bool ok = flat && (ska == 1 || d.K == 1) && (skb == 1 || d.K == 1) && lda > 0 && ldb > 0 && lda % 8 == 0 &&
+                  ldb % 8 == 0 && csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) &&
+                  (C->layout->flags & TLB_LF_INJECTIVE) && (!batched || (a_bs % 8 == 0 && b_bs % 8 == 0 && a_bs > 0 && b_bs > 0));
+        const char* a_ptr = static_cast<const char*>(A->data) + A->origin * 2;
+        const char* b_ptr = static_cast<const char*>(B->data) + B->origin * 2;
+        ok = ok && (reinterpret_cast<uintptr_t>(a_ptr) % 16 == 0) && (reinterpret_cast<uintptr_t>(b_ptr) % 16 == 0) &&
+             (!batched || ((a_bs * 2) % 16 == 0 && (b_bs * 2) % 16 == 0));
+        if (ok) {
+            UmmaProblem p;
+            std::memset(&p, 0, sizeof(p));
+            p.A = a_ptr;
+            p.B = b_ptr;
+            p.C = static_cast<float*>(C->data) + C->origin;
+            p.lda = lda;
+            p.ldb = ldb;
+            p.cs_m = csm;
+            p.cs_n = csn;
+            p.M = static_cast<int32_t>(d.M);
+            p.N = static_cast<int32_t>(d.N);
+            p.K = static_cast<int32_t>(d.K);
+            p.batch = batch_end;
+            p.a_bs = a_bs;
+            p.b_bs = b_bs;
+            p.c_bs = c_bs;
+            p.tile_begin = static_cast<uint32_t>(t0);
+            p.tile_end = static_cast<uint32_t>(t1);
+            const bool even = (t0 % 2 == 0) && (t1 % 2 == 0);
+            p.cta_group = g_gemm_path == 2 ? 1 : g_gemm_path == 3 ? 2 : 1 /* cta_group::2 is opt-in until profiled faster */;
+            if (p.cta_group == 2 && !even)
+                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
+            return umma_gemm_launch(p, stream);
+        }
+        if (g_gemm_path == 2 || g_gemm_path == 3)
+            return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: the forced tcgen05 path does not apply to these layouts");
+    }
+
+    // ---- SIMT plan
+    if (!(C->layout->flags & TLB_LF_INJECTIVE))
+        return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: C must be injective (aliased accumulators are order-dependent)");
+    SimtArgs p;
+    std::memset(&p, 0, sizeof(p));
+    p.a_origin = A->origin;
+    p.b_origin = B->origin;
+    p.c_origin = C->origin;
+    p.a_bs = a_bs;
+    p.b_bs = b_bs;
+    p.c_bs = c_bs;
+    p.M = d.M;
+    p.N = d.N;
+    p.K = d.K;
+    p.grid = grid;
+    p.tile_begin = static_cast<uint32_t>(t0);
+    p.tile_end = static_cast<uint32_t>(t1);
+    p.batch_begin = batch_begin;
+    p.batch_end = batch_end;
+    const uint64_t total = static_cast<uint64_t>(d.M) * d.N * (batch_end - batch_begin);
+    const uint64_t blocks = std::min<uint64_t>((total + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 32);
+    const int gridx = static_cast<int>(std::max<uint64_t>(blocks, 1));
+    if (i64)
+        gemm_simt_kernel<true><<<gridx, kThreads, 0, stream>>>(*A->layout, *B->layout, *C->layout, A->data, B->data, C->data, p, d_status);
+    else
+        gemm_simt_kernel<false><<<gridx, kThreads, 0, stream>>>(*A->layout, *B->layout, *C->layout, A->data, B->data, C->data, p, nullptr);
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
+    set_plan(i64 ? "simt_i64" : "simt_bf16");
+    return TLB_OK;
+}
+
+} // namespace
+
+int gemm_bf16_impl(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_bs, int64_t b_bs, int64_t c_bs,
+                   int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, cudaStream_t stream) {
+    return run_gemm(A, B, C, false, a_bs, b_bs, c_bs, batch_begin, batch_end, tile_begin, tile_end, nullptr, stream);
+}
+
+} // namespace tlb
+
+extern "C" {
+
+int tlb_gemm_bf16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin, uint32_t tile_end,
+                  void* stream) {
+    return tlb::run_gemm(A, B, C, false, 0, 0, 0, 0, 1, tile_begin, tile_end, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_batch_stride,
+                          int64_t b_batch_stride, int64_t c_batch_stride, int32_t batch_begin, int32_t batch_end,
+                          void* stream) {
+    return tlb::run_gemm(A, B, C, false, a_batch_stride, b_batch_stride, c_batch_stride, batch_begin, batch_end, 0,
+                         UINT32_MAX, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream) {
+    return tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, d_status, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_gemm_set_path(int path) {
+    const int prev = tlb::g_gemm_path;
+    if (path >= 0 && path <= 3) tlb::g_gemm_path = path;
+    return prev;
+}
+
+} // extern "C"

@@ -43,6 +43,30 @@ int position_span(const tlb_layout_desc& L, int64_t origin, Span* out);
 // can overflow while evaluating L on [0, max_index].
 int overflow_preflight(const tlb_layout_desc& L, int64_t origin, uint64_t max_index);
 bool provably_injective(const tlb_layout_desc& L);
+// Argument contract of one tensor (null pointers, accessor, element size).
+int check_tensor(const tlb_tensor* t, const char* who, bool writable);
+// Bounds pre-flight of tensor.hpp:99 for the positions origin (+|^) L(i), i in [i0, i0+n).
+int bounds_preflight(const tlb_tensor& t, uint64_t i0, uint64_t n, const char* who, cudaStream_t stream, Span* out);
+// Shared by the device-pointer and host-pointer entry points.
+int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, cudaStream_t stream);
+int gemm_bf16_impl(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_bs, int64_t b_bs, int64_t c_bs,
+                   int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, cudaStream_t stream);
+
+// ---- joint descriptor: one peel, two offsets ------------------------------------
+// The common refinement of a source and a destination layout over the same integral domain:
+// refined mode r has one extent and one stride on each side, so a single division chain
+// yields both offsets (the copy kernels' replacement for two eval_rec walks, layout.hpp:49).
+struct JointDesc {
+    int32_t n;
+    int32_t pad_;
+    int64_t extent[TLB_MAX_MODES];
+    int64_t ss[TLB_MAX_MODES]; // source stride (elements)
+    int64_t ds[TLB_MAX_MODES]; // destination stride (elements)
+    uint64_t magic[TLB_MAX_MODES];
+    uint8_t shift[TLB_MAX_MODES];
+    uint8_t log2e[TLB_MAX_MODES];
+};
+void joint_set_mode(JointDesc* J, int r, int64_t extent, int64_t ss, int64_t ds);
 
 // ---- TMA tensor maps (driver entry point resolved at run time; no libcuda link) ----
 struct TmaDesc {
@@ -119,6 +143,27 @@ __device__ __forceinline__ int64_t dev_eval_top(const tlb_layout_desc& L, int t,
         else acc += static_cast<int64_t>(c) * L.stride[r];
     }
     return acc;
+}
+
+// One peel of idx through the joint modes (last mode unbounded): both offsets at once.
+__device__ __forceinline__ void dev_joint(const JointDesc& J, uint64_t i, int64_t* so, int64_t* dof) {
+    int64_t a = 0, b = 0;
+    const int n = J.n;
+    for (int r = 0; r < n; ++r) {
+        uint64_t c;
+        if (r + 1 < n) {
+            const unsigned l2 = J.log2e[r];
+            const uint64_t q = (l2 != 0xffu) ? (i >> l2) : (__umul64hi(i, J.magic[r]) >> J.shift[r]);
+            c = i - q * static_cast<uint64_t>(J.extent[r]);
+            i = q;
+        } else {
+            c = i;
+        }
+        a += static_cast<int64_t>(c) * J.ss[r];
+        b += static_cast<int64_t>(c) * J.ds[r];
+    }
+    *so = a;
+    *dof = b;
 }
 
 // Accessor::offset (tensor.hpp:48-60): Int adds, Xor XORs into the absolute position.

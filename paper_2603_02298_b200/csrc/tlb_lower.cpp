@@ -79,6 +79,17 @@ void make_magic(int64_t d, uint64_t* magic, uint8_t* shift, uint8_t* log2e) {
     *shift = static_cast<uint8_t>(l - 1);
 }
 
+} // namespace
+
+void joint_set_mode(JointDesc* J, int r, int64_t extent, int64_t ss, int64_t ds) {
+    J->extent[r] = extent;
+    J->ss[r] = ss;
+    J->ds[r] = ds;
+    make_magic(extent, &J->magic[r], &J->shift[r], &J->log2e[r]);
+}
+
+namespace {
+
 int lower_impl(const tlb_mode* modes, int n_modes, const int32_t* top_leaves, int n_top,
                tlb_layout_desc* out) {
     if (!modes || !out) return fail(TLB_ERR_CONTRACT, "tlb_layout_lower: null argument");

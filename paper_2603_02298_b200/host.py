@@ -1,0 +1,259 @@
+"""Thin Python driver over the C ABI, used by tests/, bench.py and smoke().
+
+The reference (`tla`, header-only C++) has no Python surface; its C++ surface is mirrored by
+include/tla/ (see INTEGRATION.md). This module only does what a C++ caller would do before
+calling libtlb: spell a layout (the reference's own text syntax, text.hpp:130: `shape:stride`
+with `f9`-style Xor strides and `2*e1`-style Basis strides), flatten it to leaves (flat_modes,
+layout.hpp:111), lower it, and pass device pointers of torch tensors. No arithmetic on tensor
+contents happens here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import re
+from dataclasses import dataclass
+
+from . import abi
+
+_TOK = re.compile(r"\s*(\(|\)|,|:|\*|-?\d+|e\d+|f\d+)")
+
+
+def _tokens(text: str):
+    pos, out = 0, []
+    text = text.strip()
+    while pos < len(text):
+        m = _TOK.match(text, pos)
+        if not m:
+            raise ValueError(f"cannot parse layout text at {text[pos:]!r}")
+        out.append(m.group(1))
+        pos = m.end()
+    return out
+
+
+def _parse_tree(toks, i, leaf):
+    if toks[i] == "(":
+        kids = []
+        i += 1
+        while True:
+            node, i = _parse_tree(toks, i, leaf)
+            kids.append(node)
+            if toks[i] == ",":
+                i += 1
+                continue
+            if toks[i] == ")":
+                return tuple(kids), i + 1
+            raise ValueError("expected , or )")
+    return leaf(toks, i)
+
+
+def _shape_leaf(toks, i):
+    return int(toks[i]), i + 1
+
+
+def _stride_leaf(toks, i):
+    t = toks[i]
+    if t[0] == "f":
+        m = int(t[1:])
+        return ((abi.KIND_XOR, m, 0) if m else (abi.KIND_INT, 0, 0)), i + 1
+    if t[0] == "e":
+        return (abi.KIND_BASIS, 1, int(t[1:])), i + 1
+    v = int(t)
+    if i + 1 < len(toks) and toks[i + 1] == "*":
+        return ((abi.KIND_BASIS, v, int(toks[i + 2][1:])) if v else (abi.KIND_INT, 0, 0)), i + 3
+    if i + 1 < len(toks) and toks[i + 1][0] == "e":
+        return ((abi.KIND_BASIS, v, int(toks[i + 1][1:])) if v else (abi.KIND_INT, 0, 0)), i + 2
+    return (abi.KIND_INT, v, 0), i + 1
+
+
+def _flat_shape(tree):
+    if isinstance(tree, tuple):
+        out = []
+        for k in tree:
+            out.extend(_flat_shape(k))
+        return out
+    return [tree]
+
+
+def _flat_stride(tree):
+    # stride leaves are (kind, value, axis) triples; inner nodes are tuples of nodes
+    if isinstance(tree, tuple) and len(tree) == 3 and all(isinstance(x, int) for x in tree):
+        return [tree]
+    out = []
+    for k in tree:
+        out.extend(_flat_stride(k))
+    return out
+
+
+def _is_stride_leaf(t):
+    return isinstance(t, tuple) and len(t) == 3 and all(isinstance(x, int) for x in t)
+
+
+def _expand(shape, stride):
+    """Pairs shape leaves with stride leaves; a leaf stride under a tuple shape is not congruent."""
+    if isinstance(shape, tuple):
+        if _is_stride_leaf(stride) or len(stride) != len(shape):
+            raise ValueError("shape and stride are not congruent")
+        out = []
+        for s, d in zip(shape, stride):
+            out.extend(_expand(s, d))
+        return out
+    if not _is_stride_leaf(stride):
+        raise ValueError("shape and stride are not congruent")
+    return [(shape, stride)]
+
+
+@dataclass
+class Layout:
+    """A parsed layout: flat leaves in left-to-right order plus the top-level grouping."""
+    text: str
+    modes: list      # [(extent, kind, value, axis)]
+    top_leaves: list  # leaves per top-level mode
+
+    @staticmethod
+    def parse(text: str) -> "Layout":
+        toks = _tokens(text)
+        shape, i = _parse_tree(toks, 0, _shape_leaf)
+        if toks[i] != ":":
+            raise ValueError("expected ':' between shape and stride")
+        stride, i = _parse_tree(toks, i + 1, _stride_leaf)
+        if i != len(toks):
+            raise ValueError("trailing text after layout")
+        pairs = _expand(shape, stride)
+        modes = [(e, k, v, ax) for (e, (k, v, ax)) in pairs]
+        if isinstance(shape, tuple):
+            top = [len(_flat_shape(s)) for s in shape]
+        else:
+            top = [1]
+        return Layout(text, modes, top)
+
+    @property
+    def size(self) -> int:
+        n = 1
+        for e, *_ in self.modes:
+            n *= e
+        return n
+
+    def mode_array(self):
+        arr = (abi.tlb_mode * len(self.modes))()
+        for r, (e, k, v, ax) in enumerate(self.modes):
+            arr[r].extent, arr[r].kind, arr[r].stride, arr[r].axis = e, k, v, ax
+        return arr
+
+    def lower(self, ranked: bool = False) -> abi.tlb_layout_desc:
+        lib = abi.load()
+        d = abi.tlb_layout_desc()
+        arr = self.mode_array()
+        if ranked:
+            tl = (C.c_int32 * len(self.top_leaves))(*self.top_leaves)
+            abi.check(lib.tlb_layout_lower_ranked(arr, len(self.modes), tl, len(self.top_leaves), C.byref(d)))
+        else:
+            abi.check(lib.tlb_layout_lower(arr, len(self.modes), C.byref(d)))
+        return d
+
+
+def L(text: str) -> Layout:
+    return Layout.parse(text)
+
+
+def make_tensor(desc: abi.tlb_layout_desc, data_ptr: int | None, capacity: int, elem_bytes: int, origin: int = 0,
+                counting: bool = False) -> abi.tlb_tensor:
+    t = abi.tlb_tensor()
+    t.layout = C.pointer(desc)
+    t.data = C.c_void_p(data_ptr) if data_ptr else None
+    t.origin = origin
+    t.capacity = capacity
+    t.elem_bytes = elem_bytes
+    t.accessor = abi.ACC_COUNTING if counting else abi.ACC_BUFFER
+    return t
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def tensor_of(layout: Layout | str, buf, origin: int = 0, ranked: bool = False):
+    """(tlb_tensor, keepalive) over a torch tensor (device or host) viewed as a flat buffer of cells."""
+    lay = L(layout) if isinstance(layout, str) else layout
+    desc = lay.lower(ranked=ranked)
+    t = make_tensor(desc, buf.data_ptr(), buf.numel(), buf.element_size(), origin)
+    return t, (desc, buf)
+
+
+def counting_tensor(layout: Layout | str, base: int = 0):
+    lay = L(layout) if isinstance(layout, str) else layout
+    desc = lay.lower()
+    return make_tensor(desc, None, 0, 8, base, counting=True), (desc,)
+
+
+def copy(src, dst, i_begin: int = 0, i_end: int = 2**64 - 1, stream=None) -> str:
+    """tla::copy on device tensors built by tensor_of(); returns the plan the library chose."""
+    lib = abi.load()
+    abi.check(lib.tlb_copy(C.byref(src[0]), C.byref(dst[0]), i_begin, i_end, _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
+def copy_host(src, dst) -> None:
+    abi.check(abi.load().tlb_copy_host(C.byref(src[0]), C.byref(dst[0])))
+
+
+def gemm_bf16(a, b, c, tile_begin: int = 0, tile_end: int = 2**32 - 1, stream=None) -> str:
+    lib = abi.load()
+    abi.check(lib.tlb_gemm_bf16(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), tile_begin, tile_end, _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
+def gemm_bf16_batched(a, b, c, a_bs: int, b_bs: int, c_bs: int, batch_begin: int, batch_end: int, stream=None) -> str:
+    lib = abi.load()
+    abi.check(lib.tlb_gemm_bf16_batched(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), a_bs, b_bs, c_bs, batch_begin,
+                                        batch_end, _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
+def gemm_bf16_host(a, b, c) -> None:
+    abi.check(abi.load().tlb_gemm_bf16_host(C.byref(a[0]), C.byref(b[0]), C.byref(c[0])))
+
+
+def gemm_i64(a, b, c, status_buf=None, stream=None) -> str:
+    lib = abi.load()
+    sp = status_buf.data_ptr() if status_buf is not None else None
+    abi.check(lib.tlb_gemm_i64(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), sp, _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
+def eval_range(layout: Layout | str, i0: int, n: int, out, stream=None) -> None:
+    lay = L(layout) if isinstance(layout, str) else layout
+    d = lay.lower()
+    abi.check(abi.load().tlb_eval_range(C.byref(d), i0, n, out.data_ptr(), _stream_ptr(stream)))
+
+
+def idx2crd_range(layout: Layout | str, i0: int, n: int, out, stream=None) -> None:
+    lay = L(layout) if isinstance(layout, str) else layout
+    d = lay.lower()
+    abi.check(abi.load().tlb_idx2crd_range(C.byref(d), i0, n, out.data_ptr(), _stream_ptr(stream)))
+
+
+def crd2idx_range(layout: Layout | str, crd, n: int, out, stream=None) -> None:
+    lay = L(layout) if isinstance(layout, str) else layout
+    d = lay.lower()
+    abi.check(abi.load().tlb_crd2idx_range(C.byref(d), crd.data_ptr(), n, out.data_ptr(), _stream_ptr(stream)))
+
+
+def rinv_check_range(layout, rinv, k0: int, n: int, counter, stream=None) -> None:
+    dl = (L(layout) if isinstance(layout, str) else layout).lower()
+    dr = (L(rinv) if isinstance(rinv, str) else rinv).lower()
+    abi.check(abi.load().tlb_rinv_check_range(C.byref(dl), C.byref(dr), k0, n, counter.data_ptr(), _stream_ptr(stream)))
+
+
+def compose_check_range(a, b, r, i0: int, n: int, counter, stream=None) -> None:
+    da, db, dr = ((L(x) if isinstance(x, str) else x).lower() for x in (a, b, r))
+    abi.check(abi.load().tlb_compose_check_range(C.byref(da), C.byref(db), C.byref(dr), i0, n, counter.data_ptr(),
+                                                 _stream_ptr(stream)))
+
+
+def eval_axes_range(layout: Layout | str, n_axes: int, i0: int, n: int, out, stream=None) -> None:
+    lay = L(layout) if isinstance(layout, str) else layout
+    arr = lay.mode_array()
+    abi.check(abi.load().tlb_eval_axes_range(arr, len(lay.modes), n_axes, i0, n, out.data_ptr(), _stream_ptr(stream)))

@@ -1,0 +1,41 @@
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built():
+    """The oracle (test infrastructure) and the product library must exist before any test."""
+    if not (ROOT / "oracle" / "_build" / "liboracle.so").exists():
+        subprocess.check_call(["make", "-C", str(ROOT / "oracle"), "oracle"])
+    if not (ROOT / "paper_2603_02298_b200" / "libtlb.so").exists():
+        subprocess.check_call([sys.executable, "-m", "paper_2603_02298_b200.build"], cwd=str(ROOT))
+    yield
+
+
+def has_cuda() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def pytest_collection_modifyitems(config, items):
+    if has_cuda():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device in this container")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
