@@ -1,0 +1,236 @@
+"""GPU parity: tla::copy through the C ABI vs the oracle — bit-exact on every cell, including the
+cells the copy must NOT touch (destinations are pre-filled with -1, test_tensor.cpp:104)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_util as ou
+from gpu_util import cells, dev, run_copy_case
+from paper_2603_02298_b200 import L, TlbError, abi, host
+
+pytestmark = pytest.mark.gpu
+
+
+def test_copy_reference_fixtures():
+    """Every row of tests/golden/copy.json (Table 1 + extras), int64 cells exactly as the reference ran them."""
+    for row in ou.golden("copy.json"):
+        if "error" in row:
+            continue
+        nd = row["dst_len"]
+        tdst = dev(np.full(nd, -1, dtype=np.int64))
+        dd = L(row["dst"]).lower()
+        dst = host.make_tensor(dd, tdst.data_ptr(), nd, 8)
+        ds = L(row["src"]).lower()
+        if "counting_base" in row:
+            src = host.make_tensor(ds, None, 0, 8, row["counting_base"], counting=True)
+            keep = None
+        else:
+            keep = dev(np.arange(row["src_len"], dtype=np.int64) * 3 + 1)
+            src = host.make_tensor(ds, keep.data_ptr(), row["src_len"], 8)
+        host.copy((src, None), (dst, None))
+        torch.cuda.synchronize()
+        assert tdst.cpu().numpy().tolist() == row["dst_cells"], (row["src"], row["dst"])
+
+
+TABLE1 = [("8:1", "8:1"), ("(8,2,3):(1,16,32)", "(8,2,3):(1,16,32)"), ("(2,3,2):(42,1,128)", "12:1"),
+          ("12:1", "(2,3,2):(42,1,128)"), ("7:0", "7:1"), ("7:0", "7:0"), ("(8,3):(1,8)", "(8,3):(3,1)"),
+          ("(8,(3,5)):(1,(57,8))", "(8,15):(1,8)")]
+
+
+@pytest.mark.parametrize("eb", [1, 2, 4, 8, 16])
+def test_copy_table1_all_element_sizes(eb):
+    for s, d in TABLE1:
+        run_copy_case(s, d, eb)
+
+
+@pytest.mark.parametrize("eb", [2, 4, 8])
+@pytest.mark.parametrize("s,d", [
+    ("(256,128):(128,1)", "(256,128):(1,256)"),                           # C1 shape in small
+    ("(128,256):(1,128)", "(128,256):(256,1)"),
+    ("(96,160):(160,1)", "(96,160):(1,96)"),                              # Lb = 32 tiles
+    ("((8,128),(4,64),4):((1,2048),(8,32),262144)", "((8,128),(4,64),4):((128,1),(65536,1024),262144)"),  # C3, 4 tiles
+    ("(64,64,8):(512,1,64)", "(64,64,8):(1,512,64)"),                     # batched transpose, padded rows
+    ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))"),
+])
+def test_copy_tiled_plan(s, d, eb):
+    plan = run_copy_case(s, d, eb)
+    assert plan == "tiled", plan
+
+
+@pytest.mark.parametrize("s,d,plan", [
+    ("4096:1", "4096:1", "vec"),
+    ("(64,32):(1,64)", "(64,32):(1,128)", "vec"),                         # row gather with padding
+    ("(64,8,4):(1,256,64)", "(64,8,4):(1,64,512)", "vec"),                # mode permutation, contiguous rows
+    ("(63,5):(1,63)", "(63,5):(1,64)", "gather"),                         # nothing to vectorise along 63 with 8-byte... still ok
+])
+def test_copy_vec_plan(s, d, plan):
+    for eb in (2, 4, 8, 16):
+        got = run_copy_case(s, d, eb)
+        if plan == "vec":
+            assert got == "vec", (got, eb)
+
+
+def test_copy_forced_gather_equals_tiled():
+    s, d = "(256,128):(128,1)", "(256,128):(1,256)"
+    assert run_copy_case(s, d, 4, path=1) == "gather"
+    assert run_copy_case(s, d, 4, path=2) == "tiled"
+
+
+def test_copy_misaligned_origins_fall_back_and_stay_exact():
+    assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 4, src_origin=1, dst_origin=3) == "gather"
+    assert run_copy_case("4096:1", "4096:1", 2, src_origin=1, dst_origin=1) in ("vec", "gather")
+
+
+def test_copy_random_layout_pairs_vs_oracle():
+    rng = np.random.default_rng(3)
+    from test_oracle_pinned import _random_layout
+    done = 0
+    while done < 120:
+        s, d = _random_layout(rng), _random_layout(rng)
+        if L(s).size != L(d).size:
+            d = "%d:%d" % (L(s).size, int(rng.integers(0, 3)))
+        run_copy_case(s, d, int(rng.choice([1, 2, 4, 8, 16])), seed=done)
+        done += 1
+
+
+def test_copy_xor_layouts():
+    run_copy_case("(8,8):(f1,f9)", "64:1", 8)
+    run_copy_case("64:1", "(8,8):(f1,f9)", 4)
+    # staging layout of config C3: Swizzle<3,4,3> per 1 KiB == (128,8):(f1,f144)
+    run_copy_case("(128,8):(f1,f144)", "(128,8):(8,1)", 1)
+    # Xor offsets act on the absolute position, origin included (tensor.hpp:57)
+    ns = 64 + 64
+    src, want = cells(ns, 8, 1), cells(ns, 8, fill=-1)
+    assert ou.orc_copy("(8,8):(f1,f9)", src, "64:1", want, src_origin=64, dst_origin=5) == 0
+    tsrc, tdst = dev(src), dev(cells(ns, 8, fill=-1))
+    a = host.make_tensor(L("(8,8):(f1,f9)").lower(), tsrc.data_ptr(), ns, 8, 64)
+    b = host.make_tensor(L("64:1").lower(), tdst.data_ptr(), ns, 8, 5)
+    host.copy((a, None), (b, None))
+    torch.cuda.synchronize()
+    assert (tdst.cpu().numpy() == want).all()
+
+
+def test_copy_non_injective_destination_last_writer_wins():
+    """7:0 -> 7:0 makes dst[0] = src(6) (test_tensor.cpp:98); larger aliasing cases vs the oracle."""
+    assert run_copy_case("7:1", "7:0", 8) == "ordered"
+    assert run_copy_case("(64,64):(1,64)", "(64,64):(1,0)", 4) == "ordered"
+    assert run_copy_case("(64,64):(64,1)", "(64,64):(0,1)", 4) == "ordered"
+    assert run_copy_case("(32,32,4):(1,32,1024)", "(32,32,4):(1,31,3)", 8) == "ordered"
+
+
+def test_copy_subranges_tile_aligned_and_ragged():
+    s, d = "(256,128):(128,1)", "(256,128):(1,256)"
+    n = 256 * 128
+    src = cells(n, 4, 2)
+    for (b, e) in [(0, n // 2), (n // 2, n), (256 * 32, 256 * 96), (5, 777), (0, 0), (n, n + 5)]:
+        want = cells(n, 4, fill=-1)
+        assert ou.orc_copy(s, src, d, want, i_begin=b, i_end=min(e, n)) == 0
+        tsrc, tdst = dev(src), dev(cells(n, 4, fill=-1))
+        a = host.make_tensor(L(s).lower(), tsrc.data_ptr(), n, 4)
+        bb = host.make_tensor(L(d).lower(), tdst.data_ptr(), n, 4)
+        host.copy((a, None), (bb, None), b, e)
+        torch.cuda.synchronize()
+        assert (tdst.cpu().numpy() == want).all(), (b, e)
+
+
+def test_copy_error_contracts_write_nothing():
+    buf = dev(np.arange(8, dtype=np.int64))
+    out = dev(np.full(8, -1, dtype=np.int64))
+    src = host.make_tensor(L("4:3").lower(), buf.data_ptr(), 8, 8)
+    dst = host.make_tensor(L("4:1").lower(), out.data_ptr(), 8, 8)
+    with pytest.raises(TlbError) as e:            # 4:3 reads cell 9 of 8 -> bounds_error (test_tensor.cpp:34-40)
+        host.copy((src, None), (dst, None))
+    assert e.value.status == abi.TLB_ERR_BOUNDS
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == -1).all()         # pre-flight: nothing was written (documented difference)
+    neg = host.make_tensor(L("1:0").lower(), buf.data_ptr(), 8, 8, -1)
+    with pytest.raises(TlbError) as e:            # origin -1 (test_tensor.cpp:39)
+        host.copy((neg, None), (host.make_tensor(L("1:0").lower(), out.data_ptr(), 8, 8), None))
+    assert e.value.status == abi.TLB_ERR_BOUNDS
+    with pytest.raises(TlbError) as e:
+        host.copy((host.make_tensor(L("8:1").lower(), buf.data_ptr(), 8, 8), None), (dst, None))
+    assert e.value.status == abi.TLB_ERR_CONTRACT
+    with pytest.raises(TlbError) as e:
+        host.copy((host.make_tensor(L("(2,2):(e0,e1)").lower(), buf.data_ptr(), 8, 8), None), (dst, None))
+    assert e.value.status == abi.TLB_ERR_SEMIMODULE
+    # Xor layout whose OR-bound exceeds the buffer but whose exact image fits: (3):(f4) touches {0,4,8}
+    small = dev(np.arange(9, dtype=np.int64))
+    o3 = dev(np.full(3, -1, dtype=np.int64))
+    host.copy((host.make_tensor(L("3:f4").lower(), small.data_ptr(), 9, 8), None),
+              (host.make_tensor(L("3:1").lower(), o3.data_ptr(), 3, 8), None))
+    torch.cuda.synchronize()
+    assert o3.cpu().numpy().tolist() == [0, 4, 8]
+
+
+def test_copy_host_entry_point():
+    s, d = "(256,128):(128,1)", "(256,128):(1,256)"
+    n = 256 * 128
+    src = torch.from_numpy(cells(n, 4, 9)).pin_memory()
+    dst = torch.full((n,), -1, dtype=torch.int32).pin_memory()
+    want = np.full(n, -1, dtype=np.int32)
+    assert ou.orc_copy(s, src.numpy(), d, want) == 0
+    a = host.make_tensor(L(s).lower(), src.data_ptr(), n, 4)
+    b = host.make_tensor(L(d).lower(), dst.data_ptr(), n, 4)
+    host.copy_host((a, None), (b, None))
+    assert (dst.numpy() == want).all()
+    # a destination the copy only partly covers keeps its other cells
+    dst2 = torch.full((2 * n,), -7, dtype=torch.int32)
+    want2 = np.full(2 * n, -7, dtype=np.int32)
+    d2 = "(256,128):(2,512)"
+    assert ou.orc_copy(s, src.numpy(), d2, want2) == 0
+    host.copy_host((a, None), (host.make_tensor(L(d2).lower(), dst2.data_ptr(), 2 * n, 4), None))
+    assert (dst2.numpy() == want2).all()
+
+
+def test_c1_transpose_full_size_properties():
+    """Config C1 at BASELINE size (8192^2 fp32): involution + spot rows vs the oracle on a sub-block."""
+    n = 8192
+    src = torch.arange(n * n, dtype=torch.int32, device="cuda")          # element-index bit patterns
+    dst = torch.full((n * n,), -1, dtype=torch.int32, device="cuda")
+    s, d = f"({n},{n}):({n},1)", f"({n},{n}):(1,{n})"
+    a, ka = host.tensor_of(s, src)
+    b, kb = host.tensor_of(d, dst)
+    assert host.copy((a, ka), (b, kb)) == "tiled"
+    torch.cuda.synchronize()
+    # dst viewed as (n,n) row-major must equal src viewed row-major, transposed
+    assert torch.equal(dst.view(n, n), src.view(n, n).t())
+    # involution: transposing back restores the source bit for bit
+    back = torch.full((n * n,), -1, dtype=torch.int32, device="cuda")
+    a2, k2 = host.tensor_of(s, dst)
+    b2, k3 = host.tensor_of(d, back)
+    host.copy((a2, k2), (b2, k3))
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)
+
+
+def test_c3_permute_full_size_properties():
+    """Config C3 at BASELINE size (2^30 fp32 = 4 GiB each way): the destination is a permutation of the
+    source (checksum of checksums), sampled tiles equal the oracle, and the inverse permutation restores it."""
+    T = 4096
+    s = f"((8,128),(4,64),{T}):((1,2048),(8,32),262144)"
+    d = f"((8,128),(4,64),{T}):((128,1),(65536,1024),262144)"
+    n = 262144 * T
+    src = torch.arange(n, dtype=torch.int32, device="cuda")
+    dst = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    a, ka = host.tensor_of(s, src)
+    b, kb = host.tensor_of(d, dst)
+    assert host.copy((a, ka), (b, kb)) == "tiled"
+    torch.cuda.synchronize()
+    # per-tile checksums: every tile permutes its own 262144 cells
+    assert torch.equal(dst.view(T, -1).sum(dim=1, dtype=torch.int64), src.view(T, -1).sum(dim=1, dtype=torch.int64))
+    # tiles 0, 1234 and T-1 against the oracle
+    tile_s = "((8,128),(4,64)):((1,2048),(8,32))"
+    tile_d = "((8,128),(4,64)):((128,1),(65536,1024))"
+    for t in (0, 1234, T - 1):
+        want = np.full(262144, -1, dtype=np.int32)
+        assert ou.orc_copy(tile_s, src[t * 262144:(t + 1) * 262144].cpu().numpy(), tile_d, want) == 0
+        assert (dst[t * 262144:(t + 1) * 262144].cpu().numpy() == want).all()
+    # inverse: copy with the roles of the layouts swapped restores the source
+    back = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    a2, k2 = host.tensor_of(d, dst)
+    b2, k3 = host.tensor_of(s, back)
+    host.copy((a2, k2), (b2, k3))
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)
