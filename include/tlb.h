@@ -147,6 +147,10 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
  * order is preserved for non-injective destinations. Sizes must agree (contract_error).
  * The planner picks contiguous / tiled (swizzled smem staging, optionally TMA-fed) / gather kernels. */
 int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, void* stream);
+/* Runs the contract checks and the planner of tlb_copy without a device and without launching anything;
+ * the plan it would pick is then available from tlb_last_plan(). Pointers are only inspected for
+ * alignment. (Xor-kind bounds that need the exact device scan are assumed to pass.) */
+int tlb_copy_plan(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end);
 /* Planner knobs for tlb_copy on the calling thread: force one path (testing / profiling).
  * 0 = auto, 1 = gather only, 2 = tiled (LDG-fed), 3 = tiled TMA-fed. Returns the previous value. */
 int tlb_copy_set_path(int path);
@@ -162,14 +166,19 @@ int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const tlb_layout_d
 
 /* ---- (5) tiled GEMM (configs C2, C4) ----------------------------------- */
 /* tla::gemm(A, B, C) (tensor.hpp:214-233): C(m,n) += sum_k A(m,k) * B(n,k), all rank 2.
- * bf16 x bf16 -> fp32, accumulator starts from C. tile_begin/tile_end select a range of
- * output tiles (row-major over (m_tile, n_tile) of the 256x256 / 128x256 tiling; pass 0 and
- * UINT32_MAX for all) so 1/2/4/8 GPUs can shard one problem by tile-coordinate ranges.
+ * bf16 x bf16 -> fp32, accumulator starts from C. tile_begin/tile_end select a range of the
+ * 128 x 256 output tiles (ids from tlb_gemm_tile_count; pairs (2g, 2g+1) form 256 x 256 blocks walked in
+ * an L2-friendly order; pass 0 and UINT32_MAX for all) so 1/2/4/8 GPUs can shard one problem by
+ * tile-coordinate ranges. The ids refer to the tiling of the plan the library selects, which runs the
+ * problem transposed when C is m-contiguous; every range partition of [0, count) covers C exactly once.
  * K-major A and B with M-contiguous or N-contiguous C run on tcgen05 (TMA -> swizzled smem ->
  * UMMA -> TMEM); every other layout family (NT, BLIS strides, GETT folded modes, Xor) runs on the
  * layout-evaluating SIMT kernel. A.elem_bytes = B.elem_bytes = 2, C.elem_bytes = 4. */
 int tlb_gemm_bf16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin,
                   uint32_t tile_end, void* stream);
+/* Number of output tiles of one problem under the plan tlb_gemm_bf16 would choose (host-only, no device
+ * needed): shard [0, *tiles) across GPUs and pass each range as tile_begin / tile_end. */
+int tlb_gemm_tile_count(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t* tiles);
 /* Batched: `batch` problems, operand b at data + b * batch_stride (elements); batches
  * [batch_begin, batch_end) are executed (tile-range sharding at batch granularity, config C4). */
 int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_batch_stride,

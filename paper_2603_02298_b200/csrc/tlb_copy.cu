@@ -30,6 +30,7 @@ namespace tlb {
 namespace {
 
 thread_local int g_copy_path = 0; // 0 auto, 1 gather, 2 tiled (LDG), 3 tiled TMA
+thread_local bool g_dry_run = false; // tlb_copy_plan: run the planner, launch nothing
 
 constexpr int kThreads = 256;
 
@@ -383,6 +384,10 @@ int launch_gather(const CopyCall& c) {
     const tlb_layout_desc& S = *c.src->layout;
     const tlb_layout_desc& D = *c.dst->layout;
     const int counting = c.src->accessor == TLB_ACC_COUNTING;
+    if (g_dry_run) {
+        set_plan("gather");
+        return TLB_OK;
+    }
     const int grid = launch_grid(c.n, kThreads, 8);
 #define TLB_GATHER(EB)                                                                                        \
     gather_kernel<EB><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
@@ -406,6 +411,10 @@ int launch_ordered(const CopyCall& c, Span dspan) {
     const tlb_layout_desc& D = *c.dst->layout;
     const int counting = c.src->accessor == TLB_ACC_COUNTING;
     const uint64_t cells = static_cast<uint64_t>(dspan.hi - dspan.lo) + 1;
+    if (g_dry_run) {
+        set_plan("ordered");
+        return TLB_OK;
+    }
     unsigned long long* winner = nullptr;
     TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&winner), cells * sizeof(unsigned long long), c.stream));
     TLB_CUDA(cudaMemsetAsync(winner, 0, cells * sizeof(unsigned long long), c.stream));
@@ -496,6 +505,11 @@ int try_planned(const CopyCall& c, bool* done) {
         JointDesc J;
         TLB_TRY(fill_joint(order, &J));
         const uint64_t n_vec = c.n / static_cast<uint64_t>(v);
+        if (g_dry_run) {
+            set_plan("vec");
+            *done = true;
+            return TLB_OK;
+        }
         const int grid = launch_grid(n_vec, kThreads, 8);
         const char* sb = sp + base_s * eb;
         char* db = dp + base_d * eb;
@@ -553,6 +567,11 @@ int try_planned(const CopyCall& c, bool* done) {
         for (const JM& m : rest) tiles *= static_cast<uint64_t>(m.e);
         P.n_tiles = tiles;
         if (tiles > 0x7fffffffull) return TLB_OK;
+        if (g_dry_run) {
+            set_plan("tiled");
+            *done = true;
+            return TLB_OK;
+        }
         const char* sb = sp + base_s * eb;
         char* db = dp + base_d * eb;
         const unsigned grid = static_cast<unsigned>(tiles);
@@ -600,7 +619,8 @@ int bounds_preflight(const tlb_tensor& t, uint64_t i0, uint64_t n, const char* w
         sp.lo = static_cast<int64_t>(lo);
         sp.hi = static_cast<int64_t>(hi);
         // a sub-range narrower than the outermost mode's stride may be over-approximated; verify exactly
-        if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && n != static_cast<uint64_t>(L.size)) {
+        if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && n != static_cast<uint64_t>(L.size) &&
+            !g_dry_run) {
             long long h[2] = {INT64_MAX, INT64_MIN};
             long long* d = nullptr;
             TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), stream));
@@ -615,7 +635,7 @@ int bounds_preflight(const tlb_tensor& t, uint64_t i0, uint64_t n, const char* w
         }
     } else {
         TLB_TRY(position_span(L, t.origin, &sp));
-        if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && t.origin >= 0) {
+        if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && t.origin >= 0 && !g_dry_run) {
             long long h[2] = {INT64_MAX, INT64_MIN};
             long long* d = nullptr;
             TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), stream));
@@ -663,8 +683,11 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
         return fail(TLB_ERR_CONTRACT, "tlb_copy: a counting source produces 8-byte cells");
     const uint64_t size = static_cast<uint64_t>(S.size);
     if (i_end > size) i_end = size;
-    if (i_begin >= i_end) return TLB_OK;
-    TLB_TRY(require_device());
+    if (i_begin >= i_end) {
+        set_plan("empty");
+        return TLB_OK;
+    }
+    if (!g_dry_run) TLB_TRY(require_device());
     CopyCall c{src, dst, i_begin, i_end - i_begin, stream};
     TLB_TRY(overflow_preflight(S, src->origin, i_end - 1));
     TLB_TRY(overflow_preflight(D, dst->origin, i_end - 1));
@@ -688,6 +711,13 @@ extern "C" {
 
 int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, void* stream) {
     return tlb::copy_impl(src, dst, i_begin, i_end, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_copy_plan(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end) {
+    tlb::g_dry_run = true;
+    const int st = tlb::copy_impl(src, dst, i_begin, i_end, nullptr);
+    tlb::g_dry_run = false;
+    return st;
 }
 
 int tlb_copy_set_path(int path) {

@@ -35,6 +35,34 @@ __global__ void __launch_bounds__(kThreads) eval_range_kernel(const __grid_const
     }
 }
 
+// Grouped evaluation: G consecutive indices that share every coordinate except the low bits of the
+// first leaf (extent[0] % G == 0, i0 % G == 0) cost ONE peel: L(i + j) = L(i) + j*d0 for Int strides,
+// L(i) ^ clmul(j, mask0) for Xor strides (the leaf coordinate c0 + j equals c0 ^ j when c0 % G == 0
+// and clmul is linear over GF(2)). Each thread stores G*8 contiguous bytes with 16-byte stores.
+template <int G>
+__global__ void __launch_bounds__(kThreads) eval_group_kernel(const __grid_constant__ tlb_layout_desc L, uint64_t i0,
+                                                              uint64_t n_groups, int64_t* __restrict__ out) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const bool is_xor = L.kind == TLB_KIND_XOR;
+    const int64_t d0 = L.stride[0];
+    for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n_groups; g += stride) {
+        const int64_t base = dev_eval(L, i0 + g * G);
+        int64_t* o = out + g * G;
+#pragma unroll
+        for (int j = 0; j < G; j += 2) {
+            int64_t v0, v1;
+            if (is_xor) {
+                v0 = base ^ dev_clmul(static_cast<uint64_t>(j), static_cast<uint64_t>(d0));
+                v1 = base ^ dev_clmul(static_cast<uint64_t>(j + 1), static_cast<uint64_t>(d0));
+            } else {
+                v0 = base + j * d0;
+                v1 = base + (j + 1) * d0;
+            }
+            st_cs_v2(o + j, v0, v1);
+        }
+    }
+}
+
 // out[k*nm + r] = natural coordinate leaf r of i0+k (idx2crd, int_tuple.hpp:129).
 __global__ void __launch_bounds__(kThreads) idx2crd_kernel(const __grid_constant__ tlb_layout_desc S, uint64_t i0,
                                                            uint64_t n, int64_t* __restrict__ out) {
@@ -175,7 +203,32 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
     TLB_TRY(require_device());
     TLB_TRY(overflow_preflight(*layout, 0, i0 + n - 1));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const bool pairs = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && n >= 2;
+    const bool aligned = (reinterpret_cast<uintptr_t>(d_out) & 15) == 0;
+    // grouped fast path: the first leaf must absorb a whole group
+    int G = 1;
+    if (aligned) {
+        for (int g = 8; g >= 2; g >>= 1)
+            if (i0 % g == 0 && (layout->n_modes == 1 || layout->extent[0] % g == 0) && n >= static_cast<uint64_t>(g)) {
+                G = g;
+                break;
+            }
+    }
+    if (G > 1) {
+        const uint64_t groups = n / G;
+        if (G == 8) eval_group_kernel<8><<<grid_for(groups), kThreads, 0, s>>>(*layout, i0, groups, d_out);
+        else if (G == 4) eval_group_kernel<4><<<grid_for(groups), kThreads, 0, s>>>(*layout, i0, groups, d_out);
+        else eval_group_kernel<2><<<grid_for(groups), kThreads, 0, s>>>(*layout, i0, groups, d_out);
+        count_launch();
+        TLB_CUDA(cudaGetLastError());
+        const uint64_t done = groups * G;
+        if (done < n) {
+            eval_range_kernel<false><<<grid_for(n - done), kThreads, 0, s>>>(*layout, i0 + done, n - done, d_out + done);
+            count_launch();
+            TLB_CUDA(cudaGetLastError());
+        }
+        return TLB_OK;
+    }
+    const bool pairs = aligned && n >= 2;
     if (pairs) eval_range_kernel<true><<<grid_for(n >> 1), kThreads, 0, s>>>(*layout, i0, n, d_out);
     else eval_range_kernel<false><<<grid_for(n), kThreads, 0, s>>>(*layout, i0, n, d_out);
     count_launch();

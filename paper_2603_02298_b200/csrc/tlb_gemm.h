@@ -37,6 +37,7 @@ struct UmmaProblem {
     int64_t a_bs, b_bs, c_bs;      // batch strides (elements)
     uint32_t tile_begin, tile_end; // global tile ids (batch-major), [begin, end)
     int32_t cta_group;             // 1 or 2
+    int32_t split_tail;            // 1: split the units of the last partial wave along K (red.add epilogue)
 };
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
 

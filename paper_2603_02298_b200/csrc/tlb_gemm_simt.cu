@@ -9,6 +9,7 @@
 // from C), so for bf16 they are bit-exact against the sequential fp32 restatement
 // (bf16 x bf16 is exact in fp32, hence fma(a, b, acc) == acc + a*b).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -23,6 +24,15 @@ namespace {
 thread_local int g_gemm_path = 0; // 0 auto, 1 SIMT, 2 tcgen05 cta_group::1, 3 tcgen05 cta_group::2
 
 constexpr int kThreads = 256;
+
+// TLB_GEMM_SPLIT_TAIL=0 keeps every C cell owned by one CTA (bitwise run-to-run reproducible sums).
+bool split_tail_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TLB_GEMM_SPLIT_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 struct SimtArgs {
     int64_t a_origin, b_origin, c_origin;
@@ -153,22 +163,80 @@ int gemm_bounds(const tlb_tensor& t, int64_t bs, int b0, int b1, const char* who
     return TLB_OK;
 }
 
+// The tcgen05 plan applies to K-major A and B with single-stride C modes and TMA-legal strides. When C is
+// m-contiguous (the paper's TN row, (M,N):(1,ldc)) the problem is run transposed, C^T += B * A^T: the roles of
+// A and B swap, so the accumulator's TMEM lanes run along n and every epilogue thread holds 32 consecutive m
+// -- contiguous in memory -- which the swizzled 128-bit staging stores and the TMA reduction need.
+struct UmmaFit {
+    bool ok = false;
+    bool swapped = false;
+    UmmaProblem p;
+};
+
+UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, const GemmDims& d, int64_t a_bs,
+                 int64_t b_bs, int64_t c_bs, int batch_begin, int batch_end) {
+    UmmaFit f;
+    int64_t eM, lda, eK, ska, eN, ldb, eKb, skb, eCm, csm, eCn, csn;
+    const bool flat = A->layout->kind == TLB_KIND_INT && B->layout->kind == TLB_KIND_INT &&
+                      C->layout->kind == TLB_KIND_INT && single_stride(*A->layout, 0, &eM, &lda) &&
+                      single_stride(*A->layout, 1, &eK, &ska) && single_stride(*B->layout, 0, &eN, &ldb) &&
+                      single_stride(*B->layout, 1, &eKb, &skb) && single_stride(*C->layout, 0, &eCm, &csm) &&
+                      single_stride(*C->layout, 1, &eCn, &csn);
+    if (!flat) return f;
+    const bool batched = batch_end - batch_begin > 1 || batch_begin > 0;
+    bool ok = (ska == 1 || d.K == 1) && (skb == 1 || d.K == 1) && lda > 0 && ldb > 0 && lda % 8 == 0 && ldb % 8 == 0 &&
+              csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) &&
+              (C->layout->flags & TLB_LF_INJECTIVE) && (!batched || (a_bs % 8 == 0 && b_bs % 8 == 0 && a_bs > 0 && b_bs > 0));
+    const char* a_ptr = static_cast<const char*>(A->data) + A->origin * 2;
+    const char* b_ptr = static_cast<const char*>(B->data) + B->origin * 2;
+    ok = ok && (reinterpret_cast<uintptr_t>(a_ptr) % 16 == 0) && (reinterpret_cast<uintptr_t>(b_ptr) % 16 == 0);
+    if (!ok) return f;
+    UmmaProblem& p = f.p;
+    std::memset(&p, 0, sizeof(p));
+    f.swapped = csm == 1 && csn != 1;
+    p.A = f.swapped ? b_ptr : a_ptr;
+    p.B = f.swapped ? a_ptr : b_ptr;
+    p.C = static_cast<float*>(C->data) + C->origin;
+    p.lda = f.swapped ? ldb : lda;
+    p.ldb = f.swapped ? lda : ldb;
+    p.cs_m = f.swapped ? csn : csm;
+    p.cs_n = f.swapped ? csm : csn;
+    p.M = static_cast<int32_t>(f.swapped ? d.N : d.M);
+    p.N = static_cast<int32_t>(f.swapped ? d.M : d.N);
+    p.K = static_cast<int32_t>(d.K);
+    p.batch = batch_end;
+    p.a_bs = f.swapped ? b_bs : a_bs;
+    p.b_bs = f.swapped ? a_bs : b_bs;
+    p.c_bs = c_bs;
+    f.ok = true;
+    return f;
+}
+
 int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool i64, int64_t a_bs, int64_t b_bs,
              int64_t c_bs, int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, int* d_status,
-             cudaStream_t stream) {
+             cudaStream_t stream, uint32_t* count_only = nullptr) {
     GemmDims d;
     TLB_TRY(check_gemm(A, B, C, i64 ? 8 : 2, i64 ? 8 : 4, &d));
     if (batch_begin < 0 || batch_end < batch_begin) return fail(TLB_ERR_CONTRACT, "tlb_gemm: bad batch range");
-    if (batch_end == batch_begin) return TLB_OK;
+    if (batch_end == batch_begin && !count_only) return TLB_OK;
     if (d.M >= (1ll << 31) || d.N >= (1ll << 31) || d.K >= (1ll << 31))
         return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: extents must be below 2^31");
+    UmmaFit fit;
+    if (!i64 && g_gemm_path != 1) fit = fit_umma(A, B, C, d, a_bs, b_bs, c_bs, batch_begin, batch_end);
+    // Tiles are 128 x 256 over (rows, columns) of the problem AS THE PLAN RUNS IT (transposed for m-contiguous C).
+    const int64_t rows = fit.ok ? fit.p.M : d.M, cols = fit.ok ? fit.p.N : d.N;
+    TileGrid grid{static_cast<uint32_t>((rows + 255) / 256), static_cast<uint32_t>((cols + 255) / 256)};
+    const uint64_t tpb = tiles_per_batch(grid);
+    if (tpb * static_cast<uint64_t>(std::max(batch_end, 1)) > 0xffffffffull)
+        return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: too many tiles");
+    if (count_only) {
+        *count_only = static_cast<uint32_t>(tpb);
+        return TLB_OK;
+    }
     TLB_TRY(require_device());
     TLB_TRY(gemm_bounds(*A, a_bs, batch_begin, batch_end, "A", stream));
     TLB_TRY(gemm_bounds(*B, b_bs, batch_begin, batch_end, "B", stream));
     TLB_TRY(gemm_bounds(*C, c_bs, batch_begin, batch_end, "C", stream));
-    TileGrid grid{static_cast<uint32_t>((d.M + 255) / 256), static_cast<uint32_t>((d.N + 255) / 256)};
-    const uint64_t tpb = tiles_per_batch(grid);
-    if (tpb * static_cast<uint64_t>(batch_end) > 0xffffffffull) return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: too many tiles");
     // Global tile range: the caller's range applies inside [batch_begin, batch_end).
     uint64_t t0 = static_cast<uint64_t>(batch_begin) * tpb, t1 = static_cast<uint64_t>(batch_end) * tpb;
     if (tile_begin != 0 || tile_end != UINT32_MAX) {
@@ -177,43 +245,14 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
         if (t0 >= t1) return TLB_OK;
     }
 
-    // ---- tcgen05 plan: K-major A and B, single-stride C modes, TMA-legal strides
     if (!i64 && g_gemm_path != 1) {
-        int64_t eM, lda, eK, ska, eN, ldb, eKb, skb, eCm, csm, eCn, csn;
-        const bool flat = A->layout->kind == TLB_KIND_INT && B->layout->kind == TLB_KIND_INT &&
-                          C->layout->kind == TLB_KIND_INT && single_stride(*A->layout, 0, &eM, &lda) &&
-                          single_stride(*A->layout, 1, &eK, &ska) && single_stride(*B->layout, 0, &eN, &ldb) &&
-                          single_stride(*B->layout, 1, &eKb, &skb) && single_stride(*C->layout, 0, &eCm, &csm) &&
-                          single_stride(*C->layout, 1, &eCn, &csn);
-        const bool batched = batch_end - batch_begin > 1 || batch_begin > 0;
-        bool ok = flat && (ska == 1 || d.K == 1) && (skb == 1 || d.K == 1) && lda > 0 && ldb > 0 && lda % 8 == 0 &&
-                  ldb % 8 == 0 && csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) &&
-                  (C->layout->flags & TLB_LF_INJECTIVE) && (!batched || (a_bs % 8 == 0 && b_bs % 8 == 0 && a_bs > 0 && b_bs > 0));
-        const char* a_ptr = static_cast<const char*>(A->data) + A->origin * 2;
-        const char* b_ptr = static_cast<const char*>(B->data) + B->origin * 2;
-        ok = ok && (reinterpret_cast<uintptr_t>(a_ptr) % 16 == 0) && (reinterpret_cast<uintptr_t>(b_ptr) % 16 == 0) &&
-             (!batched || ((a_bs * 2) % 16 == 0 && (b_bs * 2) % 16 == 0));
-        if (ok) {
-            UmmaProblem p;
-            std::memset(&p, 0, sizeof(p));
-            p.A = a_ptr;
-            p.B = b_ptr;
-            p.C = static_cast<float*>(C->data) + C->origin;
-            p.lda = lda;
-            p.ldb = ldb;
-            p.cs_m = csm;
-            p.cs_n = csn;
-            p.M = static_cast<int32_t>(d.M);
-            p.N = static_cast<int32_t>(d.N);
-            p.K = static_cast<int32_t>(d.K);
-            p.batch = batch_end;
-            p.a_bs = a_bs;
-            p.b_bs = b_bs;
-            p.c_bs = c_bs;
+        if (fit.ok) {
+            UmmaProblem& p = fit.p;
             p.tile_begin = static_cast<uint32_t>(t0);
             p.tile_end = static_cast<uint32_t>(t1);
             const bool even = (t0 % 2 == 0) && (t1 % 2 == 0);
-            p.cta_group = g_gemm_path == 2 ? 1 : g_gemm_path == 3 ? 2 : 1 /* cta_group::2 is opt-in until profiled faster */;
+            p.split_tail = split_tail_enabled() ? 1 : 0;
+            p.cta_group = g_gemm_path == 2 ? 1 : g_gemm_path == 3 ? 2 : (even ? 2 : 1);
             if (p.cta_group == 2 && !even)
                 return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
             return umma_gemm_launch(p, stream);
@@ -279,6 +318,11 @@ int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_te
 
 int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream) {
     return tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, d_status, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_gemm_tile_count(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t* tiles) {
+    if (!tiles) return tlb::fail(TLB_ERR_CONTRACT, "tlb_gemm_tile_count: null output");
+    return tlb::run_gemm(A, B, C, false, 0, 0, 0, 0, 1, 0, UINT32_MAX, nullptr, nullptr, tiles);
 }
 
 int tlb_gemm_set_path(int path) {

@@ -1,21 +1,31 @@
-// tcgen05 GEMM for the TN family of tla::gemm (tensor.hpp:214-233):
-//   C(m,n) += sum_k A(m,k) * B(n,k),  A (M,K):(lda,1), B (N,K):(ldb,1) bf16, C fp32 any strides.
+// tcgen05 GEMM for the K-major family of tla::gemm (tensor.hpp:214-233):
+//   C(m,n) += sum_k A(m,k) * B(n,k),  A (M,K):(lda,1), B (N,K):(ldb,1) bf16, C fp32.
+// The dispatcher (tlb_gemm_simt.cu) hands this file a problem whose C is n-contiguous whenever C has a
+// contiguous mode at all: the paper's TN row, C = (M,N):(1,ldc), is run transposed (C^T += B * A^T).
 //
 // Partitioning follows the paper's local_tile / TiledMMA picture:
-// zipped_divide(C, [128,256]) gives the CTA tiles, zipped_divide(A, [128,64]) / (B, [256,64])
-// the k-blocks; the TMA tensor maps are exactly those divided layouts (box = tile mode,
-// globalDim/globalStrides = parent layout), the 128-byte swizzle of the staged tiles is
-// Swizzle<3,4,3> on byte offsets = the reference layout (128,8):(f1,f144).
+// zipped_divide(C, [128,256]) gives the CTA tiles, zipped_divide(A, [128,64]) / (B, [256,64]) the k-blocks;
+// the TMA tensor maps are exactly those divided layouts (box = tile mode, globalDim / globalStrides = parent
+// layout), and the 128-byte swizzle of every staged tile is Swizzle<3,4,3> on byte offsets, i.e. the reference
+// layout (128,8):(f1,f144) per 1 KiB (stride.hpp:142).
 //
-// Kernel shape (persistent, warp-specialised, 192 threads, 1 CTA per SM):
-//   warp 0   TMA producer: ring of kStages {A tile, B tile} stages, full/empty mbarriers
-//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (UMMA 128x256x16 or, with
-//            cta_group::2, 256x256x16 across a CTA pair), accumulators in TMEM, double buffered
-//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> registers -> C += acc (coalesced along the
-//            contiguous mode of C), overlapped with the next tile's MMAs
+// Kernel shape (persistent, warp-specialised, 320 threads, 1 CTA per SM):
+//   warps 0-7  epilogue. Warp w owns TMEM lane quadrant w % 4 and columns [128 * (w / 4), +128):
+//              tcgen05.ld 32x32b.x32 -> registers -> 128-byte-swizzled smem chunk (32 n x 128 m fp32) ->
+//              cp.reduce.async.bulk.tensor .add: the TMA unit / L2 performs C += chunk, the SM never loads C.
+//              (Generic C strides fall back to a register epilogue.) Overlaps the next tile's MMAs.
+//   warp 8     TMA producer: ring of kStages {A tile, B tile} stages, full / empty mbarriers
+//   warp 9     TMEM allocator + tcgen05.mma issue (one elected lane, warp-uniform control flow so that
+//              descriptors live in uniform registers): UMMA 128x256x16, or 256x256x16 across a CTA pair with
+//              cta_group::2; fp32 accumulators in TMEM, double buffered (2 x 256 columns)
+// Scheduling: static round-robin over tiles; the tiles of the last partial wave are split along K into
+// slices that run first and combine through the same reduce-add epilogue (tail-wave balancing).
 // No CUTLASS / CuTe: descriptors are encoded by hand below.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include <cuda.h>
 
@@ -29,21 +39,43 @@ constexpr int BM = 128;      // rows of C per CTA
 constexpr int BN = 256;      // columns of C per CTA (UMMA N)
 constexpr int BK = 64;       // k-block: 64 bf16 = one 128-byte swizzle row
 constexpr int UMMA_K = 16;
-constexpr int kUmmaThreads = 192;
+constexpr int kEpiWarps = 8; // two warps per TMEM lane quadrant, 128 columns each
+constexpr int kUmmaThreads = 64 + 32 * kEpiWarps;
+// The single-thread MMA issuer is latency critical; it is the last warp of the CTA.
+constexpr int kProducerWarp = kEpiWarps;
+constexpr int kMmaWarp = kEpiWarps + 1;
 constexpr uint32_t kTmemCols = 512; // two 256-column fp32 accumulators
 
-template <int CG> struct Cfg {
-    static constexpr int kStages = CG == 1 ? 4 : 7;
+// Epilogue flavours: how C += acc reaches memory.
+//   EPI_REGS   any C strides: registers; C loaded / added / stored per element (prefetched a chunk ahead),
+//              K-slices of split tiles use red.global.add
+//   EPI_TMA    C n-contiguous: 32(n) x 128(m) fp32 chunks staged with the 128-byte swizzle, TMA reduce-add
+enum { EPI_REGS = 0, EPI_TMA = 1 };
+constexpr uint32_t kEpiChunkBytes = BM * 32 * 4; // 16 KiB
+
+template <int CG, int EPI> struct Cfg {
+    static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : (CG == 1 ? 1 : 2); // staging buffers per column half
+    static constexpr int kStages = EPI == EPI_REGS ? (CG == 1 ? 4 : 7) : (CG == 1 ? 4 : 5);
     static constexpr int kBRows = CG == 1 ? BN : BN / 2; // rows of B this CTA stages
     static constexpr uint32_t kABytes = BM * BK * 2;
     static constexpr uint32_t kBBytes = kBRows * BK * 2;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr uint32_t kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t kEpiBytes = 2 * kEpiBufs * kEpiChunkBytes;
+    static constexpr uint32_t kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // ---- PTX wrappers ---------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -59,21 +91,27 @@ __device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t rank) {
     return r;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-// Bounded wait: a pipeline bug must trap, never hang the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Bounded wait: a pipeline bug must trap, never hang the GPU. The first probe is free of bookkeeping; roles
+// that idle for microseconds (epilogue, producer) back off with nanosleep between probes.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_t backoff_ns = 0) {
+    if (mbar_try(bar, parity)) return;
     const long long t0 = clock64();
     for (;;) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-        if (ok) return;
+        if (backoff_ns) __nanosleep(backoff_ns);
+        if (mbar_try(bar, parity)) return;
         if (clock64() - t0 > 6000000000ll) __trap();
     }
 }
@@ -89,6 +127,21 @@ __device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const void* map, u
         "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
         "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+}
+// C += staged chunk, performed by the TMA unit / L2 (fp32 add, element type from the tensor map).
+__device__ __forceinline__ void tma_reduce_add_3d(const void* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -130,7 +183,7 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint
             : "memory");
     }
 }
-// tcgen05.commit: the barrier is arrived on when every previously issued MMA has finished.
+// tcgen05.commit: the barrier is arrived on when every MMA previously issued by this thread has finished.
 template <int CG> __device__ __forceinline__ void umma_commit(uint32_t bar) {
     if constexpr (CG == 1) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -155,18 +208,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// Shared-memory matrix descriptor of a K-major bf16 tile staged with the 128-byte swizzle:
-// rows of 128 B, 8-row groups 1024 B apart (SBO), sm_100 descriptor version 1, layout type 2.
-__device__ __forceinline__ uint64_t make_kmajor_sw128_desc(uint32_t smem_addr) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3fffu);       // start address  [0,14)
-    d |= static_cast<uint64_t>(1) << 16;                          // LBO (unused for swizzled K-major) [16,30)
-    d |= static_cast<uint64_t>(1024 >> 4) << 32;                  // SBO = 1024 B   [32,46)
-    d |= static_cast<uint64_t>(1) << 46;                          // version = 1    [46,48)
-    d |= static_cast<uint64_t>(2) << 61;                          // SWIZZLE_128B   [61,64)
-    return d;
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+
+// Shared-memory matrix descriptor of a K-major bf16 tile staged with the 128-byte swizzle: rows of 128 B,
+// 8-row groups 1024 B apart (SBO), sm_100 descriptor version 1, layout type 2 (SWIZZLE_128B). Only the low
+// word depends on the tile address; advancing K by 16 elements inside the swizzle row adds 32 B (+2).
+constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ uint32_t desc_lo(uint32_t smem_addr) { return ((smem_addr >> 4) & 0x3fffu) | (1u << 16); }
+__device__ __forceinline__ uint64_t make_desc(uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; }
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N = 256, M = 128 * CG.
 template <int CG> __device__ __forceinline__ constexpr uint32_t make_idesc() {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -177,12 +228,44 @@ struct UmmaArgs {
     float* C;
     int64_t cs_m, cs_n, c_bs;
     int32_t M, N, K;
-    uint32_t mb, nb;           // 256x256 blocks along m and n
+    uint32_t mb, nb;               // 256x256 blocks along m and n
     uint32_t unit_begin, unit_end; // CG=1: 128x256 tile ids; CG=2: 256x256 block ids (all batches)
-    int32_t c_vec;             // 1: C rows are n-contiguous and 16-byte aligned (vector epilogue)
+    uint32_t n_split_units;        // the LAST n_split_units units of the range are split along K ...
+    uint32_t split;                // ... into `split` slices each; the slices are scheduled first
+    uint32_t work_end;             // unit_begin + n_split_units * split + (units - n_split_units)
+    int32_t c_vec;                 // register epilogue: C rows are n-contiguous and 16-byte aligned
+    uint32_t backoff_ns;           // nanosleep between barrier probes of the idle roles (0 = spin)
+    uint32_t debug;                // TLB_GEMM_DEBUG timing experiments (results are garbage): 1 = no TMA loads after
+                                   // the ring is filled once, 2 = epilogue without smem / global traffic,
+                                   // 4 = no staging stores, 8 = no TMA store
+    long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
 };
+constexpr int kTraceSlots = 128;
+#define TLB_TRACE(slot)                                                                                    \
+    do {                                                                                                   \
+        if (args.trace && (slot) < kTraceSlots) args.trace[blockIdx.x * kTraceSlots + (slot)] = clock64(); \
+    } while (0)
 
-// unit -> (batch, m_tile (128 rows), n_blk (256 cols)). Blocks are walked in groups of kGroupM
+// Work item w -> (unit, k-block range). The K-slices of the split units come first, whole units after.
+__device__ __forceinline__ void decode_work(const UmmaArgs& a, uint32_t w, int kblocks, uint32_t* unit, int* kb0, int* kb1,
+                                            bool* partial) {
+    const uint32_t r = w - a.unit_begin;
+    const uint32_t n_slices = a.n_split_units * a.split;
+    if (r >= n_slices) {
+        *unit = a.unit_begin + (r - n_slices);
+        *kb0 = 0;
+        *kb1 = kblocks;
+        *partial = false;
+        return;
+    }
+    *unit = a.unit_end - a.n_split_units + r / a.split;
+    const uint32_t sl = r % a.split;
+    *kb0 = static_cast<int>(static_cast<int64_t>(kblocks) * sl / a.split);
+    *kb1 = static_cast<int>(static_cast<int64_t>(kblocks) * (sl + 1) / a.split);
+    *partial = a.split > 1;
+}
+
+// unit -> (batch, m_tile (128 rows), n_blk (256 cols)). Blocks are walked in groups of kGemmGroupM
 // m-blocks, m fastest inside a group, so that concurrently resident CTAs share A and B panels in L2.
 template <int CG>
 __device__ __forceinline__ void decode_unit(const UmmaArgs& a, uint32_t unit, uint32_t rank, uint32_t* batch,
@@ -199,14 +282,15 @@ __device__ __forceinline__ void decode_unit(const UmmaArgs& a, uint32_t unit, ui
     *n_blk = rem / gm;
 }
 
-template <int CG>
+template <int CG, int EPI>
 __global__ void __launch_bounds__(kUmmaThreads, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                 const __grid_constant__ UmmaArgs args) {
-    using C = Cfg<CG>;
+                 const __grid_constant__ CUtensorMap map_c, const __grid_constant__ UmmaArgs args) {
+    using C = Cfg<CG, EPI>;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-    const uint32_t bar_base = smem_base + C::kStages * C::kStageBytes;
+    const uint32_t epi_base = smem_base + C::kStages * C::kStageBytes; // 1 KiB aligned (stage sizes are)
+    const uint32_t bar_base = epi_base + C::kEpiBytes;
     auto a_stage = [&](int s) { return smem_base + s * C::kStageBytes; };
     auto b_stage = [&](int s) { return smem_base + s * C::kStageBytes + C::kABytes; };
     auto full_bar = [&](int s) { return bar_base + 8u * s; };
@@ -221,154 +305,275 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const uint32_t n_workers = CG == 2 ? gridDim.x / 2 : gridDim.x;
     const uint32_t worker = CG == 2 ? blockIdx.x / 2 : blockIdx.x;
     const int kblocks = (args.K + BK - 1) / BK;
+    if (threadIdx.x == 0) {
+        TLB_TRACE(0);
+        if (args.trace) {
+            unsigned long long gt;
+            uint32_t smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            args.trace[blockIdx.x * kTraceSlots + 2] = static_cast<long long>(gt);
+            args.trace[blockIdx.x * kTraceSlots + 3] = smid;
+        }
+    }
 
-    if (warp == 0 && lane == 0) {
+    if (warp == kProducerWarp && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+        if (EPI != EPI_REGS) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
         for (int s = 0; s < C::kStages; ++s) {
-            mbar_init(full_bar(s), CG);       // CG=2: leader's own arrive + the peer's remote arrive
-            mbar_init(empty_bar(s), 1);       // one tcgen05.commit
+            mbar_init(full_bar(s), 1);  // the (leader's) producer arrive; the TMA bytes complete the phase
+            mbar_init(empty_bar(s), 1); // one tcgen05.commit
         }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(tfull_bar(s), 1);       // one tcgen05.commit
-            mbar_init(tempty_bar(s), 4 * CG); // one lane of each epilogue warp (of both CTAs)
+            mbar_init(tfull_bar(s), 1);               // one tcgen05.commit
+            mbar_init(tempty_bar(s), kEpiWarps * CG); // one lane of each epilogue warp (of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) tmem_alloc<CG>(tmem_slot, kTmemCols);
+    if (warp == kMmaWarp) tmem_alloc<CG>(tmem_slot, kTmemCols);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync_all();
     else __syncthreads();
     tc_fence_after();
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
+    if (threadIdx.x == 0) TLB_TRACE(1);
 
-    if (warp == 0) {
-        // ===== TMA producer =====
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (uint32_t u = args.unit_begin + worker; u < args.unit_end; u += n_workers) {
-                uint32_t batch, m_tile, n_blk;
-                decode_unit<CG>(args, u, rank, &batch, &m_tile, &n_blk);
-                if (CG == 1 && m_tile * BM >= static_cast<uint32_t>(args.M)) continue;
-                const int m0 = m_tile * BM;
-                const int n0 = n_blk * BN + (CG == 2 ? rank * (BN / 2) : 0);
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(empty_bar(stage), phase ^ 1u);
-                    if constexpr (CG == 1) {
+    if (warp == kProducerWarp) {
+        // ===== TMA producer (whole warp in the loops, one elected lane issues) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        bool ring_filled = false;
+        const uint32_t lbar0 = CG == 2 ? map_to_cta(full_bar(0), 0) : full_bar(0);
+        for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
+            uint32_t u, batch, m_tile, n_blk;
+            int kb0, kb1;
+            bool partial;
+            decode_work(args, w, kblocks, &u, &kb0, &kb1, &partial);
+            decode_unit<CG>(args, u, rank, &batch, &m_tile, &n_blk);
+            if (CG == 1 && m_tile * BM >= static_cast<uint32_t>(args.M)) continue;
+            const int m0 = m_tile * BM;
+            const int n0 = n_blk * BN + (CG == 2 ? rank * (BN / 2) : 0);
+            const int item = static_cast<int>((w - args.unit_begin) / n_workers);
+            if (lane == 0) TLB_TRACE(8 + item * 10 + 0);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(empty_bar(stage), phase ^ 1u, args.backoff_ns);
+                if (elect_one()) {
+                    if ((args.debug & 1u) && ring_filled) {
+                        if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
+                    } else if constexpr (CG == 1) {
                         mbar_expect_tx(full_bar(stage), C::kStageBytes);
                         tma_load_3d(a_stage(stage), &map_a, full_bar(stage), kb * BK, m0, batch);
                         tma_load_3d(b_stage(stage), &map_b, full_bar(stage), kb * BK, n0, batch);
                     } else {
-                        const uint32_t lbar = map_to_cta(full_bar(stage), 0);
+                        // The leader's barrier expects the bytes of BOTH CTAs; the peer's TMA may complete before
+                        // this expect_tx is issued (tx-count goes transiently negative, as with multicast).
+                        const uint32_t lbar = lbar0 + 8u * stage;
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
-                        else mbar_arrive_cluster(lbar);
                         tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
                         tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, n0, batch);
                     }
-                    if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
                 }
+                __syncwarp();
+                if (stage == C::kStages - 1) ring_filled = true;
+                if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
             }
+            if (lane == 0) TLB_TRACE(8 + item * 10 + 1);
         }
-    } else if (warp == 1) {
-        // ===== MMA issuer (one thread; leader CTA only under cta_group::2) =====
-        if (lane == 0 && leader) {
+    } else if (warp == kMmaWarp) {
+        // ===== MMA issuer (leader CTA only under cta_group::2). Control flow is warp-uniform; one elected
+        // lane issues the MMAs and the commits (tcgen05.commit tracks the MMAs of the issuing thread). =====
+        if (leader) {
             constexpr uint32_t idesc = make_idesc<CG>();
+            const uint32_t a_lo0 = desc_lo(a_stage(0)), b_lo0 = desc_lo(b_stage(0));
             int stage = 0;
             uint32_t phase = 0, acc = 0, acc_phase = 0;
-            for (uint32_t u = args.unit_begin + worker; u < args.unit_end; u += n_workers) {
-                uint32_t batch, m_tile, n_blk;
+            for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
+                uint32_t u, batch, m_tile, n_blk;
+                int kb0, kb1;
+                bool partial;
+                decode_work(args, w, kblocks, &u, &kb0, &kb1, &partial);
                 decode_unit<CG>(args, u, rank, &batch, &m_tile, &n_blk);
                 if (CG == 1 && m_tile * BM >= static_cast<uint32_t>(args.M)) continue;
-                mbar_wait(tempty_bar(acc), acc_phase ^ 1u); // epilogue has drained this accumulator
+                const int item = static_cast<int>((w - args.unit_begin) / n_workers);
+                mbar_wait(tempty_bar(acc), acc_phase ^ 1u); // the epilogue has drained this accumulator
                 tc_fence_after();
+                if (lane == 0) TLB_TRACE(8 + item * 10 + 2);
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full_bar(stage), phase);
                     tc_fence_after();
-                    const uint64_t da = make_kmajor_sw128_desc(a_stage(stage));
-                    const uint64_t db = make_kmajor_sw128_desc(b_stage(stage));
+                    if (kb == kb0 && lane == 0) TLB_TRACE(8 + item * 10 + 3);
+                    if (elect_one()) {
+                        const uint32_t a_lo = a_lo0 + stage * (C::kStageBytes >> 4);
+                        const uint32_t b_lo = b_lo0 + stage * (C::kStageBytes >> 4);
 #pragma unroll
-                    for (int k = 0; k < BK / UMMA_K; ++k) {
-                        // advancing K inside the 128-byte swizzle row: +32 B on the start address
-                        umma_bf16<CG>(d_tmem, da + static_cast<uint64_t>(k * 2), db + static_cast<uint64_t>(k * 2), idesc,
-                                      (kb | k) != 0 ? 1u : 0u);
+                        for (int k = 0; k < BK / UMMA_K; ++k)
+                            umma_bf16<CG>(d_tmem, make_desc(a_lo + 2 * k), make_desc(b_lo + 2 * k), idesc,
+                                          (kb != kb0 || k != 0) ? 1u : 0u);
+                        umma_commit<CG>(empty_bar(stage)); // frees the smem stage once these MMAs retire
+                        if (kb == kb1 - 1) umma_commit<CG>(tfull_bar(acc)); // accumulator complete -> epilogue
                     }
-                    umma_commit<CG>(empty_bar(stage)); // frees the smem stage once these MMAs retire
+                    __syncwarp();
                     if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
                 }
-                umma_commit<CG>(tfull_bar(acc)); // accumulator complete -> epilogue
+                if (lane == 0) TLB_TRACE(8 + item * 10 + 4);
                 acc ^= 1u;
                 if (acc == 0) acc_phase ^= 1u;
             }
         }
     } else {
-        // ===== epilogue: TMEM -> registers -> C += acc =====
-        const uint32_t quad = warp & 3;            // the TMEM lane quadrant this warp may read
+        // ===== epilogue =====
+        const uint32_t quad = warp & 3;                         // the TMEM lane quadrant this warp may read
+        const uint32_t half = static_cast<uint32_t>(warp) >> 2; // which 128 columns
         const uint32_t row = quad * 32 + lane;
         uint32_t acc = 0, acc_phase = 0;
         const uint32_t tempty_leader = CG == 2 ? map_to_cta(tempty_bar(0), 0) : 0u;
-        for (uint32_t u = args.unit_begin + worker; u < args.unit_end; u += n_workers) {
-            uint32_t batch, m_tile, n_blk;
-            decode_unit<CG>(args, u, rank, &batch, &m_tile, &n_blk);
-            if (CG == 1 && m_tile * BM >= static_cast<uint32_t>(args.M)) continue;
-            mbar_wait(tfull_bar(acc), acc_phase);
-            tc_fence_after();
-            const int64_t m = static_cast<int64_t>(m_tile) * BM + row;
-            float* crow = args.C + batch * args.c_bs + m * args.cs_m;
-            const bool m_ok = m < args.M;
+        constexpr int kChunks = BN / 2 / 32;
+        if constexpr (EPI == EPI_TMA) {
+            // ---- TMEM -> registers -> swizzled smem chunk -> cp.reduce.async.bulk.tensor (C += chunk)
+            const bool issuer = (warp & 3) == 0 && lane == 0; // one thread per column half
+            const uint32_t bar_id = 1 + half;
+            uint32_t chunk_no = 0;
+            for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
+                uint32_t u, batch, m_tile, n_blk;
+                int kb0, kb1;
+                bool partial;
+                decode_work(args, w, kblocks, &u, &kb0, &kb1, &partial);
+                decode_unit<CG>(args, u, rank, &batch, &m_tile, &n_blk);
+                if (CG == 1 && m_tile * BM >= static_cast<uint32_t>(args.M)) continue;
+                const int item = static_cast<int>((w - args.unit_begin) / n_workers);
+                if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 5);
+                mbar_wait(tfull_bar(acc), acc_phase, args.backoff_ns * 4);
+                tc_fence_after();
+                if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 6);
+                const int m0 = static_cast<int>(m_tile) * BM;
+                const int nbase = static_cast<int>(n_blk) * BN + static_cast<int>(half) * (BN / 2);
 #pragma unroll 1
-            for (int col = 0; col < BN; col += 32) {
-                uint32_t v[32];
-                __syncwarp(); // lanes of an edge tile diverge below; tcgen05.ld is .sync.aligned
-                tmem_ld32(tmem_base + ((quad * 32u) << 16) + acc * BN + col, v);
-                tmem_ld_wait();
-                const int64_t n0 = static_cast<int64_t>(n_blk) * BN + col;
-                if (!m_ok || n0 >= args.N) continue;
-                if (args.c_vec && n0 + 32 <= args.N) {
-                    float4* p = reinterpret_cast<float4*>(crow + n0);
-                    float4 c[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) c[j] = p[j];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        c[j].x += __uint_as_float(v[4 * j + 0]);
-                        c[j].y += __uint_as_float(v[4 * j + 1]);
-                        c[j].z += __uint_as_float(v[4 * j + 2]);
-                        c[j].w += __uint_as_float(v[4 * j + 3]);
-                        p[j] = c[j];
+                for (int ci = 0; ci < kChunks; ++ci, ++chunk_no) {
+                    const uint32_t buf = epi_base + (half * C::kEpiBufs + (chunk_no % C::kEpiBufs)) * kEpiChunkBytes;
+                    // the TMA store that last used this buffer must have finished reading it
+                    if (issuer) bulk_wait_read<C::kEpiBufs - 1>();
+                    named_bar(bar_id, 128);
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + ((quad * 32u) << 16) + acc * BN + half * (BN / 2) + ci * 32, v);
+                    tmem_ld_wait();
+                    if (ci == kChunks - 1) {
+                        // every TMEM read of this accumulator is done: hand it back to the MMA warp early
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (CG == 1) mbar_arrive(tempty_bar(acc));
+                            else mbar_arrive_cluster(tempty_leader + 8u * acc);
+                        }
                     }
-                } else if (n0 + 32 <= args.N) {
-                    float c[32];
+                    if (!(args.debug & (2u | 4u))) {
+                        // chunk as (n fastest, m): row = m (128 B), 16-byte chunk c stored at c ^ (m & 7)
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) c[j] = crow[(n0 + j) * args.cs_n];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) crow[(n0 + j) * args.cs_n] = c[j] + __uint_as_float(v[j]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (n0 + j < args.N) crow[(n0 + j) * args.cs_n] += __uint_as_float(v[j]);
+                        for (int c = 0; c < 8; ++c)
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + row * 128u + ((c ^ (row & 7u)) << 4)),
+                                         "r"(v[4 * c + 0]), "r"(v[4 * c + 1]), "r"(v[4 * c + 2]), "r"(v[4 * c + 3])
+                                         : "memory");
+                    }
+                    fence_async_smem();
+                    named_bar(bar_id, 128);
+                    if (issuer && !(args.debug & (2u | 8u))) {
+                        tma_reduce_add_3d(&map_c, buf, nbase + ci * 32, m0, batch);
+                        bulk_commit();
+                    }
                 }
+                if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 7);
+                acc ^= 1u;
+                if (acc == 0) acc_phase ^= 1u;
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if constexpr (CG == 1) mbar_arrive(tempty_bar(acc));
-                else mbar_arrive_cluster(tempty_leader + 8u * acc);
+            if (issuer) bulk_wait_all(); // every reduction performed before the CTA (and its smem) goes away
+        } else {
+            // ---- register epilogue: C loaded a chunk ahead, added, stored (any strides)
+            for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
+                uint32_t u, batch, m_tile, n_blk;
+                int kb0, kb1;
+                bool partial;
+                decode_work(args, w, kblocks, &u, &kb0, &kb1, &partial);
+                decode_unit<CG>(args, u, rank, &batch, &m_tile, &n_blk);
+                if (CG == 1 && m_tile * BM >= static_cast<uint32_t>(args.M)) continue;
+                const int item = static_cast<int>((w - args.unit_begin) / n_workers);
+                const int64_t m = static_cast<int64_t>(m_tile) * BM + row;
+                float* crow = args.C + batch * args.c_bs + m * args.cs_m;
+                const bool m_ok = m < args.M;
+                const int64_t nbase = static_cast<int64_t>(n_blk) * BN + half * (BN / 2);
+                const bool vec = args.c_vec && m_ok && nbase + BN / 2 <= args.N;
+                const bool no_global = (args.debug & 2u) != 0;
+                float cur[32], nxt[32];
+                auto load_c = [&](int ci, float (&dst)[32]) {
+                    const int64_t n0 = nbase + ci * 32;
+                    if (vec) {
+                        const float4* p = reinterpret_cast<const float4*>(crow + n0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 t = p[j];
+                            dst[4 * j + 0] = t.x; dst[4 * j + 1] = t.y; dst[4 * j + 2] = t.z; dst[4 * j + 3] = t.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) dst[j] = (m_ok && n0 + j < args.N) ? crow[(n0 + j) * args.cs_n] : 0.f;
+                    }
+                };
+                if (!partial && !no_global) load_c(0, cur);
+                if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 5);
+                mbar_wait(tfull_bar(acc), acc_phase, args.backoff_ns * 4);
+                tc_fence_after();
+                if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 6);
+#pragma unroll
+                for (int ci = 0; ci < kChunks; ++ci) {
+                    if (ci + 1 < kChunks && !partial && !no_global) load_c(ci + 1, nxt);
+                    uint32_t v[32];
+                    __syncwarp(); // tcgen05.ld is .sync.aligned; lanes of an edge tile may have diverged
+                    tmem_ld32(tmem_base + ((quad * 32u) << 16) + acc * BN + half * (BN / 2) + ci * 32, v);
+                    tmem_ld_wait();
+                    const int64_t n0 = nbase + ci * 32;
+                    if (no_global) {
+                        if (v[0] == 0x7fc12345u) crow[0] = 1.f; // keep the TMEM load alive
+                    } else if (partial) {
+                        // K-slice of a split tile: several CTAs add into the same C cells -> reductions at L2
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (m_ok && n0 + j < args.N) red_add_f32(crow + (n0 + j) * args.cs_n, __uint_as_float(v[j]));
+                    } else if (vec) {
+                        float4* p = reinterpret_cast<float4*>(crow + n0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            p[j] = make_float4(cur[4 * j + 0] + __uint_as_float(v[4 * j + 0]), cur[4 * j + 1] + __uint_as_float(v[4 * j + 1]),
+                                               cur[4 * j + 2] + __uint_as_float(v[4 * j + 2]), cur[4 * j + 3] + __uint_as_float(v[4 * j + 3]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (m_ok && n0 + j < args.N) crow[(n0 + j) * args.cs_n] = cur[j] + __uint_as_float(v[j]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 7);
+                if (lane == 0) {
+                    if constexpr (CG == 1) mbar_arrive(tempty_bar(acc));
+                    else mbar_arrive_cluster(tempty_leader + 8u * acc);
+                }
+                acc ^= 1u;
+                if (acc == 0) acc_phase ^= 1u;
             }
-            acc ^= 1u;
-            if (acc == 0) acc_phase ^= 1u;
         }
     }
 
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync_all();
     else __syncthreads();
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, kTmemCols);
     }
+    if (threadIdx.x == 0) TLB_TRACE(120);
 }
 
 int encode_operand_map(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch,
@@ -380,18 +585,37 @@ int encode_operand_map(TmaDesc* out, const void* base, int64_t ld, int64_t batch
     return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
 }
 
-template <int CG> int launch(const UmmaProblem& p, cudaStream_t stream) {
-    using C = Cfg<CG>;
+// Tensor map of an n-contiguous C for the reduce-add epilogue: fp32, dims (N, M, batch), box 32 x 128.
+int encode_c_map(TmaDesc* out, const UmmaProblem& p) {
+    const uint64_t dims[3] = {static_cast<uint64_t>(p.N), static_cast<uint64_t>(p.M), static_cast<uint64_t>(p.batch)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * 4,
+                                 static_cast<uint64_t>(p.batch > 1 ? p.c_bs : p.cs_m * static_cast<int64_t>(p.M)) * 4};
+    const uint32_t box[3] = {32u, static_cast<uint32_t>(BM), 1};
+    return tma_encode(out, 4, true, 3, p.C, dims, strides, box, TMA_SW_128, 0);
+}
+
+int pick_epilogue(const UmmaProblem& p) {
+    if (const char* e = std::getenv("TLB_GEMM_EPILOGUE"))
+        if (e[0] == 'r') return EPI_REGS; // "regs": keep C in registers (profiling / A-B comparisons)
+    const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
+    if (base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N) return EPI_TMA;
+    return EPI_REGS;
+}
+
+template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream) {
+    using C = Cfg<CG, EPI>;
     static bool attr_set[64] = {false};
     int dev = 0;
     TLB_CUDA(cudaGetDevice(&dev));
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-        TLB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        TLB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<CG, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         attr_set[dev] = true;
     }
-    TmaDesc ma, mb;
+    TmaDesc ma, mb, mc;
     TLB_TRY(encode_operand_map(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BM));
     TLB_TRY(encode_operand_map(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, C::kBRows));
+    if (EPI != EPI_REGS) TLB_TRY(encode_c_map(&mc, p));
+    else mc = ma; // unused by the register epilogue
     UmmaArgs a;
     std::memset(&a, 0, sizeof(a));
     a.C = p.C;
@@ -409,13 +633,37 @@ template <int CG> int launch(const UmmaProblem& p, cudaStream_t stream) {
     const uint32_t units = a.unit_end - a.unit_begin;
     if (units == 0) return TLB_OK;
     const int sms = sm_count();
+    // Tail-wave balancing: with W workers, the units of the last partial wave are split along K into slices
+    // that run FIRST (so their epilogues overlap later mainloops); slices of one unit combine through the
+    // reduce-add epilogue (TMA reduction, or red.global.add with the register epilogue).
+    {
+        const uint32_t W = CG == 1 ? static_cast<uint32_t>(sms) : static_cast<uint32_t>(sms / 2);
+        const uint32_t tail = units % W;
+        const int kblocks = (p.K + BK - 1) / BK;
+        uint32_t split = 1;
+        if (p.split_tail && tail > 0 && units > W) {
+            split = W / tail;
+            split = std::min<uint32_t>(split, 4);
+            while (split > 1 && kblocks / static_cast<int>(split) < 8) --split;
+        }
+        a.split = split;
+        a.n_split_units = split > 1 ? tail : 0;
+        a.work_end = a.unit_begin + (units - a.n_split_units) + a.n_split_units * split;
+    }
+    {
+        const char* e = std::getenv("TLB_GEMM_BACKOFF_NS");
+        a.backoff_ns = e ? static_cast<uint32_t>(std::atoi(e)) : 100u;
+        const char* d = std::getenv("TLB_GEMM_DEBUG");
+        a.debug = d ? static_cast<uint32_t>(std::atoi(d)) : 0u;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
+    const uint32_t work = a.work_end - a.unit_begin;
     if (CG == 1) {
-        cfg.gridDim = dim3(std::min<uint32_t>(units, static_cast<uint32_t>(sms)));
+        cfg.gridDim = dim3(std::min<uint32_t>(work, static_cast<uint32_t>(sms)));
         cfg.numAttrs = 0;
     } else {
-        cfg.gridDim = dim3(2 * std::min<uint32_t>(units, static_cast<uint32_t>(sms / 2)));
+        cfg.gridDim = dim3(2 * std::min<uint32_t>(work, static_cast<uint32_t>(sms / 2)));
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
         attr[0].val.clusterDim.y = 1;
@@ -426,20 +674,46 @@ template <int CG> int launch(const UmmaProblem& p, cudaStream_t stream) {
     cfg.blockDim = dim3(kUmmaThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;
-    CUtensorMap tma, tmb;
+    CUtensorMap tma, tmb, tmc;
     std::memcpy(&tma, ma.bytes, 128);
     std::memcpy(&tmb, mb.bytes, 128);
-    TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_gemm_kernel<CG>, tma, tmb, a));
+    std::memcpy(&tmc, mc.bytes, 128);
+    // Debug timeline: TLB_GEMM_TRACE=<file> makes this launch synchronous and dumps per-CTA clock64 stamps.
+    const char* trace_path = std::getenv("TLB_GEMM_TRACE");
+    const size_t trace_bytes = static_cast<size_t>(cfg.gridDim.x) * kTraceSlots * sizeof(long long);
+    if (trace_path && trace_path[0]) {
+        TLB_CUDA(cudaMalloc(reinterpret_cast<void**>(&a.trace), trace_bytes));
+        TLB_CUDA(cudaMemset(a.trace, 0, trace_bytes));
+    }
+    TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_gemm_kernel<CG, EPI>, tma, tmb, tmc, a));
     count_launch();
-    set_plan(CG == 1 ? "umma_1sm" : "umma_2sm");
+    static const char* const names[2][2] = {{"umma_1sm_regs", "umma_1sm"}, {"umma_2sm_regs", "umma_2sm"}};
+    set_plan(names[CG - 1][EPI]);
+    if (a.trace) {
+        std::vector<long long> h(trace_bytes / sizeof(long long));
+        TLB_CUDA(cudaStreamSynchronize(stream));
+        TLB_CUDA(cudaMemcpy(h.data(), a.trace, trace_bytes, cudaMemcpyDeviceToHost));
+        cudaFree(a.trace);
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            const long long hdr[4] = {static_cast<long long>(cfg.gridDim.x), kTraceSlots, CG, static_cast<long long>(a.split)};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(h.data(), 1, trace_bytes, f);
+            std::fclose(f);
+        }
+    }
     return TLB_OK;
+}
+
+template <int CG> int launch_cg(const UmmaProblem& p, cudaStream_t stream) {
+    if (pick_epilogue(p) == EPI_TMA) return launch<CG, EPI_TMA>(p, stream);
+    return launch<CG, EPI_REGS>(p, stream);
 }
 
 } // namespace
 
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream) {
-    if (p.cta_group == 2) return launch<2>(p, stream);
-    return launch<1>(p, stream);
+    if (p.cta_group == 2) return launch_cg<2>(p, stream);
+    return launch_cg<1>(p, stream);
 }
 
 } // namespace tlb

@@ -195,6 +195,20 @@ def copy(src, dst, i_begin: int = 0, i_end: int = 2**64 - 1, stream=None) -> str
     return lib.tlb_last_plan().decode()
 
 
+def copy_plan(src_layout, dst_layout, elem_bytes: int, i_begin: int = 0, i_end: int = 2**64 - 1, src_align: int = 256,
+              dst_align: int = 256) -> str:
+    """The plan tlb_copy would choose for two compact buffers at the given pointer alignments (no device needed)."""
+    lib = abi.load()
+    ls = L(src_layout) if isinstance(src_layout, str) else src_layout
+    ld = L(dst_layout) if isinstance(dst_layout, str) else dst_layout
+    ds, dd = ls.lower(), ld.lower()
+    big = 1 << 62
+    a = make_tensor(ds, src_align, big, elem_bytes)
+    b = make_tensor(dd, dst_align, big, elem_bytes)
+    abi.check(lib.tlb_copy_plan(C.byref(a), C.byref(b), i_begin, i_end))
+    return lib.tlb_last_plan().decode()
+
+
 def copy_host(src, dst) -> None:
     abi.check(abi.load().tlb_copy_host(C.byref(src[0]), C.byref(dst[0])))
 
@@ -203,6 +217,12 @@ def gemm_bf16(a, b, c, tile_begin: int = 0, tile_end: int = 2**32 - 1, stream=No
     lib = abi.load()
     abi.check(lib.tlb_gemm_bf16(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), tile_begin, tile_end, _stream_ptr(stream)))
     return lib.tlb_last_plan().decode()
+
+
+def gemm_tile_count(a, b, c) -> int:
+    n = C.c_uint32(0)
+    abi.check(abi.load().tlb_gemm_tile_count(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), C.byref(n)))
+    return n.value
 
 
 def gemm_bf16_batched(a, b, c, a_bs: int, b_bs: int, c_bs: int, batch_begin: int, batch_end: int, stream=None) -> str:

@@ -123,3 +123,17 @@ def test_no_cpu_fallback_without_a_device():
     assert lib.tlb_copy_host(C.byref(src), C.byref(src)) == abi.TLB_ERR_CUDA
     with pytest.raises(TlbError):
         abi.check(lib.tlb_copy_host(C.byref(src), C.byref(src)))
+
+
+def test_gemm_tile_count_is_host_only():
+    """Sharding input: the number of 128x256 tiles of the plan, without a device."""
+    import ctypes as C
+    from paper_2603_02298_b200 import host
+    buf = (C.c_int16 * 16)()
+    def t(text, eb):
+        return (host.make_tensor(L(text).lower(ranked=True), C.addressof(buf), 1 << 40, eb), None)
+    a, b = t("(4096,4096):(4096,1)", 2), t("(4096,4096):(4096,1)", 2)
+    assert host.gemm_tile_count(a, b, t("(4096,4096):(1,4096)", 4)) == 512
+    assert host.gemm_tile_count(t("(8192,8192):(8192,1)", 2), t("(8192,8192):(8192,1)", 2), t("(8192,8192):(1,8192)", 4)) == 2048
+    # ragged: 200 x 300 runs transposed (C m-contiguous): rows = 300 -> 2 blocks, cols = 200 -> 1 block
+    assert host.gemm_tile_count(t("(200,136):(136,1)", 2), t("(300,136):(136,1)", 2), t("(200,300):(1,200)", 4)) == 4

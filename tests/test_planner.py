@@ -1,0 +1,54 @@
+"""CPU: host logic of the copy planner (tlb_copy_plan runs the contract checks and the planner without a
+device). The plans are what the -m gpu parity tests then execute."""
+import ctypes as C
+
+import pytest
+
+from paper_2603_02298_b200 import L, TlbError, abi, host
+
+
+@pytest.mark.parametrize("s,d,eb,plan", [
+    # BASELINE configs C1 and C3 take the swizzle-staged tiled kernel
+    ("(8192,8192):(8192,1)", "(8192,8192):(1,8192)", 4, "tiled"),
+    ("((8,128),(4,64),4096):((1,2048),(8,32),262144)", "((8,128),(4,64),4096):((128,1),(65536,1024),262144)", 4, "tiled"),
+    ("((32,16),(64,4)):((1,32),(512,32768))", "((32,16),(64,4)):((64,8192),(1,2048))", 2, "tiled"),
+    ("((32,16),(64,4)):((1,32),(512,32768))", "((32,16),(64,4)):((64,8192),(1,2048))", 8, "tiled"),
+    # one mode contiguous on both sides -> vectors along it
+    ("4096:1", "4096:1", 4, "vec"),
+    ("(64,8,4):(1,256,64)", "(64,8,4):(1,64,512)", 2, "vec"),
+    # the Table-1 rows (test_tensor.cpp:93-100)
+    ("8:1", "8:1", 8, "vec"), ("(8,2,3):(1,16,32)", "(8,2,3):(1,16,32)", 8, "vec"),
+    ("(2,3,2):(42,1,128)", "12:1", 8, "gather"), ("7:0", "7:1", 8, "gather"), ("7:0", "7:0", 8, "ordered"),
+    ("(8,3):(1,8)", "(8,3):(3,1)", 8, "gather"),
+    # Xor strides, interleaved runs, ragged rows, aliasing destinations
+    ("(8,8):(f1,f9)", "64:1", 8, "gather"),
+    ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, "gather"),
+    ("(96,160):(160,1)", "(96,160):(1,96)", 2, "gather"),
+    ("(64,64):(1,64)", "(64,64):(1,0)", 4, "ordered"),
+])
+def test_plan_selection(s, d, eb, plan):
+    assert host.copy_plan(s, d, eb) == plan
+
+
+def test_plan_depends_on_alignment_and_range():
+    s, d = "(256,128):(128,1)", "(256,128):(1,256)"
+    assert host.copy_plan(s, d, 4) == "tiled"
+    assert host.copy_plan(s, d, 4, src_align=4) == "gather"            # 16-byte vectors need 16-byte bases
+    assert host.copy_plan(s, d, 4, 0, 256 * 64) == "tiled"             # whole slices of the outermost mode
+    assert host.copy_plan(s, d, 4, 5, 777) == "gather"                 # ragged range
+    assert host.copy_plan(s, d, 4, 10, 10) == "empty"
+
+
+def test_plan_contracts():
+    with pytest.raises(TlbError) as e:
+        host.copy_plan("8:1", "4:1", 8)
+    assert e.value.status == abi.TLB_ERR_CONTRACT                      # copy requires equal sizes
+    with pytest.raises(TlbError) as e:
+        host.copy_plan("(2,2):(e0,e1)", "4:1", 8)
+    assert e.value.status == abi.TLB_ERR_SEMIMODULE
+    lib = abi.load()
+    d = L("4:3").lower()
+    buf = (C.c_int64 * 8)()
+    src = host.make_tensor(d, C.addressof(buf), 8, 8)                  # 4:3 touches cell 9 of 8
+    dst = host.make_tensor(L("4:1").lower(), C.addressof(buf), 8, 8)
+    assert lib.tlb_copy_plan(C.byref(src), C.byref(dst), 0, 2**64 - 1) == abi.TLB_ERR_BOUNDS
