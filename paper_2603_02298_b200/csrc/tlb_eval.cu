@@ -38,27 +38,72 @@ __global__ void __launch_bounds__(kThreads) eval_range_kernel(const __grid_const
 // Grouped evaluation: G consecutive indices that share every coordinate except the low bits of the
 // first leaf (extent[0] % G == 0, i0 % G == 0) cost ONE peel: L(i + j) = L(i) + j*d0 for Int strides,
 // L(i) ^ clmul(j, mask0) for Xor strides (the leaf coordinate c0 + j equals c0 ^ j when c0 % G == 0
-// and clmul is linear over GF(2)). Each thread stores G*8 contiguous bytes with 16-byte stores.
-template <int G>
+// and clmul is linear over GF(2)). The map is write-bound only if an output costs about one
+// instruction, so: the peel runs in 32-bit shifts when every extent is a power of two and the index
+// fits 32 bits; the G outputs share their high word whenever the low word does not carry (one IADD
+// per output); and each thread stores whole 32-byte sectors with 256-bit stores.
+__device__ __forceinline__ void st_cs_v4(int64_t* p, int64_t a, int64_t b, int64_t c, int64_t d) {
+    asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
+// Peel for all-power-of-two extents and i < 2^32: every coordinate is an independent shift+mask.
+__device__ __forceinline__ int64_t dev_eval_pow2_u32(const tlb_layout_desc& L, uint32_t i) {
+    int64_t acc = 0;
+    const int n = L.n_modes;
+    const bool is_xor = L.kind == TLB_KIND_XOR;
+    uint32_t sh = 0;
+    for (int r = 0; r < n; ++r) {
+        uint32_t c = sh < 32 ? (i >> sh) : 0u;
+        if (r + 1 < n) c &= static_cast<uint32_t>(L.extent[r]) - 1u;
+        sh += L.log2e[r];
+        if (is_xor) acc ^= dev_clmul(c, static_cast<uint64_t>(L.stride[r]));
+        else acc += static_cast<int64_t>(c) * L.stride[r];
+    }
+    return acc;
+}
+
+template <int G, bool kPow2U32, bool kWide>
 __global__ void __launch_bounds__(kThreads) eval_group_kernel(const __grid_constant__ tlb_layout_desc L, uint64_t i0,
                                                               uint64_t n_groups, int64_t* __restrict__ out) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const bool is_xor = L.kind == TLB_KIND_XOR;
     const int64_t d0 = L.stride[0];
+    // Int strides: the low words of the G outputs stay below 2^32 past the base's low word?
+    const bool small_step = !is_xor && d0 >= 0 && static_cast<uint64_t>(d0) * (G - 1) < (1ull << 32);
     for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n_groups; g += stride) {
-        const int64_t base = dev_eval(L, i0 + g * G);
-        int64_t* o = out + g * G;
+        const uint64_t i = i0 + g * G;
+        const int64_t base = kPow2U32 ? dev_eval_pow2_u32(L, static_cast<uint32_t>(i)) : dev_eval(L, i);
+        int64_t v[G];
+        if (is_xor) {
+            v[0] = base;
 #pragma unroll
-        for (int j = 0; j < G; j += 2) {
-            int64_t v0, v1;
-            if (is_xor) {
-                v0 = base ^ dev_clmul(static_cast<uint64_t>(j), static_cast<uint64_t>(d0));
-                v1 = base ^ dev_clmul(static_cast<uint64_t>(j + 1), static_cast<uint64_t>(d0));
-            } else {
-                v0 = base + j * d0;
-                v1 = base + (j + 1) * d0;
+            for (int j = 1; j < G; ++j) {
+                // clmul(j, m) = clmul(j with its lowest set bit cleared, m) ^ (m << ctz(j))
+                const int low = j & -j;
+                int sh = 0;
+                while ((1 << sh) != low) ++sh;
+                v[j] = v[j - low] ^ static_cast<int64_t>(static_cast<uint64_t>(d0) << sh);
             }
-            st_cs_v2(o + j, v0, v1);
+        } else {
+            const uint32_t lo = static_cast<uint32_t>(base);
+            const uint32_t step = static_cast<uint32_t>(d0);
+            const uint32_t last = lo + step * static_cast<uint32_t>(G - 1);
+            if (small_step && last >= lo) {
+                const uint64_t hi = static_cast<uint64_t>(base) & 0xffffffff00000000ull;
+#pragma unroll
+                for (int j = 0; j < G; ++j) v[j] = static_cast<int64_t>(hi | (lo + step * static_cast<uint32_t>(j)));
+            } else {
+#pragma unroll
+                for (int j = 0; j < G; ++j) v[j] = base + j * d0;
+            }
+        }
+        int64_t* o = out + g * G;
+        if constexpr (kWide && G >= 4) {
+#pragma unroll
+            for (int j = 0; j < G; j += 4) st_cs_v4(o + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < G; j += 2) st_cs_v2(o + j, v[j], v[j + 1]);
         }
     }
 }
@@ -207,17 +252,38 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
     // grouped fast path: the first leaf must absorb a whole group
     int G = 1;
     if (aligned) {
-        for (int g = 8; g >= 2; g >>= 1)
-            if (i0 % g == 0 && (layout->n_modes == 1 || layout->extent[0] % g == 0) && n >= static_cast<uint64_t>(g)) {
+        for (int g = 32; g >= 2; g >>= 1)
+            if (i0 % g == 0 && (layout->n_modes == 1 || layout->extent[0] % g == 0) && n >= static_cast<uint64_t>(g) * 1024) {
                 G = g;
                 break;
             }
+        if (G == 1)
+            for (int g = 8; g >= 2; g >>= 1)
+                if (i0 % g == 0 && (layout->n_modes == 1 || layout->extent[0] % g == 0) && n >= static_cast<uint64_t>(g)) {
+                    G = g;
+                    break;
+                }
     }
     if (G > 1) {
         const uint64_t groups = n / G;
-        if (G == 8) eval_group_kernel<8><<<grid_for(groups), kThreads, 0, s>>>(*layout, i0, groups, d_out);
-        else if (G == 4) eval_group_kernel<4><<<grid_for(groups), kThreads, 0, s>>>(*layout, i0, groups, d_out);
-        else eval_group_kernel<2><<<grid_for(groups), kThreads, 0, s>>>(*layout, i0, groups, d_out);
+        const bool wide = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
+        const bool p32 = (layout->flags & TLB_LF_ALL_POW2) && (i0 + n - 1) < (1ull << 32);
+        const int grid = grid_for(groups);
+#define TLB_EVAL_G(GG)                                                                                          \
+    do {                                                                                                        \
+        if (p32 && wide) eval_group_kernel<GG, true, true><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);   \
+        else if (p32) eval_group_kernel<GG, true, false><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);     \
+        else if (wide) eval_group_kernel<GG, false, true><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);    \
+        else eval_group_kernel<GG, false, false><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);             \
+    } while (0)
+        switch (G) {
+        case 32: TLB_EVAL_G(32); break;
+        case 16: TLB_EVAL_G(16); break;
+        case 8: TLB_EVAL_G(8); break;
+        case 4: TLB_EVAL_G(4); break;
+        default: TLB_EVAL_G(2); break;
+        }
+#undef TLB_EVAL_G
         count_launch();
         TLB_CUDA(cudaGetLastError());
         const uint64_t done = groups * G;

@@ -36,6 +36,8 @@ for item in range(6):
           f" | commit->tfull_ok median {int(np.median(lag)) if len(lag) else -1}")
 
 pw, mw, mi = t[:, 100], t[:, 101], t[:, 102]
+if not (mi > 0).any():
+    raise SystemExit(0)
 lead = mi > 0
 print("producer: cycles waiting on empty barriers  median %d" % np.median(pw[pw > 0]))
 print("mma thread: waiting on full barriers median %d | issuing (wait-return -> commit issued) median %d" % (np.median(mw[lead]), np.median(mi[lead])))
