@@ -191,10 +191,13 @@ def timed(torch, dist, world, fn, steps, warmup):
     return ms / 1e3
 
 
-def traffic_for(kernel: str):
+def traffic_for(config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture of the
+    same workload (profiles/traffic.json, written by tools/ncu_summary.py); None when no capture exists."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
-        return json.loads(p.read_text()).get(kernel)
+        e = json.loads(p.read_text()).get(config)
+        return e["dram_bytes_per_launch"] if e else None
     return None
 
 
@@ -251,7 +254,7 @@ def run_ours(args):
     peak = pk["bf16_tflops"] if burst else pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops / kernel_s / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic_for("umma_gemm_kernel"), "kernel": f"umma_gemm_kernel ({plan})",
+                "traffic": traffic_for("C2"), "kernel": f"umma_gemm_kernel ({plan})",
                 "peak_source": f"{pk['_source']} {'burst' if burst else 'sustained'} cuBLAS bf16",
                 "frac_of_nominal_2250": achieved / 2250.0, "algorithmic_flop_per_launch": flops}
 
@@ -276,6 +279,11 @@ def run_ours(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # verification gather (outside every timed region): one 64-bit checksum of C per rank over NCCL
+    from paper_2603_02298_b200 import shard
+    sums = shard.gather_checksums(shard.checksum64(sets[0][2][1][1]), device="cuda")
+    verify = {"collective": "all_gather of per-rank C checksums (nccl)" if world > 1 else "none (1 GPU)",
+              "ranks_reporting": len(sums), "all_nonzero": all(x != 0 for x in sums)}
     e2e = {"value": flops * ke * world / e2e_s / 1e12, "unit": "TFLOP/s",
            "h2d_bytes_per_step": (M * Kd + N * Kd) * 2 + M * N * 4, "d2h_bytes_per_step": M * N * 4,
            "steps": ke, "ms_per_step": e2e_s / ke * 1e3, "api": "tlb_gemm_bf16_host (pinned host buffers)"}
@@ -307,7 +315,7 @@ def run_ours(args):
                        "l2": f"{nsets} rotating operand sets ({nsets * 128} MiB) > 126 MB L2",
                        "sharding": "independent problems per rank, no data-path collective"},
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
-            "other_configs": other,
+            "verify": verify, "other_configs": other,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -326,7 +334,7 @@ def other_configs(torch, dist, world, lib, host, pk, K, W):
         e = {"name": name, "metric": "copy_gbs" if name != "C5" else "index_map_gbs", "value": gbs, "unit": "GB/s",
              "ms_per_step": sec / steps * 1e3, "config": {"workload": workload, "plan": plan},
              "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": hbm, "unit": "GB/s", "frac": per_gpu / hbm,
-                          "traffic": traffic_for(kernel), "kernel": kernel, "peak_source": f"{pk['_source']} torch copy_",
+                          "traffic": traffic_for(name), "kernel": kernel, "peak_source": f"{pk['_source']} torch copy_",
                           "frac_of_nominal_8000": per_gpu / 8000.0, "algorithmic_bytes_per_launch": bytes_per_step}}
         if extra:
             e.update(extra)
@@ -374,7 +382,7 @@ def other_configs(torch, dist, world, lib, host, pk, K, W):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gemm-path", default="auto", choices=["auto", "1sm", "2sm"])

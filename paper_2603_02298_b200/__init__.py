@@ -5,8 +5,8 @@ The product is libtlb.so (hand-written CUDA, paper_2603_02298_b200/csrc). This p
 thin loader / driver; importing it does not load the library until a call needs it, and a missing
 library is an error (no CPU fallback).
 """
-from . import abi, host  # noqa: F401
+from . import abi, host, shard  # noqa: F401
 from .abi import TlbError, load  # noqa: F401
 from .host import L, Layout  # noqa: F401
 
-__all__ = ["abi", "host", "TlbError", "load", "L", "Layout"]
+__all__ = ["abi", "host", "shard", "TlbError", "load", "L", "Layout"]
