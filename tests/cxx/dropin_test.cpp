@@ -1,0 +1,192 @@
+// TEST INFRASTRUCTURE. The drop-in demonstration: the UNMODIFIED reference library builds the layouts and
+// computes the expected results on the host (tla::copy / tla::gemm / tla::eval_int), include/tla/device.hpp
+// runs the same calls on the GPU through libtlb, and every cell is compared. Mirrors proj/tests/test_tensor.cpp
+// (copy through layout pairs :86-111, gemm layout families :130-195, preconditions :113-118,:197-203) and
+// proj/demo/partition_demo.cpp (local_tile via zipped_divide + slice).
+//
+// Built only where /root/reference exists (oracle/Makefile target `dropin`), run on the GPU box as a prebuilt
+// binary by tests/test_dropin_gpu.py.
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tla/tla.hpp"
+#include "tla/device.hpp"
+
+using namespace tla;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                          \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);      \
+            ++g_fail;                                                        \
+        }                                                                    \
+    } while (0)
+#define CUDA_OK(e) do { cudaError_t err__ = (e); if (err__ != cudaSuccess) { std::printf("CUDA %s\n", cudaGetErrorString(err__)); return 2; } } while (0)
+
+template <class T> struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    explicit DevBuf(const std::vector<T>& h) : n(h.size()) {
+        cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+        cudaMemcpy(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice);
+    }
+    ~DevBuf() { cudaFree(p); }
+    std::vector<T> get() const {
+        std::vector<T> h(n);
+        cudaMemcpy(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost);
+        return h;
+    }
+};
+
+static Layout L(const char* s) { return parse_layout(s); }
+
+static uint16_t to_bf16(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return static_cast<uint16_t>((u + 0x7fff + ((u >> 16) & 1)) >> 16);
+}
+
+static void copy_pairs() {
+    struct Row { const char* src; const char* dst; };
+    for (Row row : {Row{"8:1", "8:1"}, Row{"(8,2,3):(1,16,32)", "(8,2,3):(1,16,32)"}, Row{"(2,3,2):(42,1,128)", "12:1"},
+                    Row{"12:1", "(2,3,2):(42,1,128)"}, Row{"7:0", "7:1"}, Row{"7:0", "7:0"},
+                    Row{"(8,3):(1,8)", "(8,3):(3,1)"}, Row{"(8,(3,5)):(1,(57,8))", "(8,15):(1,8)"},
+                    Row{"(256,128):(128,1)", "(256,128):(1,256)"}}) {
+        Layout src_l = L(row.src), dst_l = L(row.dst);
+        auto src_store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(src_l)));
+        std::iota(src_store->begin(), src_store->end(), 0);
+        auto dst_store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(dst_l)), -1);
+        copy(Tensor(Accessor::buffer(src_store), src_l), Tensor(Accessor::buffer(dst_store), dst_l)); // reference
+        DevBuf<Int> ds(*src_store), dd(std::vector<Int>(dst_store->size(), -1));
+        copy(DeviceTensor(ds.p, Int(ds.n), 8, src_l), DeviceTensor(dd.p, Int(dd.n), 8, dst_l));        // device
+        cudaDeviceSynchronize();
+        CHECK(dd.get() == *dst_store);
+    }
+    // size mismatch -> contract_error, exactly like the reference (test_tensor.cpp:113-118)
+    DevBuf<Int> s(std::vector<Int>(8, 0));
+    bool threw = false;
+    try { copy(DeviceTensor(s.p, 8, 8, L("8:1")), DeviceTensor(s.p, 8, 8, L("4:1"))); } catch (const contract_error&) { threw = true; }
+    CHECK(threw);
+    // out of bounds -> bounds_error (test_tensor.cpp:34-40)
+    threw = false;
+    try { copy(DeviceTensor(s.p, 8, 8, L("4:3")), DeviceTensor(s.p, 8, 8, L("4:1"))); } catch (const bounds_error&) { threw = true; }
+    CHECK(threw);
+}
+
+// local_tile: slice(Tensor(acc, zipped_divide(L, tiler)), (_, blk)) (partition_demo.cpp) on device:
+// copy tile (3,5) of a 512x512 row-major matrix into a compact tile buffer and compare with the reference copy.
+static void local_tile_copy() {
+    Layout full = L("(512,512):(512,1)");
+    Layout divided = zipped_divide(full, parse_tiler("[128,64]"));
+    auto store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(full)));
+    std::iota(store->begin(), store->end(), 7);
+    Tensor whole(Accessor::buffer(store), divided);
+    std::size_t pos = 0;
+    (void)pos;
+    std::vector<SliceCoord> blk{fix(3), fix(5)};
+    std::vector<SliceCoord> sc{keep(), SliceCoord(blk)};
+    Tensor tile = slice(whole, SliceCoord(sc));
+    Layout compact = L("(128,64):(1,128)");
+    auto out = std::make_shared<std::vector<Int>>(128 * 64, -1);
+    copy(tile, Tensor(Accessor::buffer(out), compact));                                                // reference
+    DevBuf<Int> dsrc(*store), ddst(std::vector<Int>(128 * 64, -1));
+    copy(DeviceTensor(dsrc.p, Int(dsrc.n), 8, tile.layout(), tile.accessor().position()),
+         DeviceTensor(ddst.p, 128 * 64, 8, compact));                                                  // device
+    cudaDeviceSynchronize();
+    CHECK(ddst.get() == *out);
+}
+
+static void gemm_family(const Layout& la, const Layout& lb, const Layout& lc, bool also_bf16) {
+    Int m = size(la.shape()[0]), n = size(lb.shape()[0]), k = size(la.shape()[1]);
+    auto a = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(la)), 0);
+    auto b = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(lb)), 0);
+    auto c = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(lc)), 3);
+    Tensor ta(Accessor::buffer(a), la), tb(Accessor::buffer(b), lb), tc(Accessor::buffer(c), lc);
+    auto pc = [](Int x, Int y) { std::vector<Coord> v; v.emplace_back(x); v.emplace_back(y); return Coord(std::move(v)); };
+    for (Int i = 0; i < m; ++i) for (Int p = 0; p < k; ++p) ta.store(pc(i, p), (i * 7 + p * 3 + 1) % 11);
+    for (Int j = 0; j < n; ++j) for (Int p = 0; p < k; ++p) tb.store(pc(j, p), (j * 5 + p * 2 + 2) % 13);
+    std::vector<Int> c0 = *c;
+    DevBuf<Int> da(*a), db(*b), dc(c0);
+    gemm(DeviceTensor(da.p, Int(da.n), 8, la), DeviceTensor(db.p, Int(db.n), 8, lb), DeviceTensor(dc.p, Int(dc.n), 8, lc));
+    cudaDeviceSynchronize();
+    gemm(ta, tb, tc);                                                                                   // reference
+    CHECK(dc.get() == *c);
+    if (also_bf16) {
+        std::vector<uint16_t> ha(a->size()), hb(b->size());
+        for (size_t i = 0; i < ha.size(); ++i) ha[i] = to_bf16(float((*a)[i]));
+        for (size_t i = 0; i < hb.size(); ++i) hb[i] = to_bf16(float((*b)[i]));
+        std::vector<float> hc(c0.size());
+        for (size_t i = 0; i < hc.size(); ++i) hc[i] = float(c0[i]);
+        DevBuf<uint16_t> fa(ha), fb(hb);
+        DevBuf<float> fc(hc);
+        gemm(DeviceTensor(fa.p, Int(fa.n), 2, la), DeviceTensor(fb.p, Int(fb.n), 2, lb), DeviceTensor(fc.p, Int(fc.n), 4, lc));
+        cudaDeviceSynchronize();
+        std::vector<float> got = fc.get();
+        bool same = true;
+        for (size_t i = 0; i < got.size(); ++i) same = same && (Int(got[i]) == (*c)[i]) && (float(Int(got[i])) == got[i]);
+        CHECK(same); // integer fills: fp32 accumulation is exact, must equal the checked-int64 reference
+    }
+}
+
+static void gemm_families() {
+    gemm_family(L("(4,8):(1,9)"), L("(6,8):(1,10)"), L("(4,6):(1,7)"), true);                 // NT
+    gemm_family(L("(4,8):(9,1)"), L("(6,8):(10,1)"), L("(4,6):(1,7)"), true);                 // TN
+    gemm_family(L("(6,8):(1,10)"), L("(4,8):(1,9)"), L("(6,4):(1,7)"), true);                 // NTT
+    gemm_family(L("(4,8):(3,13)"), L("(6,8):(2,17)"), L("(4,6):(5,23)"), true);               // BLIS
+    gemm_family(L("((2,2),8):((1,16),2)"), L("(6,8):(8,1)"), L("((2,2),6):((1,3),52)"), true); // GETT
+    gemm_family(L("(256,128):(128,1)"), L("(512,128):(128,1)"), L("(256,512):(1,256)"), true); // TN on tcgen05
+    DevBuf<Int> s(std::vector<Int>(64, 1));
+    bool threw = false;
+    try {
+        gemm(DeviceTensor(s.p, 64, 8, L("(4,8):(1,4)")), DeviceTensor(s.p, 64, 8, L("(6,8):(1,6)")),
+             DeviceTensor(s.p, 64, 8, L("(4,5):(1,4)")));
+    } catch (const contract_error&) { threw = true; }
+    CHECK(threw);                                                                              // test_tensor.cpp:197-203
+}
+
+static void index_maps() {
+    for (const char* t : {"((2,2),(4,2)):((1,8),(2,16))", "(8,8):(f1,f9)", "(4,8):(-1,4)", "(3,5,7):(35,7,1)"}) {
+        Layout l = L(t);
+        Int n = size(l) + 3;
+        DevBuf<Int> out(std::vector<Int>(static_cast<size_t>(n), -1));
+        eval_range(l, 0, n, out.p);
+        cudaDeviceSynchronize();
+        std::vector<Int> got = out.get();
+        bool same = true;
+        for (Int i = 0; i < n; ++i) {
+            StrideElem v = layout_eval(l, i);
+            Int want = v.is_zero() ? 0 : (v.is_xor() ? v.mask() : v.value());
+            same = same && got[static_cast<size_t>(i)] == want;
+        }
+        CHECK(same);
+    }
+    // config C5 in small: R = right_inverse(zipped_divide(...)) tabulated on device, L(R(k)) == k checked on host
+    Layout Ld = zipped_divide(L("(256,256):(256,1)"), parse_tiler("[32,16]"));
+    Layout R = right_inverse(Ld);
+    Int n = size(R);
+    DevBuf<Int> out(std::vector<Int>(static_cast<size_t>(n), -1));
+    eval_range(R, 0, n, out.p);
+    cudaDeviceSynchronize();
+    std::vector<Int> r = out.get();
+    bool ok = true;
+    for (Int k = 0; k < n; ++k) ok = ok && eval_int(Ld, r[static_cast<size_t>(k)]) == k;
+    CHECK(ok);
+}
+
+int main() {
+    int ndev = 0;
+    CUDA_OK(cudaGetDeviceCount(&ndev));
+    copy_pairs();
+    local_tile_copy();
+    gemm_families();
+    index_maps();
+    if (g_fail) std::printf("dropin: %d check(s) FAILED\n", g_fail);
+    else std::printf("dropin: all checks passed (launches=%llu)\n", (unsigned long long)tlb_launch_count());
+    return g_fail ? 1 : 0;
+}
