@@ -54,8 +54,8 @@ enum { EPI_REGS = 0, EPI_TMA = 1 };
 constexpr uint32_t kEpiChunkBytes = BM * 32 * 4; // 16 KiB
 
 template <int CG, int EPI> struct Cfg {
-    static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : (CG == 1 ? 1 : 2); // staging buffers per column half
-    static constexpr int kStages = EPI == EPI_REGS ? (CG == 1 ? 4 : 7) : (CG == 1 ? 4 : 5);
+    static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : 1; // staging buffers per column half
+    static constexpr int kStages = EPI == EPI_REGS ? (CG == 1 ? 4 : 7) : (CG == 1 ? 4 : 6);
     static constexpr int kBRows = CG == 1 ? BN : BN / 2; // rows of B this CTA stages
     static constexpr uint32_t kABytes = BM * BK * 2;
     static constexpr uint32_t kBBytes = kBRows * BK * 2;
@@ -127,6 +127,35 @@ __device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const void* map, u
         "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
         "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+}
+// L2 eviction-priority policies for the per-tensor cache hints.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const void* map, uint32_t bar, int c0, int c1, int c2, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm_hint(uint32_t dst, const void* map, uint32_t leader_bar, int c0, int c1, int c2,
+                                                     uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d_hint(const void* map, uint32_t src, int c0, int c1, int c2, uint64_t pol) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(map),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+                 : "memory");
 }
 // C += staged chunk, performed by the TMA unit / L2 (fp32 add, element type from the tensor map).
 __device__ __forceinline__ void tma_reduce_add_3d(const void* map, uint32_t src, int c0, int c1, int c2) {
@@ -235,6 +264,7 @@ struct UmmaArgs {
     uint32_t work_end;             // unit_begin + n_split_units * split + (units - n_split_units)
     int32_t c_vec;                 // register epilogue: C rows are n-contiguous and 16-byte aligned
     uint32_t backoff_ns;           // nanosleep between barrier probes of the idle roles (0 = spin)
+    uint32_t hints;                // L2 cache hints: 1 = operand loads evict_last, 2 = C reductions evict_first
     uint32_t debug;                // TLB_GEMM_DEBUG timing experiments (results are garbage): 1 = no TMA loads after
                                    // the ring is filled once, 2 = epilogue without smem / global traffic,
                                    // 4 = no staging stores, 8 = no TMA store
@@ -346,6 +376,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         uint32_t phase = 0;
         bool ring_filled = false;
         const uint32_t lbar0 = CG == 2 ? map_to_cta(full_bar(0), 0) : full_bar(0);
+        const uint64_t pol_ab = policy_evict_last();
+        const bool hint_ab = (args.hints & 1u) != 0;
         for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
             uint32_t u, batch, m_tile, n_blk;
             int kb0, kb1;
@@ -364,15 +396,25 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
                     } else if constexpr (CG == 1) {
                         mbar_expect_tx(full_bar(stage), C::kStageBytes);
-                        tma_load_3d(a_stage(stage), &map_a, full_bar(stage), kb * BK, m0, batch);
-                        tma_load_3d(b_stage(stage), &map_b, full_bar(stage), kb * BK, n0, batch);
+                        if (hint_ab) {
+                            tma_load_3d_hint(a_stage(stage), &map_a, full_bar(stage), kb * BK, m0, batch, pol_ab);
+                            tma_load_3d_hint(b_stage(stage), &map_b, full_bar(stage), kb * BK, n0, batch, pol_ab);
+                        } else {
+                            tma_load_3d(a_stage(stage), &map_a, full_bar(stage), kb * BK, m0, batch);
+                            tma_load_3d(b_stage(stage), &map_b, full_bar(stage), kb * BK, n0, batch);
+                        }
                     } else {
                         // The leader's barrier expects the bytes of BOTH CTAs; the peer's TMA may complete before
                         // this expect_tx is issued (tx-count goes transiently negative, as with multicast).
                         const uint32_t lbar = lbar0 + 8u * stage;
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
-                        tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
-                        tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, n0, batch);
+                        if (hint_ab) {
+                            tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
+                            tma_load_3d_2sm_hint(b_stage(stage), &map_b, lbar, kb * BK, n0, batch, pol_ab);
+                        } else {
+                            tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
+                            tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, n0, batch);
+                        }
                     }
                 }
                 __syncwarp();
@@ -435,6 +477,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             // ---- TMEM -> registers -> swizzled smem chunk -> cp.reduce.async.bulk.tensor (C += chunk)
             const bool issuer = (warp & 3) == 0 && lane == 0; // one thread per column half
             const uint32_t bar_id = 1 + half;
+            const uint64_t pol_c = policy_evict_first();
+            const bool hint_c = (args.hints & 2u) != 0;
             uint32_t chunk_no = 0;
             for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
                 uint32_t u, batch, m_tile, n_blk;
@@ -479,7 +523,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     fence_async_smem();
                     named_bar(bar_id, 128);
                     if (issuer && !(args.debug & (2u | 8u))) {
-                        tma_reduce_add_3d(&map_c, buf, nbase + ci * 32, m0, batch);
+                        if (hint_c) tma_reduce_add_3d_hint(&map_c, buf, nbase + ci * 32, m0, batch, pol_c);
+                        else tma_reduce_add_3d(&map_c, buf, nbase + ci * 32, m0, batch);
                         bulk_commit();
                     }
                 }
@@ -487,7 +532,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 acc ^= 1u;
                 if (acc == 0) acc_phase ^= 1u;
             }
-            if (issuer) bulk_wait_all(); // every reduction performed before the CTA (and its smem) goes away
+            // the staging buffers must have been read before the CTA (and its smem) goes away; the reductions
+            // themselves complete asynchronously and are ordered before the end of the grid
+            if (issuer) bulk_wait_read<0>();
         } else {
             // ---- register epilogue: C loaded a chunk ahead, added, stored (any strides)
             for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
@@ -655,6 +702,8 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
         a.backoff_ns = e ? static_cast<uint32_t>(std::atoi(e)) : 100u;
         const char* d = std::getenv("TLB_GEMM_DEBUG");
         a.debug = d ? static_cast<uint32_t>(std::atoi(d)) : 0u;
+        const char* h = std::getenv("TLB_GEMM_HINTS");
+        a.hints = h ? static_cast<uint32_t>(std::atoi(h)) : 0u;
     }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
