@@ -376,6 +376,36 @@ def other_configs(torch, dist, world, lib, host, pk, K, W):
                      {"steps": steps5, "evals_per_s": chunk * steps5 * world / sec}))
     del buf
     torch.cuda.empty_cache()
+    # C4: batched bf16 GEMM 64 x 8192^3, sharded by whole batches (= tile-id ranges) across the ranks (strong
+    # scaling of the 64 batches; every rank owns its batches' operands, no data-path collective)
+    from paper_2603_02298_b200 import shard
+    M = 8192
+    rank = dist.get_rank() if world > 1 else 0
+    b0, b1 = shard.batch_range(64, world, rank)
+    nb = b1 - b0
+    a = torch.empty(nb * M * M, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+    b = torch.empty(nb * M * M, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+    c = torch.zeros(nb * M * M, dtype=torch.float32, device="cuda")
+    ta = host.tensor_of(f"({M},{M}):({M},1)", a.view(torch.int16), ranked=True)
+    tb = host.tensor_of(f"({M},{M}):({M},1)", b.view(torch.int16), ranked=True)
+    tc = host.tensor_of(f"({M},{M}):(1,{M})", c, ranked=True)
+    k4 = 3
+    sec = timed(torch, dist, world, lambda i: host.gemm_bf16_batched(ta, tb, tc, M * M, M * M, M * M, 0, nb), k4, 3)
+    flops = 2.0 * M * M * M * 64
+    tf = flops * k4 / sec / 1e12
+    per_gpu = 2.0 * M * M * M * nb / (sec / k4) / 1e12
+    sustained = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    out.append({"name": "C4", "metric": "gemm_tflops", "value": tf, "unit": "TFLOP/s", "ms_per_step": sec / k4 * 1e3,
+                "steps": k4, "scaling": "strong",
+                "config": {"workload": "batched bf16 GEMM 64 x (8192^3), fp32 accumulate, batches sharded across ranks (configs[3])",
+                           "batches_this_rank": nb, "plan": lib.tlb_last_plan().decode()},
+                "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": sustained, "unit": "TFLOP/s",
+                             "frac": per_gpu / sustained, "traffic": traffic_for("C4"), "kernel": "umma_gemm_kernel",
+                             "peak_source": f"{pk['_source']} sustained cuBLAS bf16 (step >= 50 ms)",
+                             "frac_of_nominal_2250": per_gpu / 2250.0,
+                             "algorithmic_flop_per_launch": 2.0 * M * M * M * nb}})
+    del a, b, c
+    torch.cuda.empty_cache()
     return out
 
 

@@ -258,6 +258,7 @@ struct UmmaArgs {
     int64_t cs_m, cs_n, c_bs;
     int32_t M, N, K;
     uint32_t mb, nb;               // 256x256 blocks along m and n
+    uint32_t group_m;              // m-blocks per rasterisation group (L2 reuse of the A panel)
     uint32_t unit_begin, unit_end; // CG=1: 128x256 tile ids; CG=2: 256x256 block ids (all batches)
     uint32_t n_split_units;        // the LAST n_split_units units of the range are split along K ...
     uint32_t split;                // ... into `split` slices each; the slices are scheduled first
@@ -305,10 +306,10 @@ __device__ __forceinline__ void decode_unit(const UmmaArgs& a, uint32_t unit, ui
     const uint32_t half = CG == 1 ? (unit & 1u) : rank;
     *batch = g / blocks;
     const uint32_t blk = g % blocks;
-    const uint32_t per = kGemmGroupM * a.nb;
+    const uint32_t per = a.group_m * a.nb;
     const uint32_t grp = blk / per, rem = blk % per;
-    const uint32_t gm = min(static_cast<uint32_t>(kGemmGroupM), a.mb - grp * kGemmGroupM);
-    *m_tile = (grp * kGemmGroupM + rem % gm) * 2 + half;
+    const uint32_t gm = min(a.group_m, a.mb - grp * a.group_m);
+    *m_tile = (grp * a.group_m + rem % gm) * 2 + half;
     *n_blk = rem / gm;
 }
 
@@ -407,6 +408,15 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         // The leader's barrier expects the bytes of BOTH CTAs; the peer's TMA may complete before
                         // this expect_tx is issued (tx-count goes transiently negative, as with multicast).
                         const uint32_t lbar = lbar0 + 8u * stage;
+                        if ((args.debug & 16u) && (kb & 1)) {
+                            // timing experiment: 25 % less operand traffic (B reloaded every other k-block only)
+                            if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kABytes);
+                            tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
+                            __syncwarp();
+                            if (stage == C::kStages - 1) ring_filled = true;
+                            if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+                            continue;
+                        }
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
                         if (hint_ab) {
                             tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
@@ -674,6 +684,10 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
     a.K = p.K;
     a.mb = (p.M + 255) / 256;
     a.nb = (p.N + 255) / 256;
+    {
+        const char* e = std::getenv("TLB_GEMM_GROUP_M");
+        a.group_m = e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : static_cast<uint32_t>(kGemmGroupM);
+    }
     a.unit_begin = CG == 1 ? p.tile_begin : p.tile_begin / 2;
     a.unit_end = CG == 1 ? p.tile_end : p.tile_end / 2;
     a.c_vec = (p.cs_n == 1 && p.cs_m % 4 == 0 && p.c_bs % 4 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) ? 1 : 0;

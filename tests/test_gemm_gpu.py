@@ -251,3 +251,32 @@ def test_gemm_host_entry_point():
     tc, kc = host.tensor_of(lc, hc, ranked=True)
     host.gemm_bf16_host((ta, ka), (tb, kb), (tc, kc))
     assert (hc.numpy() == want).all()
+
+
+def test_c4_batched_8192_two_batches_exact():
+    """Config C4 shape (8192^3 per batch, batch strides, TN with m-contiguous C) on 2 of the 64 batches with the
+    reference's integer fills: K = 8192 keeps every partial sum below 2^24 (10 * 12 * 8192 = 983040), so the result
+    must be exact. Checked against the flat restatement on sampled tiles and against an exact fp64 product."""
+    M = N = K = 8192
+    B = 2
+    i = torch.arange(M, device="cuda").view(M, 1)
+    p = torch.arange(K, device="cuda").view(1, K)
+    a1 = ((i * 7 + p * 3 + 1) % 11).to(torch.bfloat16)
+    b1 = ((i * 5 + p * 2 + 2) % 13).to(torch.bfloat16)
+    a = torch.stack([a1, a1.flip(0)]).contiguous()
+    b = torch.stack([b1, b1.flip(0)]).contiguous()
+    c = torch.ones(B, N, M, dtype=torch.float32, device="cuda")
+    ta = host.make_tensor(L(f"({M},{K}):({K},1)").lower(ranked=True), a.data_ptr(), a.numel(), 2)
+    tb = host.make_tensor(L(f"({N},{K}):({K},1)").lower(ranked=True), b.data_ptr(), b.numel(), 2)
+    tc = host.make_tensor(L(f"({M},{N}):(1,{M})").lower(ranked=True), c.data_ptr(), c.numel(), 4)
+    plan = host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 0, B)
+    torch.cuda.synchronize()
+    assert plan == "umma_2sm"
+    for bi in range(B):
+        ref = (a[bi].double() @ b[bi].double().t()).t() + 1.0
+        assert torch.equal(c[bi].double(), ref)
+    an = a[1].view(torch.int16).cpu().numpy().view(np.uint16)
+    bn = b[1].view(torch.int16).cpu().numpy().view(np.uint16)
+    want = np.ones((N, M), dtype=np.float32)
+    ou.orc_gemm_bf16_tn_flat(an.ravel(), K, bn.ravel(), K, want.ravel(), M, M, N, K, 4096, 4104, 8000, 8008)
+    assert (c[1].cpu().numpy()[8000:8008, 4096:4104] == want[8000:8008, 4096:4104]).all()
