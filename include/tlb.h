@@ -164,6 +164,16 @@ int tlb_copy_set_path(int path);
 int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const tlb_layout_desc* tile, int elem_bytes,
                                int swizzle, void* d_base, void* out_tensormap_128B);
 
+/* The TMA dimensions the builder derives (host only): rank, and per dimension its extent, stride (elements) and
+ * box extent, innermost first. Arrays have 5 entries. A tile's TMA coordinate in dimension d is the element
+ * index where the tile starts in that dimension. */
+int tlb_tensormap_describe(const tlb_layout_desc* parent, const tlb_layout_desc* tile, int32_t* rank, uint64_t* dims5,
+                           uint64_t* strides5, uint32_t* box5);
+/* Validation aid: fetches ONE box at `coords` through the tensor map into shared memory and writes its
+ * box_bytes bytes to d_out de-swizzled (dimension 0 fastest). swizzle must be the mode the map was built with. */
+int tlb_tensormap_fetch_tile(const void* tensormap_128B, int rank, const int32_t* coords, uint32_t box_bytes, int swizzle,
+                             void* d_out, void* stream);
+
 /* ---- (5) tiled GEMM (configs C2, C4) ----------------------------------- */
 /* tla::gemm(A, B, C) (tensor.hpp:214-233): C(m,n) += sum_k A(m,k) * B(n,k), all rank 2.
  * bf16 x bf16 -> fp32, accumulator starts from C. tile_begin/tile_end select a range of the

@@ -65,6 +65,10 @@ SYMBOLS = {
     "tlb_copy_set_path": (C.c_int, [C.c_int]),
     "tlb_tensormap_from_divided": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p]),
+    "tlb_tensormap_describe": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(C.c_int32), _P(C.c_uint64),
+                                         _P(C.c_uint64), _P(C.c_uint32)]),
+    "tlb_tensormap_fetch_tile": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_int32), C.c_uint32, C.c_int, C.c_void_p,
+                                           C.c_void_p]),
     "tlb_gemm_bf16": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_uint32, C.c_uint32, C.c_void_p]),
     "tlb_gemm_tile_count": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), _P(C.c_uint32)]),
     "tlb_gemm_bf16_batched": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_int64, C.c_int64, C.c_int64,

@@ -21,8 +21,11 @@
 //
 // All contract / bounds / overflow checks happen on the host before any launch.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cuda.h>
 
 #include "tlb_internal.h"
 
@@ -31,6 +34,15 @@ namespace {
 
 thread_local int g_copy_path = 0; // 0 auto, 1 gather, 2 tiled (LDG), 3 tiled TMA
 thread_local bool g_dry_run = false; // tlb_copy_plan: run the planner, launch nothing
+
+// TLB_COPY_TMA=1 makes the TMA-fed tiled kernel the default for layouts that admit a tensor map.
+bool tma_default() {
+    static const bool on = [] {
+        const char* e = std::getenv("TLB_COPY_TMA");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 constexpr int kThreads = 256;
 
@@ -179,14 +191,41 @@ struct TileParams {
 // with the row index mod 8 == Swizzle<3,4,3> on the byte offset r*128 + c*16.
 __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return (r << 7) | ((c ^ (r & 7u)) << 4); }
 
+// phase 2 of the tiled copy: each lane owns V x V element blocks; conflict-free 128-bit smem reads, register
+// transpose, 128-bit stores along B (lanes sharing a chunk cover 32 consecutive b).
+template <int EB, int LB>
+__device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int64_t* s_offA, char* __restrict__ dst,
+                                            int64_t base_d) {
+    using T = typename Cell<EB>::type;
+    constexpr int V = 16 / EB;
+    constexpr int LOGV = (V == 2) ? 1 : (V == 4) ? 2 : 3;
+    constexpr int NR = 3 - LOGV;
+    constexpr int CW = 8 >> NR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & 7, p = lane >> 3;
+    const int bb = (q & ((1 << NR) - 1)) | (p << NR);
+    const int cl = q >> NR;
+    constexpr int GROUPS = 1 << NR;                    // warp-tiles per 128 B of A
+    constexpr int NWT = GROUPS * (LB / 32);
+    for (int wt = warp; wt < NWT; wt += kThreads / 32) {
+        const int c = (wt % GROUPS) * CW + cl;
+        const int r0 = (wt / GROUPS) * 32 + bb * V;
+        union { uint4 v; T e[V]; } in[V], out;
+#pragma unroll
+        for (int j = 0; j < V; ++j) in[j].v = *reinterpret_cast<const uint4*>(tile + swz(r0 + j, c));
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
+            stg_stream(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+        }
+    }
+}
+
 template <int EB, int LB>
 __global__ void __launch_bounds__(kThreads)
 tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src, char* __restrict__ dst) {
-    using T = typename Cell<EB>::type;
     constexpr int V = 16 / EB;                         // elements per 16-byte vector
-    constexpr int LOGV = (V == 2) ? 1 : (V == 4) ? 2 : 3;
-    constexpr int NR = 3 - LOGV;                       // row bits a lane octet contributes
-    constexpr int CW = 8 >> NR;                        // chunks a warp-tile spans (V)
     constexpr int LA = 128 / EB;                       // elements of A per row
     __shared__ __align__(1024) unsigned char tile[LB * 128];
     __shared__ int64_t s_offB[LB];                     // source offset of row b
@@ -233,26 +272,107 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
     }
     __syncthreads();
 
-    // phase 2: each lane owns V x V element blocks; conflict-free 128-bit smem reads,
-    // register transpose, 128-bit stores along B (lanes sharing a chunk cover 32 consecutive b).
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q = lane & 7, p = lane >> 3;
-    const int bb = (q & ((1 << NR) - 1)) | (p << NR);
-    const int cl = q >> NR;
-    constexpr int GROUPS = 1 << NR;                    // warp-tiles per 128 B of A
-    constexpr int NWT = GROUPS * (LB / 32);
-    for (int wt = warp; wt < NWT; wt += kThreads / 32) {
-        const int c = (wt % GROUPS) * CW + cl;
-        const int r0 = (wt / GROUPS) * 32 + bb * V;
-        union { uint4 v; T e[V]; } in[V], out;
-#pragma unroll
-        for (int j = 0; j < V; ++j) in[j].v = *reinterpret_cast<const uint4*>(tile + swz(r0 + j, c));
-#pragma unroll
-        for (int i = 0; i < V; ++i) {
-#pragma unroll
-            for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
-            stg_stream(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+    tile_phase2<EB, LB>(tile, s_offA, dst, base_d);
+}
+
+// ---------------------------------------------------------------------------------------
+// tiled, TMA-fed: phase 1 is a cp.async.bulk.tensor load through a tensor map derived from the source layout
+// (tlb_tensormap_describe: parent = the source's refined modes, tile = the A and B runs) with the hardware
+// 128-byte swizzle, which is the staging layout phase 2 already expects. Each CTA walks kTmaTilesPerCta
+// consecutive tiles through a ring of kTmaStages staged tiles, so loads run several tiles ahead of the stores.
+// ---------------------------------------------------------------------------------------
+constexpr int kTmaStages = 4;
+constexpr int kTmaTilesPerCta = 8;
+
+struct TmaTileParams {
+    TileParams t;
+    int32_t ndim;
+    int32_t pad_;
+    int64_t dim_stride[5]; // source strides (elements) of the TMA dimensions, innermost first
+};
+
+__device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, uint32_t dst, uint32_t bar, int ndim, const int* c) {
+    switch (ndim) {
+    case 2:
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]) : "memory");
+        break;
+    case 3:
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]) : "memory");
+        break;
+    case 4:
+        asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+        break;
+    default:
+        asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+        break;
+    }
+}
+
+template <int EB, int LB>
+__global__ void __launch_bounds__(kThreads)
+tiled_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ TmaTileParams P, char* __restrict__ dst) {
+    constexpr int LA = 128 / EB;
+    constexpr uint32_t kTileBytes = LB * 128;
+    extern __shared__ unsigned char smem_dyn[];
+    __shared__ int64_t s_offA[LA];
+    __shared__ int64_t s_base_d[kTmaStages];
+    __shared__ __align__(8) unsigned long long s_bar[kTmaStages];
+    const uint32_t smem0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn)) + 1023u) & ~1023u;
+    unsigned char* tiles = smem_dyn + (smem0 - static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn)));
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kTmaTilesPerCta;
+    const int count = static_cast<int>(min(static_cast<uint64_t>(kTmaTilesPerCta), P.t.n_tiles - t0));
+
+    auto issue = [&](int i) { // thread 0 only: tile t0 + i -> stage i % kTmaStages
+        const int stage = i % kTmaStages;
+        int64_t base_s, base_d;
+        dev_joint(P.t.rest, t0 + i, &base_s, &base_d);
+        s_base_d[stage] = base_d;
+        int c[5];
+        int64_t off = base_s;
+        for (int d = P.ndim - 1; d >= 1; --d) {
+            const int64_t q = off / P.dim_stride[d];
+            c[d] = static_cast<int>(q);
+            off -= q * P.dim_stride[d];
         }
+        c[0] = static_cast<int>(off);
+        const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[stage]));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kTileBytes) : "memory");
+        tma_issue_tile(&map, smem0 + stage * kTileBytes, bar, P.ndim, c);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[s]))) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < min(count, kTmaStages); ++i) issue(i);
+    }
+    for (int t = threadIdx.x; t < LA; t += kThreads) {
+        uint32_t i = t;
+        int64_t acc = 0;
+        for (int p = 0; p < P.t.nA; ++p) {
+            const uint32_t e = static_cast<uint32_t>(P.t.eA[p]);
+            const uint32_t c = (p + 1 < P.t.nA) ? i % e : i;
+            i /= e;
+            acc += static_cast<int64_t>(c) * P.t.dA[p];
+        }
+        s_offA[t] = acc;
+    }
+    __syncthreads();
+
+    for (int i = 0; i < count; ++i) {
+        const int stage = i % kTmaStages;
+        const uint32_t parity = (i / kTmaStages) & 1;
+        const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[stage]));
+        const long long t_start = clock64();
+        for (;;) {
+            uint32_t ok;
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+            if (ok) break;
+            if (clock64() - t_start > 4000000000ll) __trap();
+        }
+        tile_phase2<EB, LB>(tiles + stage * kTileBytes, s_offA, dst, s_base_d[stage]);
+        __syncthreads(); // every lane is done reading this stage
+        if (threadIdx.x == 0 && i + kTmaStages < count) issue(i + kTmaStages);
     }
 }
 
@@ -567,13 +687,80 @@ int try_planned(const CopyCall& c, bool* done) {
         for (const JM& m : rest) tiles *= static_cast<uint64_t>(m.e);
         P.n_tiles = tiles;
         if (tiles > 0x7fffffffull) return TLB_OK;
+        const char* sb = sp + base_s * eb;
+        char* db = dp + base_d * eb;
+        // ---- TMA-fed variant: tensor map derived from the source's refined modes (parent) and the A / B runs (tile)
+        if (g_copy_path == 3 || (g_copy_path == 0 && tma_default())) {
+            bool tma_ok = true;
+            for (size_t r = 0; r + 1 < B.size(); ++r) tma_ok = tma_ok && B[r].ss < B[r + 1].ss; // smem row order == b order
+            tlb_layout_desc parent, tdesc;
+            std::memset(&parent, 0, sizeof(parent));
+            std::memset(&tdesc, 0, sizeof(tdesc));
+            parent.kind = tdesc.kind = TLB_KIND_INT;
+            tma_ok = tma_ok && modes.size() <= TLB_MAX_MODES && A.size() + B.size() <= TLB_MAX_MODES;
+            if (tma_ok) {
+                parent.n_modes = static_cast<int>(modes.size());
+                for (size_t r = 0; r < modes.size(); ++r) { parent.extent[r] = modes[r].e; parent.stride[r] = modes[r].ss; }
+                int nt = 0;
+                for (const JM& m : A) { tdesc.extent[nt] = m.e; tdesc.stride[nt++] = m.ss; }
+                for (const JM& m : B) { tdesc.extent[nt] = m.e; tdesc.stride[nt++] = m.ss; }
+                tdesc.n_modes = nt;
+                int32_t rank = 0;
+                uint64_t dims[5], strides[5];
+                uint32_t box[5];
+                uint64_t rows = 1;
+                tma_ok = tlb_tensormap_describe(&parent, &tdesc, &rank, dims, strides, box) == TLB_OK && rank >= 2 &&
+                         box[0] == static_cast<uint32_t>(La);
+                for (int d2 = 1; tma_ok && d2 < rank; ++d2) rows *= box[d2];
+                tma_ok = tma_ok && rows == static_cast<uint64_t>(Lb);
+                for (int d2 = 0; tma_ok && d2 < rank; ++d2) tma_ok = dims[d2] < (1ull << 32);
+                for (int d2 = 1; tma_ok && d2 < rank; ++d2) tma_ok = (strides[d2] * static_cast<uint64_t>(eb)) % 16 == 0;
+                if (tma_ok && g_dry_run) {
+                    set_plan("tiled_tma");
+                    *done = true;
+                    return TLB_OK;
+                }
+                alignas(64) unsigned char mapbytes[128];
+                if (tma_ok)
+                    tma_ok = tlb_tensormap_from_divided(&parent, &tdesc, eb, TMA_SW_128, const_cast<char*>(sb), mapbytes) == TLB_OK;
+                if (tma_ok) {
+                    TmaTileParams TP;
+                    std::memset(&TP, 0, sizeof(TP));
+                    TP.t = P;
+                    TP.ndim = rank;
+                    for (int d2 = 0; d2 < 5; ++d2) TP.dim_stride[d2] = d2 < rank ? static_cast<int64_t>(strides[d2]) : 1;
+                    CUtensorMap map;
+                    std::memcpy(&map, mapbytes, 128);
+                    const unsigned grid_tma = static_cast<unsigned>((tiles + kTmaTilesPerCta - 1) / kTmaTilesPerCta);
+                    const size_t smem = static_cast<size_t>(kTmaStages) * Lb * 128 + 1024;
+#define TLB_TILED_TMA(EB, LB)                                                                                          \
+    do {                                                                                                               \
+        TLB_CUDA(cudaFuncSetAttribute(tiled_tma_kernel<EB, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
+        tiled_tma_kernel<EB, LB><<<grid_tma, kThreads, smem, c.stream>>>(map, TP, db);                                 \
+    } while (0)
+                    if (eb == 4) {
+                        if (Lb == 128) TLB_TILED_TMA(4, 128); else if (Lb == 64) TLB_TILED_TMA(4, 64); else TLB_TILED_TMA(4, 32);
+                    } else if (eb == 8) {
+                        if (Lb == 128) TLB_TILED_TMA(8, 128); else if (Lb == 64) TLB_TILED_TMA(8, 64); else TLB_TILED_TMA(8, 32);
+                    } else {
+                        if (Lb == 128) TLB_TILED_TMA(2, 128); else if (Lb == 64) TLB_TILED_TMA(2, 64); else TLB_TILED_TMA(2, 32);
+                    }
+#undef TLB_TILED_TMA
+                    count_launch();
+                    TLB_CUDA(cudaGetLastError());
+                    set_plan("tiled_tma");
+                    *done = true;
+                    return TLB_OK;
+                }
+            }
+            (void)cudaGetLastError();
+            if (g_copy_path == 3) return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the source layout has no TMA tensor map for this tiling");
+        }
         if (g_dry_run) {
             set_plan("tiled");
             *done = true;
             return TLB_OK;
         }
-        const char* sb = sp + base_s * eb;
-        char* db = dp + base_d * eb;
         const unsigned grid = static_cast<unsigned>(tiles);
 #define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
         if (eb == 4) {

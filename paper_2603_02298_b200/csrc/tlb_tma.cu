@@ -79,21 +79,42 @@ int tma_encode(TmaDesc* out, int dtype_bytes, bool is_float, int rank, void* bas
 
 using namespace tlb;
 
-// Public builder: parent = full layout (Int kind, non-negative strides), tile = the tile mode
-// of zipped_divide(parent, tiler). The parent is coalesced into TMA dimensions sorted by
-// stride (dimension 0 must have stride 1); every tile leaf must lie inside exactly one of them
-// (its stride a multiple of the dimension's, staying inside the dimension's extent), and
-// contributes extent -> boxDim, stride/dim_stride -> elementStrides.
-extern "C" int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const tlb_layout_desc* tile, int elem_bytes,
-                                          int swizzle, void* d_base, void* out_tensormap_128B) {
-    if (!parent || !tile || !out_tensormap_128B) return fail(TLB_ERR_CONTRACT, "tlb_tensormap_from_divided: null argument");
+// Shared derivation: parent = full layout (Int kind, non-negative strides), tile = the tile mode of
+// zipped_divide(parent, tiler). The parent is coalesced into TMA dimensions sorted by stride (dimension 0
+// must have stride 1); every tile leaf must lie inside exactly one of them (its stride a multiple of the
+// dimension's, staying inside the dimension's extent) and contributes its extent to boxDim.
+namespace tlb {
+namespace {
+struct Dim {
+    uint64_t extent, stride;
+    uint32_t box, estride;
+    bool used;
+};
+
+int derive_dims(const tlb_layout_desc* parent, const tlb_layout_desc* tile, std::vector<Dim>* out) {
+    if (!parent || !tile) return fail(TLB_ERR_CONTRACT, "tensor map derivation: null layout");
     if (parent->kind != TLB_KIND_INT || tile->kind != TLB_KIND_INT)
         return fail(TLB_ERR_SEMIMODULE, "tensor maps require integer strides");
     if (parent->flags & TLB_LF_HAS_NEG) return fail(TLB_ERR_UNSUPPORTED, "tensor maps require non-negative strides");
-    if (reinterpret_cast<uintptr_t>(out_tensormap_128B) & 63)
-        return fail(TLB_ERR_CONTRACT, "tensor map storage must be 64-byte aligned");
-    // Parent leaves sorted by stride, merged when contiguous (coalesce, layout.hpp:206, after sorting).
-    struct Dim { uint64_t extent, stride; uint32_t box, estride; bool used; };
+    // Tile leaves sorted by stride and coalesced: each surviving leaf needs a TMA dimension that STARTS at its stride.
+    std::vector<std::pair<uint64_t, uint64_t>> tl; // stride, extent
+    for (int r = 0; r < tile->n_modes; ++r) {
+        if (tile->extent[r] == 1) continue;
+        if (tile->stride[r] <= 0) return fail(TLB_ERR_UNSUPPORTED, "tile leaves must have positive strides");
+        tl.emplace_back(static_cast<uint64_t>(tile->stride[r]), static_cast<uint64_t>(tile->extent[r]));
+    }
+    std::sort(tl.begin(), tl.end());
+    std::vector<std::pair<uint64_t, uint64_t>> tiles;
+    for (auto& [st, ex] : tl) {
+        if (!tiles.empty() && tiles.back().first * tiles.back().second == st) tiles.back().second *= ex;
+        else tiles.emplace_back(st, ex);
+    }
+    auto tile_starts_at = [&](uint64_t st) {
+        for (auto& t : tiles) if (t.first == st) return true;
+        return false;
+    };
+    // Parent leaves sorted by stride, merged when contiguous (coalesce, layout.hpp:206, after sorting) unless a
+    // tile leaf starts there (the box needs that dimension boundary).
     std::vector<std::pair<uint64_t, uint64_t>> leaves; // stride, extent
     for (int r = 0; r < parent->n_modes; ++r)
         if (parent->extent[r] > 1) {
@@ -101,19 +122,15 @@ extern "C" int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const t
             leaves.emplace_back(static_cast<uint64_t>(parent->stride[r]), static_cast<uint64_t>(parent->extent[r]));
         }
     std::sort(leaves.begin(), leaves.end());
-    std::vector<Dim> dims;
+    std::vector<Dim>& dims = *out;
     for (auto& [st, ex] : leaves) {
-        if (!dims.empty() && dims.back().stride * dims.back().extent == st) dims.back().extent *= ex;
+        if (!dims.empty() && dims.back().stride * dims.back().extent == st && !tile_starts_at(st)) dims.back().extent *= ex;
         else dims.push_back({ex, st, 1, 1, false});
     }
     if (dims.empty()) dims.push_back({1, 1, 1, 1, false});
     if (dims[0].stride != 1) return fail(TLB_ERR_UNSUPPORTED, "tensor maps need a stride-1 innermost dimension");
     if (dims.size() > 5) return fail(TLB_ERR_UNSUPPORTED, "layout needs more than 5 TMA dimensions");
-    for (int r = 0; r < tile->n_modes; ++r) {
-        uint64_t e = static_cast<uint64_t>(tile->extent[r]);
-        if (e == 1) continue;
-        if (tile->stride[r] <= 0) return fail(TLB_ERR_UNSUPPORTED, "tile leaves must have positive strides");
-        uint64_t s = static_cast<uint64_t>(tile->stride[r]);
+    for (auto& [s, e] : tiles) {
         Dim* hit = nullptr;
         for (auto it = dims.rbegin(); it != dims.rend(); ++it)
             if (s >= it->stride && s % it->stride == 0) { hit = &*it; break; }
@@ -126,6 +143,60 @@ extern "C" int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const t
         hit->used = true;
     }
     for (auto& d : dims) if (d.estride != 1) return fail(TLB_ERR_UNSUPPORTED, "strided (elementStrides > 1) tiles are not built yet");
+    return TLB_OK;
+}
+
+// One-box fetch used to validate tensor maps: the box lands in shared memory (hardware swizzle as encoded in
+// the map) and is written out de-swizzled, dimension 0 fastest. The de-swizzle is Swizzle<B,4,3> on the byte
+// offset (B = 1, 2, 3 for the 32 / 64 / 128-byte modes), i.e. the reference's Xor layouts (stride.hpp:142).
+template <int RANK>
+__global__ void __launch_bounds__(128) fetch_tile_kernel(const __grid_constant__ CUtensorMap map, int c0, int c1, int c2,
+                                                         int c3, int c4, uint32_t bytes, int swizzle_bits,
+                                                         unsigned char* __restrict__ out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t base = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + 1023u) & ~1023u;
+    const uint32_t bar = base + 32768;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        if constexpr (RANK == 1)
+            asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3}], [%2];" ::"r"(base), "l"(&map), "r"(bar), "r"(c0) : "memory");
+        else if constexpr (RANK == 2)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(base), "l"(&map), "r"(bar), "r"(c0), "r"(c1) : "memory");
+        else if constexpr (RANK == 3)
+            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(base), "l"(&map), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+        else if constexpr (RANK == 4)
+            asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(base), "l"(&map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+        else
+            asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(base), "l"(&map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4) : "memory");
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    for (;;) {
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(bar) : "memory");
+        if (ok) break;
+        if (clock64() - t0 > 4000000000ll) __trap();
+    }
+    const uint32_t xor_mask = (1u << swizzle_bits) - 1u;
+    for (uint32_t o = threadIdx.x; o < bytes; o += blockDim.x) {
+        const uint32_t phys = o ^ (((o >> 7) & xor_mask) << 4);
+        unsigned int v;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(base + phys));
+        out[o] = static_cast<unsigned char>(v);
+    }
+}
+} // namespace
+} // namespace tlb
+
+extern "C" int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const tlb_layout_desc* tile, int elem_bytes,
+                                          int swizzle, void* d_base, void* out_tensormap_128B) {
+    if (!out_tensormap_128B) return fail(TLB_ERR_CONTRACT, "tlb_tensormap_from_divided: null argument");
+    if (reinterpret_cast<uintptr_t>(out_tensormap_128B) & 63)
+        return fail(TLB_ERR_CONTRACT, "tensor map storage must be 64-byte aligned");
+    std::vector<Dim> dims;
+    TLB_TRY(derive_dims(parent, tile, &dims));
     uint64_t gd[5], gs[4];
     uint32_t bx[5];
     for (size_t d = 0; d < dims.size(); ++d) {
@@ -136,5 +207,51 @@ extern "C" int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const t
     TmaDesc tmp;
     TLB_TRY(tma_encode(&tmp, elem_bytes, false, static_cast<int>(dims.size()), d_base, gd, gs, bx, swizzle, 128));
     std::memcpy(out_tensormap_128B, tmp.bytes, 128);
+    return TLB_OK;
+}
+
+extern "C" int tlb_tensormap_describe(const tlb_layout_desc* parent, const tlb_layout_desc* tile, int32_t* rank,
+                                      uint64_t* dims5, uint64_t* strides5, uint32_t* box5) {
+    if (!rank || !dims5 || !strides5 || !box5) return fail(TLB_ERR_CONTRACT, "tlb_tensormap_describe: null output");
+    std::vector<Dim> dims;
+    TLB_TRY(derive_dims(parent, tile, &dims));
+    *rank = static_cast<int32_t>(dims.size());
+    for (size_t d = 0; d < 5; ++d) {
+        dims5[d] = d < dims.size() ? dims[d].extent : 1;
+        strides5[d] = d < dims.size() ? dims[d].stride : 0;
+        box5[d] = d < dims.size() ? dims[d].box : 1;
+    }
+    return TLB_OK;
+}
+
+extern "C" int tlb_tensormap_fetch_tile(const void* tensormap_128B, int rank, const int32_t* coords, uint32_t box_bytes,
+                                        int swizzle, void* d_out, void* stream) {
+    if (!tensormap_128B || !coords || !d_out) return fail(TLB_ERR_CONTRACT, "tlb_tensormap_fetch_tile: null argument");
+    if (rank < 1 || rank > 5) return fail(TLB_ERR_CONTRACT, "tensor maps have rank 1..5");
+    if (box_bytes == 0 || box_bytes > 32768 || (box_bytes & 15)) return fail(TLB_ERR_UNSUPPORTED, "box must be 16..32768 bytes, a multiple of 16");
+    if (swizzle < 0 || swizzle > 3) return fail(TLB_ERR_CONTRACT, "swizzle mode is 0..3");
+    TLB_TRY(require_device());
+    CUtensorMap map;
+    std::memcpy(&map, tensormap_128B, 128);
+    int c[5] = {0, 0, 0, 0, 0};
+    for (int d = 0; d < rank; ++d) c[d] = coords[d];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t smem = 32768 + 1024 + 64;
+    unsigned char* out = static_cast<unsigned char*>(d_out);
+#define TLB_FETCH(R)                                                                                               \
+    do {                                                                                                           \
+        TLB_CUDA(cudaFuncSetAttribute(fetch_tile_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
+        fetch_tile_kernel<R><<<1, 128, smem, s>>>(map, c[0], c[1], c[2], c[3], c[4], box_bytes, swizzle, out);      \
+    } while (0)
+    switch (rank) {
+    case 1: TLB_FETCH(1); break;
+    case 2: TLB_FETCH(2); break;
+    case 3: TLB_FETCH(3); break;
+    case 4: TLB_FETCH(4); break;
+    default: TLB_FETCH(5); break;
+    }
+#undef TLB_FETCH
+    count_launch();
+    TLB_CUDA(cudaGetLastError());
     return TLB_OK;
 }

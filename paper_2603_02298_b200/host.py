@@ -277,3 +277,35 @@ def eval_axes_range(layout: Layout | str, n_axes: int, i0: int, n: int, out, str
     lay = L(layout) if isinstance(layout, str) else layout
     arr = lay.mode_array()
     abi.check(abi.load().tlb_eval_axes_range(arr, len(lay.modes), n_axes, i0, n, out.data_ptr(), _stream_ptr(stream)))
+
+
+def tensormap_describe(parent: Layout | str, tile: Layout | str):
+    """(rank, dims, strides, box) of the TMA dimensions derived from a divided layout (host only)."""
+    lp = (L(parent) if isinstance(parent, str) else parent).lower()
+    lt = (L(tile) if isinstance(tile, str) else tile).lower()
+    rank = C.c_int32(0)
+    dims, strides, box = (C.c_uint64 * 5)(), (C.c_uint64 * 5)(), (C.c_uint32 * 5)()
+    abi.check(abi.load().tlb_tensormap_describe(C.byref(lp), C.byref(lt), C.byref(rank), dims, strides, box))
+    r = rank.value
+    return r, list(dims)[:r], list(strides)[:r], list(box)[:r]
+
+
+def tensormap_fetch(parent: Layout | str, tile: Layout | str, buf, coords, swizzle: int = 0, stream=None):
+    """Builds the tensor map of (parent, tile) over `buf`, fetches the box at `coords` and returns it as a torch
+    uint8 tensor on the device (de-swizzled, dimension 0 fastest)."""
+    import torch
+    lib = abi.load()
+    lp = (L(parent) if isinstance(parent, str) else parent).lower()
+    lt = (L(tile) if isinstance(tile, str) else tile).lower()
+    eb = buf.element_size()
+    raw = C.create_string_buffer(128 + 64)
+    addr = (C.addressof(raw) + 63) & ~63
+    abi.check(lib.tlb_tensormap_from_divided(C.byref(lp), C.byref(lt), eb, swizzle, buf.data_ptr(), addr))
+    rank, dims, strides, box = tensormap_describe(parent, tile)
+    nbytes = eb
+    for b in box:
+        nbytes *= b
+    out = torch.empty(nbytes, dtype=torch.uint8, device=buf.device)
+    cc = (C.c_int32 * 5)(*([int(c) for c in coords] + [0] * (5 - len(coords))))
+    abi.check(lib.tlb_tensormap_fetch_tile(addr, rank, cc, nbytes, swizzle, out.data_ptr(), _stream_ptr(stream)))
+    return out

@@ -62,6 +62,22 @@ def test_copy_tiled_plan(s, d, eb):
         assert plan == "tiled", plan
 
 
+@pytest.mark.parametrize("eb", [2, 4, 8])
+@pytest.mark.parametrize("s,d", [
+    ("(256,128):(128,1)", "(256,128):(1,256)"),
+    ("(128,256):(1,128)", "(128,256):(256,1)"),
+    ("(96,160):(160,1)", "(96,160):(1,96)"),
+    ("((8,128),(4,64),20):((1,2048),(8,32),262144)", "((8,128),(4,64),20):((128,1),(65536,1024),262144)"),  # 20 tiles: ragged last CTA
+    ("(64,64,8):(512,1,64)", "(64,64,8):(1,512,64)"),
+    ("((32,16),(64,4)):((1,32),(512,32768))", "((32,16),(64,4)):((64,8192),(1,2048))"),
+])
+def test_copy_tiled_tma_plan(s, d, eb):
+    """The TMA-fed variant (tensor map derived from the source layout, hardware 128-byte swizzle) is bit-identical."""
+    if s.startswith("(96,160)") and eb == 2:
+        pytest.skip("160 two-byte cells are not a whole number of 128-byte rows")
+    assert run_copy_case(s, d, eb, path=3) == "tiled_tma"
+
+
 def test_copy_interleaved_runs_fall_back_to_gather():
     """The destination-contiguous run continues inside the source-contiguous run: no clean A x B tile."""
     assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4) == "gather"
@@ -204,6 +220,17 @@ def test_c1_transpose_full_size_properties():
     torch.cuda.synchronize()
     # dst viewed as (n,n) row-major must equal src viewed row-major, transposed
     assert torch.equal(dst.view(n, n), src.view(n, n).t())
+    # the TMA-fed variant produces the same bytes
+    dst2 = torch.full((n * n,), -1, dtype=torch.int32, device="cuda")
+    b_t, kb_t = host.tensor_of(d, dst2)
+    abi.load().tlb_copy_set_path(3)
+    try:
+        assert host.copy((a, ka), (b_t, kb_t)) == "tiled_tma"
+    finally:
+        abi.load().tlb_copy_set_path(0)
+    torch.cuda.synchronize()
+    assert torch.equal(dst2, dst)
+    del dst2
     # involution: transposing back restores the source bit for bit
     back = torch.full((n * n,), -1, dtype=torch.int32, device="cuda")
     a2, k2 = host.tensor_of(s, dst)
@@ -242,3 +269,30 @@ def test_c3_permute_full_size_properties():
     host.copy((a2, k2), (b2, k3))
     torch.cuda.synchronize()
     assert torch.equal(back, src)
+
+
+def test_tensormap_from_divided_fetches_the_tile_the_layout_names():
+    """tlb_tensormap_from_divided: the box TMA delivers for tile (i, j) of zipped_divide(parent, tiler) equals the cells
+    the divided layout addresses (oracle evaluation), for every hardware swizzle mode: the de-swizzle is
+    Swizzle<B,4,3> on byte offsets, i.e. the reference's Xor layouts."""
+    import oracle_util as ou
+    parent, tile = "(96,192):(192,1)", "(32,32):(192,1)"      # zipped_divide(parent, [32,32]) tile mode
+    buf = torch.arange(96 * 192, dtype=torch.int32, device="cuda") * 3 + 1
+    hbuf = buf.cpu().numpy()
+    tile_off = ou.orc_eval_range(tile, 0, 32 * 32).reshape(32, 32)      # [col (dim0 of TMA)][row]: colex, mode 0 = rows
+    for (ti, tj) in [(0, 0), (2, 5), (1, 3)]:
+        base = ti * 32 * 192 + tj * 32
+        want = hbuf[base + tile_off].T.copy()                            # TMA box order: dim0 (stride 1) fastest
+        want = hbuf[base + np.arange(32)[None, :] + 192 * np.arange(32)[:, None]]   # [row][col]
+        for swz in (0, 1, 2, 3):
+            got = host.tensormap_fetch(parent, tile, buf, (tj * 32, ti * 32), swizzle=swz)
+            torch.cuda.synchronize()
+            assert (got.cpu().numpy().view(np.int32).reshape(32, 32) == want).all(), (ti, tj, swz)
+    # config C3 source tile: box 32 x 128 (16 KiB) at tile 2, 128-byte swizzle
+    T = 4
+    s3 = f"((8,128),(4,64),{T}):((1,2048),(8,32),262144)"
+    b3 = torch.arange(262144 * T, dtype=torch.int32, device="cuda")
+    got = host.tensormap_fetch(s3, "((8,128),4):((1,2048),8)", b3, (64, 2 * 128), swizzle=3)
+    torch.cuda.synchronize()
+    want = (2 * 262144 + 64 + np.arange(32)[None, :] + 2048 * np.arange(128)[:, None]).astype(np.int32)
+    assert (got.cpu().numpy().view(np.int32).reshape(128, 32) == want).all()

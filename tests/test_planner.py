@@ -52,3 +52,23 @@ def test_plan_contracts():
     src = host.make_tensor(d, C.addressof(buf), 8, 8)                  # 4:3 touches cell 9 of 8
     dst = host.make_tensor(L("4:1").lower(), C.addressof(buf), 8, 8)
     assert lib.tlb_copy_plan(C.byref(src), C.byref(dst), 0, 2**64 - 1) == abi.TLB_ERR_BOUNDS
+
+
+def test_tensormap_dims_from_divided_layouts():
+    """TMA tensor maps are derived from zipped_divide results (algebra.hpp:595): parent flat modes -> globalDim /
+    globalStrides (sorted by stride, contiguous leaves merged), tile mode -> boxDim."""
+    # zipped_divide((4096,4096):(4096,1), [128,64]) = ((128,64),(32,64)):((4096,1),(524288,64))  (SURVEY.md vocabulary)
+    rank, dims, strides, box = host.tensormap_describe("(4096,4096):(4096,1)", "(128,64):(4096,1)")
+    assert (rank, dims, strides, box) == (2, [4096, 4096], [1, 4096], [64, 128])
+    # config C3 source: modes 0,2,3 merge into one contiguous 2048-element dimension
+    rank, dims, strides, box = host.tensormap_describe("((8,128),(4,64),4096):((1,2048),(8,32),262144)",
+                                                       "((8,128),4):((1,2048),8)")
+    assert (rank, dims, strides, box) == (2, [2048, 128 * 4096], [1, 2048], [32, 128])   # rows of all tiles merge too
+    # operands of the GEMM: A (M,K):(K,1) tiled [128,64] -> dims (K, M), box (64, 128)
+    assert host.tensormap_describe("(8192,4096):(4096,1)", "(128,64):(4096,1)")[3] == [64, 128]
+    with pytest.raises(TlbError) as e:
+        host.tensormap_describe("(64,64):(128,2)", "(8,8):(128,2)")          # no stride-1 dimension
+    assert e.value.status == abi.TLB_ERR_UNSUPPORTED
+    with pytest.raises(TlbError) as e:
+        host.tensormap_describe("(8,8):(f1,f9)", "(8,8):(f1,f9)")            # Xor strides
+    assert e.value.status == abi.TLB_ERR_SEMIMODULE
