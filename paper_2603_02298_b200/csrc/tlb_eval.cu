@@ -5,6 +5,8 @@
 // design rule is: one 16-byte coalesced store per thread per step, a grid of a few waves of
 // 148 SMs running a grid-stride loop, and a peel that costs a shift/mask per power-of-two
 // leaf (magic multiply otherwise) so the integer pipe stays far below the HBM write time.
+#include <cstdlib>
+
 #include "tlb_internal.h"
 
 namespace tlb {
@@ -104,6 +106,42 @@ __global__ void __launch_bounds__(kThreads) eval_group_kernel(const __grid_const
         } else {
 #pragma unroll
             for (int j = 0; j < G; j += 2) st_cs_v2(o + j, v[j], v[j + 1]);
+        }
+    }
+}
+
+// Warp-coalesced grouped evaluation: a warp owns 32 consecutive groups of G indices (32*G outputs, 256*G bytes).
+// Lane l peels group l ONCE; the bases then travel by shuffle so that store j of the warp covers the 128
+// consecutive outputs [j*128, j*128+128): lane l writes outputs j*128 + 4l .. +3 (one 32-byte sector per lane,
+// 1 KiB contiguous per STG.256 instruction -> 8 full 128-byte lines instead of 32 partial ones). The in-group
+// offsets (4l mod G) + k of a lane do not depend on j, so their stride products / carry-less products are
+// computed once per thread.
+template <int G, bool kPow2U32>
+__global__ void __launch_bounds__(kThreads) eval_warp_kernel(const __grid_constant__ tlb_layout_desc L, uint64_t i0,
+                                                             uint64_t n_super, int64_t* __restrict__ out) {
+    static_assert(G >= 4 && G <= 32 && (G & (G - 1)) == 0, "G in {4,8,16,32}");
+    constexpr int kStores = G / 4;        // STG.256 per lane per superblock
+    constexpr int kLanesPerGroup = G / 4; // lanes that share one group inside a store
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const bool is_xor = L.kind == TLB_KIND_XOR;
+    const int64_t d0 = L.stride[0];
+    const uint32_t sub = (static_cast<uint32_t>(lane) * 4u) & (G - 1);
+    int64_t off[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        off[k] = is_xor ? static_cast<int64_t>(dev_clmul(sub + k, static_cast<uint64_t>(d0))) : static_cast<int64_t>(sub + k) * d0;
+    const int src0 = lane / kLanesPerGroup;
+    for (uint64_t sb = warp0; sb < n_super; sb += warps) {
+        const uint64_t i = i0 + (sb * 32 + lane) * G;
+        const int64_t base = kPow2U32 ? dev_eval_pow2_u32(L, static_cast<uint32_t>(i)) : dev_eval(L, i);
+        int64_t* o = out + sb * (32 * G) + lane * 4;
+#pragma unroll
+        for (int j = 0; j < kStores; ++j) {
+            const int64_t b = __shfl_sync(0xffffffffu, base, j * (128 / G) + src0);
+            if (is_xor) st_cs_v4(o + j * 128, b ^ off[0], b ^ off[1], b ^ off[2], b ^ off[3]);
+            else st_cs_v4(o + j * 128, b + off[0], b + off[1], b + off[2], b + off[3]);
         }
     }
 }
@@ -227,6 +265,15 @@ int grid_for(uint64_t work_items) {
     return static_cast<int>(std::max<uint64_t>(blocks, 1));
 }
 
+// TLB_EVAL_NO_WARP=1 keeps the per-thread grouped kernel only (A/B comparisons of the store pattern).
+bool eval_no_warp() {
+    static const bool on = [] {
+        const char* e = std::getenv("TLB_EVAL_NO_WARP");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 int check_int_or_xor(const tlb_layout_desc* L, const char* who) {
     if (!L) return fail(TLB_ERR_CONTRACT, std::string(who) + ": null layout");
     if (L->kind == TLB_KIND_BASIS) return fail(TLB_ERR_SEMIMODULE, "not an integer stride");
@@ -268,15 +315,39 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
         const uint64_t groups = n / G;
         const bool wide = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
         const bool p32 = (layout->flags & TLB_LF_ALL_POW2) && (i0 + n - 1) < (1ull << 32);
-        const int grid = grid_for(groups);
+        // Warp-coalesced kernel first (whole superblocks of 32 groups), the per-thread kernel on what is left.
+        uint64_t groups_done = 0;
+        if (wide && G >= 4 && groups >= 32 && !eval_no_warp()) {
+            const uint64_t n_super = groups / 32;
+            const int gw = grid_for(n_super * 32);
+#define TLB_EVAL_W(GG)                                                                                   \
+    do {                                                                                                 \
+        if (p32) eval_warp_kernel<GG, true><<<gw, kThreads, 0, s>>>(*layout, i0, n_super, d_out);        \
+        else eval_warp_kernel<GG, false><<<gw, kThreads, 0, s>>>(*layout, i0, n_super, d_out);           \
+    } while (0)
+            switch (G) {
+            case 32: TLB_EVAL_W(32); break;
+            case 16: TLB_EVAL_W(16); break;
+            case 8: TLB_EVAL_W(8); break;
+            default: TLB_EVAL_W(4); break;
+            }
+#undef TLB_EVAL_W
+            count_launch();
+            TLB_CUDA(cudaGetLastError());
+            groups_done = n_super * 32;
+        }
+        const uint64_t groups_left = groups - groups_done;
+        const uint64_t i0g = i0 + groups_done * G;
+        int64_t* outg = d_out + groups_done * G;
+        const int grid = grid_for(groups_left);
 #define TLB_EVAL_G(GG)                                                                                          \
     do {                                                                                                        \
-        if (p32 && wide) eval_group_kernel<GG, true, true><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);   \
-        else if (p32) eval_group_kernel<GG, true, false><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);     \
-        else if (wide) eval_group_kernel<GG, false, true><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);    \
-        else eval_group_kernel<GG, false, false><<<grid, kThreads, 0, s>>>(*layout, i0, groups, d_out);             \
+        if (p32 && wide) eval_group_kernel<GG, true, true><<<grid, kThreads, 0, s>>>(*layout, i0g, groups_left, outg);   \
+        else if (p32) eval_group_kernel<GG, true, false><<<grid, kThreads, 0, s>>>(*layout, i0g, groups_left, outg);     \
+        else if (wide) eval_group_kernel<GG, false, true><<<grid, kThreads, 0, s>>>(*layout, i0g, groups_left, outg);    \
+        else eval_group_kernel<GG, false, false><<<grid, kThreads, 0, s>>>(*layout, i0g, groups_left, outg);             \
     } while (0)
-        switch (G) {
+        if (groups_left) switch (G) {
         case 32: TLB_EVAL_G(32); break;
         case 16: TLB_EVAL_G(16); break;
         case 8: TLB_EVAL_G(8); break;
@@ -284,8 +355,10 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
         default: TLB_EVAL_G(2); break;
         }
 #undef TLB_EVAL_G
-        count_launch();
-        TLB_CUDA(cudaGetLastError());
+        if (groups_left) {
+            count_launch();
+            TLB_CUDA(cudaGetLastError());
+        }
         const uint64_t done = groups * G;
         if (done < n) {
             eval_range_kernel<false><<<grid_for(n - done), kThreads, 0, s>>>(*layout, i0 + done, n - done, d_out + done);

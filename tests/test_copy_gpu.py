@@ -276,18 +276,21 @@ def test_tensormap_from_divided_fetches_the_tile_the_layout_names():
     the divided layout addresses (oracle evaluation), for every hardware swizzle mode: the de-swizzle is
     Swizzle<B,4,3> on byte offsets, i.e. the reference's Xor layouts."""
     import oracle_util as ou
-    parent, tile = "(96,192):(192,1)", "(32,32):(192,1)"      # zipped_divide(parent, [32,32]) tile mode
+    parent = "(96,192):(192,1)"
     buf = torch.arange(96 * 192, dtype=torch.int32, device="cuda") * 3 + 1
     hbuf = buf.cpu().numpy()
-    tile_off = ou.orc_eval_range(tile, 0, 32 * 32).reshape(32, 32)      # [col (dim0 of TMA)][row]: colex, mode 0 = rows
+    # the inner box extent may not exceed the swizzle span (32 / 64 / 128 bytes): 8 / 16 / 32 int32 columns
+    width = {0: 32, 1: 8, 2: 16, 3: 32}
     for (ti, tj) in [(0, 0), (2, 5), (1, 3)]:
         base = ti * 32 * 192 + tj * 32
-        want = hbuf[base + tile_off].T.copy()                            # TMA box order: dim0 (stride 1) fastest
-        want = hbuf[base + np.arange(32)[None, :] + 192 * np.arange(32)[:, None]]   # [row][col]
         for swz in (0, 1, 2, 3):
+            w = width[swz]
+            tile = f"(32,{w}):(192,1)"                                   # zipped_divide(parent, [32,w]) tile mode
+            tile_off = ou.orc_eval_range(tile, 0, 32 * w).reshape(w, 32)    # [col][row]: colex, mode 0 = rows
+            want = hbuf[base + tile_off].T                                   # TMA box order: dim0 (stride 1) fastest
             got = host.tensormap_fetch(parent, tile, buf, (tj * 32, ti * 32), swizzle=swz)
             torch.cuda.synchronize()
-            assert (got.cpu().numpy().view(np.int32).reshape(32, 32) == want).all(), (ti, tj, swz)
+            assert (got.cpu().numpy().view(np.int32).reshape(32, w) == want).all(), (ti, tj, swz)
     # config C3 source tile: box 32 x 128 (16 KiB) at tile 2, 128-byte swizzle
     T = 4
     s3 = f"((8,128),(4,64),{T}):((1,2048),(8,32),262144)"

@@ -42,12 +42,15 @@ p = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,temperatur
 threading.Thread(target=lambda: [rows.append(l.strip()) for l in p.stdout], daemon=True).start()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
+h0 = time.perf_counter()
 for i in range(steps):
     step(i)
+h1 = time.perf_counter()
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / steps
 time.sleep(0.1)
 p.terminate()
 print("clocks/power/temp:", rows[-6:])
+print(f"host launch loop: {(h1 - h0) / steps * 1e6:.1f} us/call")
 print(f"{M}x{N}x{K} batch {batch} plan {lib.tlb_last_plan().decode()}: {ms * 1e3:.1f} us/step  {2 * M * N * K * batch / ms / 1e9:.1f} TFLOP/s")
