@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "_obj"
 LIB = PKG / "libtlb.so"
 
-SOURCES = ["tlb_lower.cpp", "tlb_eval.cu", "tlb_tma.cu", "tlb_copy.cu", "tlb_gemm_simt.cu", "tlb_gemm_umma.cu",
+SOURCES = ["tlb_lower.cpp", "tlb_eval.cu", "tlb_tma.cu", "tlb_copy.cu", "tlb_gemm_simt.cu", "tlb_gemm_umma.cu", "tlb_gemm_umma_wide.cu",
            "tlb_host.cu"]
 
 NVCC_FLAGS = [

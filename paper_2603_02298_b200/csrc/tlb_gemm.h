@@ -40,5 +40,8 @@ struct UmmaProblem {
     int32_t split_tail;            // 1: split the units of the last partial wave along K (red.add epilogue)
 };
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
+// Wide plan (tlb_gemm_umma_wide.cu): 512 x 256 pair tiles, chosen when the tile range is a whole number of them.
+bool umma_wide_applies(const UmmaProblem& p);
+int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream);
 
 } // namespace tlb

@@ -27,11 +27,8 @@ constexpr int kThreads = 256;
 
 // TLB_GEMM_SPLIT_TAIL=0 keeps every C cell owned by one CTA (bitwise run-to-run reproducible sums).
 bool split_tail_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("TLB_GEMM_SPLIT_TAIL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+    const char* e = std::getenv("TLB_GEMM_SPLIT_TAIL");
+    return !(e && e[0] == '0');
 }
 
 struct SimtArgs {

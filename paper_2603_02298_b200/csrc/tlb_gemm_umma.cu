@@ -31,6 +31,7 @@
 
 #include "tlb_internal.h"
 #include "tlb_gemm.h"
+#include "tlb_umma_ptx.h"
 
 namespace tlb {
 namespace {
@@ -55,7 +56,8 @@ constexpr uint32_t kEpiChunkBytes = BM * 32 * 4; // 16 KiB
 
 template <int CG, int EPI> struct Cfg {
     static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : 1; // staging buffers per column half
-    static constexpr int kStages = EPI == EPI_REGS ? (CG == 1 ? 4 : 7) : (CG == 1 ? 4 : 6);
+    static constexpr int kStages = CG == 1 ? 4 : 6; // even: smem stages are released in pairs
+    static constexpr int kPairs = kStages / 2;
     static constexpr int kBRows = CG == 1 ? BN : BN / 2; // rows of B this CTA stages
     static constexpr uint32_t kABytes = BM * BK * 2;
     static constexpr uint32_t kBBytes = kBRows * BK * 2;
@@ -64,189 +66,8 @@ template <int CG, int EPI> struct Cfg {
     static constexpr uint32_t kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// ---- PTX wrappers ---------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+using namespace umma;
 
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "elect.sync _|P, 0xffffffff;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}"
-        : "=r"(pred));
-    return pred != 0;
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// Bounded wait: a pipeline bug must trap, never hang the GPU. The first probe is free of bookkeeping; roles
-// that idle for microseconds (epilogue, producer) back off with nanosleep between probes.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, uint32_t backoff_ns = 0) {
-    if (mbar_try(bar, parity)) return;
-    const long long t0 = clock64();
-    for (;;) {
-        if (backoff_ns) __nanosleep(backoff_ns);
-        if (mbar_try(bar, parity)) return;
-        if (clock64() - t0 > 6000000000ll) __trap();
-    }
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, uint32_t bar, int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
-        : "memory");
-}
-// cta_group::2 form: the transaction bytes complete on the LEADER CTA's barrier (cluster address).
-__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const void* map, uint32_t leader_bar, int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
-        : "memory");
-}
-// L2 eviction-priority policies for the per-tensor cache hints.
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const void* map, uint32_t bar, int c0, int c1, int c2, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
-        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_2sm_hint(uint32_t dst, const void* map, uint32_t leader_bar, int c0, int c1, int c2,
-                                                     uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
-        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ void tma_reduce_add_3d_hint(const void* map, uint32_t src, int c0, int c1, int c2, uint64_t pol) {
-    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(map),
-                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
-                 : "memory");
-}
-// C += staged chunk, performed by the TMA unit / L2 (fp32 add, element type from the tensor map).
-__device__ __forceinline__ void tma_reduce_add_3d(const void* map, uint32_t src, int c0, int c1, int c2) {
-    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-
-template <int CG> __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t cols) {
-    if constexpr (CG == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(cols) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    } else {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(cols) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
-}
-template <int CG> __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
-    if constexpr (CG == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
-    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
-}
-template <int CG>
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
-    if constexpr (CG == 1) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
-            : "memory");
-    }
-}
-// tcgen05.commit: the barrier is arrived on when every MMA previously issued by this thread has finished.
-template <int CG> __device__ __forceinline__ void umma_commit(uint32_t bar) {
-    if constexpr (CG == 1) {
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-    } else {
-        const uint16_t mask = 3; // both CTAs of the pair, same barrier offset in each
-        asm volatile(
-            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-            "h"(mask)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void red_add_f32(float* p, float v) {
-    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-// Shared-memory matrix descriptor of a K-major bf16 tile staged with the 128-byte swizzle: rows of 128 B,
-// 8-row groups 1024 B apart (SBO), sm_100 descriptor version 1, layout type 2 (SWIZZLE_128B). Only the low
-// word depends on the tile address; advancing K by 16 elements inside the swizzle row adds 32 B (+2).
-constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
-__device__ __forceinline__ uint32_t desc_lo(uint32_t smem_addr) { return ((smem_addr >> 4) & 0x3fffu) | (1u << 16); }
-__device__ __forceinline__ uint64_t make_desc(uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; }
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N = 256, M = 128 * CG.
 template <int CG> __device__ __forceinline__ constexpr uint32_t make_idesc() {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -270,6 +91,7 @@ struct UmmaArgs {
                                    // the ring is filled once, 2 = epilogue without smem / global traffic,
                                    // 4 = no staging stores, 8 = no TMA store
     long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
+    long long* clk;                // optional (TLB_GEMM_CLOCK=1): CTA 0 stamps {clock64, globaltimer} at entry and exit
 };
 constexpr int kTraceSlots = 128;
 #define TLB_TRACE(slot)                                                                                    \
@@ -336,6 +158,12 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const uint32_t n_workers = CG == 2 ? gridDim.x / 2 : gridDim.x;
     const uint32_t worker = CG == 2 ? blockIdx.x / 2 : blockIdx.x;
     const int kblocks = (args.K + BK - 1) / BK;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.clk[0] = clock64();
+        args.clk[1] = static_cast<long long>(gt);
+    }
     if (threadIdx.x == 0) {
         TLB_TRACE(0);
         if (args.trace) {
@@ -354,7 +182,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         if (EPI != EPI_REGS) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(full_bar(s), 1);  // the (leader's) producer arrive; the TMA bytes complete the phase
-            mbar_init(empty_bar(s), 1); // one tcgen05.commit
+            mbar_init(empty_bar(s), 1); // pair s < kPairs: one tcgen05.commit (leader) / one relayed arrive (peer)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(tfull_bar(s), 1);               // one tcgen05.commit
@@ -375,7 +203,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         // ===== TMA producer (whole warp in the loops, one elected lane issues) =====
         int stage = 0;
         uint32_t phase = 0;
-        bool ring_filled = false;
+        bool ring_filled = false, ring_wrapped = false;
+        const uint32_t peer_empty0 = CG == 2 ? map_to_cta(empty_bar(0), 1) : 0u;
         const uint32_t lbar0 = CG == 2 ? map_to_cta(full_bar(0), 0) : full_bar(0);
         const uint64_t pol_ab = policy_evict_last();
         const bool hint_ab = (args.hints & 1u) != 0;
@@ -391,7 +220,12 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             const int item = static_cast<int>((w - args.unit_begin) / n_workers);
             if (lane == 0) TLB_TRACE(8 + item * 10 + 0);
             for (int kb = kb0; kb < kb1; ++kb) {
-                mbar_wait(empty_bar(stage), phase ^ 1u, args.backoff_ns);
+                // Stages are released in pairs (one commit per 8 MMAs). The MMA thread commits on the LEADER's
+                // barrier only; the leader's producer relays each release to the peer CTA's barrier.
+                if ((stage & 1) == 0) {
+                    mbar_wait(empty_bar(stage >> 1), phase ^ 1u, args.backoff_ns);
+                    if (CG == 2 && leader && ring_wrapped && lane == 0) mbar_arrive_cluster(peer_empty0 + 8u * (stage >> 1));
+                }
                 if (elect_one()) {
                     if ((args.debug & 1u) && ring_filled) {
                         if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
@@ -414,7 +248,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                             tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
                             __syncwarp();
                             if (stage == C::kStages - 1) ring_filled = true;
-                            if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+                            if (++stage == C::kStages) { stage = 0; phase ^= 1u; ring_wrapped = true; }
                             continue;
                         }
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
@@ -429,7 +263,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 }
                 __syncwarp();
                 if (stage == C::kStages - 1) ring_filled = true;
-                if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+                if (++stage == C::kStages) { stage = 0; phase ^= 1u; ring_wrapped = true; }
             }
             if (lane == 0) TLB_TRACE(8 + item * 10 + 1);
         }
@@ -453,6 +287,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 tc_fence_after();
                 if (lane == 0) TLB_TRACE(8 + item * 10 + 2);
                 const uint32_t d_tmem = tmem_base + acc * BN;
+                // The issuing thread may run 4-5 MMAs ahead of the tensor pipe (measured queue depth), which hides
+                // the barrier probe; commits are the expensive part, so a smem PAIR is released per commit.
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full_bar(stage), phase);
                     tc_fence_after();
@@ -464,8 +300,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         for (int k = 0; k < BK / UMMA_K; ++k)
                             umma_bf16<CG>(d_tmem, make_desc(a_lo + 2 * k), make_desc(b_lo + 2 * k), idesc,
                                           (kb != kb0 || k != 0) ? 1u : 0u);
-                        umma_commit<CG>(empty_bar(stage)); // frees the smem stage once these MMAs retire
-                        if (kb == kb1 - 1) umma_commit<CG>(tfull_bar(acc)); // accumulator complete -> epilogue
+                        if (stage & 1) umma_commit_local<CG>(empty_bar(stage >> 1)); // both stages of the pair are consumed
+                        if (kb == kb1 - 1) umma_commit<CG>(tfull_bar(acc)); // accumulator complete -> epilogue (both CTAs)
                     }
                     __syncwarp();
                     if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
@@ -631,6 +467,49 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         tmem_dealloc<CG>(tmem_base, kTmemCols);
     }
     if (threadIdx.x == 0) TLB_TRACE(120);
+    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.clk[2] = clock64();
+        args.clk[3] = static_cast<long long>(gt);
+    }
+}
+
+// TLB_GEMM_CLOCK=1: SM clock actually seen by the kernel (cycles of CTA 0 / globaltimer ns), reported at exit.
+// The stamps land in mapped pinned host memory, one 4-word slot per launch (ring of 4096).
+constexpr int kClkSlots = 4096;
+long long* g_clk_host = nullptr;
+long long* g_clk_dev = nullptr;
+unsigned g_clk_next = 0;
+void clk_report() {
+    if (!g_clk_host) return;
+    cudaDeviceSynchronize();
+    std::vector<double> mhz, us;
+    for (int i = 0; i < kClkSlots; ++i) {
+        const long long* c = g_clk_host + 4 * i;
+        if (c[3] > c[1] && c[2] > c[0]) {
+            mhz.push_back(static_cast<double>(c[2] - c[0]) / static_cast<double>(c[3] - c[1]) * 1e3);
+            us.push_back(static_cast<double>(c[3] - c[1]) * 1e-3);
+        }
+    }
+    if (mhz.empty()) return;
+    std::sort(mhz.begin(), mhz.end());
+    std::sort(us.begin(), us.end());
+    std::fprintf(stderr, "[tlb gemm clock] %zu launches: SM clock median %.0f MHz (min %.0f, max %.0f); CTA-0 lifetime median %.1f us\n",
+                 mhz.size(), mhz[mhz.size() / 2], mhz.front(), mhz.back(), us[us.size() / 2]);
+}
+long long* clk_slot() {
+    static const bool on = [] {
+        const char* e = std::getenv("TLB_GEMM_CLOCK");
+        if (!(e && e[0] == '1')) return false;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&g_clk_host), kClkSlots * 4 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess) return false;
+        std::memset(g_clk_host, 0, kClkSlots * 4 * sizeof(long long));
+        if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_clk_dev), g_clk_host, 0) != cudaSuccess) return false;
+        std::atexit(clk_report);
+        return true;
+    }();
+    if (!on) return nullptr;
+    return g_clk_dev + 4 * (g_clk_next++ % kClkSlots);
 }
 
 int encode_operand_map(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch,
@@ -719,6 +598,7 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
         const char* h = std::getenv("TLB_GEMM_HINTS");
         a.hints = h ? static_cast<uint32_t>(std::atoi(h)) : 0u;
     }
+    a.clk = clk_slot();
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     const uint32_t work = a.work_end - a.unit_begin;
@@ -774,7 +654,10 @@ template <int CG> int launch_cg(const UmmaProblem& p, cudaStream_t stream) {
 
 } // namespace
 
+long long* umma_clk_slot() { return clk_slot(); }
+
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream) {
+    if (umma_wide_applies(p)) return umma_wide_launch(p, stream);
     if (p.cta_group == 2) return launch_cg<2>(p, stream);
     return launch_cg<1>(p, stream);
 }

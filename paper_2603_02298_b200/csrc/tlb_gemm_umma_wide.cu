@@ -1,0 +1,537 @@
+// tcgen05 GEMM, wide plan: a CTA PAIR owns a 512 x 256 tile of C (256 rows per CTA), K-major bf16 operands,
+// fp32 accumulators that fill all of TMEM.        C(m,n) += sum_k A(m,k) * B(n,k)      (tensor.hpp:214-233)
+//
+// Why this shape: on a 1 kW part the kernel is POWER bound (SM clock 1.5 GHz under load, MMA duty cycle < 80 %),
+// so the figure of merit is energy per flop, and operand movement is the largest controllable term. A 512 x 256
+// pair tile moves (512 + 256) / (512 * 256) operand bytes per MAC against (256 + 256) / (256 * 256) for the
+// 256 x 256 tile of tlb_gemm_umma.cu: 25 % less L2 -> SM traffic and shared-memory fill for the same math.
+//
+// Partitioning in the paper's terms: zipped_divide(C, [512,256]) are the pair tiles,
+// zipped_divide(A, [256,64]) / (B, [128,64]) the per-CTA k-blocks (the TMA boxes), and the TiledMMA is the 2-CTA
+// UMMA atom 256 x 256 x 16 applied to the two 128-row halves h of each CTA: half h of both CTAs forms one
+// cta_group::2 instruction whose accumulator lives in TMEM columns [256 h, 256 h + 256) of each CTA.
+//
+// Kernel shape (persistent, warp-specialised, 320 threads, 1 CTA per SM, clusters of 2):
+//   warp 8     TMA producer: 4-stage ring of {A 256 x 64, B 128 x 64} stages (48 KiB), full / empty mbarriers;
+//              also prefetches the tile's C cells into L2 so that the reduce-add epilogue does not wait on HBM
+//   warp 9     MMA issue (leader CTA): per k-block 4 + 4 UMMAs (half 0, half 1), ONE non-multicast commit per
+//              stage (a commit every 8 MMAs is free, a multicast commit is not: tools/probes/mma_rate.cu);
+//              the leader's producer relays each stage release to the peer CTA
+//   warps 0-7  epilogue: warp w drains TMEM lane quadrant w % 4, columns [128 (w / 4), +128) of each half through
+//              a PRIVATE 4 KiB staging tile (32 rows x 32 columns, 128-byte swizzle) and its own
+//              cp.reduce.async.bulk.tensor (C += chunk at L2): no CTA-wide barriers in the epilogue
+// The accumulators are single-buffered, so a tile's epilogue is overlapped per HALF: half 0 is released to the
+// epilogue one k-block early, and the next tile's half-0 MMAs of the first kStages-1 k-blocks are issued while
+// half 1 is still being drained.
+// Scheduling: the last (units mod workers) tiles are cut stream-K style into equal k-ranges, one per worker, and
+// run FIRST; whole tiles follow round-robin. Partial tiles combine through the same reduce-add epilogue.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
+
+#include "tlb_internal.h"
+#include "tlb_gemm.h"
+#include "tlb_umma_ptx.h"
+
+namespace tlb {
+namespace {
+using namespace umma;
+
+constexpr int BMH = 128;           // rows per accumulator half
+constexpr int BMC = 2 * BMH;       // rows of C per CTA
+constexpr int BN = 256;            // columns of C per pair (UMMA N)
+constexpr int BK = 64;             // one 128-byte swizzle row of bf16
+constexpr int UMMA_K = 16;
+#ifndef TLB_WIDE_STAGES
+#define TLB_WIDE_STAGES 4
+#endif
+constexpr int kStages = TLB_WIDE_STAGES;
+constexpr int kEpiBufs = kStages == 3 ? 2 : 1; // private staging tiles per epilogue warp
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsW = 64 + 32 * kEpiWarps;
+constexpr int kProducerWarp = kEpiWarps;
+constexpr int kMmaWarp = kEpiWarps + 1;
+constexpr uint32_t kABytes = BMC * BK * 2;        // 32 KiB
+constexpr uint32_t kBBytes = (BN / 2) * BK * 2;   // 16 KiB: this CTA's half of B
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kEpiWarpBytes = 32 * 32 * 4;   // 4 KiB private staging tile per epilogue warp
+constexpr uint32_t kSmemW = kStages * kStageBytes + kEpiWarps * kEpiBufs * kEpiWarpBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kMinSeg = 4;                        // stream-K cuts closer than this to a tile boundary snap to it
+
+struct WideArgs {
+    int32_t M, N, K;
+    uint32_t mb, nb;          // 256 x 256 blocks along m and n (mb is even)
+    uint32_t group_m;         // m-blocks per rasterisation group (even)
+    uint32_t unit_begin;      // first 512 x 256 pair tile of the range (all batches)
+    uint32_t dp_units;        // whole tiles, dealt round-robin
+    uint32_t sk_units;        // the tiles after them, cut into one k-range per worker
+    uint32_t prefetch_c;      // 1: map_cp is valid
+    uint32_t hints;           // L2 hints: 1 = operand loads evict_last, 2 = C reductions evict_first
+    uint32_t stagger_kb;      // rotation of the first whole tile: phi(worker) = stagger_kb * worker / workers k-blocks
+    uint32_t debug;           // TLB_GEMM_DEBUG timing experiments (garbage results): 1 = no TMA loads once the ring is
+                              // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only
+    long long* clk;
+};
+
+struct Item {
+    uint32_t unit;
+    int kb0, kb1;
+};
+
+__device__ __forceinline__ uint64_t snap_cut(uint64_t x, uint32_t kblocks) {
+    const uint32_t r = static_cast<uint32_t>(x % kblocks);
+    const uint32_t lim = kblocks >= 2 * kMinSeg ? kMinSeg : (kblocks + 1) / 2;
+    if (r < lim) return x - r;
+    if (kblocks - r < lim) return x + (kblocks - r);
+    return x;
+}
+
+// Work list of one worker, as an iterator every role walks identically:
+//   1. its k-range of the stream-K tiles (the partial wave), cut at tile boundaries;
+//   2. its whole tiles, round-robin. The FIRST whole tile is rotated: the worker runs k-blocks [phi, KB) now and
+//      [0, phi) as its very last item, with phi growing with the worker index. Every worker still does the same
+//      number of k-blocks, but tile boundaries (and with them the bursts of C traffic of the epilogues, 256 KiB per
+//      CTA) no longer coincide across the chip: one pair's epilogue overlaps its neighbours' main loops.
+struct Sched {
+    uint64_t sk_lo, sk_hi;
+    uint32_t worker, n_workers, dp_next;
+    int phi;
+    bool first_done, tail_pending;
+    __device__ void init(const WideArgs& a, uint32_t w, uint32_t W, int kblocks) {
+        worker = w;
+        n_workers = W;
+        dp_next = w;
+        first_done = false;
+        tail_pending = false;
+        sk_lo = sk_hi = 0;
+        if (a.sk_units) {
+            const uint64_t total = static_cast<uint64_t>(a.sk_units) * kblocks;
+            sk_lo = snap_cut(total * w / W, kblocks);
+            sk_hi = snap_cut(total * (w + 1) / W, kblocks);
+        }
+        phi = static_cast<int>(static_cast<uint64_t>(a.stagger_kb) * w / W);
+        if (phi < kMinSeg || kblocks - phi < kMinSeg) phi = 0;
+    }
+    __device__ __forceinline__ bool next(const WideArgs& a, int kblocks, Item* it) {
+        if (sk_lo < sk_hi) {
+            const uint32_t t = static_cast<uint32_t>(sk_lo / kblocks);
+            it->kb0 = static_cast<int>(sk_lo % kblocks);
+            it->kb1 = static_cast<int>(min(static_cast<uint64_t>(kblocks), it->kb0 + (sk_hi - sk_lo)));
+            it->unit = a.unit_begin + a.dp_units + t;
+            sk_lo += static_cast<uint64_t>(it->kb1 - it->kb0);
+            return true;
+        }
+        if (dp_next < a.dp_units) {
+            it->unit = a.unit_begin + dp_next;
+            it->kb0 = 0;
+            it->kb1 = kblocks;
+            if (!first_done && phi > 0) {
+                it->kb0 = phi;
+                tail_pending = true;
+            }
+            first_done = true;
+            dp_next += n_workers;
+            return true;
+        }
+        if (tail_pending) {
+            tail_pending = false;
+            it->unit = a.unit_begin + worker;
+            it->kb0 = 0;
+            it->kb1 = phi;
+            return true;
+        }
+        return false;
+    }
+};
+
+// pair tile id -> (batch, first 128-row tile index (multiple of 4), 256-column block). Pair tile g is the two
+// m-adjacent 256 x 256 blocks 2g, 2g+1 of the tile order of tlb_gemm.h (groups of group_m m-blocks, m fastest).
+__device__ __forceinline__ void decode_pair_tile(const WideArgs& a, uint32_t g, uint32_t* batch, uint32_t* m_tile, uint32_t* n_blk) {
+    const uint32_t blocks = a.mb * a.nb;
+    const uint32_t b0 = 2u * g;
+    *batch = b0 / blocks;
+    const uint32_t blk = b0 % blocks;
+    const uint32_t per = a.group_m * a.nb;
+    const uint32_t grp = blk / per, rem = blk % per;
+    const uint32_t gm = min(a.group_m, a.mb - grp * a.group_m);
+    *m_tile = (grp * a.group_m + rem % gm) * 2;
+    *n_blk = rem / gm;
+}
+
+__device__ __forceinline__ void tma_prefetch_3d(const void* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+// Sleeping wait: try_wait suspends the thread in hardware for up to the hint (ns) instead of spinning.
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(hint_ns)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const long long t0 = clock64();
+    for (;;) {
+        if (mbar_try_sleep(bar, parity, 20000u)) return;
+        if (clock64() - t0 > 6000000000ll) __trap();
+    }
+}
+
+constexpr uint32_t kIdescW = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
+
+__global__ void __launch_bounds__(kThreadsW, 1)
+umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_cp,
+                 const __grid_constant__ WideArgs args) {
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t epi_base = smem_base + kStages * kStageBytes;
+    const uint32_t bar_base = epi_base + kEpiWarps * kEpiBufs * kEpiWarpBytes;
+    auto a_stage = [&](int s) { return smem_base + s * kStageBytes; };
+    auto b_stage = [&](int s) { return smem_base + s * kStageBytes + kABytes; };
+    auto full_bar = [&](int s) { return bar_base + 8u * s; };
+    auto empty_bar = [&](int s) { return bar_base + 8u * (kStages + s); };
+    auto tfull_bar = [&](int h) { return bar_base + 8u * (2 * kStages + h); };
+    auto tempty_bar = [&](int h) { return bar_base + 8u * (2 * kStages + 2 + h); };
+    const uint32_t tmem_slot = bar_base + 8u * (2 * kStages + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const uint32_t n_workers = gridDim.x / 2, worker = blockIdx.x / 2;
+    const int kblocks = (args.K + BK - 1) / BK;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.clk[0] = clock64();
+        args.clk[1] = static_cast<long long>(gt);
+    }
+
+    if (warp == kProducerWarp && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full_bar(s), 1);  // the leader's producer arrive; the TMA bytes of both CTAs complete the phase
+            mbar_init(empty_bar(s), 1); // one tcgen05.commit (leader) / one relayed arrive (peer)
+        }
+        for (int h = 0; h < 2; ++h) {
+            mbar_init(tfull_bar(h), 1);              // one multicast tcgen05.commit
+            mbar_init(tempty_bar(h), kEpiWarps * 2); // one lane of every epilogue warp of both CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kMmaWarp) tmem_alloc<2>(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    uint32_t tmem_base;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
+
+    Sched sched;
+    sched.init(args, worker, n_workers, kblocks);
+
+    if (warp == kProducerWarp) {
+        // ===== TMA producer (whole warp in the loops, one elected lane issues) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        bool ring_wrapped = false;
+        const uint32_t peer_empty0 = map_to_cta(empty_bar(0), 1);
+        const uint32_t lbar0 = map_to_cta(full_bar(0), 0);
+        const uint64_t pol_ab = policy_evict_last();
+        Item it;
+        while (sched.next(args, kblocks, &it)) {
+            uint32_t batch, m_tile, n_blk;
+            decode_pair_tile(args, it.unit, &batch, &m_tile, &n_blk);
+            const int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC;
+            const int n0 = static_cast<int>(n_blk) * BN;
+            if (args.prefetch_c && lane < 2) {
+                // this CTA's 256 x 256 cells of C -> L2 (two 128-row boxes), long before the reductions need them
+                tma_prefetch_3d(&map_cp, n0, m0 + lane * BMH, static_cast<int>(batch));
+            }
+            for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                mbar_wait(empty_bar(stage), phase ^ 1u, 64);
+                if (elect_one()) {
+                    if (leader && ring_wrapped) mbar_arrive_cluster(peer_empty0 + 8u * stage); // relay the release
+                    if ((args.debug & 1u) && ring_wrapped) {
+                        if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
+                    } else {
+                        const uint32_t lbar = lbar0 + 8u * stage;
+                        if (leader) mbar_expect_tx(full_bar(stage), 2 * kStageBytes);
+                        if (args.hints & 1u) {
+                            tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
+                            tma_load_3d_2sm_hint(b_stage(stage), &map_b, lbar, kb * BK, n0 + static_cast<int>(rank) * (BN / 2), batch, pol_ab);
+                        } else {
+                            tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
+                            tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, n0 + static_cast<int>(rank) * (BN / 2), batch);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (++stage == kStages) { stage = 0; phase ^= 1u; ring_wrapped = true; }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ===== MMA issuer (leader CTA). Warp-uniform control flow, one elected lane issues. =====
+        if (leader) {
+            const uint32_t a_lo0 = desc_lo(a_stage(0)), b_lo0 = desc_lo(b_stage(0));
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            // 4 UMMAs of k-block `kb` in ring slot s into accumulator half h
+            auto issue_half = [&](int s, int h, bool first_kb) {
+                const uint32_t a_lo = a_lo0 + s * (kStageBytes >> 4) + h * ((BMH * BK * 2) >> 4);
+                const uint32_t b_lo = b_lo0 + s * (kStageBytes >> 4);
+                const uint32_t d_tmem = tmem_base + h * BN;
+#pragma unroll
+                for (int k = 0; k < BK / UMMA_K; ++k)
+                    umma_bf16<2>(d_tmem, make_desc(a_lo + 2 * k), make_desc(b_lo + 2 * k), kIdescW, (first_kb && k == 0) ? 0u : 1u);
+            };
+            Item it;
+            while (sched.next(args, kblocks, &it)) {
+                const int n = it.kb1 - it.kb0;
+                const int pre = min(n, kStages - 1);
+                // --- head: half-0 MMAs of the first `pre` k-blocks run while the epilogue still drains half 1
+                mbar_wait(tempty_bar(0), acc_phase ^ 1u);
+                tc_fence_after();
+                {
+                    int s = stage;
+                    uint32_t ph = phase;
+                    for (int j = 0; j < pre; ++j) {
+                        mbar_wait(full_bar(s), ph);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            issue_half(s, 0, j == 0);
+                            if (j == n - 1) umma_commit<2>(tfull_bar(0));
+                        }
+                        __syncwarp();
+                        if (++s == kStages) { s = 0; ph ^= 1u; }
+                    }
+                }
+                mbar_wait(tempty_bar(1), acc_phase ^ 1u);
+                tc_fence_after();
+                for (int j = 0; j < pre; ++j) {
+                    if (elect_one()) {
+                        issue_half(stage, 1, j == 0);
+                        umma_commit_local<2>(empty_bar(stage)); // both halves of this stage are consumed
+                        if (j == n - 1) umma_commit<2>(tfull_bar(1));
+                    }
+                    __syncwarp();
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+                // --- steady state
+                for (int j = pre; j < n; ++j) {
+                    mbar_wait(full_bar(stage), phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        issue_half(stage, 0, false);
+                        if (j == n - 1) umma_commit<2>(tfull_bar(0)); // half 0 complete: its epilogue starts a k-block early
+                        issue_half(stage, 1, false);
+                        umma_commit_local<2>(empty_bar(stage));
+                        if (j == n - 1) umma_commit<2>(tfull_bar(1));
+                    }
+                    __syncwarp();
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+                acc_phase ^= 1u;
+            }
+        }
+    } else {
+        // ===== epilogue: TMEM -> registers -> private swizzled 4 KiB tile -> cp.reduce.async.bulk.tensor (C += tile)
+        const uint32_t quad = warp & 3;                         // TMEM lane quadrant this warp may read
+        const uint32_t colh = static_cast<uint32_t>(warp) >> 2; // which 128 columns of a half
+        const uint32_t buf0 = epi_base + static_cast<uint32_t>(warp) * kEpiBufs * kEpiWarpBytes;
+        uint32_t chunk_no = 0;
+        const uint32_t tempty_leader = map_to_cta(tempty_bar(0), 0);
+        const uint64_t pol_c = policy_evict_first();
+        const uint32_t row = lane;
+        uint32_t acc_phase = 0;
+        Item it;
+        while (sched.next(args, kblocks, &it)) {
+            uint32_t batch, m_tile, n_blk;
+            decode_pair_tile(args, it.unit, &batch, &m_tile, &n_blk);
+            const int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC + static_cast<int>(quad) * 32;
+            const int n0 = static_cast<int>(n_blk) * BN + static_cast<int>(colh) * (BN / 2);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                mbar_wait_sleep(tfull_bar(h), acc_phase);
+                tc_fence_after();
+#pragma unroll 1
+                for (int ci = 0; ci < 4; ++ci, ++chunk_no) {
+                    const uint32_t buf = buf0 + (chunk_no % kEpiBufs) * kEpiWarpBytes;
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + ((quad * 32u) << 16) + h * BN + colh * (BN / 2) + ci * 32, v);
+                    // the reduction that last used this warp's staging tile must have read it
+                    if (lane == 0) bulk_wait_read<kEpiBufs - 1>();
+                    tmem_ld_wait();
+                    if (ci == 3) {
+                        // every TMEM read of this half is done: hand it back to the MMA warp
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(tempty_leader + 8u * h);
+                    } else {
+                        __syncwarp();
+                    }
+                    if (!(args.debug & 2u)) {
+                        // staging tile: row = m (128 B = 32 n), 16-byte chunk c stored at c ^ (m & 7)
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + row * 128u + ((c ^ (row & 7u)) << 4)),
+                                         "r"(v[4 * c + 0]), "r"(v[4 * c + 1]), "r"(v[4 * c + 2]), "r"(v[4 * c + 3])
+                                         : "memory");
+                        fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0 && !(args.debug & 8u)) {
+                            if (args.debug & 4u)  // timing experiment: plain store instead of the L2 reduction
+                                asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&map_c),
+                                             "r"(buf), "r"(n0 + ci * 32), "r"(m0 + h * BMH), "r"(static_cast<int>(batch)) : "memory");
+                            else if (args.hints & 2u)
+                                tma_reduce_add_3d_hint(&map_c, buf, n0 + ci * 32, m0 + h * BMH, static_cast<int>(batch), pol_c);
+                            else
+                                tma_reduce_add_3d(&map_c, buf, n0 + ci * 32, m0 + h * BMH, static_cast<int>(batch));
+                            bulk_commit();
+                        }
+                    }
+                }
+            }
+            acc_phase ^= 1u;
+        }
+        if (lane == 0) bulk_wait_read<0>();
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        tmem_dealloc<2>(tmem_base, 512);
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.clk[2] = clock64();
+        args.clk[3] = static_cast<long long>(gt);
+    }
+}
+
+int encode_operand(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch, int box_rows) {
+    const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(rows), static_cast<uint64_t>(batch)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(ld) * 2,
+                                 static_cast<uint64_t>(batch > 1 ? batch_stride : ld * static_cast<int64_t>(rows)) * 2};
+    const uint32_t box[3] = {BK, static_cast<uint32_t>(box_rows), 1};
+    return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
+}
+
+int encode_c(TmaDesc* out, const UmmaProblem& p, uint32_t box_n, uint32_t box_m, int swizzle) {
+    const uint64_t dims[3] = {static_cast<uint64_t>(p.N), static_cast<uint64_t>(p.M), static_cast<uint64_t>(p.batch)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * 4,
+                                 static_cast<uint64_t>(p.batch > 1 ? p.c_bs : p.cs_m * static_cast<int64_t>(p.M)) * 4};
+    const uint32_t box[3] = {box_n, box_m, 1};
+    return tma_encode(out, 4, true, 3, p.C, dims, strides, box, swizzle, 0);
+}
+
+} // namespace
+
+bool umma_wide_applies(const UmmaProblem& p) {
+    if (const char* e = std::getenv("TLB_GEMM_WIDE"))
+        if (e[0] == '0') return false;
+    if (p.cta_group != 2) return false;
+    const uint32_t mb = static_cast<uint32_t>((p.M + 255) / 256);
+    if (mb % 2 != 0) return false;                                   // pair tiles are two m-adjacent 256 x 256 blocks
+    if (p.tile_begin % 4 != 0 || p.tile_end % 4 != 0) return false;  // 4 tiles of 128 x 256 per pair tile
+    const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
+    return base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N;   // TMA reduce-add epilogue only
+}
+
+long long* umma_clk_slot();
+
+int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    TLB_CUDA(cudaGetDevice(&dev));
+    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+        TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
+        attr_set[dev] = true;
+    }
+    TmaDesc ma, mb, mc, mcp;
+    TLB_TRY(encode_operand(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BMC));
+    TLB_TRY(encode_operand(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, BN / 2));
+    TLB_TRY(encode_c(&mc, p, 32, 32, TMA_SW_128));
+    WideArgs a;
+    std::memset(&a, 0, sizeof(a));
+    // C prefetch into L2 is off by default: measured, it evicts operand lines and costs 1.5 % (8192^3) to 7 % (4096^3).
+    a.prefetch_c = 0;
+    if (const char* e = std::getenv("TLB_GEMM_PREFETCH_C"))
+        if (e[0] == '1') a.prefetch_c = 1;
+    if (a.prefetch_c && encode_c(&mcp, p, 256, BMH, TMA_SW_NONE) != TLB_OK) a.prefetch_c = 0;
+    if (!a.prefetch_c) mcp = mc;
+    a.M = p.M;
+    a.N = p.N;
+    a.K = p.K;
+    a.mb = static_cast<uint32_t>((p.M + 255) / 256);
+    a.nb = static_cast<uint32_t>((p.N + 255) / 256);
+    {
+        const char* e = std::getenv("TLB_GEMM_GROUP_M");
+        a.group_m = e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : static_cast<uint32_t>(kGemmGroupM);
+        if (a.group_m % 2) ++a.group_m;
+        const char* d = std::getenv("TLB_GEMM_DEBUG");
+        a.debug = d ? static_cast<uint32_t>(std::atoi(d)) : 0u;
+        const char* h = std::getenv("TLB_GEMM_HINTS");
+        a.hints = h ? static_cast<uint32_t>(std::atoi(h)) : 0u;
+    }
+    a.unit_begin = p.tile_begin / 4;
+    const uint32_t units = p.tile_end / 4 - a.unit_begin;
+    if (units == 0) return TLB_OK;
+    const uint32_t W = static_cast<uint32_t>(sm_count() / 2);
+    const int kblocks = (p.K + BK - 1) / BK;
+    // Tail balancing: the (units mod W) tiles of the partial wave become one k-range per worker (run first). With
+    // split_tail off (TLB_GEMM_SPLIT_TAIL=0) every tile is summed by one CTA pair in k order: bitwise reproducible.
+    // Partial tiles cost an extra epilogue (C traffic is the expensive part), so the partial wave is only cut when whole
+    // tiles would leave more than TLB_GEMM_SK_PCT % (default 4) of the CTA pairs idle in the last wave.
+    a.sk_units = (p.split_tail && kblocks >= 2 * kMinSeg) ? units % W : 0;
+    if (a.sk_units && units > W) {
+        int pct = 4;
+        if (const char* e = std::getenv("TLB_GEMM_SK_PCT")) pct = std::atoi(e);
+        const uint32_t waves = (units + W - 1) / W;
+        const double idle = 1.0 - static_cast<double>(units) / (static_cast<double>(waves) * W);
+        if (idle * 100.0 <= pct) a.sk_units = 0;
+    }
+    a.dp_units = units - a.sk_units;
+    const uint32_t workers = a.sk_units ? W : std::min(units, W);
+    {
+        // stagger: sixteenths of a tile's k-blocks over which the tile boundaries of the workers are spread
+        int sixteenths = 0; // measured: staggering does not pay (the extra partial epilogue costs more than the overlap gains)
+        if (const char* e = std::getenv("TLB_GEMM_STAGGER")) sixteenths = std::max(0, std::min(16, std::atoi(e)));
+        a.stagger_kb = (p.split_tail && workers == W) ? static_cast<uint32_t>(static_cast<int64_t>(kblocks) * sixteenths / 16) : 0u;
+    }
+    a.clk = umma_clk_slot();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3(2 * workers);
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(kThreadsW);
+    cfg.dynamicSmemBytes = kSmemW;
+    cfg.stream = stream;
+    CUtensorMap tma, tmb, tmc, tmcp;
+    std::memcpy(&tma, ma.bytes, 128);
+    std::memcpy(&tmb, mb.bytes, 128);
+    std::memcpy(&tmc, mc.bytes, 128);
+    std::memcpy(&tmcp, mcp.bytes, 128);
+    TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel, tma, tmb, tmc, tmcp, a));
+    count_launch();
+    set_plan("umma_2sm_wide");
+    return TLB_OK;
+}
+
+} // namespace tlb

@@ -193,6 +193,46 @@ def test_c2_gemm_4096_full_size_exact(cg):
     _flat_tn_check(4096, 4096, 4096, cg)
 
 
+WIDE_SHAPES = [
+    # (A, B, C) as the kernel runs them: C n-contiguous -> rows = M; 512 x 256 pair tiles need ceil(M/256) even
+    ("(512,64):(64,1)", "(256,64):(64,1)", "(512,256):(256,1)"),          # one pair tile, one k-block
+    ("(512,1024):(1024,1)", "(512,1024):(1024,1)", "(512,512):(1,512)"),  # m-contiguous C (runs transposed), 16 k-blocks
+    ("(1000,200):(200,1)", "(300,200):(200,1)", "(1000,300):(300,1)"),    # ragged M, N, K: TMA zero fill / clipping
+    ("(1024,520):(528,1)", "(768,520):(536,1)", "(1024,768):(800,1)"),    # padded leading dimensions
+    ("(1024,1024):(1024,1)", "(1536,1024):(1024,1)", "(1024,1536):(1,1024)"),  # 12 pair tiles cut into k-ranges per worker
+]
+
+
+@pytest.mark.parametrize("shape", WIDE_SHAPES)
+def test_gemm_bf16_wide_plan_kat_exact(shape):
+    """512 x 256 pair tiles (tlb_gemm_umma_wide.cu): exact on the reference's integer fills, including the stream-K
+    cut of the partial wave (partial tiles combine through the reduce-add epilogue)."""
+    assert _bf16_case(*shape, kat=True, path=3) == "umma_2sm_wide"
+
+
+@pytest.mark.parametrize("shape", WIDE_SHAPES[1:])
+def test_gemm_bf16_wide_plan_random_within_tolerance(shape):
+    assert _bf16_case(*shape, kat=False, seed=11, path=3) == "umma_2sm_wide"
+
+
+def test_gemm_wide_plan_whole_tiles_then_k_ranges():
+    """128 pair tiles on 74 CTA pairs: 54 tiles are cut into one k-range per pair and run first, 74 whole tiles follow."""
+    _flat_tn_check(4096, 4096, 1024, 3)
+
+
+def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
+    # ceil(M/256) odd: no m-adjacent block pairs -> 256 x 256 plan
+    assert _bf16_case("(768,128):(128,1)", "(256,128):(128,1)", "(768,256):(256,1)", kat=True, path=3) == "umma_2sm"
+    monkeypatch.setenv("TLB_GEMM_WIDE", "0")
+    assert _bf16_case(*WIDE_SHAPES[1], kat=True, path=3) == "umma_2sm"
+
+
+def test_gemm_wide_plan_without_k_split_is_reproducible(monkeypatch):
+    """TLB_GEMM_SPLIT_TAIL=0: every tile is summed by one CTA pair in k order, so two runs agree bit for bit."""
+    monkeypatch.setenv("TLB_GEMM_SPLIT_TAIL", "0")
+    assert _bf16_case(*WIDE_SHAPES[4], kat=False, seed=5, path=3) == "umma_2sm_wide"
+
+
 def test_gemm_register_epilogue_matches_tma_epilogue(monkeypatch):
     monkeypatch.setenv("TLB_GEMM_EPILOGUE", "regs")
     assert _bf16_case(*UMMA_SHAPES[1], kat=True, path=2) == "umma_1sm_regs"
@@ -271,7 +311,7 @@ def test_c4_batched_8192_two_batches_exact():
     tc = host.make_tensor(L(f"({M},{N}):(1,{M})").lower(ranked=True), c.data_ptr(), c.numel(), 4)
     plan = host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 0, B)
     torch.cuda.synchronize()
-    assert plan == "umma_2sm"
+    assert plan == "umma_2sm_wide"
     for bi in range(B):
         ref = (a[bi].double() @ b[bi].double().t()).t() + 1.0
         assert torch.equal(c[bi].double(), ref)
