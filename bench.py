@@ -213,6 +213,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ.setdefault("TLB_GEMM_CLOCK", "1")  # the GEMM kernels stamp {clock64, globaltimer}: SM clock under load
     lib = abi.load()
     pk = peaks()
     K, W = args.steps, args.warmup
@@ -247,6 +248,18 @@ def run_ours(args):
     plan = lib.tlb_last_plan().decode()
     launches = int(lib.tlb_launch_count() - n0) - W  # warm-up launches are outside the timed region
     clocks = sampler.stop(w0, w1) if rank == 0 else None
+    if rank == 0:
+        # nvidia-smi samples every 100 ms and a 50-step region lasts ~5 ms, so the SM clock the kernel actually ran
+        # at is measured inside the kernel (CTA 0: clock64 delta / globaltimer delta, median over the launches)
+        import ctypes as C
+        mhz, us, nl = C.c_double(0), C.c_double(0), C.c_uint32(0)
+        lib.tlb_gemm_clock_stats(C.byref(mhz), C.byref(us), C.byref(nl))
+        if nl.value:
+            clocks["sm_mhz_in_kernel"] = round(mhz.value, 1)
+            clocks["kernel_us_in_kernel"] = round(us.value, 2)
+            clocks["launches_sampled"] = nl.value
+            if clocks.get("sm_max_mhz") and mhz.value < 0.97 * clocks["sm_max_mhz"] and not clocks["reasons"]:
+                clocks["note"] = "SM clock below max inside the kernel: power management under tensor load (sw_power_cap regime)"
     flops = 2.0 * M * N * Kd
     value = flops * K * world / sec / 1e12
     kernel_s = sec / K
@@ -254,7 +267,7 @@ def run_ours(args):
     peak = pk["bf16_tflops"] if burst else pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops / kernel_s / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic_for("C2"), "kernel": f"umma_gemm_kernel ({plan})",
+                "traffic": traffic_for("C2"), "kernel": f"{'umma_wide_kernel' if plan.endswith('wide') else 'umma_gemm_kernel'} ({plan})",
                 "peak_source": f"{pk['_source']} {'burst' if burst else 'sustained'} cuBLAS bf16",
                 "frac_of_nominal_2250": achieved / 2250.0, "algorithmic_flop_per_launch": flops}
 

@@ -200,6 +200,10 @@ int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_te
 int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream);
 /* Planner knob for tlb_gemm_bf16: 0 auto, 1 SIMT only, 2 tcgen05 cta_group::1, 3 tcgen05 cta_group::2. */
 int tlb_gemm_set_path(int path);
+/* Diagnostics: SM clock the tcgen05 GEMM kernels actually ran at (cycles of CTA 0 / globaltimer), recorded per launch
+ * when TLB_GEMM_CLOCK=1 is in the environment at the first GEMM launch. Synchronises the device, returns the medians
+ * over the recorded launches (ring of 4096) and clears the record. *launches = 0 when recording is off. */
+int tlb_gemm_clock_stats(double* median_mhz, double* median_us, uint32_t* launches);
 
 /* ---- host-buffer convenience (the reference-facing call, used for e2e) -- */
 /* Same contracts with HOST pointers in the tlb_tensor.data fields: stages through device memory

@@ -75,6 +75,7 @@ SYMBOLS = {
                                         C.c_int32, C.c_int32, C.c_void_p]),
     "tlb_gemm_i64": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_void_p, C.c_void_p]),
     "tlb_gemm_set_path": (C.c_int, [C.c_int]),
+    "tlb_gemm_clock_stats": (C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_uint32)]),
     "tlb_copy_host": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor)]),
     "tlb_gemm_bf16_host": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor)]),
 }

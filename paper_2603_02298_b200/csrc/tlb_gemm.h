@@ -41,6 +41,8 @@ struct UmmaProblem {
 };
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
 // Wide plan (tlb_gemm_umma_wide.cu): 512 x 256 pair tiles, chosen when the tile range is a whole number of them.
+bool umma_pdl_enabled();      // programmatic dependent launch (TLB_GEMM_PDL=0 turns it off)
+long long* umma_clk_slot();   // TLB_GEMM_CLOCK=1: where CTA 0 stamps {clock64, globaltimer}; nullptr when off
 bool umma_wide_applies(const UmmaProblem& p);
 int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream);
 

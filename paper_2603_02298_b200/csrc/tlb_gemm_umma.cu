@@ -158,12 +158,6 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const uint32_t n_workers = CG == 2 ? gridDim.x / 2 : gridDim.x;
     const uint32_t worker = CG == 2 ? blockIdx.x / 2 : blockIdx.x;
     const int kblocks = (args.K + BK - 1) / BK;
-    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
-        unsigned long long gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        args.clk[0] = clock64();
-        args.clk[1] = static_cast<long long>(gt);
-    }
     if (threadIdx.x == 0) {
         TLB_TRACE(0);
         if (args.trace) {
@@ -197,6 +191,15 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     tc_fence_after();
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
+    // the prologue above may overlap the tail of the previous kernel of the stream (programmatic dependent launch)
+    griddep_wait();
+    griddep_launch_dependents();
+    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.clk[0] = clock64();
+        args.clk[1] = static_cast<long long>(gt);
+    }
     if (threadIdx.x == 0) TLB_TRACE(1);
 
     if (warp == kProducerWarp) {
@@ -481,9 +484,13 @@ constexpr int kClkSlots = 4096;
 long long* g_clk_host = nullptr;
 long long* g_clk_dev = nullptr;
 unsigned g_clk_next = 0;
+void clk_fetch() {
+    cudaDeviceSynchronize();
+    cudaMemcpy(g_clk_host, g_clk_dev, kClkSlots * 4 * sizeof(long long), cudaMemcpyDeviceToHost);
+}
 void clk_report() {
     if (!g_clk_host) return;
-    cudaDeviceSynchronize();
+    clk_fetch();
     std::vector<double> mhz, us;
     for (int i = 0; i < kClkSlots; ++i) {
         const long long* c = g_clk_host + 4 * i;
@@ -502,9 +509,13 @@ long long* clk_slot() {
     static const bool on = [] {
         const char* e = std::getenv("TLB_GEMM_CLOCK");
         if (!(e && e[0] == '1')) return false;
-        if (cudaHostAlloc(reinterpret_cast<void**>(&g_clk_host), kClkSlots * 4 * sizeof(long long), cudaHostAllocMapped) != cudaSuccess) return false;
-        std::memset(g_clk_host, 0, kClkSlots * 4 * sizeof(long long));
-        if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_clk_dev), g_clk_host, 0) != cudaSuccess) return false;
+        // device memory, fetched on demand: stamps in mapped host memory would put a PCIe round trip into every
+        // kernel's completion (measured: about +4 us per launch)
+        const size_t bytes = kClkSlots * 4 * sizeof(long long);
+        g_clk_host = static_cast<long long*>(std::malloc(bytes));
+        if (!g_clk_host || cudaMalloc(reinterpret_cast<void**>(&g_clk_dev), bytes) != cudaSuccess) return false;
+        if (cudaMemset(g_clk_dev, 0, bytes) != cudaSuccess) return false;
+        std::memset(g_clk_host, 0, bytes);
         std::atexit(clk_report);
         return true;
     }();
@@ -600,11 +611,12 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
     }
     a.clk = clk_slot();
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     const uint32_t work = a.work_end - a.unit_begin;
     if (CG == 1) {
         cfg.gridDim = dim3(std::min<uint32_t>(work, static_cast<uint32_t>(sms)));
         cfg.numAttrs = 0;
+        cfg.attrs = attr;
     } else {
         cfg.gridDim = dim3(2 * std::min<uint32_t>(work, static_cast<uint32_t>(sms / 2)));
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -613,6 +625,11 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+    }
+    if (umma_pdl_enabled()) {
+        attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+        ++cfg.numAttrs;
     }
     cfg.blockDim = dim3(kUmmaThreads);
     cfg.dynamicSmemBytes = C::kSmem;
@@ -655,6 +672,40 @@ template <int CG> int launch_cg(const UmmaProblem& p, cudaStream_t stream) {
 } // namespace
 
 long long* umma_clk_slot() { return clk_slot(); }
+// TLB_GEMM_PDL=0 turns programmatic dependent launch off (A/B comparisons).
+bool umma_pdl_enabled() {
+    const char* e = std::getenv("TLB_GEMM_PDL");
+    return !(e && e[0] == '0');
+}
+
+} // namespace tlb
+
+extern "C" int tlb_gemm_clock_stats(double* median_mhz, double* median_us, uint32_t* launches) {
+    using namespace tlb;
+    if (!median_mhz || !median_us || !launches) return fail(TLB_ERR_CONTRACT, "tlb_gemm_clock_stats: null output");
+    *median_mhz = *median_us = 0.0;
+    *launches = 0;
+    if (!g_clk_host) return TLB_OK;
+    clk_fetch();
+    TLB_CUDA(cudaMemset(g_clk_dev, 0, kClkSlots * 4 * sizeof(long long)));
+    std::vector<double> mhz, us;
+    for (int i = 0; i < kClkSlots; ++i) {
+        long long* c = g_clk_host + 4 * i;
+        if (c[3] > c[1] && c[2] > c[0]) {
+            mhz.push_back(static_cast<double>(c[2] - c[0]) / static_cast<double>(c[3] - c[1]) * 1e3);
+            us.push_back(static_cast<double>(c[3] - c[1]) * 1e-3);
+        }
+    }
+    if (mhz.empty()) return TLB_OK;
+    std::sort(mhz.begin(), mhz.end());
+    std::sort(us.begin(), us.end());
+    *median_mhz = mhz[mhz.size() / 2];
+    *median_us = us[us.size() / 2];
+    *launches = static_cast<uint32_t>(mhz.size());
+    return TLB_OK;
+}
+
+namespace tlb {
 
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream) {
     if (umma_wide_applies(p)) return umma_wide_launch(p, stream);

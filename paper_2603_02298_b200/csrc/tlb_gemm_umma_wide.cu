@@ -59,6 +59,7 @@ constexpr uint32_t kBBytes = (BN / 2) * BK * 2;   // 16 KiB: this CTA's half of 
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr uint32_t kEpiWarpBytes = 32 * 32 * 4;   // 4 KiB private staging tile per epilogue warp
 constexpr uint32_t kSmemW = kStages * kStageBytes + kEpiWarps * kEpiBufs * kEpiWarpBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kMaxWorkers = 80;                   // CTA pairs (74 on a 148-SM part)
 constexpr int kMinSeg = 4;                        // stream-K cuts closer than this to a tile boundary snap to it
 
 struct WideArgs {
@@ -73,21 +74,15 @@ struct WideArgs {
     uint32_t stagger_kb;      // rotation of the first whole tile: phi(worker) = stagger_kb * worker / workers k-blocks
     uint32_t debug;           // TLB_GEMM_DEBUG timing experiments (garbage results): 1 = no TMA loads once the ring is
                               // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only
+    uint32_t sk_cut[kMaxWorkers + 1]; // k-range [sk_cut[w], sk_cut[w+1]) of the stream-K tiles owned by worker w
     long long* clk;
+    long long* cta_times;     // optional (TLB_GEMM_CTA_TIMES=<file>): {globaltimer at entry, at exit} of every CTA
 };
 
 struct Item {
     uint32_t unit;
     int kb0, kb1;
 };
-
-__device__ __forceinline__ uint64_t snap_cut(uint64_t x, uint32_t kblocks) {
-    const uint32_t r = static_cast<uint32_t>(x % kblocks);
-    const uint32_t lim = kblocks >= 2 * kMinSeg ? kMinSeg : (kblocks + 1) / 2;
-    if (r < lim) return x - r;
-    if (kblocks - r < lim) return x + (kblocks - r);
-    return x;
-}
 
 // Work list of one worker, as an iterator every role walks identically:
 //   1. its k-range of the stream-K tiles (the partial wave), cut at tile boundaries;
@@ -108,9 +103,8 @@ struct Sched {
         tail_pending = false;
         sk_lo = sk_hi = 0;
         if (a.sk_units) {
-            const uint64_t total = static_cast<uint64_t>(a.sk_units) * kblocks;
-            sk_lo = snap_cut(total * w / W, kblocks);
-            sk_hi = snap_cut(total * (w + 1) / W, kblocks);
+            sk_lo = a.sk_cut[w];
+            sk_hi = a.sk_cut[w + 1];
         }
         phi = static_cast<int>(static_cast<uint64_t>(a.stagger_kb) * w / W);
         if (phi < kMinSeg || kblocks - phi < kMinSeg) phi = 0;
@@ -208,11 +202,10 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const bool leader = rank == 0;
     const uint32_t n_workers = gridDim.x / 2, worker = blockIdx.x / 2;
     const int kblocks = (args.K + BK - 1) / BK;
-    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+    if (threadIdx.x == 0 && args.cta_times) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        args.clk[0] = clock64();
-        args.clk[1] = static_cast<long long>(gt);
+        args.cta_times[2 * blockIdx.x] = static_cast<long long>(gt);
     }
 
     if (warp == kProducerWarp && lane == 0) {
@@ -235,6 +228,15 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     tc_fence_after();
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
+    // everything above (barriers, TMEM, cluster handshake) may overlap the tail of the previous kernel of the stream
+    griddep_wait();
+    griddep_launch_dependents();
+    if (threadIdx.x == 0 && blockIdx.x == 0 && args.clk) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.clk[0] = clock64();
+        args.clk[1] = static_cast<long long>(gt);
+    }
 
     Sched sched;
     sched.init(args, worker, n_workers, kblocks);
@@ -418,6 +420,45 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         args.clk[2] = clock64();
         args.clk[3] = static_cast<long long>(gt);
     }
+    if (threadIdx.x == 0 && args.cta_times) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.cta_times[2 * blockIdx.x + 1] = static_cast<long long>(gt);
+    }
+}
+
+// TLB_GEMM_CTA_TIMES=<file>: per-CTA entry / exit times of the last 64 launches (debug; dumped at process exit).
+constexpr int kCtaRing = 64, kCtaSlots = 2 * 160;
+long long* g_cta_host = nullptr;
+long long* g_cta_dev = nullptr;
+unsigned g_cta_next = 0;
+void cta_times_dump() {
+    const char* path = std::getenv("TLB_GEMM_CTA_TIMES");
+    if (!g_cta_host || !path) return;
+    cudaDeviceSynchronize();
+    cudaMemcpy(g_cta_host, g_cta_dev, static_cast<size_t>(kCtaRing) * kCtaSlots * sizeof(long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(path, "wb")) {
+        const long long hdr[4] = {kCtaRing, kCtaSlots, static_cast<long long>(g_cta_next), 0};
+        std::fwrite(hdr, sizeof(hdr), 1, f);
+        std::fwrite(g_cta_host, sizeof(long long), static_cast<size_t>(kCtaRing) * kCtaSlots, f);
+        std::fclose(f);
+    }
+}
+long long* cta_times_slot() {
+    static const bool on = [] {
+        const char* e = std::getenv("TLB_GEMM_CTA_TIMES");
+        if (!(e && e[0])) return false;
+        const size_t bytes = static_cast<size_t>(kCtaRing) * kCtaSlots * sizeof(long long);
+        // device memory, copied back at exit: stamps written to mapped host memory would add a PCIe round trip to
+        // every kernel's completion (measured: +4 us per launch)
+        g_cta_host = static_cast<long long*>(std::malloc(bytes));
+        if (!g_cta_host || cudaMalloc(reinterpret_cast<void**>(&g_cta_dev), bytes) != cudaSuccess) return false;
+        if (cudaMemset(g_cta_dev, 0, bytes) != cudaSuccess) return false;
+        std::atexit(cta_times_dump);
+        return true;
+    }();
+    if (!on) return nullptr;
+    return g_cta_dev + static_cast<size_t>(g_cta_next++ % kCtaRing) * kCtaSlots;
 }
 
 int encode_operand(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch, int box_rows) {
@@ -438,6 +479,50 @@ int encode_c(TmaDesc* out, const UmmaProblem& p, uint32_t box_n, uint32_t box_m,
 
 } // namespace
 
+// Cuts of the stream-K k-block space [0, sk_units * kblocks) into one range per worker, balanced by COST: a range
+// pays `epi` k-block equivalents for every tile it touches (each touched tile is one more reduce-add epilogue, about
+// 7 us against 0.65 us per k-block), so workers whose range straddles a tile boundary get fewer k-blocks. Cuts closer
+// than kMinSeg to a tile boundary snap to it.
+void stream_k_cuts(uint32_t sk_units, uint32_t kblocks, uint32_t W, uint32_t epi, uint32_t* cut) {
+    const uint64_t total = static_cast<uint64_t>(sk_units) * kblocks;
+    auto snap = [&](uint64_t x) {
+        const uint32_t r = static_cast<uint32_t>(x % kblocks);
+        if (r < static_cast<uint32_t>(kMinSeg)) return x - r;
+        if (kblocks - r < static_cast<uint32_t>(kMinSeg)) return x + (kblocks - r);
+        return x;
+    };
+    auto assign = [&](uint64_t T) {
+        uint64_t pos = 0;
+        cut[0] = 0;
+        for (uint32_t w = 0; w < W; ++w) {
+            int64_t budget = static_cast<int64_t>(T);
+            uint64_t q = pos;
+            while (q < total) {
+                budget -= epi; // the tile this range is about to touch
+                if (budget < kMinSeg) break;
+                const uint64_t to_boundary = kblocks - q % kblocks;
+                const uint64_t step = std::min<uint64_t>(to_boundary, static_cast<uint64_t>(budget));
+                q += step;
+                budget -= static_cast<int64_t>(step);
+                if (step < to_boundary) break;
+            }
+            q = std::min<uint64_t>(snap(q), total);
+            if (q < pos) q = pos;
+            pos = q;
+            cut[w + 1] = static_cast<uint32_t>(pos);
+        }
+        return pos >= total;
+    };
+    uint64_t lo = total / W, hi = total / W + 4ull * epi + kblocks + 8;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (assign(mid)) hi = mid;
+        else lo = mid + 1;
+    }
+    assign(lo);
+    cut[W] = static_cast<uint32_t>(total);
+}
+
 bool umma_wide_applies(const UmmaProblem& p) {
     if (const char* e = std::getenv("TLB_GEMM_WIDE"))
         if (e[0] == '0') return false;
@@ -449,7 +534,6 @@ bool umma_wide_applies(const UmmaProblem& p) {
     return base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N;   // TMA reduce-add epilogue only
 }
 
-long long* umma_clk_slot();
 
 int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     static bool attr_set[64] = {false};
@@ -503,6 +587,15 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
         if (idle * 100.0 <= pct) a.sk_units = 0;
     }
     a.dp_units = units - a.sk_units;
+    if (a.sk_units && (W > static_cast<uint32_t>(kMaxWorkers) || static_cast<uint64_t>(a.sk_units) * kblocks > 0xffffffffull)) {
+        a.sk_units = 0;
+        a.dp_units = units;
+    }
+    if (a.sk_units) {
+        uint32_t epi = 10;
+        if (const char* e = std::getenv("TLB_GEMM_EPI_KB")) epi = static_cast<uint32_t>(std::max(0, std::atoi(e)));
+        stream_k_cuts(a.sk_units, static_cast<uint32_t>(kblocks), W, epi, a.sk_cut);
+    }
     const uint32_t workers = a.sk_units ? W : std::min(units, W);
     {
         // stagger: sixteenths of a tile's k-blocks over which the tile boundaries of the workers are spread
@@ -511,15 +604,18 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
         a.stagger_kb = (p.split_tail && workers == W) ? static_cast<uint32_t>(static_cast<int64_t>(kblocks) * sixteenths / 16) : 0u;
     }
     a.clk = umma_clk_slot();
+    a.cta_times = cta_times_slot();
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cfg.gridDim = dim3(2 * workers);
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = umma_pdl_enabled() ? 2 : 1;
     cfg.blockDim = dim3(kThreadsW);
     cfg.dynamicSmemBytes = kSmemW;
     cfg.stream = stream;
