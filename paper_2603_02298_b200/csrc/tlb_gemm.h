@@ -28,8 +28,8 @@ __host__ __device__ inline uint32_t tile_of(const TileGrid& g, int64_t m, int64_
 }
 
 struct UmmaProblem {
-    const void* A;   // bf16, (M,K):(lda,1)
-    const void* B;   // bf16, (N,K):(ldb,1)
+    const void* A;   // bf16, (M,K):(lda,1), or (M,K):(1,lda) when a_mn
+    const void* B;   // bf16, (N,K):(ldb,1), or (N,K):(1,ldb) when b_mn
     float* C;        // fp32, (M,N):(cs_m,cs_n)
     int64_t lda, ldb, cs_m, cs_n;
     int32_t M, N, K;
@@ -38,6 +38,8 @@ struct UmmaProblem {
     uint32_t tile_begin, tile_end; // global tile ids (batch-major), [begin, end)
     int32_t cta_group;             // 1 or 2
     int32_t split_tail;            // 1: split the units of the last partial wave along K (red.add epilogue)
+    int32_t a_mn, b_mn;            // operand is MN-major (its m / n mode is the contiguous one): wide plan only
+    int32_t full_range;            // [tile_begin, tile_end) is every tile of every batch
 };
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
 // Wide plan (tlb_gemm_umma_wide.cu): 512 x 256 pair tiles, chosen when the tile range is a whole number of them.

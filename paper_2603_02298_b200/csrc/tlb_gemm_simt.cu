@@ -181,8 +181,25 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
                       single_stride(*C->layout, 1, &eCn, &csn);
     if (!flat) return f;
     const bool batched = batch_end - batch_begin > 1 || batch_begin > 0;
-    bool ok = (ska == 1 || d.K == 1) && (skb == 1 || d.K == 1) && lda > 0 && ldb > 0 && lda % 8 == 0 && ldb % 8 == 0 &&
-              csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) &&
+    // Operand majorness: K-major (k stride 1, the paper's "T" operands) or MN-major (m / n stride 1, the "N" operands of
+    // the NT / NTT rows). ld is the stride of the other mode.
+    auto major = [&](int64_t s_mn, int64_t s_k, int64_t e_mn, bool* mn, int64_t* ld) {
+        if (s_k == 1 || d.K == 1) {
+            *mn = false;
+            *ld = s_mn;
+            return s_mn > 0 || e_mn == 1;
+        }
+        if (s_mn == 1 || e_mn == 1) {
+            *mn = true;
+            *ld = s_k;
+            return s_k > 0;
+        }
+        return false;
+    };
+    bool a_mn = false, b_mn = false;
+    int64_t a_ld = 0, b_ld = 0;
+    bool ok = major(lda, ska, d.M, &a_mn, &a_ld) && major(ldb, skb, d.N, &b_mn, &b_ld) && a_ld > 0 && b_ld > 0 &&
+              a_ld % 8 == 0 && b_ld % 8 == 0 && csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) &&
               (C->layout->flags & TLB_LF_INJECTIVE) && (!batched || (a_bs % 8 == 0 && b_bs % 8 == 0 && a_bs > 0 && b_bs > 0));
     const char* a_ptr = static_cast<const char*>(A->data) + A->origin * 2;
     const char* b_ptr = static_cast<const char*>(B->data) + B->origin * 2;
@@ -194,8 +211,10 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
     p.A = f.swapped ? b_ptr : a_ptr;
     p.B = f.swapped ? a_ptr : b_ptr;
     p.C = static_cast<float*>(C->data) + C->origin;
-    p.lda = f.swapped ? ldb : lda;
-    p.ldb = f.swapped ? lda : ldb;
+    p.lda = f.swapped ? b_ld : a_ld;
+    p.ldb = f.swapped ? a_ld : b_ld;
+    p.a_mn = (f.swapped ? b_mn : a_mn) ? 1 : 0;
+    p.b_mn = (f.swapped ? a_mn : b_mn) ? 1 : 0;
     p.cs_m = f.swapped ? csn : csm;
     p.cs_n = f.swapped ? csm : csn;
     p.M = static_cast<int32_t>(f.swapped ? d.N : d.M);
@@ -250,12 +269,19 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
             const bool even = (t0 % 2 == 0) && (t1 % 2 == 0);
             p.split_tail = split_tail_enabled() ? 1 : 0;
             p.cta_group = g_gemm_path == 2 ? 1 : g_gemm_path == 3 ? 2 : (even ? 2 : 1);
-            if (p.cta_group == 2 && !even)
-                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
-            return umma_gemm_launch(p, stream);
-        }
-        if (g_gemm_path == 2 || g_gemm_path == 3)
+            p.full_range = (t0 == 0 && t1 == tpb * static_cast<uint64_t>(batch_end)) ? 1 : 0;
+            const bool mn_major = p.a_mn || p.b_mn;
+            if (!mn_major || umma_wide_applies(p)) {
+                if (p.cta_group == 2 && !even)
+                    return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
+                return umma_gemm_launch(p, stream);
+            }
+            // MN-major operands are staged by the wide plan only; anything it does not cover runs on the SIMT plan
+            if (g_gemm_path == 2 || g_gemm_path == 3)
+                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: MN-major operands need the wide tcgen05 plan (whole pair tiles, n-contiguous C)");
+        } else if (g_gemm_path == 2 || g_gemm_path == 3) {
             return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: the forced tcgen05 path does not apply to these layouts");
+        }
     }
 
     // ---- SIMT plan

@@ -64,8 +64,9 @@ constexpr int kMinSeg = 4;                        // stream-K cuts closer than t
 
 struct WideArgs {
     int32_t M, N, K;
-    uint32_t mb, nb;          // 256 x 256 blocks along m and n (mb is even)
-    uint32_t group_m;         // m-blocks per rasterisation group (even)
+    uint32_t mbw, nb;         // 512-row pair tiles along m, 256-column blocks along n
+    uint32_t group_w;         // pair tiles (along m) per rasterisation group
+    uint32_t a_mn, b_mn;      // operand is MN-major: staged as 64-row chunks of [64 k][128 B], MN-major UMMA descriptors
     uint32_t unit_begin;      // first 512 x 256 pair tile of the range (all batches)
     uint32_t dp_units;        // whole tiles, dealt round-robin
     uint32_t sk_units;        // the tiles after them, cut into one k-range per worker
@@ -141,18 +142,18 @@ struct Sched {
     }
 };
 
-// pair tile id -> (batch, first 128-row tile index (multiple of 4), 256-column block). Pair tile g is the two
-// m-adjacent 256 x 256 blocks 2g, 2g+1 of the tile order of tlb_gemm.h (groups of group_m m-blocks, m fastest).
+// pair tile id -> (batch, first 128-row tile index (multiple of 4), 256-column block). Pair tiles are walked in groups
+// of group_w tiles along m, m fastest inside a group, then n: when ceil(M/256) is even this is exactly the order of the
+// 128 x 256 tile ids of tlb_gemm.h (pair tile g = tiles 4g .. 4g+3), which is what lets tile-id ranges select pair tiles.
 __device__ __forceinline__ void decode_pair_tile(const WideArgs& a, uint32_t g, uint32_t* batch, uint32_t* m_tile, uint32_t* n_blk) {
-    const uint32_t blocks = a.mb * a.nb;
-    const uint32_t b0 = 2u * g;
-    *batch = b0 / blocks;
-    const uint32_t blk = b0 % blocks;
-    const uint32_t per = a.group_m * a.nb;
-    const uint32_t grp = blk / per, rem = blk % per;
-    const uint32_t gm = min(a.group_m, a.mb - grp * a.group_m);
-    *m_tile = (grp * a.group_m + rem % gm) * 2;
-    *n_blk = rem / gm;
+    const uint32_t tiles = a.mbw * a.nb;
+    *batch = g / tiles;
+    const uint32_t t = g % tiles;
+    const uint32_t per = a.group_w * a.nb;
+    const uint32_t grp = t / per, rem = t % per;
+    const uint32_t gw = min(a.group_w, a.mbw - grp * a.group_w);
+    *m_tile = (grp * a.group_w + rem % gw) * 4;
+    *n_blk = rem / gw;
 }
 
 __device__ __forceinline__ void tma_prefetch_3d(const void* map, int c0, int c1, int c2) {
@@ -268,12 +269,24 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     } else {
                         const uint32_t lbar = lbar0 + 8u * stage;
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * kStageBytes);
-                        if (args.hints & 1u) {
-                            tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
-                            tma_load_3d_2sm_hint(b_stage(stage), &map_b, lbar, kb * BK, n0 + static_cast<int>(rank) * (BN / 2), batch, pol_ab);
+                        const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
+                        if (!args.a_mn) {
+                            // K-major A: one box of 256 rows x 64 k (rows of 128 B)
+                            if (args.hints & 1u) tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
+                            else tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
                         } else {
-                            tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
-                            tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, n0 + static_cast<int>(rank) * (BN / 2), batch);
+                            // MN-major A: four chunks of 64 rows, each [64 k][64 m] (the map's dimension 0 is m)
+#pragma unroll
+                            for (int c = 0; c < BMC / 64; ++c)
+                                tma_load_3d_2sm(a_stage(stage) + c * 8192, &map_a, lbar, m0 + c * 64, kb * BK, batch);
+                        }
+                        if (!args.b_mn) {
+                            if (args.hints & 1u) tma_load_3d_2sm_hint(b_stage(stage), &map_b, lbar, kb * BK, nb0, batch, pol_ab);
+                            else tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, nb0, batch);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BN / 2 / 64; ++c)
+                                tma_load_3d_2sm(b_stage(stage) + c * 8192, &map_b, lbar, nb0 + c * 64, kb * BK, batch);
                         }
                     }
                 }
@@ -284,17 +297,23 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     } else if (warp == kMmaWarp) {
         // ===== MMA issuer (leader CTA). Warp-uniform control flow, one elected lane issues. =====
         if (leader) {
-            const uint32_t a_lo0 = desc_lo(a_stage(0)), b_lo0 = desc_lo(b_stage(0));
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
             // 4 UMMAs of k-block `kb` in ring slot s into accumulator half h
+            // Descriptors: K-major tiles are rows of 128 B with 8-row groups 1024 B apart (SBO), a k-step of 16 advances
+            // the start by 32 B; MN-major tiles are 64-row chunks of [64 k][128 B]: 8-k groups 1024 B apart (SBO), chunks
+            // 8192 B apart (LBO), a k-step of 16 advances the start by 2 KiB. idesc bits 15 / 16 select MN-major A / B.
+            const uint32_t idesc = kIdescW | (args.a_mn ? (1u << 15) : 0u) | (args.b_mn ? (1u << 16) : 0u);
+            const uint32_t a_lbo = args.a_mn ? ((8192u >> 4) << 16) : (1u << 16), b_lbo = args.b_mn ? ((8192u >> 4) << 16) : (1u << 16);
+            const uint32_t a_kstep = args.a_mn ? (2048u >> 4) : 2u, b_kstep = args.b_mn ? (2048u >> 4) : 2u;
+            const uint32_t a_base = ((a_stage(0) >> 4) & 0x3fffu), b_base = ((b_stage(0) >> 4) & 0x3fffu);
             auto issue_half = [&](int s, int h, bool first_kb) {
-                const uint32_t a_lo = a_lo0 + s * (kStageBytes >> 4) + h * ((BMH * BK * 2) >> 4);
-                const uint32_t b_lo = b_lo0 + s * (kStageBytes >> 4);
+                const uint32_t a_lo = (a_base + s * (kStageBytes >> 4) + h * ((BMH * BK * 2) >> 4)) | a_lbo;
+                const uint32_t b_lo = (b_base + s * (kStageBytes >> 4)) | b_lbo;
                 const uint32_t d_tmem = tmem_base + h * BN;
 #pragma unroll
                 for (int k = 0; k < BK / UMMA_K; ++k)
-                    umma_bf16<2>(d_tmem, make_desc(a_lo + 2 * k), make_desc(b_lo + 2 * k), kIdescW, (first_kb && k == 0) ? 0u : 1u);
+                    umma_bf16<2>(d_tmem, make_desc(a_lo + a_kstep * k), make_desc(b_lo + b_kstep * k), idesc, (first_kb && k == 0) ? 0u : 1u);
             };
             Item it;
             while (sched.next(args, kblocks, &it)) {
@@ -469,6 +488,15 @@ int encode_operand(TmaDesc* out, const void* base, int64_t ld, int64_t batch_str
     return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
 }
 
+// MN-major operand (r, k) at r + k * ld: dimension 0 is the row index, box = 64 rows x 64 k (one staged chunk).
+int encode_operand_mn(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch) {
+    const uint64_t dims[3] = {static_cast<uint64_t>(rows), static_cast<uint64_t>(K), static_cast<uint64_t>(batch)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(ld) * 2,
+                                 static_cast<uint64_t>(batch > 1 ? batch_stride : ld * static_cast<int64_t>(K)) * 2};
+    const uint32_t box[3] = {64, BK, 1};
+    return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
+}
+
 int encode_c(TmaDesc* out, const UmmaProblem& p, uint32_t box_n, uint32_t box_m, int swizzle) {
     const uint64_t dims[3] = {static_cast<uint64_t>(p.N), static_cast<uint64_t>(p.M), static_cast<uint64_t>(p.batch)};
     const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * 4,
@@ -527,9 +555,12 @@ bool umma_wide_applies(const UmmaProblem& p) {
     if (const char* e = std::getenv("TLB_GEMM_WIDE"))
         if (e[0] == '0') return false;
     if (p.cta_group != 2) return false;
+    // A range of 128 x 256 tile ids selects whole pair tiles when ceil(M/256) is even (pair tile g = tiles 4g .. 4g+3);
+    // the full range of a problem does for any M (the last pair tile is clipped by the TMA bounds).
     const uint32_t mb = static_cast<uint32_t>((p.M + 255) / 256);
-    if (mb % 2 != 0) return false;                                   // pair tiles are two m-adjacent 256 x 256 blocks
-    if (p.tile_begin % 4 != 0 || p.tile_end % 4 != 0) return false;  // 4 tiles of 128 x 256 per pair tile
+    if (!p.full_range && (mb % 2 != 0 || p.tile_begin % 4 != 0 || p.tile_end % 4 != 0)) return false;
+    // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue) unless an operand is MN-major
+    if (!(p.a_mn || p.b_mn) && mb % 2 != 0) return false;
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
     return base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N;   // TMA reduce-add epilogue only
 }
@@ -544,8 +575,10 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
         attr_set[dev] = true;
     }
     TmaDesc ma, mb, mc, mcp;
-    TLB_TRY(encode_operand(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BMC));
-    TLB_TRY(encode_operand(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, BN / 2));
+    if (p.a_mn) TLB_TRY(encode_operand_mn(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch));
+    else TLB_TRY(encode_operand(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BMC));
+    if (p.b_mn) TLB_TRY(encode_operand_mn(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch));
+    else TLB_TRY(encode_operand(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, BN / 2));
     TLB_TRY(encode_c(&mc, p, 32, 32, TMA_SW_128));
     WideArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -558,21 +591,24 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     a.M = p.M;
     a.N = p.N;
     a.K = p.K;
-    a.mb = static_cast<uint32_t>((p.M + 255) / 256);
+    a.mbw = static_cast<uint32_t>((p.M + 511) / 512);
     a.nb = static_cast<uint32_t>((p.N + 255) / 256);
+    a.a_mn = p.a_mn ? 1u : 0u;
+    a.b_mn = p.b_mn ? 1u : 0u;
     {
         const char* e = std::getenv("TLB_GEMM_GROUP_M");
-        a.group_m = e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : static_cast<uint32_t>(kGemmGroupM);
-        if (a.group_m % 2) ++a.group_m;
+        const uint32_t group_m = e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : static_cast<uint32_t>(kGemmGroupM);
+        a.group_w = std::max(1u, group_m / 2);
         const char* d = std::getenv("TLB_GEMM_DEBUG");
         a.debug = d ? static_cast<uint32_t>(std::atoi(d)) : 0u;
         const char* h = std::getenv("TLB_GEMM_HINTS");
         a.hints = h ? static_cast<uint32_t>(std::atoi(h)) : 0u;
     }
-    a.unit_begin = p.tile_begin / 4;
-    const uint32_t units = p.tile_end / 4 - a.unit_begin;
+    a.unit_begin = p.full_range ? 0u : p.tile_begin / 4;
+    const uint32_t units = p.full_range ? a.mbw * a.nb * static_cast<uint32_t>(std::max(p.batch, 1)) : p.tile_end / 4 - a.unit_begin;
     if (units == 0) return TLB_OK;
-    const uint32_t W = static_cast<uint32_t>(sm_count() / 2);
+    uint32_t W = static_cast<uint32_t>(sm_count() / 2);
+    if (const char* e = std::getenv("TLB_GEMM_WORKERS")) W = std::max(1u, std::min(W, static_cast<uint32_t>(std::atoi(e))));
     const int kblocks = (p.K + BK - 1) / BK;
     // Tail balancing: the (units mod W) tiles of the partial wave become one k-range per worker (run first). With
     // split_tail off (TLB_GEMM_SPLIT_TAIL=0) every tile is summed by one CTA pair in k order: bitwise reproducible.

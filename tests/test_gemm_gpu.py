@@ -215,6 +215,28 @@ def test_gemm_bf16_wide_plan_random_within_tolerance(shape):
     assert _bf16_case(*shape, kat=False, seed=11, path=3) == "umma_2sm_wide"
 
 
+MN_MAJOR_SHAPES = [
+    # the "N" operands of the paper's layout table: the m / n mode is the contiguous one
+    ("(512,256):(1,512)", "(256,256):(1,256)", "(512,256):(1,512)"),      # NT: A, B MN-major, C m-contiguous (runs transposed)
+    ("(512,256):(1,512)", "(256,256):(1,256)", "(512,256):(256,1)"),      # NTT: C n-contiguous
+    ("(512,256):(256,1)", "(256,256):(1,256)", "(512,256):(256,1)"),      # A K-major, B N-major
+    ("(512,256):(1,512)", "(256,256):(256,1)", "(512,256):(256,1)"),      # A M-major, B K-major
+    ("(200,136):(1,208)", "(300,136):(1,304)", "(200,300):(1,200)"),      # ragged M, N, K with padded leading dimensions
+    ("(640,1000):(1,648)", "(384,1000):(1,392)", "(640,384):(384,1)"),    # odd number of 256-row blocks, K % 64 != 0
+]
+
+
+@pytest.mark.parametrize("shape", MN_MAJOR_SHAPES)
+def test_gemm_bf16_mn_major_operands_on_tensor_cores_kat_exact(shape):
+    """NT / NTT families on tcgen05: MN-major tiles staged as 64-row chunks, MN-major UMMA descriptors (idesc bits 15/16)."""
+    assert _bf16_case(*shape, kat=True) == "umma_2sm_wide"
+
+
+@pytest.mark.parametrize("shape", MN_MAJOR_SHAPES[:2] + MN_MAJOR_SHAPES[4:])
+def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape):
+    assert _bf16_case(*shape, kat=False, seed=13) == "umma_2sm_wide"
+
+
 def test_gemm_wide_plan_whole_tiles_then_k_ranges():
     """128 pair tiles on 74 CTA pairs: 54 tiles are cut into one k-range per pair and run first, 74 whole tiles follow."""
     _flat_tn_check(4096, 4096, 1024, 3)
