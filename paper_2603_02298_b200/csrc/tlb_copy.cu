@@ -46,6 +46,13 @@ bool tma_default() {
 
 constexpr int kThreads = 256;
 
+// The tiled plan prefers 256-row tiles (1 KiB destination segments, 32 KiB of smem per CTA; C1 5.90 -> 6.09 TB/s);
+// TLB_COPY_LB256=0 caps the tile at 128 rows (A/B comparisons).
+bool lb256_enabled() {
+    const char* e = std::getenv("TLB_COPY_LB256");
+    return !(e && e[0] == '0');
+}
+
 // ---------------------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------------------
@@ -653,8 +660,9 @@ int try_planned(const CopyCall& c, bool* done) {
     for (const JM& m : modes)
         if (m.ss < 0 || m.ds < 0) return TLB_OK;
     if (!aligned_to(sp, base_s, eb, 16) || !aligned_to(dp, base_d, eb, 16)) return TLB_OK;
-    static const int64_t kLb[] = {128, 64, 32};
+    static const int64_t kLb[] = {256, 128, 64, 32};
     for (int64_t Lb : kLb) {
+        if (Lb == 256 && !lb256_enabled()) continue;
         std::vector<JM> work = modes, A, B;
         if (!take_run(&work, true, La, &A)) break; // the A run does not depend on Lb
         if (!take_run(&work, false, Lb, &B)) continue;
@@ -739,11 +747,11 @@ int try_planned(const CopyCall& c, bool* done) {
         tiled_tma_kernel<EB, LB><<<grid_tma, kThreads, smem, c.stream>>>(map, TP, db);                                 \
     } while (0)
                     if (eb == 4) {
-                        if (Lb == 128) TLB_TILED_TMA(4, 128); else if (Lb == 64) TLB_TILED_TMA(4, 64); else TLB_TILED_TMA(4, 32);
+                        if (Lb == 256) TLB_TILED_TMA(4, 256); else if (Lb == 128) TLB_TILED_TMA(4, 128); else if (Lb == 64) TLB_TILED_TMA(4, 64); else TLB_TILED_TMA(4, 32);
                     } else if (eb == 8) {
-                        if (Lb == 128) TLB_TILED_TMA(8, 128); else if (Lb == 64) TLB_TILED_TMA(8, 64); else TLB_TILED_TMA(8, 32);
+                        if (Lb == 256) TLB_TILED_TMA(8, 256); else if (Lb == 128) TLB_TILED_TMA(8, 128); else if (Lb == 64) TLB_TILED_TMA(8, 64); else TLB_TILED_TMA(8, 32);
                     } else {
-                        if (Lb == 128) TLB_TILED_TMA(2, 128); else if (Lb == 64) TLB_TILED_TMA(2, 64); else TLB_TILED_TMA(2, 32);
+                        if (Lb == 256) TLB_TILED_TMA(2, 256); else if (Lb == 128) TLB_TILED_TMA(2, 128); else if (Lb == 64) TLB_TILED_TMA(2, 64); else TLB_TILED_TMA(2, 32);
                     }
 #undef TLB_TILED_TMA
                     count_launch();
@@ -764,11 +772,11 @@ int try_planned(const CopyCall& c, bool* done) {
         const unsigned grid = static_cast<unsigned>(tiles);
 #define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
         if (eb == 4) {
-            if (Lb == 128) TLB_TILED(4, 128); else if (Lb == 64) TLB_TILED(4, 64); else TLB_TILED(4, 32);
+            if (Lb == 256) TLB_TILED(4, 256); else if (Lb == 128) TLB_TILED(4, 128); else if (Lb == 64) TLB_TILED(4, 64); else TLB_TILED(4, 32);
         } else if (eb == 8) {
-            if (Lb == 128) TLB_TILED(8, 128); else if (Lb == 64) TLB_TILED(8, 64); else TLB_TILED(8, 32);
+            if (Lb == 256) TLB_TILED(8, 256); else if (Lb == 128) TLB_TILED(8, 128); else if (Lb == 64) TLB_TILED(8, 64); else TLB_TILED(8, 32);
         } else {
-            if (Lb == 128) TLB_TILED(2, 128); else if (Lb == 64) TLB_TILED(2, 64); else TLB_TILED(2, 32);
+            if (Lb == 256) TLB_TILED(2, 256); else if (Lb == 128) TLB_TILED(2, 128); else if (Lb == 64) TLB_TILED(2, 64); else TLB_TILED(2, 32);
         }
 #undef TLB_TILED
         count_launch();
