@@ -86,6 +86,26 @@ def test_compose_check_on_device():
     assert int(cnt.item()) > 0
 
 
+def test_locate_offsets_verification_on_device():
+    """locate_offsets (analysis.hpp:40-56) = compose(left_inverse(A), T) on the host, then the O(size(T)) loop
+    A(R(i)) == T(i) that decides admissibility. That loop is tlb_compose_check_range(A, R, T); goldens are the
+    reference's own (test_analysis.cpp:84-108): the TMEM-style lane-major accumulator row is admissible, the offset
+    that falls into the stride gap of (4,8):(1,5) is not."""
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    # (128,512):(16384,1) located by (1,128):(1,16384) is R = (1,128):(0,1)
+    host.compose_check_range("(128,512):(16384,1)", "(1,128):(0,1)", "(1,128):(1,16384)", 0, 128, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    # (4,8):(1,4) located by 5:7: R from the reference evaluates back to 7 i
+    host.compose_check_range("(4,8):(1,4)", "5:7", "5:7", 0, 5, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+    # (4,8):(1,5) against 2:4: compose(left_inverse(A), T) = 2:4, and A(4) = 5 != 4 -> admissibility_error upstream
+    host.compose_check_range("(4,8):(1,5)", "2:4", "2:4", 0, 2, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 1
+
+
 def test_idx2crd_and_crd2idx_roundtrip():
     text = "((3,2),((2,3),2)):((4,1),((2,15),100))"
     n = L(text).size
