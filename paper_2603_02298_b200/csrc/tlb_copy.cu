@@ -166,7 +166,22 @@ vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, ch
            uint64_t n_vec) {
     using T = typename Cell<VB>::type;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n_vec; v += stride) {
+    uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if constexpr (VB == 16) {
+        // four independent 16-byte loads in flight per thread before the first store (memory-level parallelism)
+        constexpr int U = 4;
+        for (; v + (U - 1) * stride < n_vec; v += U * stride) {
+            int64_t so[U], dof[U];
+            uint4 val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) dev_joint(J, v + u * stride, &so[u], &dof[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) val[u] = ldg_stream(src + so[u] * eb);
+#pragma unroll
+            for (int u = 0; u < U; ++u) stg_stream(dst + dof[u] * eb, val[u]);
+        }
+    }
+    for (; v < n_vec; v += stride) {
         int64_t so, dof;
         dev_joint(J, v, &so, &dof); // offsets in elements
         if constexpr (VB == 16) {

@@ -5,6 +5,7 @@
 // design rule is: one 16-byte coalesced store per thread per step, a grid of a few waves of
 // 148 SMs running a grid-stride loop, and a peel that costs a shift/mask per power-of-two
 // leaf (magic multiply otherwise) so the integer pipe stays far below the HBM write time.
+#include <algorithm>
 #include <cstdlib>
 
 #include "tlb_internal.h"
@@ -319,7 +320,9 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
         uint64_t groups_done = 0;
         if (wide && G >= 4 && groups >= 32 && !eval_no_warp()) {
             const uint64_t n_super = groups / 32;
-            const int gw = grid_for(n_super * 32);
+            // one superblock per warp: a grid-stride loop over a few waves leaves a ragged last pass (6 or 7
+            // superblocks per warp on C5: 7.03 TB/s against 7.34 TB/s with exactly one each)
+            const int gw = static_cast<int>(std::min<uint64_t>((n_super + kThreads / 32 - 1) / (kThreads / 32), 1u << 22));
 #define TLB_EVAL_W(GG)                                                                                   \
     do {                                                                                                 \
         if (p32) eval_warp_kernel<GG, true><<<gw, kThreads, 0, s>>>(*layout, i0, n_super, d_out);        \
