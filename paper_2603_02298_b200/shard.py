@@ -4,8 +4,9 @@ tests) is used only afterwards, to gather per-shard checksums for verification.
 
     copy / index maps   contiguous ranges of the integral coordinate, cut at whole slices of the outermost
                         mode so that every rank keeps the planned (vec / tiled) kernels
-    gemm                contiguous ranges of 128 x 256 output tiles (tlb_gemm_tile_count), cut at tile pairs
-                        so that every rank can run the cta_group::2 kernel; batched problems by whole batches
+    gemm                contiguous ranges of 128 x 256 output tiles (tlb_gemm_tile_count), cut at groups of 4 tiles
+                        (512 x 256 pair tiles) so that every rank keeps the wide cta_group::2 plan; batched problems
+                        by whole batches
 """
 from __future__ import annotations
 
@@ -37,8 +38,10 @@ def copy_range(layout: Layout | str, world: int, rank: int) -> tuple[int, int]:
 
 
 def gemm_tile_range(tile_count: int, world: int, rank: int) -> tuple[int, int]:
-    """Tile ids [begin, end) of `rank`; cuts fall on tile pairs (256 x 256 blocks)."""
-    return even_split(tile_count, world, rank, align=2)
+    """Tile ids [begin, end) of `rank`. Cuts fall on groups of 4 tiles (one 512 x 256 pair tile of the wide tcgen05
+    plan, which is two 256 x 256 blocks of the cta_group::2 plan) whenever that still deals every rank the same
+    number of tiles, else on tile pairs."""
+    return even_split(tile_count, world, rank, align=4 if tile_count % (4 * world) == 0 else 2)
 
 
 def batch_range(batches: int, world: int, rank: int) -> tuple[int, int]:
