@@ -74,7 +74,7 @@ struct WideArgs {
     uint32_t hints;           // L2 hints: 1 = operand loads evict_last, 2 = C reductions evict_first
     uint32_t stagger_kb;      // rotation of the first whole tile: phi(worker) = stagger_kb * worker / workers k-blocks
     uint32_t debug;           // TLB_GEMM_DEBUG timing experiments (garbage results): 1 = no TMA loads once the ring is
-                              // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only
+                              // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only, 32 = all reductions into the first tile
     uint32_t sk_cut[kMaxWorkers + 1]; // k-range [sk_cut[w], sk_cut[w+1]) of the stream-K tiles owned by worker w
     long long* clk;
     long long* cta_times;     // optional (TLB_GEMM_CTA_TIMES=<file>): {globaltimer at entry, at exit} of every CTA
@@ -378,8 +378,12 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         while (sched.next(args, kblocks, &it)) {
             uint32_t batch, m_tile, n_blk;
             decode_pair_tile(args, it.unit, &batch, &m_tile, &n_blk);
-            const int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC + static_cast<int>(quad) * 32;
-            const int n0 = static_cast<int>(n_blk) * BN + static_cast<int>(colh) * (BN / 2);
+            int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC + static_cast<int>(quad) * 32;
+            int n0 = static_cast<int>(n_blk) * BN + static_cast<int>(colh) * (BN / 2);
+            if (args.debug & 32u) {  // timing experiment: every CTA reduces into the first tile (L2-resident, no DRAM traffic)
+                m0 = static_cast<int>(rank) * BMC + static_cast<int>(quad) * 32;
+                n0 = static_cast<int>(colh) * (BN / 2);
+            }
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 mbar_wait_sleep(tfull_bar(h), acc_phase);
@@ -388,10 +392,14 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 for (int ci = 0; ci < 4; ++ci, ++chunk_no) {
                     const uint32_t buf = buf0 + (chunk_no % kEpiBufs) * kEpiWarpBytes;
                     uint32_t v[32];
+                    long long* et = (args.cta_times && blockIdx.x == 0 && warp == 0 && lane == 0 && chunk_no < 12) ? args.cta_times + 320 + chunk_no * 5 : nullptr;
+                    if (et) et[0] = clock64();
                     tmem_ld32(tmem_base + ((quad * 32u) << 16) + h * BN + colh * (BN / 2) + ci * 32, v);
                     // the reduction that last used this warp's staging tile must have read it
                     if (lane == 0) bulk_wait_read<kEpiBufs - 1>();
+                    if (et) et[1] = clock64();
                     tmem_ld_wait();
+                    if (et) et[2] = clock64();
                     if (ci == 3) {
                         // every TMEM read of this half is done: hand it back to the MMA warp
                         tc_fence_before();
@@ -409,6 +417,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                                          : "memory");
                         fence_async_smem();
                         __syncwarp();
+                        if (et) et[3] = clock64();
                         if (lane == 0 && !(args.debug & 8u)) {
                             if (args.debug & 4u)  // timing experiment: plain store instead of the L2 reduction
                                 asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&map_c),
@@ -418,6 +427,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                             else
                                 tma_reduce_add_3d(&map_c, buf, n0 + ci * 32, m0 + h * BMH, static_cast<int>(batch));
                             bulk_commit();
+                            if (et) et[4] = clock64();
                         }
                     }
                 }
@@ -447,7 +457,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 }
 
 // TLB_GEMM_CTA_TIMES=<file>: per-CTA entry / exit times of the last 64 launches (debug; dumped at process exit).
-constexpr int kCtaRing = 64, kCtaSlots = 2 * 160;
+constexpr int kCtaRing = 64, kCtaSlots = 2 * 160 + 64; // + 64: epilogue step stamps of CTA 0 / warp 0 (debug)
 long long* g_cta_host = nullptr;
 long long* g_cta_dev = nullptr;
 unsigned g_cta_next = 0;
