@@ -133,6 +133,22 @@ class Layout:
             n *= e
         return n
 
+    @property
+    def cosize(self) -> int:
+        """Buffer extent the layout addresses (cosize, layout.hpp:277), from the lowered descriptor."""
+        return int(self.lower().cosize)
+
+    def top_sizes(self) -> list:
+        """Size of every top-level mode (product of its leaves)."""
+        out, r = [], 0
+        for n in self.top_leaves:
+            s = 1
+            for e, *_ in self.modes[r:r + n]:
+                s *= e
+            out.append(s)
+            r += n
+        return out
+
     def mode_array(self):
         arr = (abi.tlb_mode * len(self.modes))()
         for r, (e, k, v, ax) in enumerate(self.modes):

@@ -72,3 +72,14 @@ def test_tensormap_dims_from_divided_layouts():
     with pytest.raises(TlbError) as e:
         host.tensormap_describe("(8,8):(f1,f9)", "(8,8):(f1,f9)")            # Xor strides
     assert e.value.status == abi.TLB_ERR_SEMIMODULE
+
+
+def test_cli_plan_and_exit_codes(capsys):
+    """python -m paper_2603_02298_b200: exit codes follow the reference CLI (cli.hpp:215-221)."""
+    import json
+    from paper_2603_02298_b200.__main__ import main
+    assert main(["plan", "(8192,8192):(8192,1)", "(8192,8192):(1,8192)", "--elem-bytes", "4"]) == 0
+    assert json.loads(capsys.readouterr().out)["plan"] == "tiled"
+    assert main(["plan", "8:1", "4:1"]) == 1            # contract_error: sizes differ
+    assert main(["plan", "8:1", "(4"]) == 2             # parse error
+    assert main(["nonsense"]) == 2                      # usage
