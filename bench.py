@@ -52,10 +52,10 @@ class ClockSampler:
         self.rows = []
         self.proc = None
 
-    def start(self):
+    def start(self, period_ms: int = 100):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", str(period_ms), "-i", str(self.index)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._pump, daemon=True).start()
         except OSError:
@@ -71,18 +71,19 @@ class ClockSampler:
         time.sleep(0.15)
         self.proc.terminate()
         rows = [r for (t, r) in self.rows if t0 - 0.05 <= t <= t1 + 0.15] or [r for (_, r) in self.rows]
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = float(r[2])
+                pw.append(float(r[3]))
             except (ValueError, IndexError):
                 continue
             for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[5:9]):
                 if val.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 def dist_env():
@@ -261,6 +262,21 @@ def run_ours(args):
             if clocks.get("sm_max_mhz") and mhz.value < 0.97 * clocks["sm_max_mhz"] and not clocks["reasons"]:
                 clocks["note"] = "SM clock below max inside the kernel: power management under tensor load (sw_power_cap regime)"
     flops = 2.0 * M * N * Kd
+    if rank == 0 and world == 1:
+        # An untimed half-second loop of the same step with nvidia-smi sampling every 20 ms: long enough for the samples
+        # to see the load (the timed region is not), it records the power-capped operating point as context.
+        probe = ClockSampler(local)
+        probe.start(20)
+        time.sleep(0.1)
+        n_probe = max(50, int(0.5 / max(sec / K, 1e-6)))
+        p0 = time.time()
+        psec = timed(torch, dist, 1, gemm_step, n_probe, 0)
+        p1 = time.time()
+        pc = probe.stop(p0 + 0.1, p1)
+        clocks["sustained_probe"] = {"steps": n_probe, "seconds": round(psec, 3), "tflops": flops * n_probe / psec / 1e12,
+                                     "sm_mhz": pc["sm_mhz"], "power_w": pc.get("power_w"), "reasons": pc["reasons"],
+                                     "samples": pc.get("samples")}
+        lib.tlb_gemm_clock_stats(C.byref(mhz), C.byref(us), C.byref(nl))   # drop the probe's stamps
     value = flops * K * world / sec / 1e12
     kernel_s = sec / K
     burst = sec < 1.0
@@ -304,14 +320,14 @@ def run_ours(args):
     # does not read it; this path reads and writes fp32 C), and torch's copy_ on the C1 footprint
     library = None
     if rank == 0 and world == 1:
-        la_, lb_ = [(torch.rand(M, Kd, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)]
-        lsec = timed(torch, dist, 1, lambda i: torch.matmul(la_, lb_.t()), K, W)
+        lsets = [[(torch.rand(M, Kd, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)] for _ in range(nsets)]
+        lsec = timed(torch, dist, 1, lambda i: torch.matmul(lsets[i % nsets][0], lsets[i % nsets][1].t()), K, W)
         x_ = torch.empty(8192 * 8192, dtype=torch.float32, device="cuda")
         y_ = torch.empty_like(x_)
         csec = timed(torch, dist, 1, lambda i: y_.copy_(x_), K, W)
         library = {"cublas_bf16_4096_tflops": flops * K / lsec / 1e12, "torch_copy_512MiB_gbs": 2 * x_.numel() * 4 * K / csec / 1e9,
                    "note": "torch.matmul bf16->bf16 / torch copy_ timed in this process with the same recipe"}
-        del la_, lb_, x_, y_
+        del lsets, x_, y_
     del ha, hb, hc, sets
     torch.cuda.empty_cache()
 
