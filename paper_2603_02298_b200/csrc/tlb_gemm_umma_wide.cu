@@ -72,7 +72,6 @@ struct WideArgs {
     uint32_t sk_units;        // the tiles after them, cut into one k-range per worker
     uint32_t prefetch_c;      // 1: map_cp is valid
     uint32_t hints;           // L2 hints: 1 = operand loads evict_last, 2 = C reductions evict_first
-    uint32_t stagger_kb;      // rotation of the first whole tile: phi(worker) = stagger_kb * worker / workers k-blocks
     uint32_t debug;           // TLB_GEMM_DEBUG timing experiments (garbage results): 1 = no TMA loads once the ring is
                               // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only, 32 = all reductions into the first tile
     uint32_t sk_cut[kMaxWorkers + 1]; // k-range [sk_cut[w], sk_cut[w+1]) of the stream-K tiles owned by worker w
@@ -85,30 +84,19 @@ struct Item {
     int kb0, kb1;
 };
 
-// Work list of one worker, as an iterator every role walks identically:
-//   1. its k-range of the stream-K tiles (the partial wave), cut at tile boundaries;
-//   2. its whole tiles, round-robin. The FIRST whole tile is rotated: the worker runs k-blocks [phi, KB) now and
-//      [0, phi) as its very last item, with phi growing with the worker index. Every worker still does the same
-//      number of k-blocks, but tile boundaries (and with them the bursts of C traffic of the epilogues, 256 KiB per
-//      CTA) no longer coincide across the chip: one pair's epilogue overlaps its neighbours' main loops.
+// Work list of one worker, as an iterator every role walks identically: first its k-range of the stream-K tiles (the
+// partial wave), cut at tile boundaries, then its whole tiles, round-robin.
 struct Sched {
     uint64_t sk_lo, sk_hi;
-    uint32_t worker, n_workers, dp_next;
-    int phi;
-    bool first_done, tail_pending;
-    __device__ void init(const WideArgs& a, uint32_t w, uint32_t W, int kblocks) {
-        worker = w;
+    uint32_t n_workers, dp_next;
+    __device__ void init(const WideArgs& a, uint32_t w, uint32_t W) {
         n_workers = W;
         dp_next = w;
-        first_done = false;
-        tail_pending = false;
         sk_lo = sk_hi = 0;
         if (a.sk_units) {
             sk_lo = a.sk_cut[w];
             sk_hi = a.sk_cut[w + 1];
         }
-        phi = static_cast<int>(static_cast<uint64_t>(a.stagger_kb) * w / W);
-        if (phi < kMinSeg || kblocks - phi < kMinSeg) phi = 0;
     }
     __device__ __forceinline__ bool next(const WideArgs& a, int kblocks, Item* it) {
         if (sk_lo < sk_hi) {
@@ -123,19 +111,7 @@ struct Sched {
             it->unit = a.unit_begin + dp_next;
             it->kb0 = 0;
             it->kb1 = kblocks;
-            if (!first_done && phi > 0) {
-                it->kb0 = phi;
-                tail_pending = true;
-            }
-            first_done = true;
             dp_next += n_workers;
-            return true;
-        }
-        if (tail_pending) {
-            tail_pending = false;
-            it->unit = a.unit_begin + worker;
-            it->kb0 = 0;
-            it->kb1 = phi;
             return true;
         }
         return false;
@@ -240,7 +216,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     }
 
     Sched sched;
-    sched.init(args, worker, n_workers, kblocks);
+    sched.init(args, worker, n_workers);
 
     if (warp == kProducerWarp) {
         // ===== TMA producer (whole warp in the loops, one elected lane issues) =====
@@ -643,12 +619,6 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
         stream_k_cuts(a.sk_units, static_cast<uint32_t>(kblocks), W, epi, a.sk_cut);
     }
     const uint32_t workers = a.sk_units ? W : std::min(units, W);
-    {
-        // stagger: sixteenths of a tile's k-blocks over which the tile boundaries of the workers are spread
-        int sixteenths = 0; // measured: staggering does not pay (the extra partial epilogue costs more than the overlap gains)
-        if (const char* e = std::getenv("TLB_GEMM_STAGGER")) sixteenths = std::max(0, std::min(16, std::atoi(e)));
-        a.stagger_kb = (p.split_tail && workers == W) ? static_cast<uint32_t>(static_cast<int64_t>(kblocks) * sixteenths / 16) : 0u;
-    }
     a.clk = umma_clk_slot();
     a.cta_times = cta_times_slot();
     cudaLaunchConfig_t cfg = {};
