@@ -220,10 +220,44 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
                                             int64_t base_d) {
     using T = typename Cell<EB>::type;
     constexpr int V = 16 / EB;
-    constexpr int LOGV = (V == 2) ? 1 : (V == 4) ? 2 : 3;
-    constexpr int NR = 3 - LOGV;
-    constexpr int CW = 8 >> NR;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr ((EB == 2 && LB % 64 == 0) || (EB == 1 && LB % 128 == 0)) {
+        // 1- and 2-byte cells: 8 lanes x V b are one full 128-byte destination line, so the 8 lanes that share a chunk
+        // must sit in ONE shared-memory phase. Their rows r0 + j agree mod 8 (an 8-way bank conflict under the
+        // swizzle), so lane bb reads its rows rotated, r0 + ((j + bb) mod V), which makes the phase conflict free, and
+        // a 3-stage barrel rotation of the V vectors puts them back in row order before the register transpose.
+        const int bb = lane & 7, cg = lane >> 3;
+        constexpr int NWT2 = (LB / (8 * V)) * 2;       // 8 V rows x 4 chunks per warp-tile
+        for (int wt = warp; wt < NWT2; wt += kThreads / 32) {
+            const int c = (wt & 1) * 4 + cg;
+            const int r0 = (wt >> 1) * (8 * V) + bb * V;
+            union { uint4 v; T e[V]; } in[V], out;
+#pragma unroll
+            for (int j = 0; j < V; ++j) in[j].v = *reinterpret_cast<const uint4*>(tile + swz(r0 + ((j + bb) & (V - 1)), c));
+            // in[j] holds row r0 + ((j + bb) mod V); rotate so that in[k] holds row r0 + k: new[k] = old[(k - bb) mod V]
+#pragma unroll
+            for (int s = 1; s < 8; s <<= 1) {
+                if (bb & s) {
+                    uint4 t[V];
+#pragma unroll
+                    for (int k = 0; k < V; ++k) t[k] = in[(k - s) & (V - 1)].v;
+#pragma unroll
+                    for (int k = 0; k < V; ++k) in[k].v = t[k];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+#pragma unroll
+                for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
+                stg_stream(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+            }
+        }
+        return;
+    }
+    static_assert(EB != 1 || LB % 128 == 0, "1-byte cells need 128-row tiles");
+    constexpr int LOGV = (V == 2) ? 1 : (V == 4) ? 2 : 3;
+    constexpr int NR = EB == 1 ? 0 : 3 - LOGV;
+    constexpr int CW = 8 >> NR;
     const int q = lane & 7, p = lane >> 3;
     const int bb = (q & ((1 << NR) - 1)) | (p << NR);
     const int cl = q >> NR;
@@ -670,7 +704,7 @@ int try_planned(const CopyCall& c, bool* done) {
     if (ia == ib) return TLB_OK;
 
     // ---- tiled plan
-    if (eb != 2 && eb != 4 && eb != 8) return TLB_OK;
+    if (eb != 1 && eb != 2 && eb != 4 && eb != 8) return TLB_OK;
     const int64_t V = 16 / eb, La = 128 / eb;
     for (const JM& m : modes)
         if (m.ss < 0 || m.ds < 0) return TLB_OK;
@@ -678,6 +712,7 @@ int try_planned(const CopyCall& c, bool* done) {
     static const int64_t kLb[] = {256, 128, 64, 32};
     for (int64_t Lb : kLb) {
         if (Lb == 256 && !lb256_enabled()) continue;
+        if (eb == 1 && (Lb < 128 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 1-byte cells: LDG-staged, 128+ rows
         std::vector<JM> work = modes, A, B;
         if (!take_run(&work, true, La, &A)) break; // the A run does not depend on Lb
         if (!take_run(&work, false, Lb, &B)) continue;
@@ -786,7 +821,9 @@ int try_planned(const CopyCall& c, bool* done) {
         }
         const unsigned grid = static_cast<unsigned>(tiles);
 #define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
-        if (eb == 4) {
+        if (eb == 1) {
+            if (Lb == 256) TLB_TILED(1, 256); else TLB_TILED(1, 128);
+        } else if (eb == 4) {
             if (Lb == 256) TLB_TILED(4, 256); else if (Lb == 128) TLB_TILED(4, 128); else if (Lb == 64) TLB_TILED(4, 64); else TLB_TILED(4, 32);
         } else if (eb == 8) {
             if (Lb == 256) TLB_TILED(8, 256); else if (Lb == 128) TLB_TILED(8, 128); else if (Lb == 64) TLB_TILED(8, 64); else TLB_TILED(8, 32);

@@ -45,6 +45,18 @@ def test_copy_table1_all_element_sizes(eb):
         run_copy_case(s, d, eb)
 
 
+@pytest.mark.parametrize("s,d", [
+    ("(256,128):(128,1)", "(256,128):(1,256)"),                           # 256-row tiles
+    ("(128,384):(1,128)", "(128,384):(384,1)"),                           # 128-row tiles, three 128-byte column blocks
+    ("((8,128),(4,64),4):((1,2048),(8,32),262144)", "((8,128),(4,64),4):((128,1),(65536,1024),262144)"),  # C3, 4 tiles
+    ("(512,128,3):(128,1,65536)", "(512,128,3):(1,512,65536)"),           # batched transpose
+])
+def test_copy_tiled_plan_one_byte_cells(s, d):
+    """1-byte cells (fp8-sized): 16 x 16 byte blocks per lane, rotated row reads + barrel rotation, full-line stores."""
+    assert run_copy_case(s, d, 1) == "tiled"
+    assert run_copy_case("(96,160):(160,1)", "(96,160):(1,96)", 1) == "gather"   # no 128-row B run
+
+
 @pytest.mark.parametrize("eb", [2, 4, 8])
 @pytest.mark.parametrize("s,d", [
     ("(256,128):(128,1)", "(256,128):(1,256)"),                           # C1 shape in small
