@@ -177,13 +177,19 @@ int tlb_tensormap_fetch_tile(const void* tensormap_128B, int rank, const int32_t
 /* ---- (5) tiled GEMM (configs C2, C4) ----------------------------------- */
 /* tla::gemm(A, B, C) (tensor.hpp:214-233): C(m,n) += sum_k A(m,k) * B(n,k), all rank 2.
  * bf16 x bf16 -> fp32, accumulator starts from C. tile_begin/tile_end select a range of the
- * 128 x 256 output tiles (ids from tlb_gemm_tile_count; pairs (2g, 2g+1) form 256 x 256 blocks walked in
- * an L2-friendly order; pass 0 and UINT32_MAX for all) so 1/2/4/8 GPUs can shard one problem by
- * tile-coordinate ranges. The ids refer to the tiling of the plan the library selects, which runs the
- * problem transposed when C is m-contiguous; every range partition of [0, count) covers C exactly once.
- * K-major A and B with M-contiguous or N-contiguous C run on tcgen05 (TMA -> swizzled smem ->
- * UMMA -> TMEM); every other layout family (NT, BLIS strides, GETT folded modes, Xor) runs on the
- * layout-evaluating SIMT kernel. A.elem_bytes = B.elem_bytes = 2, C.elem_bytes = 4. */
+ * 128 x 256 output tiles (ids from tlb_gemm_tile_count; pairs (2g, 2g+1) form 256 x 256 blocks and, when
+ * ceil(rows / 256) is even, quadruples (4g .. 4g+3) form 512 x 256 pair tiles, walked in an L2-friendly order;
+ * pass 0 and UINT32_MAX for all) so 1/2/4/8 GPUs can shard one problem by tile-coordinate ranges. Ranges
+ * aligned to 4 tiles keep the wide (512 x 256) tcgen05 plan, ranges aligned to 2 the 256 x 256 plan. The ids
+ * refer to the tiling of the plan the library selects, which runs the problem transposed when C is
+ * m-contiguous; every range partition of [0, count) covers C exactly once.
+ * Operands whose modes coalesce to one stride each with either mode contiguous (K-major "T" or MN-major "N":
+ * the TN, NT and NTT rows of PAPER.md:1766-1771) and an M- or N-contiguous C run on tcgen05 (TMA -> swizzled
+ * smem -> UMMA -> TMEM -> TMA reduce-add); every other layout family (BLIS strides, GETT folded modes, Xor,
+ * leading dimensions TMA cannot address) runs on the layout-evaluating SIMT kernel.
+ * Partial tiles of the last wave are summed by several CTA pairs through L2 reductions, so fp32 sums are not
+ * bitwise reproducible from run to run unless TLB_GEMM_SPLIT_TAIL=0 is set in the environment.
+ * A.elem_bytes = B.elem_bytes = 2, C.elem_bytes = 4. */
 int tlb_gemm_bf16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin,
                   uint32_t tile_end, void* stream);
 /* Number of output tiles of one problem under the plan tlb_gemm_bf16 would choose (host-only, no device
