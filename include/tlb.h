@@ -200,6 +200,13 @@ int tlb_gemm_tile_count(const tlb_tensor* A, const tlb_tensor* B, const tlb_tens
 int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_batch_stride,
                           int64_t b_batch_stride, int64_t c_batch_stride, int32_t batch_begin,
                           int32_t batch_end, void* stream);
+/* Same contracts with IEEE fp16 operands (fp16 x fp16 products are exact in fp32 as well; tcgen05 kind::f16 takes
+ * either format through the instruction descriptor). */
+int tlb_gemm_f16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin, uint32_t tile_end,
+                 void* stream);
+int tlb_gemm_f16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_batch_stride,
+                         int64_t b_batch_stride, int64_t c_batch_stride, int32_t batch_begin, int32_t batch_end,
+                         void* stream);
 /* The reference's own value type: int64 cells, wrapping detected as overflow_error
  * (checked_add/checked_mul, common.hpp:99-109) through *d_status (int32 on device, caller zeroes;
  * set to TLB_ERR_OVERFLOW). All elem_bytes = 8. Any layouts. */

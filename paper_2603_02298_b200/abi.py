@@ -73,6 +73,9 @@ SYMBOLS = {
     "tlb_gemm_tile_count": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), _P(C.c_uint32)]),
     "tlb_gemm_bf16_batched": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_int64, C.c_int64, C.c_int64,
                                         C.c_int32, C.c_int32, C.c_void_p]),
+    "tlb_gemm_f16": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_uint32, C.c_uint32, C.c_void_p]),
+    "tlb_gemm_f16_batched": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_int64, C.c_int64, C.c_int64,
+                                       C.c_int32, C.c_int32, C.c_void_p]),
     "tlb_gemm_i64": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_void_p, C.c_void_p]),
     "tlb_gemm_set_path": (C.c_int, [C.c_int]),
     "tlb_gemm_clock_stats": (C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_uint32)]),

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "tlb_internal.h"
 #include "tlb_gemm.h"
@@ -38,6 +39,7 @@ struct SimtArgs {
     TileGrid grid;
     uint32_t tile_begin, tile_end; // global tile ids (batch-major)
     int32_t batch_begin, batch_end;
+    int32_t ab_f16; // 2-byte operands are fp16 instead of bf16
 };
 
 __device__ __forceinline__ int64_t combine(int kind, int64_t a, int64_t b) { return kind == TLB_KIND_XOR ? (a ^ b) : (a + b); }
@@ -84,13 +86,16 @@ gemm_simt_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_consta
                 c[cp] = acc;
             }
         } else {
-            const __nv_bfloat16* a = static_cast<const __nv_bfloat16*>(A) + batch * p.a_bs;
-            const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(B) + batch * p.b_bs;
+            const uint16_t* a = static_cast<const uint16_t*>(A) + batch * p.a_bs;
+            const uint16_t* b = static_cast<const uint16_t*>(B) + batch * p.b_bs;
             float* c = static_cast<float*>(C);
             float acc = c[cp];
+            // bf16 x bf16 and fp16 x fp16 products are exact in fp32, so fma(x, y, acc) == acc + x * y
             for (int64_t k = 0; k < p.K; ++k) {
-                const float x = __bfloat162float(a[dev_position(LA, p.a_origin, combine(LA.kind, a_m, dev_eval_top(LA, 1, k)))]);
-                const float y = __bfloat162float(b[dev_position(LB, p.b_origin, combine(LB.kind, b_n, dev_eval_top(LB, 1, k)))]);
+                const uint16_t xb = a[dev_position(LA, p.a_origin, combine(LA.kind, a_m, dev_eval_top(LA, 1, k)))];
+                const uint16_t yb = b[dev_position(LB, p.b_origin, combine(LB.kind, b_n, dev_eval_top(LB, 1, k)))];
+                const float x = p.ab_f16 ? __half2float(__ushort_as_half(xb)) : __uint_as_float(static_cast<uint32_t>(xb) << 16);
+                const float y = p.ab_f16 ? __half2float(__ushort_as_half(yb)) : __uint_as_float(static_cast<uint32_t>(yb) << 16);
                 acc = __fmaf_rn(x, y, acc);
             }
             c[cp] = acc;
@@ -230,7 +235,7 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
 
 int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool i64, int64_t a_bs, int64_t b_bs,
              int64_t c_bs, int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, int* d_status,
-             cudaStream_t stream, uint32_t* count_only = nullptr) {
+             cudaStream_t stream, uint32_t* count_only = nullptr, bool f16 = false) {
     GemmDims d;
     TLB_TRY(check_gemm(A, B, C, i64 ? 8 : 2, i64 ? 8 : 4, &d));
     if (batch_begin < 0 || batch_end < batch_begin) return fail(TLB_ERR_CONTRACT, "tlb_gemm: bad batch range");
@@ -270,6 +275,7 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
             p.split_tail = split_tail_enabled() ? 1 : 0;
             p.cta_group = g_gemm_path == 2 ? 1 : g_gemm_path == 3 ? 2 : (even ? 2 : 1);
             p.full_range = (t0 == 0 && t1 == tpb * static_cast<uint64_t>(batch_end)) ? 1 : 0;
+            p.ab_f16 = f16 ? 1 : 0;
             const bool mn_major = p.a_mn || p.b_mn;
             if (!mn_major || umma_wide_applies(p)) {
                 if (p.cta_group == 2 && !even)
@@ -303,6 +309,7 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
     p.tile_end = static_cast<uint32_t>(t1);
     p.batch_begin = batch_begin;
     p.batch_end = batch_end;
+    p.ab_f16 = f16 ? 1 : 0;
     const uint64_t total = static_cast<uint64_t>(d.M) * d.N * (batch_end - batch_begin);
     const uint64_t blocks = std::min<uint64_t>((total + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 32);
     const int gridx = static_cast<int>(std::max<uint64_t>(blocks, 1));
@@ -312,7 +319,7 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
         gemm_simt_kernel<false><<<gridx, kThreads, 0, stream>>>(*A->layout, *B->layout, *C->layout, A->data, B->data, C->data, p, nullptr);
     count_launch();
     TLB_CUDA(cudaGetLastError());
-    set_plan(i64 ? "simt_i64" : "simt_bf16");
+    set_plan(i64 ? "simt_i64" : f16 ? "simt_f16" : "simt_bf16");
     return TLB_OK;
 }
 
@@ -337,6 +344,19 @@ int tlb_gemm_bf16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_te
                           void* stream) {
     return tlb::run_gemm(A, B, C, false, a_batch_stride, b_batch_stride, c_batch_stride, batch_begin, batch_end, 0,
                          UINT32_MAX, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int tlb_gemm_f16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin, uint32_t tile_end,
+                 void* stream) {
+    return tlb::run_gemm(A, B, C, false, 0, 0, 0, 0, 1, tile_begin, tile_end, nullptr, static_cast<cudaStream_t>(stream),
+                         nullptr, true);
+}
+
+int tlb_gemm_f16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_batch_stride,
+                         int64_t b_batch_stride, int64_t c_batch_stride, int32_t batch_begin, int32_t batch_end,
+                         void* stream) {
+    return tlb::run_gemm(A, B, C, false, a_batch_stride, b_batch_stride, c_batch_stride, batch_begin, batch_end, 0,
+                         UINT32_MAX, nullptr, static_cast<cudaStream_t>(stream), nullptr, true);
 }
 
 int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream) {

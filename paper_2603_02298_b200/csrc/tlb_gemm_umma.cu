@@ -91,6 +91,7 @@ struct UmmaArgs {
                                    // the ring is filled once, 2 = epilogue without smem / global traffic,
                                    // 4 = no staging stores, 8 = no TMA store
     long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
+    uint32_t ab_f16;               // operands are fp16 (A / B format fields of the instruction descriptor = 0)
     long long* clk;                // optional (TLB_GEMM_CLOCK=1): CTA 0 stamps {clock64, globaltimer} at entry and exit
 };
 constexpr int kTraceSlots = 128;
@@ -274,7 +275,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         // ===== MMA issuer (leader CTA only under cta_group::2). Control flow is warp-uniform; one elected
         // lane issues the MMAs and the commits (tcgen05.commit tracks the MMAs of the issuing thread). =====
         if (leader) {
-            constexpr uint32_t idesc = make_idesc<CG>();
+            // A / B format fields (bits 7-9, 10-12): 1 = bf16, 0 = fp16
+            const uint32_t idesc = args.ab_f16 ? (make_idesc<CG>() & ~((1u << 7) | (1u << 10))) : make_idesc<CG>();
             const uint32_t a_lo0 = desc_lo(a_stage(0)), b_lo0 = desc_lo(b_stage(0));
             int stage = 0;
             uint32_t phase = 0, acc = 0, acc_phase = 0;
@@ -572,6 +574,7 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
     a.M = p.M;
     a.N = p.N;
     a.K = p.K;
+    a.ab_f16 = p.ab_f16 ? 1u : 0u;
     a.mb = (p.M + 255) / 256;
     a.nb = (p.N + 255) / 256;
     {

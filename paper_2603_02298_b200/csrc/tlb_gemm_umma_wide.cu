@@ -66,6 +66,7 @@ struct WideArgs {
     int32_t M, N, K;
     uint32_t mbw, nb;         // 512-row pair tiles along m, 256-column blocks along n
     uint32_t group_w;         // pair tiles (along m) per rasterisation group
+    uint32_t ab_f16;          // operands are fp16 instead of bf16
     uint32_t a_mn, b_mn;      // operand is MN-major: staged as 64-row chunks of [64 k][128 B], MN-major UMMA descriptors
     uint32_t unit_begin;      // first 512 x 256 pair tile of the range (all batches)
     uint32_t dp_units;        // whole tiles, dealt round-robin
@@ -279,7 +280,8 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             // Descriptors: K-major tiles are rows of 128 B with 8-row groups 1024 B apart (SBO), a k-step of 16 advances
             // the start by 32 B; MN-major tiles are 64-row chunks of [64 k][128 B]: 8-k groups 1024 B apart (SBO), chunks
             // 8192 B apart (LBO), a k-step of 16 advances the start by 2 KiB. idesc bits 15 / 16 select MN-major A / B.
-            const uint32_t idesc = kIdescW | (args.a_mn ? (1u << 15) : 0u) | (args.b_mn ? (1u << 16) : 0u);
+            const uint32_t idesc = (args.ab_f16 ? (kIdescW & ~((1u << 7) | (1u << 10))) : kIdescW) | (args.a_mn ? (1u << 15) : 0u) |
+                                   (args.b_mn ? (1u << 16) : 0u);
             const uint32_t a_lbo = args.a_mn ? ((8192u >> 4) << 16) : (1u << 16), b_lbo = args.b_mn ? ((8192u >> 4) << 16) : (1u << 16);
             const uint32_t a_kstep = args.a_mn ? (2048u >> 4) : 2u, b_kstep = args.b_mn ? (2048u >> 4) : 2u;
             const uint32_t a_base = ((a_stage(0) >> 4) & 0x3fffu), b_base = ((b_stage(0) >> 4) & 0x3fffu);
@@ -579,6 +581,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     a.K = p.K;
     a.mbw = static_cast<uint32_t>((p.M + 511) / 512);
     a.nb = static_cast<uint32_t>((p.N + 255) / 256);
+    a.ab_f16 = p.ab_f16 ? 1u : 0u;
     a.a_mn = p.a_mn ? 1u : 0u;
     a.b_mn = p.b_mn ? 1u : 0u;
     {

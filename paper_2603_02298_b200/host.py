@@ -235,6 +235,12 @@ def gemm_bf16(a, b, c, tile_begin: int = 0, tile_end: int = 2**32 - 1, stream=No
     return lib.tlb_last_plan().decode()
 
 
+def gemm_f16(a, b, c, tile_begin: int = 0, tile_end: int = 2**32 - 1, stream=None) -> str:
+    lib = abi.load()
+    abi.check(lib.tlb_gemm_f16(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), tile_begin, tile_end, _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
 def gemm_tile_count(a, b, c) -> int:
     n = C.c_uint32(0)
     abi.check(abi.load().tlb_gemm_tile_count(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), C.byref(n)))

@@ -39,6 +39,7 @@ def orc():
         _orc.orc_copy.restype = C.c_int
         _orc.orc_gemm_i64.restype = C.c_int
         _orc.orc_gemm_bf16.restype = C.c_int
+        _orc.orc_gemm_f16.restype = C.c_int
         _orc.orc_gemm_bf16_tn_flat.restype = C.c_int
         _orc.orc_crd2idx_range.restype = C.c_int
     return _orc
@@ -128,8 +129,9 @@ def orc_gemm_i64(la, a: np.ndarray, lb, b: np.ndarray, lc, c: np.ndarray) -> int
 
 
 def orc_gemm_bf16(la, a_bits: np.ndarray, lb, b_bits: np.ndarray, lc, c: np.ndarray, want_abs=False, m_begin=0,
-                  m_end=None):
-    """Sequential-k fp32 restatement on bf16 bit patterns (uint16). Returns (status, abs_sum or None)."""
+                  m_end=None, f16=False):
+    """Sequential-k fp32 restatement on bf16 (or, with f16=True, IEEE fp16) bit patterns (uint16).
+    Returns (status, abs_sum or None)."""
     la, lb, lc = as_layout(la), as_layout(lb), as_layout(lc)
     am, an = modes_of(la)
     bm, bn = modes_of(lb)
@@ -138,7 +140,8 @@ def orc_gemm_bf16(la, a_bits: np.ndarray, lb, b_bits: np.ndarray, lc, c: np.ndar
     for e, *_ in la.modes[:la.top_leaves[0]]:
         M *= e
     ab = np.zeros(c.size, dtype=np.float32) if want_abs else None
-    st = orc().orc_gemm_bf16(am, an, la.top_leaves[0], _p(a_bits), C.c_int64(a_bits.size), bm, bn, lb.top_leaves[0],
+    fn = orc().orc_gemm_f16 if f16 else orc().orc_gemm_bf16
+    st = fn(am, an, la.top_leaves[0], _p(a_bits), C.c_int64(a_bits.size), bm, bn, lb.top_leaves[0],
                              _p(b_bits), C.c_int64(b_bits.size), cm, cn, lc.top_leaves[0], _p(c), C.c_int64(c.size),
                              _p(ab) if want_abs else None, C.c_int64(m_begin), C.c_int64(M if m_end is None else m_end))
     return st, ab

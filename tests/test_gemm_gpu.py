@@ -64,7 +64,7 @@ def test_gemm_zero_a_and_preconditions():
     assert e.value.status == abi.TLB_ERR_CONTRACT
 
 
-def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True):
+def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True, f16=False):
     M, N, K = _dims(la, lb)
     na, nb, nc = ou.cosize_of(la), ou.cosize_of(lb), ou.cosize_of(lc)
     rng = np.random.default_rng(seed)
@@ -82,9 +82,12 @@ def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True):
         a[ao] = rng.uniform(-1, 1, (M, K))
         b[bo] = rng.uniform(-1, 1, (N, K))
         c0 = rng.uniform(-1, 1, nc).astype(np.float32) if c_init else np.zeros(nc, dtype=np.float32)
-    ab, bb = ou.f32_to_bf16_bits(a), ou.f32_to_bf16_bits(b)
+    if f16:
+        ab, bb = a.astype(np.float16).view(np.uint16), b.astype(np.float16).view(np.uint16)
+    else:
+        ab, bb = ou.f32_to_bf16_bits(a), ou.f32_to_bf16_bits(b)
     want = c0.copy()
-    st, sabs = ou.orc_gemm_bf16(la, ab, lb, bb, lc, want, want_abs=True)
+    st, sabs = ou.orc_gemm_bf16(la, ab, lb, bb, lc, want, want_abs=True, f16=f16)
     assert st == 0
     ta_, tb_, tc_ = dev(ab.view(np.int16)), dev(bb.view(np.int16)), dev(c0)
     ta, ka = host.tensor_of(la, ta_, ranked=True)
@@ -92,7 +95,7 @@ def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True):
     tc, kc = host.tensor_of(lc, tc_, ranked=True)
     prev = abi.load().tlb_gemm_set_path(path)
     try:
-        plan = host.gemm_bf16((ta, ka), (tb, kb), (tc, kc))
+        plan = (host.gemm_f16 if f16 else host.gemm_bf16)((ta, ka), (tb, kb), (tc, kc))
     finally:
         abi.load().tlb_gemm_set_path(prev)
     torch.cuda.synchronize()
@@ -235,6 +238,18 @@ def test_gemm_bf16_mn_major_operands_on_tensor_cores_kat_exact(shape):
 @pytest.mark.parametrize("shape", MN_MAJOR_SHAPES[:2] + MN_MAJOR_SHAPES[4:])
 def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape):
     assert _bf16_case(*shape, kat=False, seed=13) == "umma_2sm_wide"
+
+
+@pytest.mark.parametrize("shape,path,plan", [
+    (UMMA_SHAPES[1], 2, "umma_1sm"), (UMMA_SHAPES[2], 3, "umma_2sm"), (UMMA_SHAPES[6], 3, "umma_2sm_regs"),
+    (WIDE_SHAPES[1], 0, "umma_2sm_wide"), (WIDE_SHAPES[2], 0, "umma_2sm_wide"), (MN_MAJOR_SHAPES[0], 0, "umma_2sm_wide"),
+    (("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)"), 0, "simt_f16"),
+])
+def test_gemm_f16_operands(shape, path, plan):
+    """tlb_gemm_f16: IEEE fp16 operands on every plan (instruction-descriptor formats 0 instead of 1), exact on the
+    reference's integer fills and within the stated tolerance on random data."""
+    assert _bf16_case(*shape, kat=True, path=path, f16=True) == plan
+    assert _bf16_case(*shape, kat=False, seed=17, path=path, f16=True) == plan
 
 
 def test_gemm_wide_plan_whole_tiles_then_k_ranges():
