@@ -215,7 +215,21 @@ __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return (r << 7
 
 // phase 2 of the tiled copy: each lane owns V x V element blocks; conflict-free 128-bit smem reads, register
 // transpose, 128-bit stores along B (lanes sharing a chunk cover 32 consecutive b).
-template <int EB, int LB>
+// 16 staged bytes -> global: one 128-bit store when the layouts guarantee 16-byte alignment (AL), V cell-sized stores
+// otherwise (unaligned bases / leading dimensions: the L2 merges them into full sectors before they reach HBM).
+template <int EB, bool AL> __device__ __forceinline__ void store_vec(char* p, const uint4& v) {
+    if constexpr (AL) {
+        stg_stream(p, v);
+    } else {
+        using T = typename Cell<EB>::type;
+        union { uint4 v; T e[16 / EB]; } u;
+        u.v = v;
+#pragma unroll
+        for (int k = 0; k < 16 / EB; ++k) reinterpret_cast<T*>(p)[k] = u.e[k];
+    }
+}
+
+template <int EB, int LB, bool AL = true>
 __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int64_t* s_offA, char* __restrict__ dst,
                                             int64_t base_d) {
     using T = typename Cell<EB>::type;
@@ -249,7 +263,7 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
             for (int i = 0; i < V; ++i) {
 #pragma unroll
                 for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
-                stg_stream(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+                store_vec<EB, AL>(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
             }
         }
         return;
@@ -273,12 +287,12 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
         for (int i = 0; i < V; ++i) {
 #pragma unroll
             for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
-            stg_stream(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+            store_vec<EB, AL>(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
         }
     }
 }
 
-template <int EB, int LB>
+template <int EB, int LB, bool AL = true>
 __global__ void __launch_bounds__(kThreads)
 tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src, char* __restrict__ dst) {
     constexpr int V = 16 / EB;                         // elements per 16-byte vector
@@ -315,7 +329,16 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
         const int v = threadIdx.x + u * kThreads;
         if (NVEC % kThreads == 0 || v < NVEC) {
             const int c = v & 7, b = v >> 3;
-            stage[u] = ldg_stream(src + (base_s + s_offB[b] + c * V) * EB);
+            const char* gp = src + (base_s + s_offB[b] + c * V) * EB;
+            if constexpr (AL) {
+                stage[u] = ldg_stream(gp);
+            } else {
+                using T = typename Cell<EB>::type;
+                union { uint4 v; T e[V]; } t;
+#pragma unroll
+                for (int k = 0; k < V; ++k) t.e[k] = reinterpret_cast<const T*>(gp)[k];
+                stage[u] = t.v;
+            }
         }
     }
 #pragma unroll
@@ -328,7 +351,7 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
     }
     __syncthreads();
 
-    tile_phase2<EB, LB>(tile, s_offA, dst, base_d);
+    tile_phase2<EB, LB, AL>(tile, s_offA, dst, base_d);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -708,7 +731,9 @@ int try_planned(const CopyCall& c, bool* done) {
     const int64_t V = 16 / eb, La = 128 / eb;
     for (const JM& m : modes)
         if (m.ss < 0 || m.ds < 0) return TLB_OK;
-    if (!aligned_to(sp, base_s, eb, 16) || !aligned_to(dp, base_d, eb, 16)) return TLB_OK;
+    // Bases or strides that are not multiples of 16 bytes (padded leading dimensions, odd origins) keep the tiled
+    // plan with cell-sized global accesses ("tiled_u": 128- and 32-row tiles, 4- and 8-byte cells).
+    const bool base_al = aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
     static const int64_t kLb[] = {256, 128, 64, 32};
     for (int64_t Lb : kLb) {
         if (Lb == 256 && !lb256_enabled()) continue;
@@ -717,7 +742,7 @@ int try_planned(const CopyCall& c, bool* done) {
         if (!take_run(&work, true, La, &A)) break; // the A run does not depend on Lb
         if (!take_run(&work, false, Lb, &B)) continue;
         if (A.size() > kMaxPieces || B.size() > kMaxPieces) continue;
-        bool ok = true;
+        bool ok = base_al;
         for (const JM& m : A) ok = ok && (m.ds % V == 0);
         for (const JM& m : B) ok = ok && (m.ss % V == 0);
         std::vector<JM> rest;
@@ -726,7 +751,8 @@ int try_planned(const CopyCall& c, bool* done) {
                 ok = ok && (m.ss % V == 0) && (m.ds % V == 0);
                 rest.push_back(m);
             }
-        if (!ok) continue;
+        const bool unaligned = !ok;
+        if (unaligned && ((eb != 4 && eb != 8) || (Lb != 128 && Lb != 32) || g_copy_path == 3)) continue;
         // B must be contiguous on the destination (row b -> +b) and A on the source: by construction.
         TileParams P;
         std::memset(&P, 0, sizeof(P));
@@ -748,7 +774,7 @@ int try_planned(const CopyCall& c, bool* done) {
         const char* sb = sp + base_s * eb;
         char* db = dp + base_d * eb;
         // ---- TMA-fed variant: tensor map derived from the source's refined modes (parent) and the A / B runs (tile)
-        if (g_copy_path == 3 || (g_copy_path == 0 && tma_default())) {
+        if (!unaligned && (g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) {
             bool tma_ok = true;
             for (size_t r = 0; r + 1 < B.size(); ++r) tma_ok = tma_ok && B[r].ss < B[r + 1].ss; // smem row order == b order
             tlb_layout_desc parent, tdesc;
@@ -815,11 +841,25 @@ int try_planned(const CopyCall& c, bool* done) {
             if (g_copy_path == 3) continue; // this |B| has no tensor map: a shorter B run may have one
         }
         if (g_dry_run) {
-            set_plan("tiled");
+            set_plan(unaligned ? "tiled_u" : "tiled");
             *done = true;
             return TLB_OK;
         }
         const unsigned grid = static_cast<unsigned>(tiles);
+        if (unaligned) {
+            if (eb == 4) {
+                if (Lb == 128) tiled_kernel<4, 128, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
+                else tiled_kernel<4, 32, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
+            } else {
+                if (Lb == 128) tiled_kernel<8, 128, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
+                else tiled_kernel<8, 32, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
+            }
+            count_launch();
+            TLB_CUDA(cudaGetLastError());
+            set_plan("tiled_u");
+            *done = true;
+            return TLB_OK;
+        }
 #define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
         if (eb == 1) {
             if (Lb == 256) TLB_TILED(1, 256); else TLB_TILED(1, 128);

@@ -57,6 +57,18 @@ def test_copy_tiled_plan_one_byte_cells(s, d):
     assert run_copy_case("(96,160):(160,1)", "(96,160):(1,96)", 1) == "gather"   # no 128-row B run
 
 
+@pytest.mark.parametrize("eb", [4, 8])
+@pytest.mark.parametrize("s,d,so,do", [
+    ("(256,128):(129,1)", "(256,128):(1,256)", 0, 0),                     # padded source rows: not a multiple of 16 bytes
+    ("(256,128):(128,1)", "(256,128):(1,257)", 0, 0),                     # padded destination columns
+    ("(256,128):(128,1)", "(256,128):(1,256)", 1, 3),                     # odd origins on both sides
+    ("(96,160):(161,1)", "(96,160):(1,97)", 0, 1),                        # 32-row tiles
+])
+def test_copy_tiled_plan_unaligned(s, d, so, do, eb):
+    """Leading dimensions / origins that break 16-byte alignment keep the staged plan with cell-sized global accesses."""
+    assert run_copy_case(s, d, eb, src_origin=so, dst_origin=do) == "tiled_u"
+
+
 @pytest.mark.parametrize("eb", [2, 4, 8])
 @pytest.mark.parametrize("s,d", [
     ("(256,128):(128,1)", "(256,128):(1,256)"),                           # C1 shape in small
@@ -115,7 +127,8 @@ def test_copy_forced_gather_equals_tiled():
 
 
 def test_copy_misaligned_origins_fall_back_and_stay_exact():
-    assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 4, src_origin=1, dst_origin=3) == "gather"
+    assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 4, src_origin=1, dst_origin=3) == "tiled_u"
+    assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 2, src_origin=1, dst_origin=3) == "gather"
     assert run_copy_case("4096:1", "4096:1", 2, src_origin=1, dst_origin=1) in ("vec", "gather")
 
 
