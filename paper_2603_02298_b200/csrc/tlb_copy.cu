@@ -269,8 +269,18 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
         return;
     }
     static_assert(EB != 1 || LB % 128 == 0, "1-byte cells need 128-row tiles");
+    if constexpr (EB == 16) {
+        // 16-byte cells are their own vectors: nothing to transpose in registers. A warp reads chunk c of 32
+        // consecutive rows (conflict free under the swizzle) and writes 512 contiguous destination bytes.
+        for (int wt = warp; wt < 8 * (LB / 32); wt += kThreads / 32) {
+            const int c = wt & 7, r = (wt >> 3) * 32 + lane;
+            const uint4 v = *reinterpret_cast<const uint4*>(tile + swz(r, c));
+            store_vec<EB, AL>(dst + (base_d + s_offA[c] + r) * 16, v);
+        }
+        return;
+    }
     constexpr int LOGV = (V == 2) ? 1 : (V == 4) ? 2 : 3;
-    constexpr int NR = EB == 1 ? 0 : 3 - LOGV;
+    constexpr int NR = (EB == 1 || EB == 16) ? 0 : 3 - LOGV;
     constexpr int CW = 8 >> NR;
     const int q = lane & 7, p = lane >> 3;
     const int bb = (q & ((1 << NR) - 1)) | (p << NR);
@@ -727,7 +737,7 @@ int try_planned(const CopyCall& c, bool* done) {
     if (ia == ib) return TLB_OK;
 
     // ---- tiled plan
-    if (eb != 1 && eb != 2 && eb != 4 && eb != 8) return TLB_OK;
+    if (eb != 1 && eb != 2 && eb != 4 && eb != 8 && eb != 16) return TLB_OK;
     const int64_t V = 16 / eb, La = 128 / eb;
     for (const JM& m : modes)
         if (m.ss < 0 || m.ds < 0) return TLB_OK;
@@ -738,6 +748,7 @@ int try_planned(const CopyCall& c, bool* done) {
     for (int64_t Lb : kLb) {
         if (Lb == 256 && !lb256_enabled()) continue;
         if (eb == 1 && (Lb < 128 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 1-byte cells: LDG-staged, 128+ rows
+        if (eb == 16 && (Lb == 64 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 16-byte cells: LDG-staged, 256 / 128 / 32 rows
         std::vector<JM> work = modes, A, B;
         if (!take_run(&work, true, La, &A)) break; // the A run does not depend on Lb
         if (!take_run(&work, false, Lb, &B)) continue;
@@ -863,6 +874,8 @@ int try_planned(const CopyCall& c, bool* done) {
 #define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
         if (eb == 1) {
             if (Lb == 256) TLB_TILED(1, 256); else TLB_TILED(1, 128);
+        } else if (eb == 16) {
+            if (Lb == 256) TLB_TILED(16, 256); else if (Lb == 128) TLB_TILED(16, 128); else TLB_TILED(16, 32);
         } else if (eb == 4) {
             if (Lb == 256) TLB_TILED(4, 256); else if (Lb == 128) TLB_TILED(4, 128); else if (Lb == 64) TLB_TILED(4, 64); else TLB_TILED(4, 32);
         } else if (eb == 8) {

@@ -69,7 +69,7 @@ def test_copy_tiled_plan_unaligned(s, d, so, do, eb):
     assert run_copy_case(s, d, eb, src_origin=so, dst_origin=do) == "tiled_u"
 
 
-@pytest.mark.parametrize("eb", [2, 4, 8])
+@pytest.mark.parametrize("eb", [2, 4, 8, 16])
 @pytest.mark.parametrize("s,d", [
     ("(256,128):(128,1)", "(256,128):(1,256)"),                           # C1 shape in small
     ("(128,256):(1,128)", "(128,256):(256,1)"),
