@@ -739,8 +739,8 @@ int try_planned(const CopyCall& c, bool* done) {
     // ---- tiled plan
     if (eb != 1 && eb != 2 && eb != 4 && eb != 8 && eb != 16) return TLB_OK;
     const int64_t V = 16 / eb, La = 128 / eb;
-    for (const JM& m : modes)
-        if (m.ss < 0 || m.ds < 0) return TLB_OK;
+    // Negative strides (reversed modes) are fine everywhere except along the two contiguous runs themselves, which
+    // take_run only builds from +1 stride chains; the offset tables and the tile index carry signed strides.
     // Bases or strides that are not multiples of 16 bytes (padded leading dimensions, odd origins) keep the tiled
     // plan with cell-sized global accesses ("tiled_u": 128- and 32-row tiles, 4- and 8-byte cells).
     const bool base_al = aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
@@ -769,7 +769,7 @@ int try_planned(const CopyCall& c, bool* done) {
         std::memset(&P, 0, sizeof(P));
         // neighbouring CTAs should touch neighbouring memory: order the rest modes by locality
         std::stable_sort(rest.begin(), rest.end(), [](const JM& a, const JM& b) {
-            return std::min(a.ss, a.ds) < std::min(b.ss, b.ds);
+            return std::min(std::llabs(a.ss), std::llabs(a.ds)) < std::min(std::llabs(b.ss), std::llabs(b.ds));
         });
         TLB_TRY(fill_joint(rest, &P.rest));
         P.nA = static_cast<int>(A.size());
@@ -787,6 +787,7 @@ int try_planned(const CopyCall& c, bool* done) {
         // ---- TMA-fed variant: tensor map derived from the source's refined modes (parent) and the A / B runs (tile)
         if (!unaligned && (g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) {
             bool tma_ok = true;
+            for (const JM& m : modes) tma_ok = tma_ok && m.ss >= 0; // tensor maps carry unsigned strides
             for (size_t r = 0; r + 1 < B.size(); ++r) tma_ok = tma_ok && B[r].ss < B[r + 1].ss; // smem row order == b order
             tlb_layout_desc parent, tdesc;
             std::memset(&parent, 0, sizeof(parent));

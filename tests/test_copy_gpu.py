@@ -102,6 +102,27 @@ def test_copy_tiled_tma_plan(s, d, eb):
     assert run_copy_case(s, d, eb, path=3) == "tiled_tma"
 
 
+@pytest.mark.parametrize("s,d", [
+    ("(256,128,4):(128,1,-32768)", "(256,128,4):(1,256,32768)"),          # reversed batch mode on the source
+    ("(256,128):(-128,1)", "(256,128):(1,256)"),                          # reversed rows: the B run's source stride is negative
+    ("(256,128):(128,1)", "(256,128):(1,-256)"),                          # reversed columns on the destination
+])
+def test_copy_tiled_plan_with_reversed_modes(s, d):
+    """Negative strides (test_layout.cpp:183-186 evaluates them) stay on the tiled plan when they are not along the two
+    contiguous runs; origins put the most negative offset at cell 0."""
+    ds, dd = L(s).lower(), L(d).lower()
+    so, do = max(0, -ds.min_offset), max(0, -dd.min_offset)
+    ns, nd = ds.max_offset + so + 1, dd.max_offset + do + 1
+    src, want = cells(ns, 4, 5), cells(nd, 4, fill=-1)
+    assert ou.orc_copy(s, src, d, want, so, do) == 0
+    tsrc, tdst = dev(src), dev(cells(nd, 4, fill=-1))
+    a = host.make_tensor(ds, tsrc.data_ptr(), ns, 4, so)
+    b = host.make_tensor(dd, tdst.data_ptr(), nd, 4, do)
+    assert host.copy((a, None), (b, None)) == "tiled"
+    torch.cuda.synchronize()
+    assert (tdst.cpu().numpy() == want).all()
+
+
 def test_copy_interleaved_runs_fall_back_to_gather():
     """The destination-contiguous run continues inside the source-contiguous run: no clean A x B tile."""
     assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4) == "gather"
