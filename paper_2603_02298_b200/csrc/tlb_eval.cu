@@ -147,22 +147,41 @@ __global__ void __launch_bounds__(kThreads) eval_warp_kernel(const __grid_consta
     }
 }
 
-// out[k*nm + r] = natural coordinate leaf r of i0+k (idx2crd, int_tuple.hpp:129).
+// out[k*nm + r] = natural coordinate leaf r of i0+k (idx2crd, int_tuple.hpp:129). NM = 2 / 4 leaves: the whole
+// coordinate of one index is 16 / 32 contiguous bytes and leaves as ONE vector store (a loop of 8-byte stores writes
+// a quarter of every 32-byte sector per instruction: 1.9 TB/s against 6+ TB/s); NM = 0 is the general loop.
+template <int NM>
 __global__ void __launch_bounds__(kThreads) idx2crd_kernel(const __grid_constant__ tlb_layout_desc S, uint64_t i0,
                                                            uint64_t n, int64_t* __restrict__ out) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const int nm = S.n_modes;
+    const int nm = NM ? NM : S.n_modes;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
         uint64_t i = i0 + k;
         int64_t* o = out + k * nm;
-        for (int r = 0; r < nm; ++r) {
-            if (r + 1 < nm) {
-                const uint64_t q = dev_div(S, r, i);
-                o[r] = static_cast<int64_t>(i - q * static_cast<uint64_t>(S.extent[r]));
-                i = q;
-            } else {
-                o[r] = static_cast<int64_t>(i);
+        if constexpr (NM == 0) {
+            for (int r = 0; r < nm; ++r) {
+                if (r + 1 < nm) {
+                    const uint64_t q = dev_div(S, r, i);
+                    o[r] = static_cast<int64_t>(i - q * static_cast<uint64_t>(S.extent[r]));
+                    i = q;
+                } else {
+                    o[r] = static_cast<int64_t>(i);
+                }
             }
+        } else {
+            int64_t c[NM];
+#pragma unroll
+            for (int r = 0; r < NM; ++r) {
+                if (r + 1 < NM) {
+                    const uint64_t q = dev_div(S, r, i);
+                    c[r] = static_cast<int64_t>(i - q * static_cast<uint64_t>(S.extent[r]));
+                    i = q;
+                } else {
+                    c[r] = static_cast<int64_t>(i);
+                }
+            }
+            if constexpr (NM == 2) st_cs_v2(o, c[0], c[1]);
+            else st_cs_v4(o, c[0], c[1], c[2], c[3]);
         }
     }
 }
@@ -384,7 +403,15 @@ int tlb_idx2crd_range(const tlb_layout_desc* shape, uint64_t i0, uint64_t n, int
     if (!d_out) return fail(TLB_ERR_CONTRACT, "tlb_idx2crd_range: null output");
     if (i0 + n < i0 || (i0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
     TLB_TRY(require_device());
-    idx2crd_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*shape, i0, n, d_out);
+    {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const uintptr_t al = reinterpret_cast<uintptr_t>(d_out);
+        // one CTA pass per element block (no ragged grid-stride tail), vector stores when the coordinate is 16 / 32 bytes
+        const int grid = static_cast<int>(std::min<uint64_t>((n + kThreads - 1) / kThreads, 1u << 22));
+        if (shape->n_modes == 4 && (al & 31) == 0) idx2crd_kernel<4><<<grid, kThreads, 0, st>>>(*shape, i0, n, d_out);
+        else if (shape->n_modes == 2 && (al & 15) == 0) idx2crd_kernel<2><<<grid, kThreads, 0, st>>>(*shape, i0, n, d_out);
+        else idx2crd_kernel<0><<<grid_for(n), kThreads, 0, st>>>(*shape, i0, n, d_out);
+    }
     count_launch();
     TLB_CUDA(cudaGetLastError());
     return TLB_OK;
