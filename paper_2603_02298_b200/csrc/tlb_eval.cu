@@ -255,25 +255,49 @@ struct AxesModes {
     int32_t axis[TLB_MAX_MODES]; // -1 for Int(0) leaves
 };
 
-// Per-axis offsets of a coordinate (Basis) layout (layout_eval_axes, layout.hpp:103).
+// Per-axis offsets of a coordinate (Basis) layout (layout_eval_axes, layout.hpp:103). NA = 1..4 axes (the TMA
+// coordinate tensors of rank <= 4): accumulators in registers, one vector store per index. NA = 0: any axis count,
+// accumulating in the output cells.
+template <int NA>
 __global__ void __launch_bounds__(kThreads) eval_axes_kernel(const __grid_constant__ AxesModes M, uint64_t i0,
                                                              uint64_t n, int64_t* __restrict__ out) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
         uint64_t i = i0 + k;
         int64_t* o = out + k * M.n_axes;
-        for (int a = 0; a < M.n_axes; ++a) o[a] = 0;
+        int64_t acc[NA ? NA : 1];
+        if constexpr (NA == 0) {
+            for (int a = 0; a < M.n_axes; ++a) o[a] = 0;
+        } else {
+#pragma unroll
+            for (int a = 0; a < NA; ++a) acc[a] = 0;
+        }
         for (int r = 0; r < M.n_modes; ++r) {
             uint64_t c;
             if (r + 1 < M.n_modes) {
                 const uint64_t e = static_cast<uint64_t>(M.extent[r]);
-                c = i % e;
-                i /= e;
+                if ((e & (e - 1)) == 0) {
+                    c = i & (e - 1);
+                    i >>= __ffsll(static_cast<long long>(e)) - 1;
+                } else {
+                    c = i % e;
+                    i /= e;
+                }
             } else {
                 c = i;
             }
-            if (M.axis[r] >= 0) o[M.axis[r]] += static_cast<int64_t>(c) * M.scale[r];
+            const int64_t v = static_cast<int64_t>(c) * M.scale[r];
+            if constexpr (NA == 0) {
+                if (M.axis[r] >= 0) o[M.axis[r]] += v;
+            } else {
+#pragma unroll
+                for (int a = 0; a < NA; ++a) acc[a] += (M.axis[r] == a) ? v : 0;
+            }
         }
+        if constexpr (NA == 1) o[0] = acc[0];
+        else if constexpr (NA == 2) st_cs_v2(o, acc[0], acc[1]);
+        else if constexpr (NA == 3) { o[0] = acc[0]; o[1] = acc[1]; o[2] = acc[2]; }
+        else if constexpr (NA == 4) st_cs_v4(o, acc[0], acc[1], acc[2], acc[3]);
     }
 }
 
@@ -486,7 +510,16 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
     if (n == 0) return TLB_OK;
     if (!d_out) return fail(TLB_ERR_CONTRACT, "tlb_eval_axes_range: null output");
     TLB_TRY(require_device());
-    eval_axes_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(M, i0, n, d_out);
+    {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const uintptr_t al = reinterpret_cast<uintptr_t>(d_out);
+        const int grid = static_cast<int>(std::min<uint64_t>((n + kThreads - 1) / kThreads, 1u << 22));
+        if (n_axes == 1) eval_axes_kernel<1><<<grid, kThreads, 0, st>>>(M, i0, n, d_out);
+        else if (n_axes == 2 && (al & 15) == 0) eval_axes_kernel<2><<<grid, kThreads, 0, st>>>(M, i0, n, d_out);
+        else if (n_axes == 3) eval_axes_kernel<3><<<grid, kThreads, 0, st>>>(M, i0, n, d_out);
+        else if (n_axes == 4 && (al & 31) == 0) eval_axes_kernel<4><<<grid, kThreads, 0, st>>>(M, i0, n, d_out);
+        else eval_axes_kernel<0><<<grid_for(n), kThreads, 0, st>>>(M, i0, n, d_out);
+    }
     count_launch();
     TLB_CUDA(cudaGetLastError());
     return TLB_OK;

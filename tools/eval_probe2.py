@@ -26,3 +26,5 @@ s = t(lambda: host.idx2crd_range(Lt, 2**31, n, crd)); print(f"idx2crd           
 s = t(lambda: host.crd2idx_range(Lt, crd, n, out)); print(f"crd2idx           : {n/s/1e9:7.1f} G elems/s  {n*40/s/1e9:7.0f} GB/s moved")
 s = t(lambda: host.rinv_check_range(Lt, Rt, 2**31, n, cnt)); print(f"rinv check L(R(k)): {n/s/1e9:7.1f} G checks/s (no memory traffic)")
 s = t(lambda: host.compose_check_range("(8192,8192):(1,8192)", "(8192,8192):(8192,1)", "(8192,8192):(8192,1)", 0, n, cnt)); print(f"compose check     : {n/s/1e9:7.1f} G checks/s")
+ax = torch.empty(n, 2, dtype=torch.int64, device="cuda")
+s = t(lambda: host.eval_axes_range("((128,64),(512,1024)):((e0,e1),(128*e0,64*e1))", 2, 2**31, n, ax)); print(f"eval_axes (2 axes) : {n/s/1e9:7.1f} G elems/s  {n*16/s/1e9:7.0f} GB/s written")
