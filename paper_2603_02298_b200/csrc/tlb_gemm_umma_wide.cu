@@ -547,8 +547,16 @@ bool umma_wide_applies(const UmmaProblem& p) {
     // the full range of a problem does for any M (the last pair tile is clipped by the TMA bounds).
     const uint32_t mb = static_cast<uint32_t>((p.M + 255) / 256);
     if (!p.full_range && (mb % 2 != 0 || p.tile_begin % 4 != 0 || p.tile_end % 4 != 0)) return false;
-    // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue) unless an operand is MN-major
-    if (!(p.a_mn || p.b_mn) && mb % 2 != 0) return false;
+    // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue; measured better up to 2048^3, worse from
+    // 3072^3) unless an operand is MN-major or the wide plan is forced (TLB_GEMM_WIDE=1)
+    if (!(p.a_mn || p.b_mn)) {
+        if (mb % 2 != 0) return false;
+        const uint64_t nb = static_cast<uint64_t>((p.N + 255) / 256);
+        const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
+                                                 : (p.tile_end - p.tile_begin) / 4;
+        const char* e = std::getenv("TLB_GEMM_WIDE");
+        if (!(e && e[0] == '1') && pair_tiles < 48) return false;
+    }
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
     return base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N;   // TMA reduce-add epilogue only
 }

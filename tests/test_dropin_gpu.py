@@ -26,6 +26,6 @@ def test_cli_runs_the_hot_path_on_device(capsys):
     assert main(["copy", "(512,256):(256,1)", "(512,256):(1,512)", "--elem-bytes", "4", "--steps", "2"]) == 0
     assert json.loads(capsys.readouterr().out)["plan"] == "tiled"
     assert main(["gemm", "(512,256):(256,1)", "(256,256):(256,1)", "(512,256):(256,1)", "--steps", "2"]) == 0
-    assert json.loads(capsys.readouterr().out)["plan"] == "umma_2sm_wide"
+    assert json.loads(capsys.readouterr().out)["plan"] == "umma_2sm"
     assert main(["eval", "(4,8):(1,4)", "--count", "32", "--steps", "1"]) == 0
     assert json.loads(capsys.readouterr().out)["first"] == [0, 1, 2, 3, 4, 5, 6, 7]

@@ -196,6 +196,13 @@ def test_c2_gemm_4096_full_size_exact(cg):
     _flat_tn_check(4096, 4096, 4096, cg)
 
 
+@pytest.fixture
+def force_wide(monkeypatch):
+    """K-major problems below 48 pair tiles default to the 256 x 256 plan; TLB_GEMM_WIDE=1 keeps the small parity shapes
+    on the wide kernel."""
+    monkeypatch.setenv("TLB_GEMM_WIDE", "1")
+
+
 WIDE_SHAPES = [
     # (A, B, C) as the kernel runs them: C n-contiguous -> rows = M; 512 x 256 pair tiles need ceil(M/256) even
     ("(512,64):(64,1)", "(256,64):(64,1)", "(512,256):(256,1)"),          # one pair tile, one k-block
@@ -207,14 +214,14 @@ WIDE_SHAPES = [
 
 
 @pytest.mark.parametrize("shape", WIDE_SHAPES)
-def test_gemm_bf16_wide_plan_kat_exact(shape):
+def test_gemm_bf16_wide_plan_kat_exact(shape, force_wide):
     """512 x 256 pair tiles (tlb_gemm_umma_wide.cu): exact on the reference's integer fills, including the stream-K
     cut of the partial wave (partial tiles combine through the reduce-add epilogue)."""
     assert _bf16_case(*shape, kat=True, path=3) == "umma_2sm_wide"
 
 
 @pytest.mark.parametrize("shape", WIDE_SHAPES[1:])
-def test_gemm_bf16_wide_plan_random_within_tolerance(shape):
+def test_gemm_bf16_wide_plan_random_within_tolerance(shape, force_wide):
     assert _bf16_case(*shape, kat=False, seed=11, path=3) == "umma_2sm_wide"
 
 
@@ -245,7 +252,7 @@ def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape):
     (WIDE_SHAPES[1], 0, "umma_2sm_wide"), (WIDE_SHAPES[2], 0, "umma_2sm_wide"), (MN_MAJOR_SHAPES[0], 0, "umma_2sm_wide"),
     (("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)"), 0, "simt_f16"),
 ])
-def test_gemm_f16_operands(shape, path, plan):
+def test_gemm_f16_operands(shape, path, plan, force_wide):
     """tlb_gemm_f16: IEEE fp16 operands on every plan (instruction-descriptor formats 0 instead of 1), exact on the
     reference's integer fills and within the stated tolerance on random data."""
     assert _bf16_case(*shape, kat=True, path=path, f16=True) == plan
@@ -260,13 +267,15 @@ def test_gemm_wide_plan_whole_tiles_then_k_ranges():
 def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
     # ceil(M/256) odd: no m-adjacent block pairs -> 256 x 256 plan
     assert _bf16_case("(768,128):(128,1)", "(256,128):(128,1)", "(768,256):(256,1)", kat=True, path=3) == "umma_2sm"
+    assert _bf16_case(*WIDE_SHAPES[1], kat=True, path=3) == "umma_2sm"          # 2 pair tiles: too small for the wide plan
     monkeypatch.setenv("TLB_GEMM_WIDE", "0")
-    assert _bf16_case(*WIDE_SHAPES[1], kat=True, path=3) == "umma_2sm"
+    assert _bf16_case("(4096,64):(64,1)", "(4096,64):(64,1)", "(4096,4096):(4096,1)", kat=True, path=3) == "umma_2sm"
 
 
 def test_gemm_wide_plan_without_k_split_is_reproducible(monkeypatch):
     """TLB_GEMM_SPLIT_TAIL=0: every tile is summed by one CTA pair in k order, so two runs agree bit for bit."""
     monkeypatch.setenv("TLB_GEMM_SPLIT_TAIL", "0")
+    monkeypatch.setenv("TLB_GEMM_WIDE", "1")
     assert _bf16_case(*WIDE_SHAPES[4], kat=False, seed=5, path=3) == "umma_2sm_wide"
 
 
