@@ -29,3 +29,47 @@ def test_cli_runs_the_hot_path_on_device(capsys):
     assert json.loads(capsys.readouterr().out)["plan"] == "umma_2sm"
     assert main(["eval", "(4,8):(1,4)", "--count", "32", "--steps", "1"]) == 0
     assert json.loads(capsys.readouterr().out)["first"] == [0, 1, 2, 3, 4, 5, 6, 7]
+
+
+def test_calls_are_capturable_in_a_cuda_graph():
+    """The launch path does no allocation or synchronisation (tensor maps travel as kernel parameters), so a stream of
+    copy / eval / GEMM calls can be captured once and replayed: same results as eager, replay after replay."""
+    import numpy as np
+    import torch
+    from paper_2603_02298_b200 import host
+    M = 1024
+    i = torch.arange(M, device="cuda").view(M, 1)
+    p = torch.arange(M, device="cuda").view(1, M)
+    a = ((i * 7 + p * 3 + 1) % 11).to(torch.bfloat16).contiguous()
+    b = ((i * 5 + p * 2 + 2) % 13).to(torch.bfloat16).contiguous()
+    at = torch.empty(M * M, dtype=torch.int16, device="cuda")             # A transposed by tlb_copy inside the graph
+    c = torch.zeros(M, M, dtype=torch.float32, device="cuda")
+    idx = torch.empty(M * M, dtype=torch.int64, device="cuda")
+    ta = host.tensor_of(f"({M},{M}):({M},1)", a.view(-1).view(torch.int16), ranked=True)
+    tb = host.tensor_of(f"({M},{M}):({M},1)", b.view(-1).view(torch.int16), ranked=True)
+    tat = host.tensor_of(f"({M},{M}):(1,{M})", at, ranked=True)           # same logical A, M-major storage
+    tc = host.tensor_of(f"({M},{M}):({M},1)", c.view(-1), ranked=True)
+    ca, cat = host.tensor_of(f"({M},{M}):({M},1)", a.view(-1).view(torch.int16)), host.tensor_of(f"({M},{M}):(1,{M})", at)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):                                               # warm up outside the capture (attribute set-up)
+            host.copy(ca, cat)
+            host.gemm_bf16(tat, tb, tc)
+            host.eval_range(f"({M},{M}):({M},1)", 0, M * M, idx)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    c.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        host.copy(ca, cat)                                               # A -> M-major copy (tiled plan)
+        host.gemm_bf16(tat, tb, tc)                                      # NT-style operand on tcgen05, C += A B^T
+        host.eval_range(f"({M},{M}):({M},1)", 0, M * M, idx)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    ref = a.double() @ b.double().t()
+    assert torch.equal(c.double(), 3 * ref)                              # three replays accumulated into C, exactly
+    assert torch.equal(at.view(M, M), a.view(torch.int16).t().contiguous())
+    ii = torch.arange(M * M, device="cuda")
+    assert torch.equal(idx, (ii % M) * M + ii // M)                      # L(i) of (M,M):(M,1) over the colex index
