@@ -325,6 +325,20 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
 
 } // namespace
 
+bool gemm_flat_view(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, GemmFlat* out) {
+    GemmDims d;
+    if (check_gemm(A, B, C, 2, 4, &d) != TLB_OK) return false;
+    if (A->layout->kind != TLB_KIND_INT || B->layout->kind != TLB_KIND_INT || C->layout->kind != TLB_KIND_INT) return false;
+    int64_t e;
+    GemmFlat f{d.M, d.N, d.K, 0, 0, 0, 0, 0, 0};
+    if (!single_stride(*A->layout, 0, &e, &f.a_sm) || !single_stride(*A->layout, 1, &e, &f.a_sk) ||
+        !single_stride(*B->layout, 0, &e, &f.b_sn) || !single_stride(*B->layout, 1, &e, &f.b_sk) ||
+        !single_stride(*C->layout, 0, &e, &f.c_sm) || !single_stride(*C->layout, 1, &e, &f.c_sn))
+        return false;
+    *out = f;
+    return true;
+}
+
 int gemm_bf16_impl(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_bs, int64_t b_bs, int64_t c_bs,
                    int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, cudaStream_t stream) {
     return run_gemm(A, B, C, false, a_bs, b_bs, c_bs, batch_begin, batch_end, tile_begin, tile_end, nullptr, stream);

@@ -52,6 +52,14 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
 int gemm_bf16_impl(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int64_t a_bs, int64_t b_bs, int64_t c_bs,
                    int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, cudaStream_t stream);
 
+// Flat view of a GEMM whose every mode coalesces to one stride (what the tcgen05 plans and the pipelined host path
+// need): extents, the two strides of every operand, in elements.
+struct GemmFlat {
+    int64_t M, N, K;
+    int64_t a_sm, a_sk, b_sn, b_sk, c_sm, c_sn;
+};
+bool gemm_flat_view(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, GemmFlat* out);
+
 // ---- joint descriptor: one peel, two offsets ------------------------------------
 // The common refinement of a source and a destination layout over the same integral domain:
 // refined mode r has one extent and one stride on each side, so a single division chain

@@ -339,6 +339,40 @@ def test_gemm_host_entry_point():
     assert (hc.numpy() == want).all()
 
 
+@pytest.mark.parametrize("lc_kind", ["m_contiguous", "n_contiguous"])
+def test_gemm_host_entry_point_pipelined_panels(lc_kind, monkeypatch):
+    """tlb_gemm_bf16_host on a problem with several 512-row panels (ragged last panel, padded leading dimensions): the
+    upload / compute / download pipeline must produce exactly what the one-shot path does, and the oracle's cells."""
+    monkeypatch.setenv("TLB_HOST_PANEL", "512")
+    M, N, K = 1300, 1400, 72
+    lda, ldb = 80, 88
+    rng = np.random.default_rng(21)
+    i, p = np.meshgrid(np.arange(M), np.arange(K), indexing="ij")
+    j, p2 = np.meshgrid(np.arange(N), np.arange(K), indexing="ij")
+    a = np.zeros(M * lda, dtype=np.float32)
+    b = np.zeros(N * ldb, dtype=np.float32)
+    a[(i * lda + p).ravel()] = ((i * 7 + p * 3 + 1) % 11).ravel()
+    b[(j * ldb + p2).ravel()] = ((j * 5 + p2 * 2 + 2) % 13).ravel()
+    ab, bb = ou.f32_to_bf16_bits(a), ou.f32_to_bf16_bits(b)
+    la, lb = f"({M},{K}):({lda},1)", f"({N},{K}):({ldb},1)"
+    lc = f"({M},{N}):(1,{M + 4})" if lc_kind == "m_contiguous" else f"({M},{N}):({N + 4},1)"
+    nc = ou.cosize_of(lc)
+    c0 = (np.arange(nc) % 7 - 3).astype(np.float32)
+    want = c0.copy()
+    st, _ = ou.orc_gemm_bf16(la, ab, lb, bb, lc, want)
+    assert st == 0
+    outs = []
+    for pipe in ("1", "0"):
+        monkeypatch.setenv("TLB_HOST_PIPELINE", pipe)
+        ha, hb, hc = (torch.from_numpy(x.copy()) for x in (ab.view(np.int16), bb.view(np.int16), c0))
+        ta, ka = host.tensor_of(la, ha, ranked=True)
+        tb, kb = host.tensor_of(lb, hb, ranked=True)
+        tc, kc = host.tensor_of(lc, hc, ranked=True)
+        host.gemm_bf16_host((ta, ka), (tb, kb), (tc, kc))
+        outs.append(hc.numpy().copy())
+    assert (outs[0] == want).all() and (outs[1] == want).all()
+
+
 def test_c4_batched_8192_two_batches_exact():
     """Config C4 shape (8192^3 per batch, batch strides, TN with m-contiguous C) on 2 of the 64 batches with the
     reference's integer fills: K = 8192 keeps every partial sum below 2^24 (10 * 12 * 8192 = 983040), so the result
