@@ -264,6 +264,15 @@ def test_gemm_wide_plan_whole_tiles_then_k_ranges():
     _flat_tn_check(4096, 4096, 1024, 3)
 
 
+def test_gemm_wide_plan_tile_ranges_partition_the_output(force_wide):
+    """Sharding on groups of 4 tile ids (512 x 256 pair tiles, shard.gemm_tile_range): every shard runs the wide plan and
+    disjoint ranges compose to the full product."""
+    tiles = (1024 // 256) * (2048 // 256) * 2
+    cuts = [0, 16, 20, 48, tiles]
+    _flat_tn_check(1024, 2048, 512, 3, tile_ranges=list(zip(cuts[:-1], cuts[1:])))
+    assert abi.load().tlb_last_plan().decode() == "umma_2sm_wide"
+
+
 def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
     # ceil(M/256) odd: no m-adjacent block pairs -> 256 x 256 plan
     assert _bf16_case("(768,128):(128,1)", "(256,128):(128,1)", "(768,256):(256,1)", kat=True, path=3) == "umma_2sm"
