@@ -550,7 +550,6 @@ bool umma_wide_applies(const UmmaProblem& p) {
     // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue; measured better up to 2048^3, worse from
     // 3072^3) unless an operand is MN-major or the wide plan is forced (TLB_GEMM_WIDE=1)
     if (!(p.a_mn || p.b_mn)) {
-        if (mb % 2 != 0) return false;
         const uint64_t nb = static_cast<uint64_t>((p.N + 255) / 256);
         const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
                                                  : (p.tile_end - p.tile_begin) / 4;

@@ -252,9 +252,11 @@ def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape):
     (WIDE_SHAPES[1], 0, "umma_2sm_wide"), (WIDE_SHAPES[2], 0, "umma_2sm_wide"), (MN_MAJOR_SHAPES[0], 0, "umma_2sm_wide"),
     (("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)"), 0, "simt_f16"),
 ])
-def test_gemm_f16_operands(shape, path, plan, force_wide):
+def test_gemm_f16_operands(shape, path, plan, monkeypatch):
     """tlb_gemm_f16: IEEE fp16 operands on every plan (instruction-descriptor formats 0 instead of 1), exact on the
     reference's integer fills and within the stated tolerance on random data."""
+    if plan.endswith("wide"):
+        monkeypatch.setenv("TLB_GEMM_WIDE", "1")
     assert _bf16_case(*shape, kat=True, path=path, f16=True) == plan
     assert _bf16_case(*shape, kat=False, seed=17, path=path, f16=True) == plan
 
@@ -271,6 +273,12 @@ def test_gemm_wide_plan_tile_ranges_partition_the_output(force_wide):
     cuts = [0, 16, 20, 48, tiles]
     _flat_tn_check(1024, 2048, 512, 3, tile_ranges=list(zip(cuts[:-1], cuts[1:])))
     assert abi.load().tlb_last_plan().decode() == "umma_2sm_wide"
+
+
+def test_gemm_wide_plan_takes_large_problems_with_an_odd_number_of_row_blocks():
+    """ceil(M/256) odd: the full range of a large problem still runs 512 x 256 pair tiles (the last one is clipped by the
+    TMA bounds); 3 x 16 = 48 pair tiles."""
+    assert _bf16_case("(1280,64):(64,1)", "(4096,64):(64,1)", "(1280,4096):(4096,1)", kat=True) == "umma_2sm_wide"
 
 
 def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
