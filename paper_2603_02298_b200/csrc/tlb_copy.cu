@@ -311,6 +311,7 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
     __shared__ int64_t s_offB[LB];                     // source offset of row b
     __shared__ int64_t s_offA[LA];                     // destination offset of column a
 
+    pdl_wait();
     int64_t base_s, base_d;
     dev_joint(P.rest, blockIdx.x, &base_s, &base_d);
 
@@ -872,7 +873,7 @@ int try_planned(const CopyCall& c, bool* done) {
             *done = true;
             return TLB_OK;
         }
-#define TLB_TILED(EB, LB) tiled_kernel<EB, LB><<<grid, kThreads, 0, c.stream>>>(P, sb, db)
+#define TLB_TILED(EB, LB) TLB_CUDA(launch_pdl(tiled_kernel<EB, LB, true>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db))
         if (eb == 1) {
             if (Lb == 256) TLB_TILED(1, 256); else TLB_TILED(1, 128);
         } else if (eb == 16) {

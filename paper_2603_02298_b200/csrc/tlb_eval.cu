@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kThreads) eval_warp_kernel(const __grid_consta
     static_assert(G >= 4 && G <= 32 && (G & (G - 1)) == 0, "G in {4,8,16,32}");
     constexpr int kStores = G / 4;        // STG.256 per lane per superblock
     constexpr int kLanesPerGroup = G / 4; // lanes that share one group inside a store
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
     const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -368,8 +369,8 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
             const int gw = static_cast<int>(std::min<uint64_t>((n_super + kThreads / 32 - 1) / (kThreads / 32), 1u << 22));
 #define TLB_EVAL_W(GG)                                                                                   \
     do {                                                                                                 \
-        if (p32) eval_warp_kernel<GG, true><<<gw, kThreads, 0, s>>>(*layout, i0, n_super, d_out);        \
-        else eval_warp_kernel<GG, false><<<gw, kThreads, 0, s>>>(*layout, i0, n_super, d_out);           \
+        if (p32) TLB_CUDA(launch_pdl(eval_warp_kernel<GG, true>, dim3(gw), dim3(kThreads), 0, s, *layout, i0, n_super, d_out)); \
+        else TLB_CUDA(launch_pdl(eval_warp_kernel<GG, false>, dim3(gw), dim3(kThreads), 0, s, *layout, i0, n_super, d_out));   \
     } while (0)
             switch (G) {
             case 32: TLB_EVAL_W(32); break;

@@ -9,6 +9,9 @@
 
 #include "tlb.h"
 
+#include <cstdlib>
+#include <utility>
+
 namespace tlb {
 
 // ---- error plumbing ---------------------------------------------------------
@@ -59,6 +62,35 @@ struct GemmFlat {
     int64_t a_sm, a_sk, b_sn, b_sk, c_sm, c_sn;
 };
 bool gemm_flat_view(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, GemmFlat* out);
+
+// Launch with programmatic stream serialisation: the kernel may be scheduled while the previous kernel of the stream
+// drains. Kernels launched this way execute pdl_wait() before their first global-memory access, which blocks until
+// that previous kernel has completed and flushed; without the attribute pdl_wait() is a no-op. Hides the 2-4 us of
+// launch latency and scheduling ramp between back-to-back kernels (TLB_PDL=0 turns it off).
+inline bool pdl_enabled() {
+    const char* e = std::getenv("TLB_PDL");
+    return !(e && e[0] == '0');
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
 
 // ---- joint descriptor: one peel, two offsets ------------------------------------
 // The common refinement of a source and a destination layout over the same integral domain:
