@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kThreads)
 vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, char* __restrict__ dst, int eb,
            uint64_t n_vec) {
     using T = typename Cell<VB>::type;
+    pdl_wait();
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if constexpr (VB == 16) {
@@ -724,10 +725,10 @@ int try_planned(const CopyCall& c, bool* done) {
         const char* sb = sp + base_s * eb;
         char* db = dp + base_d * eb;
         switch (vb) {
-        case 2: vec_kernel<2><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
-        case 4: vec_kernel<4><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
-        case 8: vec_kernel<8><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
-        default: vec_kernel<16><<<grid, kThreads, 0, c.stream>>>(J, sb, db, eb, n_vec); break;
+        case 2: TLB_CUDA(launch_pdl(vec_kernel<2>, dim3(grid), dim3(kThreads), 0, c.stream, J, sb, db, eb, n_vec)); break;
+        case 4: TLB_CUDA(launch_pdl(vec_kernel<4>, dim3(grid), dim3(kThreads), 0, c.stream, J, sb, db, eb, n_vec)); break;
+        case 8: TLB_CUDA(launch_pdl(vec_kernel<8>, dim3(grid), dim3(kThreads), 0, c.stream, J, sb, db, eb, n_vec)); break;
+        default: TLB_CUDA(launch_pdl(vec_kernel<16>, dim3(grid), dim3(kThreads), 0, c.stream, J, sb, db, eb, n_vec)); break;
         }
         count_launch();
         TLB_CUDA(cudaGetLastError());
