@@ -100,6 +100,22 @@ gather_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__
     }
 }
 
+// gather over the common refinement: one peel yields both offsets (half the index arithmetic of two evaluations), and,
+// the destination being injective, the refined modes may be walked in any order: the host sorts them by destination
+// stride so that consecutive threads store to neighbouring cells.
+template <int EB>
+__global__ void __launch_bounds__(kThreads)
+gather_joint_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, char* __restrict__ dst, uint64_t n) {
+    using T = typename Cell<EB>::type;
+    pdl_wait();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        int64_t so, dof;
+        dev_joint(J, k, &so, &dof);
+        reinterpret_cast<T*>(dst)[dof] = reinterpret_cast<const T*>(src)[so];
+    }
+}
+
 // ordered pass 1: winner[dp - lo] = max(i + 1) over the i that store to dp
 __global__ void __launch_bounds__(kThreads)
 winner_kernel(const __grid_constant__ tlb_layout_desc D, int64_t d_origin, int64_t lo, uint64_t i0, uint64_t n,
@@ -617,6 +633,40 @@ int launch_gather(const CopyCall& c) {
     return TLB_OK;
 }
 
+// The refined modes of a call restricted to its index range, for the joint gather fallback.
+struct Refined {
+    bool ok = false;
+    std::vector<JM> modes;
+    int64_t base_s = 0, base_d = 0;
+};
+
+int launch_gather_joint(const CopyCall& c, const Refined& R) {
+    std::vector<JM> order = R.modes;
+    std::stable_sort(order.begin(), order.end(), [](const JM& a, const JM& b) { return std::llabs(a.ds) < std::llabs(b.ds); });
+    JointDesc J;
+    TLB_TRY(fill_joint(order, &J));
+    if (g_dry_run) {
+        set_plan("gather");
+        return TLB_OK;
+    }
+    const int eb = c.dst->elem_bytes;
+    const char* sb = static_cast<const char*>(c.src->data) + R.base_s * eb;
+    char* db = static_cast<char*>(c.dst->data) + R.base_d * eb;
+    const int grid = launch_grid(c.n, kThreads, 8);
+#define TLB_GJ(EB) TLB_CUDA(launch_pdl(gather_joint_kernel<EB>, dim3(grid), dim3(kThreads), 0, c.stream, J, sb, db, c.n))
+    switch (eb) {
+    case 1: TLB_GJ(1); break;
+    case 2: TLB_GJ(2); break;
+    case 4: TLB_GJ(4); break;
+    case 8: TLB_GJ(8); break;
+    default: TLB_GJ(16); break;
+    }
+#undef TLB_GJ
+    count_launch();
+    set_plan("gather");
+    return TLB_OK;
+}
+
 int launch_ordered(const CopyCall& c, Span dspan) {
     const tlb_layout_desc& S = *c.src->layout;
     const tlb_layout_desc& D = *c.dst->layout;
@@ -655,7 +705,7 @@ bool aligned_to(const void* p, int64_t origin, int eb, int bytes) {
 }
 
 // Tries the vec and tiled plans. Returns TLB_OK with *done = true when a kernel was launched.
-int try_planned(const CopyCall& c, bool* done) {
+int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     *done = false;
     const tlb_tensor& s = *c.src;
     const tlb_tensor& d = *c.dst;
@@ -680,6 +730,10 @@ int try_planned(const CopyCall& c, bool* done) {
         if (last.e == 1) modes.pop_back();
         if (modes.empty()) return TLB_OK;
     }
+    refined->ok = true;
+    refined->modes = modes;
+    refined->base_s = base_s;
+    refined->base_d = base_d;
     int ia = -1, ib = -1;
     for (size_t r = 0; r < modes.size(); ++r) {
         if (modes[r].ss == 1 && ia < 0) ia = static_cast<int>(r);
@@ -1001,10 +1055,12 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
     if (!(D.flags & TLB_LF_INJECTIVE)) return launch_ordered(c, dspan);
     if (g_copy_path != 1) {
         bool done = false;
-        TLB_TRY(try_planned(c, &done));
+        Refined refined;
+        TLB_TRY(try_planned(c, &done, &refined));
         if (done) return TLB_OK;
         if (g_copy_path == 2 || g_copy_path == 3)
             return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the forced tiled path does not apply to these layouts");
+        if (refined.ok && refined.modes.size() <= TLB_MAX_MODES) return launch_gather_joint(c, refined);
     }
     return launch_gather(c);
 }
