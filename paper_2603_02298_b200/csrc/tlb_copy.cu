@@ -798,7 +798,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     // Negative strides (reversed modes) are fine everywhere except along the two contiguous runs themselves, which
     // take_run only builds from +1 stride chains; the offset tables and the tile index carry signed strides.
     // Bases or strides that are not multiples of 16 bytes (padded leading dimensions, odd origins) keep the tiled
-    // plan with cell-sized global accesses ("tiled_u": 128- and 32-row tiles, 4- and 8-byte cells).
+    // plan with cell-sized global accesses ("tiled_u": 128- and 32-row tiles, 2-, 4- and 8-byte cells).
     const bool base_al = aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
     static const int64_t kLb[] = {256, 128, 64, 32};
     for (int64_t Lb : kLb) {
@@ -819,7 +819,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
                 rest.push_back(m);
             }
         const bool unaligned = !ok;
-        if (unaligned && ((eb != 4 && eb != 8) || (Lb != 128 && Lb != 32) || g_copy_path == 3)) continue;
+        if (unaligned && ((eb != 2 && eb != 4 && eb != 8) || (Lb != 128 && Lb != 32) || g_copy_path == 3)) continue;
         // B must be contiguous on the destination (row b -> +b) and A on the source: by construction.
         TileParams P;
         std::memset(&P, 0, sizeof(P));
@@ -915,7 +915,10 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         }
         const unsigned grid = static_cast<unsigned>(tiles);
         if (unaligned) {
-            if (eb == 4) {
+            if (eb == 2) {
+                if (Lb == 128) tiled_kernel<2, 128, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
+                else tiled_kernel<2, 32, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
+            } else if (eb == 4) {
                 if (Lb == 128) tiled_kernel<4, 128, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
                 else tiled_kernel<4, 32, false><<<grid, kThreads, 0, c.stream>>>(P, sb, db);
             } else {
