@@ -1,5 +1,5 @@
-// tcgen05 GEMM, wide plan: a CTA PAIR owns a 512 x 256 tile of C (256 rows per CTA), K-major bf16 operands,
-// fp32 accumulators that fill all of TMEM.        C(m,n) += sum_k A(m,k) * B(n,k)      (tensor.hpp:214-233)
+// tcgen05 GEMM, wide plan: a CTA PAIR owns a 512 x 256 tile of C (256 rows per CTA), bf16 or fp16 operands that are
+// K-major or MN-major, fp32 accumulators that fill all of TMEM.        C(m,n) += sum_k A(m,k) * B(n,k)      (tensor.hpp:214-233)
 //
 // Why this shape: on a 1 kW part the kernel is POWER bound (SM clock 1.5 GHz under load, MMA duty cycle < 80 %),
 // so the figure of merit is energy per flop, and operand movement is the largest controllable term. A 512 x 256
@@ -12,8 +12,9 @@
 // cta_group::2 instruction whose accumulator lives in TMEM columns [256 h, 256 h + 256) of each CTA.
 //
 // Kernel shape (persistent, warp-specialised, 320 threads, 1 CTA per SM, clusters of 2):
-//   warp 8     TMA producer: 4-stage ring of {A 256 x 64, B 128 x 64} stages (48 KiB), full / empty mbarriers;
-//              also prefetches the tile's C cells into L2 so that the reduce-add epilogue does not wait on HBM
+//   warp 8     TMA producer: 4-stage ring of {A 256 x 64, B 128 x 64} stages (48 KiB), full / empty mbarriers
+//              (MN-major operands arrive as 64-row chunks of [64 k][128 B]); optional L2 prefetch of the tile's C
+//              cells (TLB_GEMM_PREFETCH_C=1; off: measured, it evicts operand lines and loses 1.5-7 %)
 //   warp 9     MMA issue (leader CTA): per k-block 4 + 4 UMMAs (half 0, half 1), ONE non-multicast commit per
 //              stage (a commit every 8 MMAs is free, a multicast commit is not: tools/probes/mma_rate.cu);
 //              the leader's producer relays each stage release to the peer CTA
@@ -23,8 +24,9 @@
 // The accumulators are single-buffered, so a tile's epilogue is overlapped per HALF: half 0 is released to the
 // epilogue one k-block early, and the next tile's half-0 MMAs of the first kStages-1 k-blocks are issued while
 // half 1 is still being drained.
-// Scheduling: the last (units mod workers) tiles are cut stream-K style into equal k-ranges, one per worker, and
-// run FIRST; whole tiles follow round-robin. Partial tiles combine through the same reduce-add epilogue.
+// Scheduling: the last (units mod workers) tiles are cut stream-K style into one k-range per worker, balanced by cost
+// (every tile a range touches is one more epilogue), and run FIRST; whole tiles follow round-robin. Partial tiles
+// combine through the same reduce-add epilogue. The prologue overlaps the previous kernel's tail (griddepcontrol).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
