@@ -209,7 +209,7 @@ WIDE_SHAPES = [
     ("(512,1024):(1024,1)", "(512,1024):(1024,1)", "(512,512):(1,512)"),  # m-contiguous C (runs transposed), 16 k-blocks
     ("(1000,200):(200,1)", "(300,200):(200,1)", "(1000,300):(300,1)"),    # ragged M, N, K: TMA zero fill / clipping
     ("(1024,520):(528,1)", "(768,520):(536,1)", "(1024,768):(800,1)"),    # padded leading dimensions
-    ("(1024,1024):(1024,1)", "(1536,1024):(1024,1)", "(1024,1536):(1,1024)"),  # 12 pair tiles cut into k-ranges per worker
+    ("(1024,512):(512,1)", "(1536,512):(512,1)", "(1024,1536):(1,1024)"),  # 12 pair tiles cut into k-ranges per worker
 ]
 
 
@@ -286,7 +286,7 @@ def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
     assert _bf16_case("(768,128):(128,1)", "(256,128):(128,1)", "(768,256):(256,1)", kat=True, path=3) == "umma_2sm"
     assert _bf16_case(*WIDE_SHAPES[1], kat=True, path=3) == "umma_2sm"          # 2 pair tiles: too small for the wide plan
     monkeypatch.setenv("TLB_GEMM_WIDE", "0")
-    assert _bf16_case("(4096,64):(64,1)", "(4096,64):(64,1)", "(4096,4096):(4096,1)", kat=True, path=3) == "umma_2sm"
+    assert _bf16_case("(2048,64):(64,1)", "(4096,64):(64,1)", "(2048,4096):(4096,1)", kat=True, path=3) == "umma_2sm"
 
 
 def test_gemm_wide_plan_without_k_split_is_reproducible(monkeypatch):
