@@ -5,7 +5,7 @@
 // Layouts keep being built by the reference's host algebra (compose, logical_divide, zipped_divide,
 // right_inverse, ... algebra.hpp); this header only lowers them (flat_modes, layout.hpp:111) and dispatches
 //   tla::copy  (tensor.hpp:195)   -> tlb_copy
-//   tla::gemm  (tensor.hpp:214)   -> tlb_gemm_bf16 / tlb_gemm_i64
+//   tla::gemm  (tensor.hpp:214)   -> tlb_gemm_bf16 / tlb_gemm_f16 / tlb_gemm_i64
 //   tla::eval_int over a range (layout.hpp:74) -> tlb_eval_range
 // to the C ABI of include/tlb.h when the cells live in device memory. Same argument meaning, same exception
 // types (common.hpp:13-97). Device pointers are borrowed, never owned.
@@ -111,6 +111,15 @@ inline void gemm(const DeviceTensor& a, const DeviceTensor& b, const DeviceTenso
     tlb_tensor ta = device_detail::view(da, a), tb = device_detail::view(db, b), tc = device_detail::view(dc, c);
     if (c.elem_bytes == 8) device_detail::rethrow(tlb_gemm_i64(&ta, &tb, &tc, nullptr, c.stream));
     else device_detail::rethrow(tlb_gemm_bf16(&ta, &tb, &tc, tile_begin, tile_end, c.stream));
+}
+
+// Same contract with IEEE fp16 operands (elem_bytes 2/2/4).
+inline void gemm_f16(const DeviceTensor& a, const DeviceTensor& b, const DeviceTensor& c, std::uint32_t tile_begin = 0,
+                     std::uint32_t tile_end = UINT32_MAX) {
+    tlb_layout_desc da = device_detail::lower(a.layout, true), db = device_detail::lower(b.layout, true),
+                    dc = device_detail::lower(c.layout, true);
+    tlb_tensor ta = device_detail::view(da, a), tb = device_detail::view(db, b), tc = device_detail::view(dc, c);
+    device_detail::rethrow(tlb_gemm_f16(&ta, &tb, &tc, tile_begin, tile_end, c.stream));
 }
 
 // d_out[k] = L(i0 + k), k < n: eval_int (layout.hpp:74) over a range, int64 out, extended domain allowed.
