@@ -290,10 +290,27 @@ def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
 
 
 def test_gemm_wide_plan_without_k_split_is_reproducible(monkeypatch):
-    """TLB_GEMM_SPLIT_TAIL=0: every tile is summed by one CTA pair in k order, so two runs agree bit for bit."""
+    """TLB_GEMM_SPLIT_TAIL=0: every tile is summed by one CTA pair in k order, so two runs agree bit for bit (with the
+    k-range cut of the partial wave the partial sums meet in L2 in arrival order)."""
     monkeypatch.setenv("TLB_GEMM_SPLIT_TAIL", "0")
     monkeypatch.setenv("TLB_GEMM_WIDE", "1")
     assert _bf16_case(*WIDE_SHAPES[4], kat=False, seed=5, path=3) == "umma_2sm_wide"
+    M, N, K = 2048, 2304, 512                                            # 36 pair tiles on 74 CTA pairs
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = (torch.rand(M * K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    b = (torch.rand(N * K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    outs = []
+    for _ in range(2):
+        c = torch.zeros(M * N, dtype=torch.float32, device="cuda")
+        ta = host.tensor_of(f"({M},{K}):({K},1)", a.view(torch.int16), ranked=True)
+        tb = host.tensor_of(f"({N},{K}):({K},1)", b.view(torch.int16), ranked=True)
+        tc = host.tensor_of(f"({M},{N}):({N},1)", c, ranked=True)
+        assert host.gemm_bf16(ta, tb, tc) == "umma_2sm_wide"
+        torch.cuda.synchronize()
+        outs.append(c)
+    assert torch.equal(outs[0], outs[1])
+    ref = a.view(M, K).float() @ b.view(N, K).float().t()
+    assert torch.allclose(outs[0].view(M, N), ref, rtol=1e-3, atol=1e-2)
 
 
 def test_gemm_register_epilogue_matches_tma_epilogue(monkeypatch):
