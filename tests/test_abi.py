@@ -103,6 +103,14 @@ def test_contracts_are_checked_before_any_device_work():
     c_bad = host.make_tensor(L("(4,5):(1,4)").lower(ranked=True), C.addressof(buf), 64, 8)
     assert lib.tlb_gemm_i64(C.byref(a), C.byref(b), C.byref(c_bad), None, None) == abi.TLB_ERR_CONTRACT
     assert b"extents do not agree" in lib.tlb_last_error()
+    # the 2-byte entry points reject other cell sizes, and both check extents before looking for a device
+    for fn in (lib.tlb_gemm_bf16, lib.tlb_gemm_f16):
+        assert fn(C.byref(a), C.byref(b), C.byref(c_bad), 0, 2**32 - 1, None) == abi.TLB_ERR_CONTRACT
+        a2 = host.make_tensor(L("(4,8):(8,1)").lower(ranked=True), C.addressof(buf), 64, 2)
+        b2 = host.make_tensor(L("(6,8):(8,1)").lower(ranked=True), C.addressof(buf), 64, 2)
+        c8 = host.make_tensor(L("(4,6):(6,1)").lower(ranked=True), C.addressof(buf), 64, 8)
+        assert fn(C.byref(a2), C.byref(b2), C.byref(c8), 0, 2**32 - 1, None) == abi.TLB_ERR_CONTRACT
+        assert b"element sizes" in lib.tlb_last_error()
     flat = host.make_tensor(L("32:1").lower(ranked=True), C.addressof(buf), 64, 8)
     assert lib.tlb_gemm_i64(C.byref(flat), C.byref(b), C.byref(c_bad), None, None) == abi.TLB_ERR_CONTRACT
     assert b"rank-2" in lib.tlb_last_error()
@@ -121,6 +129,13 @@ def test_no_cpu_fallback_without_a_device():
     src = host.make_tensor(d, C.addressof(out), 8, 8)
     assert lib.tlb_copy(C.byref(src), C.byref(src), 0, 2**64 - 1, None) == abi.TLB_ERR_CUDA
     assert lib.tlb_copy_host(C.byref(src), C.byref(src)) == abi.TLB_ERR_CUDA
+    h16 = (C.c_int16 * 64)()
+    hc = (C.c_float * 64)()
+    a2 = host.make_tensor(L("(4,8):(8,1)").lower(ranked=True), C.addressof(h16), 64, 2)
+    c4 = host.make_tensor(L("(4,4):(4,1)").lower(ranked=True), C.addressof(hc), 64, 4)
+    for fn in (lib.tlb_gemm_bf16, lib.tlb_gemm_f16):
+        assert fn(C.byref(a2), C.byref(a2), C.byref(c4), 0, 2**32 - 1, None) == abi.TLB_ERR_CUDA
+    assert lib.tlb_gemm_bf16_host(C.byref(a2), C.byref(a2), C.byref(c4)) == abi.TLB_ERR_CUDA
     with pytest.raises(TlbError):
         abi.check(lib.tlb_copy_host(C.byref(src), C.byref(src)))
 
