@@ -419,6 +419,30 @@ def other_configs(torch, dist, world, lib, host, pk, K, W):
                               "of 2 GiB) measured 7533 GB/s on this pool, so frac may exceed 1"}))
     del buf
     torch.cuda.empty_cache()
+    # C2 with C in the operands' type (bf16 C += A B^T, fp32 accumulation in TMEM, one rounding, bf16 reduction at L2): the
+    # like-for-like workload of the cuBLAS bf16 -> bf16 figure that MEASURED_PEAKS.json and library_same_box quote
+    M2 = 4096
+    sets16 = []
+    g2 = torch.Generator(device="cuda").manual_seed(7)
+    for _ in range(3):
+        a16 = (torch.rand(M2 * M2, device="cuda", generator=g2) * 2 - 1).to(torch.bfloat16)
+        b16 = (torch.rand(M2 * M2, device="cuda", generator=g2) * 2 - 1).to(torch.bfloat16)
+        c16 = torch.zeros(M2 * M2, dtype=torch.bfloat16, device="cuda")
+        sets16.append((host.tensor_of(f"({M2},{M2}):({M2},1)", a16.view(torch.int16), ranked=True),
+                       host.tensor_of(f"({M2},{M2}):({M2},1)", b16.view(torch.int16), ranked=True),
+                       host.tensor_of(f"({M2},{M2}):(1,{M2})", c16.view(torch.int16), ranked=True)))
+    sec = timed(torch, dist, world, lambda i: host.gemm_bf16(*sets16[i % 3]), K, W)
+    tf16 = 2.0 * M2 ** 3 * K * world / sec / 1e12
+    per16 = 2.0 * M2 ** 3 / (sec / K) / 1e12
+    out.append({"name": "C2_bf16_c", "metric": "gemm_tflops", "value": tf16, "unit": "TFLOP/s", "ms_per_step": sec / K * 1e3,
+                "config": {"workload": "C2 shape with C in bf16 (C += A B^T, fp32 accumulation in TMEM, bf16 L2 reduction): the output "
+                                       "type of the cuBLAS figure the peak was measured with", "plan": lib.tlb_last_plan().decode()},
+                "roofline": {"bound": "tensor", "achieved": per16, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                             "frac": per16 / pk["bf16_tflops"], "traffic": None, "kernel": "umma_wide_kernel",
+                             "peak_source": f"{pk['_source']} burst cuBLAS bf16", "frac_of_nominal_2250": per16 / 2250.0,
+                             "algorithmic_flop_per_launch": 2.0 * M2 ** 3}})
+    del sets16
+    torch.cuda.empty_cache()
     # C4: batched bf16 GEMM 64 x 8192^3, sharded by whole batches (= tile-id ranges) across the ranks (strong
     # scaling of the 64 batches; every rank owns its batches' operands, no data-path collective)
     from paper_2603_02298_b200 import shard

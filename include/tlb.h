@@ -189,7 +189,8 @@ int tlb_tensormap_fetch_tile(const void* tensormap_128B, int rank, const int32_t
  * leading dimensions TMA cannot address) runs on the layout-evaluating SIMT kernel.
  * Partial tiles of the last wave are summed by several CTA pairs through L2 reductions, so fp32 sums are not
  * bitwise reproducible from run to run unless TLB_GEMM_SPLIT_TAIL=0 is set in the environment.
- * A.elem_bytes = B.elem_bytes = 2, C.elem_bytes = 4. */
+ * A.elem_bytes = B.elem_bytes = 2; C.elem_bytes = 4 (fp32 C) or 2 (C in the operands' type: fp32 accumulation, one
+ * rounding to bf16 / fp16, added to C in that type; tcgen05 wide plan or SIMT). */
 int tlb_gemm_bf16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin,
                   uint32_t tile_end, void* stream);
 /* Number of output tiles of one problem under the plan tlb_gemm_bf16 would choose (host-only, no device

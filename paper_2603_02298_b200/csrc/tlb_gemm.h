@@ -41,6 +41,7 @@ struct UmmaProblem {
     int32_t a_mn, b_mn;            // operand is MN-major (its m / n mode is the contiguous one): wide plan only
     int32_t full_range;            // [tile_begin, tile_end) is every tile of every batch
     int32_t ab_f16;                // operands are IEEE fp16 instead of bf16 (instruction-descriptor formats 0 / 1)
+    int32_t c_16;                  // C has the operands' 2-byte type (C points at 2-byte cells): wide plan only
 };
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
 // Wide plan (tlb_gemm_umma_wide.cu): 512 x 256 pair tiles, chosen when the tile range is a whole number of them.

@@ -40,6 +40,7 @@ struct SimtArgs {
     uint32_t tile_begin, tile_end; // global tile ids (batch-major)
     int32_t batch_begin, batch_end;
     int32_t ab_f16; // 2-byte operands are fp16 instead of bf16
+    int32_t c_16;   // C cells have the operands' 2-byte type
 };
 
 __device__ __forceinline__ int64_t combine(int kind, int64_t a, int64_t b) { return kind == TLB_KIND_XOR ? (a ^ b) : (a + b); }
@@ -89,7 +90,10 @@ gemm_simt_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_consta
             const uint16_t* a = static_cast<const uint16_t*>(A) + batch * p.a_bs;
             const uint16_t* b = static_cast<const uint16_t*>(B) + batch * p.b_bs;
             float* c = static_cast<float*>(C);
-            float acc = c[cp];
+            uint16_t* c16 = static_cast<uint16_t*>(C);
+            float acc;
+            if (p.c_16) acc = p.ab_f16 ? __half2float(__ushort_as_half(c16[cp])) : __uint_as_float(static_cast<uint32_t>(c16[cp]) << 16);
+            else acc = c[cp];
             // bf16 x bf16 and fp16 x fp16 products are exact in fp32, so fma(x, y, acc) == acc + x * y
             for (int64_t k = 0; k < p.K; ++k) {
                 const uint16_t xb = a[dev_position(LA, p.a_origin, combine(LA.kind, a_m, dev_eval_top(LA, 1, k)))];
@@ -98,7 +102,8 @@ gemm_simt_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_consta
                 const float y = p.ab_f16 ? __half2float(__ushort_as_half(yb)) : __uint_as_float(static_cast<uint32_t>(yb) << 16);
                 acc = __fmaf_rn(x, y, acc);
             }
-            c[cp] = acc;
+            if (p.c_16) c16[cp] = p.ab_f16 ? __half_as_ushort(__float2half_rn(acc)) : __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+            else c[cp] = acc;
         }
     }
 }
@@ -147,7 +152,8 @@ int check_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, in
     d->K = top_size(*A->layout, 1);
     if (d->M != top_size(*C->layout, 0) || d->N != top_size(*C->layout, 1) || d->K != top_size(*B->layout, 1))
         return fail(TLB_ERR_CONTRACT, "gemm mode extents do not agree");
-    if (A->elem_bytes != ab_bytes || B->elem_bytes != ab_bytes || C->elem_bytes != c_bytes)
+    const bool c_ok = C->elem_bytes == c_bytes || (ab_bytes == 2 && C->elem_bytes == 2); // C may share the operands' type
+    if (A->elem_bytes != ab_bytes || B->elem_bytes != ab_bytes || !c_ok)
         return fail(TLB_ERR_CONTRACT, "tlb_gemm: element sizes do not match the entry point");
     return TLB_OK;
 }
@@ -215,7 +221,8 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
     f.swapped = csm == 1 && csn != 1;
     p.A = f.swapped ? b_ptr : a_ptr;
     p.B = f.swapped ? a_ptr : b_ptr;
-    p.C = static_cast<float*>(C->data) + C->origin;
+    p.C = reinterpret_cast<float*>(static_cast<char*>(C->data) + C->origin * C->elem_bytes);
+    p.c_16 = C->elem_bytes == 2 ? 1 : 0;
     p.lda = f.swapped ? b_ld : a_ld;
     p.ldb = f.swapped ? a_ld : b_ld;
     p.a_mn = (f.swapped ? b_mn : a_mn) ? 1 : 0;
@@ -277,12 +284,12 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
             p.full_range = (t0 == 0 && t1 == tpb * static_cast<uint64_t>(batch_end)) ? 1 : 0;
             p.ab_f16 = f16 ? 1 : 0;
             const bool mn_major = p.a_mn || p.b_mn;
-            if (!mn_major || umma_wide_applies(p)) {
+            if ((!mn_major && !p.c_16) || umma_wide_applies(p)) {
                 if (p.cta_group == 2 && !even)
                     return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
                 return umma_gemm_launch(p, stream);
             }
-            // MN-major operands are staged by the wide plan only; anything it does not cover runs on the SIMT plan
+            // MN-major operands and 2-byte C are handled by the wide plan only; anything it does not cover runs on the SIMT plan
             if (g_gemm_path == 2 || g_gemm_path == 3)
                 return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: MN-major operands need the wide tcgen05 plan (whole pair tiles, n-contiguous C)");
         } else if (g_gemm_path == 2 || g_gemm_path == 3) {
@@ -310,6 +317,7 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
     p.batch_begin = batch_begin;
     p.batch_end = batch_end;
     p.ab_f16 = f16 ? 1 : 0;
+    p.c_16 = C->elem_bytes == 2 ? 1 : 0;
     const uint64_t total = static_cast<uint64_t>(d.M) * d.N * (batch_end - batch_begin);
     const uint64_t blocks = std::min<uint64_t>((total + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 32);
     const int gridx = static_cast<int>(std::max<uint64_t>(blocks, 1));

@@ -69,6 +69,7 @@ struct WideArgs {
     uint32_t mbw, nb;         // 512-row pair tiles along m, 256-column blocks along n
     uint32_t group_w;         // pair tiles (along m) per rasterisation group
     uint32_t ab_f16;          // operands are fp16 instead of bf16
+    uint32_t c_16;            // C has the operands' 2-byte type: the epilogue rounds to it, 64-column chunks
     uint32_t a_mn, b_mn;      // operand is MN-major: staged as 64-row chunks of [64 k][128 B], MN-major UMMA descriptors
     uint32_t unit_begin;      // first 512 x 256 pair tile of the range (all batches)
     uint32_t dp_units;        // whole tiles, dealt round-robin
@@ -368,6 +369,50 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             for (int h = 0; h < 2; ++h) {
                 mbar_wait_sleep(tfull_bar(h), acc_phase);
                 tc_fence_after();
+                if (args.c_16) {
+                    // C in the operands' 2-byte type: two 32-column TMEM loads make one staged row of 64 cells (128 B),
+                    // rounded to nearest even from the fp32 accumulator; the TMA reduction adds in that type at L2.
+#pragma unroll 1
+                    for (int ci = 0; ci < 2; ++ci, ++chunk_no) {
+                        const uint32_t buf = buf0 + (chunk_no % kEpiBufs) * kEpiWarpBytes;
+                        uint32_t v[32], w[32];
+                        const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + h * BN + colh * (BN / 2) + ci * 64;
+                        tmem_ld32(taddr, v);
+                        tmem_ld32(taddr + 32, w);
+                        if (lane == 0) bulk_wait_read<kEpiBufs - 1>();
+                        tmem_ld_wait();
+                        if (ci == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(tempty_leader + 8u * h);
+                        } else {
+                            __syncwarp();
+                        }
+                        uint32_t pk[32];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (args.ab_f16) {
+                                asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(pk[j]) : "f"(__uint_as_float(v[2 * j + 1])), "f"(__uint_as_float(v[2 * j])));
+                                asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(pk[16 + j]) : "f"(__uint_as_float(w[2 * j + 1])), "f"(__uint_as_float(w[2 * j])));
+                            } else {
+                                asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk[j]) : "f"(__uint_as_float(v[2 * j + 1])), "f"(__uint_as_float(v[2 * j])));
+                                asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk[16 + j]) : "f"(__uint_as_float(w[2 * j + 1])), "f"(__uint_as_float(w[2 * j])));
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + row * 128u + ((c ^ (row & 7u)) << 4)),
+                                         "r"(pk[4 * c + 0]), "r"(pk[4 * c + 1]), "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
+                                         : "memory");
+                        fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_reduce_add_3d(&map_c, buf, n0 + ci * 64, m0 + h * BMH, static_cast<int>(batch));
+                            bulk_commit();
+                        }
+                    }
+                    continue;
+                }
 #pragma unroll 1
                 for (int ci = 0; ci < 4; ++ci, ++chunk_no) {
                     const uint32_t buf = buf0 + (chunk_no % kEpiBufs) * kEpiWarpBytes;
@@ -488,11 +533,12 @@ int encode_operand_mn(TmaDesc* out, const void* base, int64_t ld, int64_t batch_
 }
 
 int encode_c(TmaDesc* out, const UmmaProblem& p, uint32_t box_n, uint32_t box_m, int swizzle) {
+    const uint64_t cb = p.c_16 ? 2 : 4;
     const uint64_t dims[3] = {static_cast<uint64_t>(p.N), static_cast<uint64_t>(p.M), static_cast<uint64_t>(p.batch)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * 4,
-                                 static_cast<uint64_t>(p.batch > 1 ? p.c_bs : p.cs_m * static_cast<int64_t>(p.M)) * 4};
+    const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * cb,
+                                 static_cast<uint64_t>(p.batch > 1 ? p.c_bs : p.cs_m * static_cast<int64_t>(p.M)) * cb};
     const uint32_t box[3] = {box_n, box_m, 1};
-    return tma_encode(out, 4, true, 3, p.C, dims, strides, box, swizzle, 0);
+    return tma_encode(out, static_cast<int>(cb), p.c_16 && p.ab_f16 ? 2 : 1, 3, p.C, dims, strides, box, swizzle, 0);
 }
 
 } // namespace
@@ -551,7 +597,7 @@ bool umma_wide_applies(const UmmaProblem& p) {
     if (!p.full_range && (mb % 2 != 0 || p.tile_begin % 4 != 0 || p.tile_end % 4 != 0)) return false;
     // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue; measured better up to 2048^3, worse from
     // 3072^3) unless an operand is MN-major or the wide plan is forced (TLB_GEMM_WIDE=1)
-    if (!(p.a_mn || p.b_mn)) {
+    if (!(p.a_mn || p.b_mn || p.c_16)) {
         const uint64_t nb = static_cast<uint64_t>((p.N + 255) / 256);
         const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
                                                  : (p.tile_end - p.tile_begin) / 4;
@@ -559,7 +605,8 @@ bool umma_wide_applies(const UmmaProblem& p) {
         if (!(e && e[0] == '1') && pair_tiles < 48) return false;
     }
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
-    return base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N;   // TMA reduce-add epilogue only
+    return base_ok && p.cs_n == 1 && p.cs_m % (p.c_16 ? 8 : 4) == 0 && p.cs_m >= p.N &&   // TMA reduce-add epilogue only
+           (!p.c_16 || p.batch <= 1 || p.c_bs % 8 == 0);
 }
 
 
@@ -576,14 +623,14 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     else TLB_TRY(encode_operand(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BMC));
     if (p.b_mn) TLB_TRY(encode_operand_mn(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch));
     else TLB_TRY(encode_operand(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, BN / 2));
-    TLB_TRY(encode_c(&mc, p, 32, 32, TMA_SW_128));
+    TLB_TRY(encode_c(&mc, p, p.c_16 ? 64 : 32, 32, TMA_SW_128));
     WideArgs a;
     std::memset(&a, 0, sizeof(a));
     // C prefetch into L2 is off by default: measured, it evicts operand lines and costs 1.5 % (8192^3) to 7 % (4096^3).
     a.prefetch_c = 0;
     if (const char* e = std::getenv("TLB_GEMM_PREFETCH_C"))
         if (e[0] == '1') a.prefetch_c = 1;
-    if (a.prefetch_c && encode_c(&mcp, p, 256, BMH, TMA_SW_NONE) != TLB_OK) a.prefetch_c = 0;
+    if (a.prefetch_c && (p.c_16 || encode_c(&mcp, p, 256, BMH, TMA_SW_NONE) != TLB_OK)) a.prefetch_c = 0;
     if (!a.prefetch_c) mcp = mc;
     a.M = p.M;
     a.N = p.N;
@@ -591,6 +638,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     a.mbw = static_cast<uint32_t>((p.M + 511) / 512);
     a.nb = static_cast<uint32_t>((p.N + 255) / 256);
     a.ab_f16 = p.ab_f16 ? 1u : 0u;
+    a.c_16 = p.c_16 ? 1u : 0u;
     a.a_mn = p.a_mn ? 1u : 0u;
     a.b_mn = p.b_mn ? 1u : 0u;
     {
@@ -612,7 +660,8 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     // split_tail off (TLB_GEMM_SPLIT_TAIL=0) every tile is summed by one CTA pair in k order: bitwise reproducible.
     // Partial tiles cost an extra epilogue (C traffic is the expensive part), so the partial wave is only cut when whole
     // tiles would leave more than TLB_GEMM_SK_PCT % (default 4) of the CTA pairs idle in the last wave.
-    a.sk_units = (p.split_tail && kblocks >= 2 * kMinSeg) ? units % W : 0;
+    // (2-byte C: every partial tile would be one more rounding step at L2, so the partial wave is never cut)
+    a.sk_units = (p.split_tail && !p.c_16 && kblocks >= 2 * kMinSeg) ? units % W : 0;
     if (a.sk_units && units > W) {
         int pct = 4;
         if (const char* e = std::getenv("TLB_GEMM_SK_PCT")) pct = std::atoi(e);

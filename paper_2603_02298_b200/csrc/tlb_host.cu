@@ -99,7 +99,7 @@ bool gemm_host_pipelined(const tlb_tensor* A, const tlb_tensor* B, const tlb_ten
     if (const char* e = std::getenv("TLB_HOST_PIPELINE"))
         if (e[0] == '0') return false;
     GemmFlat f;
-    if (!gemm_flat_view(A, B, C, &f)) return false;
+    if (C->elem_bytes != 4 || !gemm_flat_view(A, B, C, &f)) return false;
     if (f.a_sk != 1 || f.b_sk != 1 || f.a_sm < f.K || f.b_sn < f.K) return false;
     const bool c_m_contig = f.c_sm == 1 && f.c_sn >= f.M;         // C (M,N):(1,ldc): slice along n (B and C panels)
     const bool c_n_contig = f.c_sn == 1 && f.c_sm >= f.N;         // C (M,N):(ldc,1): slice along m (A and C panels)

@@ -113,8 +113,8 @@ struct TmaDesc {
     alignas(64) unsigned char bytes[128];
 };
 enum TmaSwizzle { TMA_SW_NONE = 0, TMA_SW_32 = 1, TMA_SW_64 = 2, TMA_SW_128 = 3 };
-// dtype_bytes: 1,2,4,8; is_float selects bf16 / fp32 element types (needed by TMA reductions).
-int tma_encode(TmaDesc* out, int dtype_bytes, bool is_float, int rank, void* base, const uint64_t* dims,
+// dtype_bytes: 1,2,4,8; is_float: 0 unsigned integers, 1 bf16 / fp32, 2 fp16 (the element type matters to TMA reductions).
+int tma_encode(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base, const uint64_t* dims,
                const uint64_t* strides_bytes /* rank-1 entries, dims 1.. */, const uint32_t* box,
                int swizzle, int l2_promotion_bytes);
 

@@ -33,7 +33,7 @@ EncodeTiledFn encode_fn() {
 }
 } // namespace
 
-int tma_encode(TmaDesc* out, int dtype_bytes, bool is_float, int rank, void* base, const uint64_t* dims,
+int tma_encode(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base, const uint64_t* dims,
                const uint64_t* strides_bytes, const uint32_t* box, int swizzle, int l2_promotion_bytes) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(TLB_ERR_CUDA, "cuTensorMapEncodeTiled is not available from this driver");
@@ -41,7 +41,7 @@ int tma_encode(TmaDesc* out, int dtype_bytes, bool is_float, int rank, void* bas
     CUtensorMapDataType dt;
     switch (dtype_bytes) {
     case 1: dt = CU_TENSOR_MAP_DATA_TYPE_UINT8; break;
-    case 2: dt = is_float ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT16; break;
+    case 2: dt = is_float == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : is_float ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT16; break;
     case 4: dt = is_float ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT32; break;
     case 8: dt = CU_TENSOR_MAP_DATA_TYPE_UINT64; break;
     default: return fail(TLB_ERR_UNSUPPORTED, "TMA element size must be 1, 2, 4 or 8 bytes");

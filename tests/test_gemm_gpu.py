@@ -261,6 +261,54 @@ def test_gemm_f16_operands(shape, path, plan, monkeypatch):
     assert _bf16_case(*shape, kat=False, seed=17, path=path, f16=True) == plan
 
 
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("shape", [
+    ("(512,256):(256,1)", "(256,256):(256,1)", "(512,256):(256,1)"),      # n-contiguous C in the operands' type
+    ("(512,256):(256,1)", "(256,256):(256,1)", "(512,256):(1,512)"),      # m-contiguous C (runs transposed)
+    ("(1000,200):(200,1)", "(300,200):(200,1)", "(1000,300):(304,1)"),    # ragged, padded C rows
+    ("(512,256):(1,512)", "(256,256):(1,256)", "(512,256):(256,1)"),      # MN-major operands
+    ("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)"),                     # SIMT plan
+])
+def test_gemm_c_in_the_operand_type(shape, f16):
+    """C with the operands' 2-byte type (the reference's tensors share one value type): fp32 accumulation in TMEM, one
+    rounding to bf16 / fp16, added to C in that type (L2 reduction on the wide plan, in registers on the SIMT plan).
+    Tolerance: one unit in the last place of the result type on |C| + sum |a b| (2^-7 bf16, 2^-10 fp16)."""
+    la, lb, lc = shape
+    M, N, K = _dims(la, lb)
+    rng = np.random.default_rng(31)
+    na, nb, nc = ou.cosize_of(la), ou.cosize_of(lb), ou.cosize_of(lc)
+    ao = ou.orc_eval_range(la, 0, M * K).reshape(K, M).T
+    bo = ou.orc_eval_range(lb, 0, N * K).reshape(K, N).T
+    a, b = np.zeros(na, dtype=np.float32), np.zeros(nb, dtype=np.float32)
+    a[ao] = rng.uniform(-1, 1, (M, K))
+    b[bo] = rng.uniform(-1, 1, (N, K))
+    c0 = rng.uniform(-1, 1, nc).astype(np.float32)
+    if f16:
+        conv = lambda x: x.astype(np.float16).view(np.uint16)
+        back = lambda u: u.view(np.float16).astype(np.float32)
+        ulp = 2.0 ** -10
+    else:
+        conv = ou.f32_to_bf16_bits
+        back = lambda u: (u.astype(np.uint32) << 16).view(np.float32)
+        ulp = 2.0 ** -7
+    ab, bb, cb = conv(a), conv(b), conv(c0)
+    want = back(cb).copy()                                               # fp32 restatement starting from the rounded C
+    st, sabs = ou.orc_gemm_bf16(la, ab, lb, bb, lc, want, want_abs=True, f16=f16)
+    assert st == 0
+    ta_, tb_, tc_ = dev(ab.view(np.int16)), dev(bb.view(np.int16)), dev(cb.view(np.int16))
+    ta, ka = host.tensor_of(la, ta_, ranked=True)
+    tb, kb = host.tensor_of(lb, tb_, ranked=True)
+    tc, kc = host.tensor_of(lc, tc_, ranked=True)
+    plan = (host.gemm_f16 if f16 else host.gemm_bf16)((ta, ka), (tb, kb), (tc, kc))
+    torch.cuda.synchronize()
+    assert plan == ("simt_f16" if f16 else "simt_bf16") if la.startswith("(4,8)") else plan == "umma_2sm_wide"
+    got = back(tc_.cpu().numpy().view(np.uint16))
+    scale = np.abs(back(cb)) + sabs
+    touched = sabs > 0
+    assert (np.abs(got - want)[touched] <= 2 * ulp * scale[touched] + 1e-6).all()
+    assert (got[~touched] == back(cb)[~touched]).all()                   # cells the layout does not address stay untouched
+
+
 def test_gemm_wide_plan_whole_tiles_then_k_ranges():
     """128 pair tiles on 74 CTA pairs: 54 tiles are cut into one k-range per pair and run first, 74 whole tiles follow."""
     _flat_tn_check(4096, 4096, 1024, 3)

@@ -11,17 +11,17 @@ from paper_2603_02298_b200 import abi, host
 M, N, K = (int(x) for x in sys.argv[1:4])
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
 batch = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+import os
 lib = abi.load()
 sets = []
-import os
 nsets = int(os.environ.get('PROBE_SETS', 3 if batch == 1 else 1))
 for s in range(nsets):
     a = torch.empty(batch * M * K, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
     b = torch.empty(batch * N * K, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
-    c = torch.zeros(batch * M * N, dtype=torch.float32, device="cuda")
+    c = torch.zeros(batch * M * N, dtype=torch.bfloat16 if os.environ.get('PROBE_C16') else torch.float32, device="cuda")
     sets.append((host.tensor_of(f"({M},{K}):({K},1)", a.view(torch.int16), ranked=True),
                  host.tensor_of(f"({N},{K}):({K},1)", b.view(torch.int16), ranked=True),
-                 host.tensor_of(f"({M},{N}):(1,{M})", c, ranked=True)))
+                 host.tensor_of(f"({M},{N}):(1,{M})", c.view(torch.int16) if c.dtype == torch.bfloat16 else c, ranked=True)))
 
 
 def step(i):
