@@ -262,21 +262,6 @@ def run_ours(args):
             if clocks.get("sm_max_mhz") and mhz.value < 0.97 * clocks["sm_max_mhz"] and not clocks["reasons"]:
                 clocks["note"] = "SM clock below max inside the kernel: power management under tensor load (sw_power_cap regime)"
     flops = 2.0 * M * N * Kd
-    if rank == 0 and world == 1:
-        # An untimed half-second loop of the same step with nvidia-smi sampling every 20 ms: long enough for the samples
-        # to see the load (the timed region is not), it records the power-capped operating point as context.
-        probe = ClockSampler(local)
-        probe.start(20)
-        time.sleep(0.1)
-        n_probe = max(50, int(0.5 / max(sec / K, 1e-6)))
-        p0 = time.time()
-        psec = timed(torch, dist, 1, gemm_step, n_probe, 0)
-        p1 = time.time()
-        pc = probe.stop(p0 + 0.1, p1)
-        clocks["sustained_probe"] = {"steps": n_probe, "seconds": round(psec, 3), "tflops": flops * n_probe / psec / 1e12,
-                                     "sm_mhz": pc["sm_mhz"], "power_w": pc.get("power_w"), "reasons": pc["reasons"],
-                                     "samples": pc.get("samples")}
-        lib.tlb_gemm_clock_stats(C.byref(mhz), C.byref(us), C.byref(nl))   # drop the probe's stamps
     value = flops * K * world / sec / 1e12
     kernel_s = sec / K
     burst = sec < 1.0
@@ -334,6 +319,34 @@ def run_ours(args):
     other = []
     if not args.gemm_only:
         other = other_configs(torch, dist, world, lib, host, pk, K, W)
+
+    if rank == 0 and world == 1:
+        # LAST, so that it does not pre-heat the other configs: an untimed half-second loop of the C2 step with nvidia-smi
+        # sampling every 20 ms. Long enough for the samples to see the load (the timed region is not); it records the
+        # power-capped operating point as context.
+        psets = []
+        for s_ in range(nsets):
+            a_ = (torch.rand(M * Kd, device="cuda") * 2 - 1).to(torch.bfloat16)
+            b_ = (torch.rand(N * Kd, device="cuda") * 2 - 1).to(torch.bfloat16)
+            c_ = torch.zeros(M * N, dtype=torch.float32, device="cuda")
+            psets.append((host.tensor_of(f"({M},{Kd}):({Kd},1)", a_.view(torch.int16), ranked=True),
+                          host.tensor_of(f"({N},{Kd}):({Kd},1)", b_.view(torch.int16), ranked=True),
+                          host.tensor_of(f"({M},{N}):(1,{M})", c_, ranked=True)))
+        for i in range(3):
+            host.gemm_bf16(*psets[i % nsets])
+        torch.cuda.synchronize()
+        probe = ClockSampler(local)
+        probe.start(20)
+        time.sleep(0.1)
+        n_probe = max(50, int(0.5 / max(sec / K, 1e-6)))
+        p0 = time.time()
+        psec = timed(torch, dist, 1, lambda i: host.gemm_bf16(*psets[i % nsets]), n_probe, 0)
+        p1 = time.time()
+        pc = probe.stop(p0 + 0.1, p1)
+        clocks["sustained_probe"] = {"steps": n_probe, "seconds": round(psec, 3), "tflops": flops * n_probe / psec / 1e12,
+                                     "sm_mhz": pc["sm_mhz"], "power_w": pc.get("power_w"), "reasons": pc["reasons"],
+                                     "samples": pc.get("samples")}
+        del psets
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
