@@ -403,6 +403,30 @@ def test_gemm_batched_matches_per_batch(cg):
         assert (np.abs(got[bi].ravel() - want) <= RTOL * sabs + ATOL).all()
 
 
+def test_gemm_batched_with_c_in_the_operand_type():
+    """Batches 1..2 of a 3-batch problem with bf16 C: batch strides and a batch range on the 2-byte reduction epilogue."""
+    M, N, K, B = 256, 512, 192, 3
+    rng = np.random.default_rng(4)
+    a = ou.f32_to_bf16_bits(rng.uniform(-1, 1, (B, M, K)).astype(np.float32))
+    b = ou.f32_to_bf16_bits(rng.uniform(-1, 1, (B, N, K)).astype(np.float32))
+    c0 = ou.f32_to_bf16_bits(rng.uniform(-1, 1, (B, N, M)).astype(np.float32))
+    back = lambda u: (u.astype(np.uint32) << 16).view(np.float32)
+    ta_, tb_, tc_ = dev(a.view(np.int16)), dev(b.view(np.int16)), dev(c0.view(np.int16))
+    la, lb, lc = f"({M},{K}):({K},1)", f"({N},{K}):({K},1)", f"({M},{N}):(1,{M})"
+    ta = host.make_tensor(L(la).lower(ranked=True), ta_.data_ptr(), ta_.numel(), 2)
+    tb = host.make_tensor(L(lb).lower(ranked=True), tb_.data_ptr(), tb_.numel(), 2)
+    tc = host.make_tensor(L(lc).lower(ranked=True), tc_.data_ptr(), tc_.numel(), 2)
+    assert host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 1, 3) == "umma_2sm_wide"
+    torch.cuda.synchronize()
+    got = back(tc_.cpu().numpy().view(np.uint16))
+    assert (got[0] == back(c0[0])).all()                                 # batch 0 untouched
+    for bi in (1, 2):
+        want = back(c0[bi]).copy().ravel()
+        st, sabs = ou.orc_gemm_bf16(la, a[bi].ravel(), lb, b[bi].ravel(), lc, want, want_abs=True)
+        assert st == 0
+        assert (np.abs(got[bi].ravel() - want) <= 2 * 2.0 ** -7 * (np.abs(back(c0[bi]).ravel()) + sabs) + 1e-6).all()
+
+
 def test_gemm_host_entry_point():
     M, N, K = 256, 256, 128
     i, p = np.meshgrid(np.arange(M), np.arange(K), indexing="ij")
