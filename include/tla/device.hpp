@@ -102,15 +102,18 @@ inline void copy_counting(const Layout& src_layout, Int base, const DeviceTensor
 }
 
 // C(m,n) += A(m,k) * B(n,k), rank-2 tensors with modes addressed by 1-D coordinates (tensor.hpp:214).
-// elem_bytes 8/8/8: the reference's checked int64 arithmetic (overflow_error on wrap, reported after a
-// stream synchronise). elem_bytes 2/2/4: bf16 operands, fp32 accumulator starting from C.
+// elem_bytes 8/8/8: the reference's checked int64 arithmetic; the call waits for the kernel and throws overflow_error
+// on a wrap (tlb_gemm_i64 with a NULL status word is synchronous), and takes no tile range (contract_error otherwise).
+// elem_bytes 2/2/4: bf16 operands, fp32 accumulator starting from C, asynchronous on c.stream.
 inline void gemm(const DeviceTensor& a, const DeviceTensor& b, const DeviceTensor& c, std::uint32_t tile_begin = 0,
                  std::uint32_t tile_end = UINT32_MAX) {
     tlb_layout_desc da = device_detail::lower(a.layout, true), db = device_detail::lower(b.layout, true),
                     dc = device_detail::lower(c.layout, true);
     tlb_tensor ta = device_detail::view(da, a), tb = device_detail::view(db, b), tc = device_detail::view(dc, c);
-    if (c.elem_bytes == 8) device_detail::rethrow(tlb_gemm_i64(&ta, &tb, &tc, nullptr, c.stream));
-    else device_detail::rethrow(tlb_gemm_bf16(&ta, &tb, &tc, tile_begin, tile_end, c.stream));
+    if (c.elem_bytes == 8) {
+        if (tile_begin != 0 || tile_end != UINT32_MAX) throw contract_error("gemm: tile ranges apply to the bf16 / fp16 paths only");
+        device_detail::rethrow(tlb_gemm_i64(&ta, &tb, &tc, nullptr, c.stream));
+    } else device_detail::rethrow(tlb_gemm_bf16(&ta, &tb, &tc, tile_begin, tile_end, c.stream));
 }
 
 // Same contract with IEEE fp16 operands (elem_bytes 2/2/4).

@@ -20,8 +20,15 @@
  *    nothing. (The reference writes partially before a mid-copy bounds_error;
  *    documented difference.)
  *  - `stream` is a cudaStream_t passed as void*. Calls are asynchronous with
- *    respect to the host unless stated otherwise. Thread-safe; the only global
- *    state is a mutex-guarded per-device cache of TMA tensor maps.
+ *    respect to the host unless stated otherwise. Callable from any host thread:
+ *    planner knobs, last error and last plan are per thread; the only shared state
+ *    is a launch counter (atomic) and a mutex-guarded cache of encoded TMA tensor
+ *    maps keyed by (device, pointer, shape, strides, box).
+ *  - Aliasing. tlb_copy: source and destination may overlap in memory (the
+ *    reference's views share one storage, tensor.hpp:29); overlap is detected from
+ *    the two position spans and resolved to the reference's serial ascending-i
+ *    result (plan "aliased" / "serial"). tlb_gemm_*: C must not overlap A or B
+ *    (TLB_ERR_UNSUPPORTED); A and B may alias each other.
  *  - There is no CPU fallback. Without a CUDA device every compute entry point
  *    returns TLB_ERR_CUDA.
  */
@@ -107,7 +114,8 @@ int tlb_abi_version(void);
 const char* tlb_last_error(void);
 /* Number of kernels this library has launched on the calling process (for bench.py's gpu_launches). */
 uint64_t tlb_launch_count(void);
-/* Name of the plan the last tlb_copy/tlb_gemm_* call on this thread selected ("contig", "tiled", "tiled_tma", "gather", "ordered", "umma_2sm", ...). */
+/* Name of the plan the last tlb_copy / tlb_gemm_* / tlb_eval_range call on this thread selected ("vec", "tiled", "tiled_tma",
+ * "gather", "ordered", "aliased", "umma_2sm_wide", "eval_warp32", ...). */
 const char* tlb_last_plan(void);
 
 /* ---- (1) lowering: host layout -> device evaluator parameters --------- */
@@ -129,6 +137,12 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
 int tlb_idx2crd_range(const tlb_layout_desc* shape, uint64_t i0, uint64_t n, int64_t* d_out, void* stream);
 /* d_out[k] = crd2idx(d_crd[k*n_modes ..], shape): tla::crd2idx (int_tuple.hpp:148) on natural coordinates. */
 int tlb_crd2idx_range(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out, void* stream);
+/* Same with the reference's checked arithmetic made visible: like tla::crd2idx, any coordinate VALUES are accepted (the
+ * reference validates only the tree shape, which the flat [n][n_modes] input fixes) and a checked_mul / checked_add
+ * wrap (int_tuple.hpp:154) sets *d_status = TLB_ERR_OVERFLOW (int32 on device, caller zeroes) and leaves d_out[k]
+ * unwritten. tlb_crd2idx_range is this call with d_status = NULL (wrapped elements are skipped silently). */
+int tlb_crd2idx_range_checked(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out,
+                              int32_t* d_status, void* stream);
 /* Counts k in [k0, k0+n) with L(R(k)) != k into *d_mismatch (uint64, device, accumulated with atomicAdd;
  * caller zeroes it): the defining property of tla::right_inverse (algebra.hpp:474) checked in bulk. */
 int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uint64_t k0, uint64_t n,
@@ -209,8 +223,10 @@ int tlb_gemm_f16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_ten
                          int64_t b_batch_stride, int64_t c_batch_stride, int32_t batch_begin, int32_t batch_end,
                          void* stream);
 /* The reference's own value type: int64 cells, wrapping detected as overflow_error
- * (checked_add/checked_mul, common.hpp:99-109) through *d_status (int32 on device, caller zeroes;
- * set to TLB_ERR_OVERFLOW). All elem_bytes = 8. Any layouts. */
+ * (checked_add/checked_mul, common.hpp:99-109). With d_status (int32 on device, caller zeroes) the call is
+ * asynchronous and a wrap sets *d_status = TLB_ERR_OVERFLOW (the wrapped cell keeps its old value). With
+ * d_status == NULL the call owns the status word, waits for the kernel and RETURNS TLB_ERR_OVERFLOW, so a wrap can
+ * never pass silently (this is what tla::gemm in include/tla/device.hpp uses). All elem_bytes = 8. Any layouts. */
 int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream);
 /* Planner knob for tlb_gemm_bf16: 0 auto, 1 SIMT only, 2 tcgen05 cta_group::1, 3 tcgen05 cta_group::2. */
 int tlb_gemm_set_path(int path);
@@ -221,7 +237,8 @@ int tlb_gemm_clock_stats(double* median_mhz, double* median_us, uint32_t* launch
 
 /* ---- host-buffer convenience (the reference-facing call, used for e2e) -- */
 /* Same contracts with HOST pointers in the tlb_tensor.data fields: stages through device memory
- * the library allocates per call, copies in, runs, copies the destination back, synchronises. */
+ * the library keeps per calling thread (grown on demand, with a private stream pair), copies in, runs, copies
+ * the destination back, synchronises. */
 int tlb_copy_host(const tlb_tensor* src, const tlb_tensor* dst);
 int tlb_gemm_bf16_host(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C);
 

@@ -58,6 +58,30 @@ GEMM_FAMILIES = [
 ]
 
 
+AXES_LAYOUTS = [
+    # coordinate_identity goldens (proj/tests/test_layout.cpp:158-160), Table 2's (8,8):(e0,e1), the per-axis
+    # coordinates of test_layout.cpp:99 and TMA-style coordinate tensors of a divided identity
+    ["(4,8):(e0,e1)", 2], ["7:e0", 1], ["(4,(3,2)):(e0,(e1,3*e1))", 2], ["(8,8):(e0,e1)", 2],
+    ["((4,2),(8,4)):((e0,4*e0),(e1,8*e1))", 2], ["((128,64),(4,8)):((e0,e1),(128*e0,64*e1))", 2],
+    ["(3,5,7):(e2,e0,e1)", 3], ["(4,6):(0,e1)", 2], ["(2,3,2,5):(e0,2*e1,e2,7*e3)", 4], ["(6,4):(e0,e0)", 1],
+    ["(2,2,2,2,2):(e0,e1,e2,e3,e4)", 5],
+]
+
+ALIAS_CASES = [
+    # [src layout, src origin, dst layout, dst origin, storage cells]: both tensors view ONE storage (tensor.hpp:29)
+    ["16:1", 0, "16:1", 1, 20],          # shift right by one: every cell becomes cell 0 (read-after-write chain)
+    ["16:1", 1, "16:1", 0, 20],          # shift left by one: a plain move (reads stay ahead of the writes)
+    ["16:1", 0, "16:1", 0, 16],          # in place
+    ["(4,4):(4,1)", 0, "(4,4):(1,4)", 0, 16],   # in-place transpose under the serial order
+    ["(8,2):(1,8)", 0, "(8,2):(2,1)", 3, 24],
+    ["12:1", 0, "12:2", 1, 30],
+    ["(4,6):(1,4)", 2, "(4,6):(6,1)", 0, 30],
+    ["(4,6):(1,4)", 0, "(4,6):(0,1)", 2, 30],   # non-injective destination AND overlap
+    ["7:0", 3, "7:1", 0, 8],
+    ["(8,8):(f1,f9)", 0, "64:1", 8, 80],
+]
+
+
 def cosize(text):
     st, r = ou.ref_op("cosize", text)
     if st == 0:
@@ -142,6 +166,24 @@ def main():
     ops["C5_L_values"] = [int(ou.ref_eval_range(ops["C5_L"], int(i), 1)[0]) for i in idx]
     ops["C5_R_values"] = [int(ou.ref_eval_range(ops["C5_R"], int(i), 1)[0]) for i in idx]
     (OUT / "ops.json").write_text(json.dumps(ops, indent=1))
+    ax = []
+    for t, na in AXES_LAYOUTS:
+        n = int(ou.ref_op("size", t)[1])
+        # whole domain + 3 extended-domain points when small, else a head window and a tail window
+        wins = [(0, n + 3)] if n <= 2048 else [(0, 1024), (n - 1024, 1027)]
+        ax.append({"layout": t, "n_axes": na, "size": n,
+                   "windows": [{"i0": i0, "values": ou.ref_eval_axes_range(t, na, i0, cnt).tolist()} for i0, cnt in wins]})
+    st, ci = ou.ref_op("coordinate_identity", "(8,8)")
+    assert st == 0 and ci == "(8,8):(e0,e1)", ci
+    (OUT / "axes.json").write_text(json.dumps(ax))
+
+    al = []
+    for s, so, d, do, cells in ALIAS_CASES:
+        buf = np.arange(cells, dtype=np.int64) * 3 + 1
+        st = ou.ref_copy_shared(s, d, buf, so, do)
+        al.append({"src": s, "src_origin": so, "dst": d, "dst_origin": do, "cells": cells, "status": st,
+                   "result": buf.tolist()})
+    (OUT / "alias.json").write_text(json.dumps(al))
     print("golden fixtures written to", OUT)
 
 

@@ -239,6 +239,34 @@ int ref_copy(const char* src_layout, const std::int64_t* src_cells, std::int64_t
     return st;
 }
 
+// tla::copy verbatim where source and destination are views of ONE shared storage (tensor.hpp:29): the serial
+// ascending-i order decides what overlapping cells end up holding.
+int ref_copy_shared(const char* src_layout, std::int64_t src_origin, const char* dst_layout, std::int64_t dst_origin,
+                    std::int64_t* cells, std::int64_t len) {
+    std::shared_ptr<std::vector<Int>> st_;
+    int st = guarded([&] {
+        st_ = wrap(cells, len);
+        Tensor src(Accessor::buffer(st_, src_origin), parse_layout(src_layout));
+        Tensor dst(Accessor::buffer(st_, dst_origin), parse_layout(dst_layout));
+        copy(src, dst);
+    });
+    if (st_) std::memcpy(cells, st_->data(), static_cast<std::size_t>(len) * sizeof(Int));
+    return st;
+}
+
+// layout_eval_axes (layout.hpp:103) over a range: out[k*n_axes + a], axes the reference's vector does not reach are 0.
+int ref_eval_axes_range(const char* layout, std::int64_t i0, std::int64_t n, int n_axes, std::int64_t* out) {
+    return guarded([&] {
+        Layout l = parse_layout(layout);
+        for (Int k = 0; k < n; ++k) {
+            std::vector<Int> v = layout_eval_axes(l, Coord(i0 + k));
+            if (static_cast<int>(v.size()) > n_axes) throw contract_error("ref_eval_axes_range: more axes than n_axes");
+            for (int a = 0; a < n_axes; ++a)
+                out[static_cast<std::size_t>(k) * n_axes + a] = a < static_cast<int>(v.size()) ? v[static_cast<std::size_t>(a)] : 0;
+        }
+    });
+}
+
 // The loop body of tla::copy (dst.store(i, src(i)), tensor.hpp:198) run by
 // `threads` std::threads over disjoint i-ranges, operating in place on the
 // caller's arrays. Only meaningful for injective destinations. Used as the

@@ -55,6 +55,7 @@ SYMBOLS = {
     "tlb_eval_range": (C.c_int, [_P(tlb_layout_desc), C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
     "tlb_idx2crd_range": (C.c_int, [_P(tlb_layout_desc), C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
     "tlb_crd2idx_range": (C.c_int, [_P(tlb_layout_desc), C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "tlb_crd2idx_range_checked": (C.c_int, [_P(tlb_layout_desc), C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tlb_rinv_check_range": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), C.c_uint64, C.c_uint64, C.c_void_p,
                                        C.c_void_p]),
     "tlb_compose_check_range": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(tlb_layout_desc), C.c_uint64,

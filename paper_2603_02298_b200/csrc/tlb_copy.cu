@@ -18,6 +18,9 @@
 //           one element per thread through the device evaluator. Always correct, never fast.
 //   ordered non-injective destinations: last writer wins in ascending i (tensor.hpp:198), kept
 //           by a two-pass winner election (atomicMax of i per destination cell).
+//   aliased source and destination ranges overlap in one buffer (views share storage, tensor.hpp:29):
+//           the serial read-after-write chains are resolved by pointer jumping, then one snapshot
+//           and one scatter ("serial", one thread, when the destination is also non-injective).
 //
 // All contract / bounds / overflow checks happen on the host before any launch.
 #include <algorithm>
@@ -148,6 +151,72 @@ ordered_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant_
             }
         }
         static_cast<T*>(dst)[dp] = static_cast<const T*>(src)[sp];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// aliased: source and destination position spans overlap inside one buffer. The reference copies serially in
+// ascending i over shared storage (tensor.hpp:29,195-199), so src(i) may read what an earlier dst(j) wrote:
+//   value(i) = value(pred(i))   where pred(i) = the writer j < i of the cell src(i) reads   (else the original cell)
+// Injective destinations have at most one writer per cell, so pred is a forest; pointer jumping resolves every i to
+// the root whose ORIGINAL cell it ends up copying. Values are snapshotted before anything is stored.
+// ---------------------------------------------------------------------------------------
+// pass 2 (pass 1 is winner_kernel: writer[dp - lo] = i + 1): root[k] = pred(i0 + k) - i0, or k when there is none.
+// `shift` = (src.data - dst.data) / elem_bytes converts a source position into the destination buffer's cell index.
+__global__ void __launch_bounds__(kThreads)
+alias_pred_kernel(const __grid_constant__ tlb_layout_desc S, int64_t s_origin, int64_t shift, int64_t dlo, int64_t dhi,
+                  uint64_t i0, uint64_t n, const unsigned long long* writer, unsigned long long* root) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint64_t i = i0 + k;
+        const int64_t p = dev_position(S, s_origin, dev_eval(S, i)) + shift;
+        unsigned long long r = k;
+        if (p >= dlo && p <= dhi) {
+            const unsigned long long w = writer[p - dlo];
+            if (w != 0 && w - 1 < i) r = w - 1 - i0;
+        }
+        root[k] = r;
+    }
+}
+// pass 3, ceil(log2 n) times: root[k] = root[root[k]] (in place: a concurrently updated entry is still an ancestor)
+__global__ void __launch_bounds__(kThreads) alias_jump_kernel(uint64_t n, unsigned long long* root) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const unsigned long long r = root[k];
+        const unsigned long long rr = root[r];
+        if (rr != r) root[k] = rr;
+    }
+}
+// pass 4: vals[k] = original source cell of the root; pass 5: dst(i0 + k) = vals[k]
+template <int EB>
+__global__ void __launch_bounds__(kThreads)
+alias_fetch_kernel(const __grid_constant__ tlb_layout_desc S, const void* src, int64_t s_origin, uint64_t i0, uint64_t n,
+                   const unsigned long long* root, void* vals) {
+    using T = typename Cell<EB>::type;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride)
+        static_cast<T*>(vals)[k] = static_cast<const T*>(src)[dev_position(S, s_origin, dev_eval(S, i0 + root[k]))];
+}
+template <int EB>
+__global__ void __launch_bounds__(kThreads)
+alias_store_kernel(const __grid_constant__ tlb_layout_desc D, void* dst, int64_t d_origin, uint64_t i0, uint64_t n,
+                   const void* vals) {
+    using T = typename Cell<EB>::type;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride)
+        static_cast<T*>(dst)[dev_position(D, d_origin, dev_eval(D, i0 + k))] = static_cast<const T*>(vals)[k];
+}
+// Non-injective destination AND aliasing: the reference's loop itself, one thread, ascending i (small copies only).
+template <int EB>
+__global__ void serial_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__ tlb_layout_desc D,
+                              const void* src, void* dst, int64_t s_origin, int64_t d_origin, uint64_t i0, uint64_t n) {
+    using T = typename Cell<EB>::type;
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (uint64_t k = 0; k < n; ++k) {
+        const uint64_t i = i0 + k;
+        // src and dst are not __restrict__: program order of one thread's loads and stores is kept
+        const T v = static_cast<const T*>(src)[dev_position(S, s_origin, dev_eval(S, i))];
+        static_cast<T*>(dst)[dev_position(D, d_origin, dev_eval(D, i))] = v;
     }
 }
 
@@ -700,6 +769,79 @@ int launch_ordered(const CopyCall& c, Span dspan) {
     return TLB_OK;
 }
 
+// Source and destination spans overlap in memory (see the alias kernels above).
+int launch_aliased(const CopyCall& c, Span dspan, bool injective) {
+    const tlb_layout_desc& S = *c.src->layout;
+    const tlb_layout_desc& D = *c.dst->layout;
+    const int eb = c.dst->elem_bytes;
+    const intptr_t delta = reinterpret_cast<intptr_t>(c.src->data) - reinterpret_cast<intptr_t>(c.dst->data);
+    if (delta % eb != 0)
+        return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: source and destination overlap at a sub-cell offset");
+    if (!injective) {
+        if (c.n > (1ull << 20))
+            return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: overlapping source and non-injective destination above 2^20 elements");
+        if (g_dry_run) {
+            set_plan("serial");
+            return TLB_OK;
+        }
+#define TLB_SERIAL(EB) serial_kernel<EB><<<1, 32, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, c.i0, c.n)
+        switch (eb) {
+        case 1: TLB_SERIAL(1); break;
+        case 2: TLB_SERIAL(2); break;
+        case 4: TLB_SERIAL(4); break;
+        case 8: TLB_SERIAL(8); break;
+        default: TLB_SERIAL(16); break;
+        }
+#undef TLB_SERIAL
+        count_launch();
+        TLB_CUDA(cudaGetLastError());
+        set_plan("serial");
+        return TLB_OK;
+    }
+    if (g_dry_run) {
+        set_plan("aliased");
+        return TLB_OK;
+    }
+    const uint64_t cells = static_cast<uint64_t>(dspan.hi - dspan.lo) + 1;
+    unsigned long long *writer = nullptr, *root = nullptr;
+    void* vals = nullptr;
+    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&writer), cells * 8, c.stream));
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&root), c.n * 8, c.stream);
+    if (e == cudaSuccess) e = cudaMallocAsync(&vals, c.n * static_cast<uint64_t>(eb), c.stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(writer, 0, cells * 8, c.stream);
+    int launches = 0;
+    if (e == cudaSuccess) {
+        const int grid = launch_grid(c.n, kThreads, 8);
+        winner_kernel<<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, writer);
+        alias_pred_kernel<<<grid, kThreads, 0, c.stream>>>(S, c.src->origin, static_cast<int64_t>(delta / eb), dspan.lo, dspan.hi,
+                                                           c.i0, c.n, writer, root);
+        launches = 2;
+        for (uint64_t span = 1; span < c.n; span <<= 1, ++launches) alias_jump_kernel<<<grid, kThreads, 0, c.stream>>>(c.n, root);
+#define TLB_ALIAS(EB)                                                                                                   \
+    do {                                                                                                                \
+        alias_fetch_kernel<EB><<<grid, kThreads, 0, c.stream>>>(S, c.src->data, c.src->origin, c.i0, c.n, root, vals);  \
+        alias_store_kernel<EB><<<grid, kThreads, 0, c.stream>>>(D, c.dst->data, c.dst->origin, c.i0, c.n, vals);        \
+    } while (0)
+        switch (eb) {
+        case 1: TLB_ALIAS(1); break;
+        case 2: TLB_ALIAS(2); break;
+        case 4: TLB_ALIAS(4); break;
+        case 8: TLB_ALIAS(8); break;
+        default: TLB_ALIAS(16); break;
+        }
+#undef TLB_ALIAS
+        launches += 2;
+        e = cudaGetLastError();
+    }
+    count_launch(launches);
+    if (writer) cudaFreeAsync(writer, c.stream);
+    if (root) cudaFreeAsync(root, c.stream);
+    if (vals) cudaFreeAsync(vals, c.stream);
+    TLB_CUDA(e);
+    set_plan("aliased");
+    return TLB_OK;
+}
+
 bool aligned_to(const void* p, int64_t origin, int eb, int bytes) {
     return ((reinterpret_cast<uintptr_t>(p) + static_cast<uintptr_t>(origin) * eb) % bytes) == 0;
 }
@@ -1055,6 +1197,16 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
     Span sspan, dspan;
     TLB_TRY(bounds_preflight(*src, c.i0, c.n, "source", stream, &sspan));
     TLB_TRY(bounds_preflight(*dst, c.i0, c.n, "destination", stream, &dspan));
+    // Aliasing (tensor.hpp:29: every sliced view shares one storage): when the byte ranges the two tensors touch
+    // intersect, the reference's serial order decides the result; the parallel plans below assume disjoint ranges.
+    if (src->accessor == TLB_ACC_BUFFER) {
+        const uintptr_t eb = static_cast<uintptr_t>(dst->elem_bytes);
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(src->data) + static_cast<uintptr_t>(sspan.lo) * eb;
+        const uintptr_t s1 = reinterpret_cast<uintptr_t>(src->data) + (static_cast<uintptr_t>(sspan.hi) + 1) * eb;
+        const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst->data) + static_cast<uintptr_t>(dspan.lo) * eb;
+        const uintptr_t d1 = reinterpret_cast<uintptr_t>(dst->data) + (static_cast<uintptr_t>(dspan.hi) + 1) * eb;
+        if (s0 < d1 && d0 < s1) return launch_aliased(c, dspan, (D.flags & TLB_LF_INJECTIVE) != 0);
+    }
     if (!(D.flags & TLB_LF_INJECTIVE)) return launch_ordered(c, dspan);
     if (g_copy_path != 1) {
         bool done = false;

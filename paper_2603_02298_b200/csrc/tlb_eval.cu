@@ -187,20 +187,34 @@ __global__ void __launch_bounds__(kThreads) idx2crd_kernel(const __grid_constant
     }
 }
 
-// out[k] = sum_r crd[k*nm + r] * prod_{q<r} extent[q]  (crd2idx, int_tuple.hpp:148).
+// out[k] = sum_r crd[k*nm + r] * prod_{q<r} extent[q]  (crd2idx, int_tuple.hpp:148-158). The reference accepts any
+// coordinate VALUES (only the tree shape is validated, which the flat [n][n_modes] input fixes by construction) and
+// detects wrapping through checked_mul / checked_add (common.hpp:99-109); so does this kernel: a wrapped element
+// is not written and *d_status (when given) becomes TLB_ERR_OVERFLOW. The prefix products themselves are proven to
+// fit on the host (the lowering rejects shapes whose size overflows).
 __global__ void __launch_bounds__(kThreads) crd2idx_kernel(const __grid_constant__ tlb_layout_desc S,
                                                            const int64_t* __restrict__ crd, uint64_t n,
-                                                           int64_t* __restrict__ out) {
+                                                           int64_t* __restrict__ out, int* d_status) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const int nm = S.n_modes;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
         const int64_t* c = crd + k * nm;
         int64_t idx = 0, scale = 1;
+        bool ovf = false;
         for (int r = 0; r < nm; ++r) {
-            idx += c[r] * scale;
+            const int64_t x = c[r];
+            const int64_t lo = static_cast<int64_t>(static_cast<uint64_t>(x) * static_cast<uint64_t>(scale));
+            ovf |= __mul64hi(x, scale) != (lo >> 63);
+            const int64_t sum = static_cast<int64_t>(static_cast<uint64_t>(idx) + static_cast<uint64_t>(lo));
+            ovf |= ((idx ^ sum) & (lo ^ sum)) < 0;
+            idx = sum;
             scale *= S.extent[r];
         }
-        out[k] = idx;
+        if (ovf) {
+            if (d_status) atomicExch(d_status, TLB_ERR_OVERFLOW);
+        } else {
+            out[k] = idx;
+        }
     }
 }
 
@@ -382,6 +396,9 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
             count_launch();
             TLB_CUDA(cudaGetLastError());
             groups_done = n_super * 32;
+            set_plan(G == 32 ? "eval_warp32" : G == 16 ? "eval_warp16" : G == 8 ? "eval_warp8" : "eval_warp4");
+        } else {
+            set_plan(G == 32 ? "eval_group32" : G == 16 ? "eval_group16" : G == 8 ? "eval_group8" : G == 4 ? "eval_group4" : "eval_group2");
         }
         const uint64_t groups_left = groups - groups_done;
         const uint64_t i0g = i0 + groups_done * G;
@@ -414,6 +431,7 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
         }
         return TLB_OK;
     }
+    set_plan("eval_scalar");
     const bool pairs = aligned && n >= 2;
     if (pairs) eval_range_kernel<true><<<grid_for(n >> 1), kThreads, 0, s>>>(*layout, i0, n, d_out);
     else eval_range_kernel<false><<<grid_for(n), kThreads, 0, s>>>(*layout, i0, n, d_out);
@@ -442,15 +460,23 @@ int tlb_idx2crd_range(const tlb_layout_desc* shape, uint64_t i0, uint64_t n, int
     return TLB_OK;
 }
 
-int tlb_crd2idx_range(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out, void* stream) {
+int tlb_crd2idx_range_checked(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out,
+                              int32_t* d_status, void* stream) {
     if (!shape) return fail(TLB_ERR_CONTRACT, "tlb_crd2idx_range: null shape");
     if (n == 0) return TLB_OK;
     if (!d_crd || !d_out) return fail(TLB_ERR_CONTRACT, "tlb_crd2idx_range: null buffer");
+    // scale = checked_mul(scale, size(mode)) runs for every mode, the last included (int_tuple.hpp:155): the
+    // lowering has already proven that the full product fits (shape->size), so no prefix product can wrap.
+    if (shape->size < 1) return fail(TLB_ERR_OVERFLOW, "integer overflow in multiplication");
     TLB_TRY(require_device());
-    crd2idx_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*shape, d_crd, n, d_out);
+    crd2idx_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*shape, d_crd, n, d_out, d_status);
     count_launch();
     TLB_CUDA(cudaGetLastError());
     return TLB_OK;
+}
+
+int tlb_crd2idx_range(const tlb_layout_desc* shape, const int64_t* d_crd, uint64_t n, int64_t* d_out, void* stream) {
+    return tlb_crd2idx_range_checked(shape, d_crd, n, d_out, nullptr, stream);
 }
 
 int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uint64_t k0, uint64_t n,
@@ -462,7 +488,8 @@ int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uin
     if (k0 + n < k0 || (k0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
     TLB_TRY(require_device());
     TLB_TRY(overflow_preflight(*R, 0, k0 + n - 1));
-    if (R->max_offset >= 0) TLB_TRY(overflow_preflight(*L, 0, static_cast<uint64_t>(R->max_offset)));
+    // L is evaluated at R(k), and k may lie in R's extended domain: bound |R(k)| over [0, k0 + n)
+    TLB_TRY(overflow_preflight(*L, 0, max_abs_offset(*R, k0 + n - 1)));
     rinv_check_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*L, *R, k0, n, d_mismatch);
     count_launch();
     TLB_CUDA(cudaGetLastError());
@@ -481,7 +508,7 @@ int tlb_compose_check_range(const tlb_layout_desc* A, const tlb_layout_desc* B, 
     TLB_TRY(require_device());
     TLB_TRY(overflow_preflight(*B, 0, i0 + n - 1));
     TLB_TRY(overflow_preflight(*R, 0, i0 + n - 1));
-    if (B->max_offset >= 0) TLB_TRY(overflow_preflight(*A, 0, static_cast<uint64_t>(B->max_offset)));
+    TLB_TRY(overflow_preflight(*A, 0, max_abs_offset(*B, i0 + n - 1)));
     compose_check_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*A, *B, *R, i0, n, d_mismatch);
     count_launch();
     TLB_CUDA(cudaGetLastError());
@@ -510,6 +537,22 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
     }
     if (n == 0) return TLB_OK;
     if (!d_out) return fail(TLB_ERR_CONTRACT, "tlb_eval_axes_range: null output");
+    if (i0 + n < i0 || (i0 + n - 1) >> 63) return fail(TLB_ERR_OVERFLOW, "index range exceeds int64");
+    {
+        // checked_mul / checked_add of layout_eval_axes (stride.hpp:152, layout.hpp:92): prove per axis that the sum of
+        // the largest leaf contributions over [0, i0 + n) fits in int64 (the last leaf is unbounded)
+        unsigned __int128 per_axis[TLB_MAX_MODES] = {};
+        uint64_t rest = i0 + n - 1;
+        for (int r = 0; r < n_modes; ++r) {
+            const uint64_t e = static_cast<uint64_t>(M.extent[r]);
+            const uint64_t cmax = (r + 1 < n_modes) ? std::min<uint64_t>(rest, e - 1) : rest;
+            rest /= e;
+            if (M.axis[r] < 0) continue;
+            const uint64_t a = M.scale[r] < 0 ? 0 - static_cast<uint64_t>(M.scale[r]) : static_cast<uint64_t>(M.scale[r]);
+            per_axis[M.axis[r]] += static_cast<unsigned __int128>(cmax) * a;
+            if (per_axis[M.axis[r]] >> 63) return fail(TLB_ERR_OVERFLOW, "integer overflow in layout evaluation");
+        }
+    }
     TLB_TRY(require_device());
     {
         cudaStream_t st = static_cast<cudaStream_t>(stream);

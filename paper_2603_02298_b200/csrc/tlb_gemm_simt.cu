@@ -41,6 +41,7 @@ struct SimtArgs {
     int32_t batch_begin, batch_end;
     int32_t ab_f16; // 2-byte operands are fp16 instead of bf16
     int32_t c_16;   // C cells have the operands' 2-byte type
+    int32_t swapped; // tile ids refer to the TRANSPOSED problem (the tcgen05 plans run m-contiguous C as C^T): tile_of(n, m)
 };
 
 __device__ __forceinline__ int64_t combine(int kind, int64_t a, int64_t b) { return kind == TLB_KIND_XOR ? (a ^ b) : (a + b); }
@@ -59,7 +60,7 @@ gemm_simt_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_consta
         const uint64_t e = idx % per_batch;
         const int64_t m = static_cast<int64_t>(e % static_cast<uint64_t>(p.M));
         const int64_t n = static_cast<int64_t>(e / static_cast<uint64_t>(p.M));
-        const uint64_t tile = static_cast<uint64_t>(batch) * tpb + tile_of(p.grid, m, n);
+        const uint64_t tile = static_cast<uint64_t>(batch) * tpb + (p.swapped ? tile_of(p.grid, n, m) : tile_of(p.grid, m, n));
         if (tile < p.tile_begin || tile >= p.tile_end) continue;
         const int64_t a_m = dev_eval_top(LA, 0, m), b_n = dev_eval_top(LB, 0, n);
         const int64_t cp = dev_position(LC, p.c_origin, combine(LC.kind, dev_eval_top(LC, 0, m), dev_eval_top(LC, 1, n))) +
@@ -171,6 +172,18 @@ int gemm_bounds(const tlb_tensor& t, int64_t bs, int b0, int b1, const char* who
     return TLB_OK;
 }
 
+// Byte range [lo, hi) that a (batched) operand may touch (conservative: span of the whole offset image).
+bool byte_range(const tlb_tensor& t, int64_t bs, int b0, int b1, uintptr_t* lo, uintptr_t* hi) {
+    Span sp;
+    if (position_span(*t.layout, t.origin, &sp) != TLB_OK) return false;
+    const int64_t first = bs * b0, last = bs * (b1 - 1);
+    const int64_t plo = sp.lo + std::min(first, last), phi = sp.hi + std::max(first, last);
+    const uintptr_t base = reinterpret_cast<uintptr_t>(t.data);
+    *lo = base + static_cast<uintptr_t>(plo) * static_cast<uintptr_t>(t.elem_bytes);
+    *hi = base + (static_cast<uintptr_t>(phi) + 1) * static_cast<uintptr_t>(t.elem_bytes);
+    return true;
+}
+
 // The tcgen05 plan applies to K-major A and B with single-stride C modes and TMA-legal strides. When C is
 // m-contiguous (the paper's TN row, (M,N):(1,ldc)) the problem is run transposed, C^T += B * A^T: the roles of
 // A and B swap, so the accumulator's TMEM lanes run along n and every epilogue thread holds 32 consecutive m
@@ -265,6 +278,15 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
     TLB_TRY(gemm_bounds(*A, a_bs, batch_begin, batch_end, "A", stream));
     TLB_TRY(gemm_bounds(*B, b_bs, batch_begin, batch_end, "B", stream));
     TLB_TRY(gemm_bounds(*C, c_bs, batch_begin, batch_end, "C", stream));
+    {
+        // Aliasing rule (include/tlb.h): C must not overlap A or B. In the reference the three tensors may share storage
+        // (tensor.hpp:29) and the serial m, n, k order then decides what later cells read; no parallel plan keeps that.
+        uintptr_t clo, chi, olo, ohi;
+        if (byte_range(*C, c_bs, batch_begin, batch_end, &clo, &chi))
+            for (const tlb_tensor* o : {A, B})
+                if (byte_range(*o, o == A ? a_bs : b_bs, batch_begin, batch_end, &olo, &ohi) && olo < chi && clo < ohi)
+                    return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: C overlaps an operand in memory (aliased accumulators are order-dependent)");
+    }
     // Global tile range: the caller's range applies inside [batch_begin, batch_end).
     uint64_t t0 = static_cast<uint64_t>(batch_begin) * tpb, t1 = static_cast<uint64_t>(batch_end) * tpb;
     if (tile_begin != 0 || tile_end != UINT32_MAX) {
@@ -318,6 +340,9 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
     p.batch_end = batch_end;
     p.ab_f16 = f16 ? 1 : 0;
     p.c_16 = C->elem_bytes == 2 ? 1 : 0;
+    // the grid above was built from the problem as the tcgen05 plans run it; keep the SAME tile ids when this call falls
+    // through to SIMT (sharded ranges may mix plans across ranks), i.e. index the grid with (n, m) when it is transposed
+    p.swapped = (fit.ok && fit.swapped) ? 1 : 0;
     const uint64_t total = static_cast<uint64_t>(d.M) * d.N * (batch_end - batch_begin);
     const uint64_t blocks = std::min<uint64_t>((total + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 32);
     const int gridx = static_cast<int>(std::max<uint64_t>(blocks, 1));
@@ -382,7 +407,25 @@ int tlb_gemm_f16_batched(const tlb_tensor* A, const tlb_tensor* B, const tlb_ten
 }
 
 int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, int32_t* d_status, void* stream) {
-    return tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, d_status, static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (d_status) return tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, d_status, s);
+    // No status word from the caller: the call owns one, waits for the kernel and reports the reference's
+    // overflow_error (common.hpp:99-109) as its return value, so a wrap can never pass silently.
+    int32_t* d = nullptr;
+    int32_t h = 0;
+    uint32_t tiles = 0;
+    TLB_TRY(tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, nullptr, nullptr, &tiles)); // contracts first, no device needed
+    if (tlb::require_device() != TLB_OK) return TLB_ERR_CUDA;
+    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int32_t), s));
+    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(int32_t), s);
+    int st = e == cudaSuccess ? tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, d, s) : TLB_OK;
+    if (e == cudaSuccess && st == TLB_OK) e = cudaMemcpyAsync(&h, d, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && st == TLB_OK) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(d, s);
+    TLB_CUDA(e);
+    if (st != TLB_OK) return st;
+    if (h == TLB_ERR_OVERFLOW) return tlb::fail(TLB_ERR_OVERFLOW, "integer overflow in gemm accumulation");
+    return TLB_OK;
 }
 
 int tlb_gemm_tile_count(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t* tiles) {

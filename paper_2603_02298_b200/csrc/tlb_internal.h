@@ -45,6 +45,8 @@ int position_span(const tlb_layout_desc& L, int64_t origin, Span* out);
 // Conservative proof that no checked_add/checked_mul of the reference (common.hpp:99-109)
 // can overflow while evaluating L on [0, max_index].
 int overflow_preflight(const tlb_layout_desc& L, int64_t origin, uint64_t max_index);
+// Upper bound of |L(i)| over 0 <= i <= max_index (extended domain), saturating at INT64_MAX.
+uint64_t max_abs_offset(const tlb_layout_desc& L, uint64_t max_index);
 bool provably_injective(const tlb_layout_desc& L);
 // Argument contract of one tensor (null pointers, accessor, element size).
 int check_tensor(const tlb_tensor* t, const char* who, bool writable);

@@ -243,6 +243,29 @@ int position_span(const tlb_layout_desc& L, int64_t origin, Span* out) {
     return fail(TLB_ERR_SEMIMODULE, "integer accessor cannot take a coordinate offset");
 }
 
+// Upper bound of |L(i)| over 0 <= i <= max_index (extended domain: the last leaf is unbounded), saturating at 2^63 - 1.
+uint64_t max_abs_offset(const tlb_layout_desc& L, uint64_t max_index) {
+    unsigned __int128 total = 0;
+    uint64_t rest = max_index, orb = 0;
+    for (int r = 0; r < L.n_modes; ++r) {
+        const uint64_t e = static_cast<uint64_t>(L.extent[r]);
+        const uint64_t cmax = (r + 1 < L.n_modes) ? std::min<uint64_t>(rest, e - 1) : rest;
+        rest /= e;
+        if (L.kind == TLB_KIND_XOR) {
+            const uint64_t m = static_cast<uint64_t>(L.stride[r]);
+            if (cmax == 0 || m == 0) continue;
+            const int top = ilog2_floor(cmax);
+            if (top >= 62 || (m << top) >= (1ull << 62)) return INT64_MAX;
+            for (int b = 0; b <= top; ++b) orb |= m << b;
+        } else {
+            const uint64_t a = L.stride[r] < 0 ? 0 - static_cast<uint64_t>(L.stride[r]) : static_cast<uint64_t>(L.stride[r]);
+            total += static_cast<unsigned __int128>(cmax) * a;
+            if (total >> 63) return INT64_MAX;
+        }
+    }
+    return L.kind == TLB_KIND_XOR ? orb : static_cast<uint64_t>(total);
+}
+
 int overflow_preflight(const tlb_layout_desc& L, int64_t origin, uint64_t max_index) {
     // Largest coordinate each leaf sees for i <= max_index; the last leaf is unbounded.
     unsigned __int128 total = origin < 0 ? static_cast<unsigned __int128>(0 - static_cast<uint64_t>(origin))

@@ -218,9 +218,10 @@ def copy_plan(src_layout, dst_layout, elem_bytes: int, i_begin: int = 0, i_end: 
     ls = L(src_layout) if isinstance(src_layout, str) else src_layout
     ld = L(dst_layout) if isinstance(dst_layout, str) else dst_layout
     ds, dd = ls.lower(), ld.lower()
-    big = 1 << 62
-    a = make_tensor(ds, src_align, big, elem_bytes)
-    b = make_tensor(dd, dst_align, big, elem_bytes)
+    big = 1 << 40
+    # two disjoint fake buffers (overlapping byte ranges would select the aliased plan)
+    a = make_tensor(ds, src_align + (1 << 48), big, elem_bytes)
+    b = make_tensor(dd, dst_align + (1 << 52), big, elem_bytes)
     abi.check(lib.tlb_copy_plan(C.byref(a), C.byref(b), i_begin, i_end))
     return lib.tlb_last_plan().decode()
 
@@ -277,10 +278,13 @@ def idx2crd_range(layout: Layout | str, i0: int, n: int, out, stream=None) -> No
     abi.check(abi.load().tlb_idx2crd_range(C.byref(d), i0, n, out.data_ptr(), _stream_ptr(stream)))
 
 
-def crd2idx_range(layout: Layout | str, crd, n: int, out, stream=None) -> None:
+def crd2idx_range(layout: Layout | str, crd, n: int, out, stream=None, status_buf=None) -> None:
+    """tla::crd2idx over n natural coordinates; with status_buf (int32 on device, zeroed) a checked_mul / checked_add
+    wrap is reported there as TLB_ERR_OVERFLOW."""
     lay = L(layout) if isinstance(layout, str) else layout
     d = lay.lower()
-    abi.check(abi.load().tlb_crd2idx_range(C.byref(d), crd.data_ptr(), n, out.data_ptr(), _stream_ptr(stream)))
+    sp = status_buf.data_ptr() if status_buf is not None else None
+    abi.check(abi.load().tlb_crd2idx_range_checked(C.byref(d), crd.data_ptr(), n, out.data_ptr(), sp, _stream_ptr(stream)))
 
 
 def rinv_check_range(layout, rinv, k0: int, n: int, counter, stream=None) -> None:

@@ -148,6 +148,20 @@ static void gemm_families() {
              DeviceTensor(s.p, 64, 8, L("(4,5):(1,4)")));
     } catch (const contract_error&) { threw = true; }
     CHECK(threw);                                                                              // test_tensor.cpp:197-203
+    // checked_mul wraps (common.hpp:105): the reference throws overflow_error, and so does the device path
+    DevBuf<Int> big(std::vector<Int>(4, Int(1) << 62)), acc(std::vector<Int>(4, 0));
+    threw = false;
+    try {
+        gemm(DeviceTensor(big.p, 4, 8, L("(2,2):(1,2)")), DeviceTensor(big.p, 4, 8, L("(2,2):(1,2)")), DeviceTensor(acc.p, 4, 8, L("(2,2):(1,2)")));
+    } catch (const overflow_error&) { threw = true; }
+    CHECK(threw);
+    bool ref_threw = false;
+    try {
+        auto hb = std::make_shared<std::vector<Int>>(4, Int(1) << 62);
+        auto hc = std::make_shared<std::vector<Int>>(4, 0);
+        gemm(Tensor(Accessor::buffer(hb), L("(2,2):(1,2)")), Tensor(Accessor::buffer(hb), L("(2,2):(1,2)")), Tensor(Accessor::buffer(hc), L("(2,2):(1,2)")));
+    } catch (const overflow_error&) { ref_threw = true; }
+    CHECK(ref_threw);
 }
 
 static void index_maps() {

@@ -83,6 +83,17 @@ def orc_eval_range(lay, i0: int, n: int) -> np.ndarray:
     return out
 
 
+def orc_eval_axes_range(lay, n_axes: int, i0: int, n: int) -> np.ndarray:
+    m, k = modes_of(lay)
+    out = np.empty((n, n_axes), dtype=np.int64)
+    fn = orc().orc_eval_axes_range
+    fn.restype = C.c_int
+    st = fn(m, k, n_axes, C.c_int64(i0), C.c_int64(n), _p(out))
+    if st:
+        raise RuntimeError(f"oracle status {st}")
+    return out
+
+
 def orc_idx2crd_range(lay, i0: int, n: int) -> np.ndarray:
     lay = as_layout(lay)
     ext = np.array([e for e, *_ in lay.modes], dtype=np.int64)
@@ -176,6 +187,21 @@ def ref_copy(src_text: str, src_cells: np.ndarray | None, dst_text: str, dst_cel
     return ref().ref_copy(src_text.encode(), _p(src_cells) if src_cells is not None else None,
                           C.c_int64(src_cells.size if src_cells is not None else 0), C.c_int64(src_origin),
                           dst_text.encode(), _p(dst_cells), C.c_int64(dst_cells.size), C.c_int64(dst_origin))
+
+
+def ref_copy_shared(src_text: str, dst_text: str, cells: np.ndarray, src_origin=0, dst_origin=0) -> int:
+    """tla::copy verbatim with both tensors viewing ONE storage (cells modified in place)."""
+    assert cells.dtype == np.int64
+    return ref().ref_copy_shared(src_text.encode(), C.c_int64(src_origin), dst_text.encode(), C.c_int64(dst_origin),
+                                 _p(cells), C.c_int64(cells.size))
+
+
+def ref_eval_axes_range(text: str, n_axes: int, i0: int, n: int) -> np.ndarray:
+    out = np.empty((n, n_axes), dtype=np.int64)
+    st = ref().ref_eval_axes_range(text.encode(), C.c_int64(i0), C.c_int64(n), n_axes, _p(out))
+    if st:
+        raise RuntimeError(f"reference status {st}: {ref().ref_last_error().decode()}")
+    return out
 
 
 def ref_gemm(la: str, a: np.ndarray, lb: str, b: np.ndarray, lc: str, c: np.ndarray) -> int:

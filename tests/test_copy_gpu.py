@@ -195,6 +195,48 @@ def test_copy_non_injective_destination_last_writer_wins():
     assert run_copy_case("(32,32,4):(1,32,1024)", "(32,32,4):(1,31,3)", 8) == "ordered"
 
 
+def _alias_case(s, d, so, do, cells_n, eb=8, seed=0):
+    """Both tensors view ONE device buffer; compare with the restatement run in place on the same cells."""
+    buf = cells(cells_n, eb, seed)
+    want = buf.copy()
+    if eb == 16:
+        wv = want.view([("a", np.int64), ("b", np.int64)])
+        assert ou.orc_copy(s, wv, d, wv, so, do) == 0
+    else:
+        assert ou.orc_copy(s, want, d, want, so, do) == 0
+    t = dev(buf)
+    a = host.make_tensor(L(s).lower(), t.data_ptr(), cells_n, eb, so)
+    b = host.make_tensor(L(d).lower(), t.data_ptr(), cells_n, eb, do)
+    plan = host.copy((a, None), (b, None))
+    torch.cuda.synchronize()
+    got = t.cpu().numpy()
+    assert (got == want).all(), f"aliased copy {s}@{so} -> {d}@{do} plan={plan}: {int((got != want).sum())} cells differ"
+    return plan
+
+
+def test_copy_aliased_views_of_one_buffer_keep_the_serial_order():
+    """Source and destination ranges overlap inside one buffer (the reference's views share storage, tensor.hpp:29):
+    the result is the serial ascending-i one. Reference fixtures first (tests/golden/alias.json), then larger cases."""
+    for row in ou.golden("alias.json"):
+        t = dev(np.arange(row["cells"], dtype=np.int64) * 3 + 1)
+        a = host.make_tensor(L(row["src"]).lower(), t.data_ptr(), row["cells"], 8, row["src_origin"])
+        b = host.make_tensor(L(row["dst"]).lower(), t.data_ptr(), row["cells"], 8, row["dst_origin"])
+        plan = host.copy((a, None), (b, None))
+        torch.cuda.synchronize()
+        assert t.cpu().numpy().tolist() == row["result"], (row["src"], row["dst"], plan)
+        assert plan in ("aliased", "serial")
+    n = 1 << 18
+    assert _alias_case(f"{n}:1", f"{n}:1", 0, 1, n + 1) == "aliased"      # shift right: a read-after-write chain of length n
+    assert _alias_case(f"{n}:1", f"{n}:1", 1, 0, n + 1, eb=4) == "aliased"  # shift left: a plain move
+    assert _alias_case(f"{n}:1", f"{n}:1", 0, 7, n + 7, eb=2) == "aliased"  # period-7 propagation
+    assert _alias_case("(512,512):(512,1)", "(512,512):(1,512)", 0, 0, 512 * 512, eb=4) == "aliased"   # in-place transpose
+    assert _alias_case("(512,512):(512,1)", "(512,512):(1,512)", 0, 0, 512 * 512, eb=16) == "aliased"
+    assert _alias_case("(256,128):(128,1)", "(256,128):(1,256)", 5, 1000, 256 * 128 + 1000, eb=1) == "aliased"
+    assert _alias_case("(64,64):(1,64)", "(64,64):(1,0)", 0, 10, 4096 + 64) == "serial"    # non-injective destination too
+    # disjoint halves of one allocation are NOT aliased: the planned kernels keep running
+    assert _alias_case("(256,128):(128,1)", "(256,128):(1,256)", 0, 256 * 128, 2 * 256 * 128, eb=4) == "tiled"
+
+
 def test_copy_subranges_tile_aligned_and_ragged():
     s, d = "(256,128):(128,1)", "(256,128):(1,256)"
     n = 256 * 128

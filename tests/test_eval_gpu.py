@@ -61,6 +61,32 @@ def test_c5_index_maps_sampled_at_full_size():
         assert _eval(Lt, i, 1)[0] == lv and _eval(Rt, i, 1)[0] == rv
 
 
+@pytest.mark.parametrize("i0", [0, 15 * 2**28, 2**32 - 2**21, 5 * 2**28 + 96])
+def test_c5_windows_through_the_kernel_the_bench_times(i0):
+    """bench.py materialises C5 in 2^28-element chunks, which selects eval_warp_kernel<32> (groups of 32 indices, one peel
+    per lane, bases by shuffle). The 4096-element windows above select G = 8, so this runs 2^21-element windows through
+    the G = 32 warp kernel (asserted through tlb_last_plan) at the first chunk, the last chunk, the end of the domain and
+    a start that is 32- but not 128-aligned, against the oracle on every element. The output is 32-byte aligned as in
+    the bench."""
+    ops = ou.golden("ops.json")
+    n = 2**21
+    for text in (ops["C5_L"], ops["C5_R"]):
+        got = _eval(text, i0, n)
+        assert abi.load().tlb_last_plan().decode() == "eval_warp32"
+        assert (got == ou.orc_eval_range(text, i0, n)).all()
+
+
+def test_c5_non_group_aligned_start_falls_back_and_stays_exact():
+    ops = ou.golden("ops.json")
+    n = 2**20 + 5
+    got = _eval(ops["C5_L"], 7 * 2**28 + 3, n)                # i0 % 2 != 0: the scalar kernel
+    assert abi.load().tlb_last_plan().decode() == "eval_scalar"
+    assert (got == ou.orc_eval_range(ops["C5_L"], 7 * 2**28 + 3, n)).all()
+    got = _eval(ops["C5_L"], 7 * 2**28 + 16, n)               # i0 % 16 == 0: G = 16 warp kernel + group + scalar tails
+    assert abi.load().tlb_last_plan().decode() == "eval_warp16"
+    assert (got == ou.orc_eval_range(ops["C5_L"], 7 * 2**28 + 16, n)).all()
+
+
 def test_c5_right_inverse_identity_on_device():
     """L(R(k)) == k for all k of a 2^26 slice at both ends of the 2^32 domain (property at full size)."""
     ops = ou.golden("ops.json")
@@ -125,6 +151,63 @@ def test_idx2crd_and_crd2idx_roundtrip():
     torch.cuda.synchronize()
     assert (crd.cpu().numpy() == ou.orc_idx2crd_range(big, 2**32 - 4096, 4096)).all()
     assert (idx.cpu().numpy() == np.arange(2**32 - 4096, 2**32)).all()
+
+
+def test_eval_axes_matches_reference_fixtures_and_oracle():
+    """tlb_eval_axes_range (layout_eval_axes, layout.hpp:103) over whole domains: the reference's fixtures (incl.
+    coordinate_identity((8,8)) = (8,8):(e0,e1), Table 2: L(c) = c) and the oracle on every index of larger windows."""
+    for row in ou.golden("axes.json"):
+        na = row["n_axes"]
+        for w in row["windows"]:
+            want = np.array(w["values"], dtype=np.int64).reshape(-1, na)
+            out = torch.empty(want.shape[0], na, dtype=torch.int64, device="cuda")
+            host.eval_axes_range(row["layout"], na, w["i0"], want.shape[0], out)
+            torch.cuda.synchronize()
+            assert (out.cpu().numpy() == want).all(), row["layout"]
+    # TMA coordinates of a tiled identity: zipped_divide(coordinate_identity((4096,8192)), [128,64]) evaluated over 2^20
+    # indices from a start far from zero; coordinate (tile, in-tile) -> (row, column) of the tile's elements
+    t = "((128,64),(32,128)):((e0,e1),(128*e0,64*e1))"
+    i0, n = 17 * 2**20 + 13, 2**20
+    out = torch.empty(n, 2, dtype=torch.int64, device="cuda")
+    host.eval_axes_range(t, 2, i0, n, out)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == ou.orc_eval_axes_range(t, 2, i0, n)).all()
+    for t, na in [("(3,5,7):(e2,e0,e1)", 3), ("(2,3,2,5):(e0,2*e1,e2,7*e3)", 4), ("(2,2,2,2,2):(e0,e1,e2,e3,e4)", 5), ("(6,4):(e0,e0)", 1)]:
+        n = L(t).size + 3
+        out = torch.empty(n + 1, na, dtype=torch.int64, device="cuda")
+        for view in (out[:n], out[1:]):                        # aligned and misaligned outputs (vector / scalar stores)
+            host.eval_axes_range(t, na, 0, n, view)
+            torch.cuda.synchronize()
+            assert (view.cpu().numpy() == ou.orc_eval_axes_range(t, na, 0, n)).all(), t
+
+
+def test_eval_axes_overflow_is_proven_before_launch():
+    out = torch.empty(8, 2, dtype=torch.int64, device="cuda")
+    with pytest.raises(TlbError) as e:                         # checked_mul in eval_leaf (stride.hpp:152) would wrap
+        host.eval_axes_range("(4,8):(4611686018427387904*e0,e1)", 2, 0, 8, out)
+    assert e.value.status == abi.TLB_ERR_OVERFLOW
+
+
+def test_crd2idx_checked_arithmetic():
+    """tla::crd2idx accepts any coordinate values and throws overflow_error on a checked_mul / checked_add wrap
+    (int_tuple.hpp:154): out-of-range and negative coordinates produce the reference's (oracle's) value, a wrap is
+    reported through the status word and leaves the output cell untouched."""
+    text = "(4,8,16):(1,4,32)"
+    crd = np.array([[1, 2, 3], [7, 9, 20], [-1, 3, 2], [3, -8, 1], [0, 0, 2**40]], dtype=np.int64)
+    got = torch.full((5,), -7, dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    host.crd2idx_range(text, dev(crd), 5, got, status_buf=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert (got.cpu().numpy() == ou.orc_crd2idx_range(text, crd)).all()
+    bad = np.array([[1, 2, 3], [0, 0, 2**62], [2, 2, 2]], dtype=np.int64)     # 2^62 * 32 wraps
+    got = torch.full((3,), -7, dtype=torch.int64, device="cuda")
+    host.crd2idx_range(text, dev(bad), 3, got, status_buf=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == abi.TLB_ERR_OVERFLOW
+    assert got.cpu().numpy().tolist() == [1 + 2 * 4 + 3 * 32, -7, 2 + 2 * 4 + 2 * 32]
+    with pytest.raises(RuntimeError):
+        ou.orc_crd2idx_range(text, bad)                        # the oracle (and the reference) raise on the same input
 
 
 def test_eval_axes_coordinate_layout():

@@ -64,7 +64,7 @@ def test_gemm_zero_a_and_preconditions():
     assert e.value.status == abi.TLB_ERR_CONTRACT
 
 
-def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True, f16=False):
+def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True, f16=False, tile_ranges=None):
     M, N, K = _dims(la, lb)
     na, nb, nc = ou.cosize_of(la), ou.cosize_of(lb), ou.cosize_of(lc)
     rng = np.random.default_rng(seed)
@@ -95,7 +95,12 @@ def _bf16_case(la, lb, lc, kat, seed=0, path=0, c_init=True, f16=False):
     tc, kc = host.tensor_of(lc, tc_, ranked=True)
     prev = abi.load().tlb_gemm_set_path(path)
     try:
-        plan = (host.gemm_f16 if f16 else host.gemm_bf16)((ta, ka), (tb, kb), (tc, kc))
+        fn = host.gemm_f16 if f16 else host.gemm_bf16
+        if tile_ranges is None:
+            plan = fn((ta, ka), (tb, kb), (tc, kc))
+        else:
+            for (t0, t1) in tile_ranges:
+                plan = fn((ta, ka), (tb, kb), (tc, kc), t0, t1)
     finally:
         abi.load().tlb_gemm_set_path(prev)
     torch.cuda.synchronize()
@@ -121,6 +126,26 @@ def test_gemm_bf16_layout_families_simt(fam):
     """NT / TN / NTT / BLIS / GETT (test_tensor.cpp:176-189) in bf16: bit-exact vs the sequential restatement."""
     assert _bf16_case(*fam, kat=True).startswith("simt")
     assert _bf16_case(*fam, kat=False, seed=4).startswith("simt")
+
+
+def _tile_count(la, lb, lc):
+    t = lambda s, eb: (host.make_tensor(L(s).lower(ranked=True), 256, 1 << 40, eb), None)
+    return host.gemm_tile_count(t(la, 2), t(lb, 2), t(lc, 4))
+
+
+def test_gemm_simt_fallback_keeps_the_transposed_tile_ids():
+    """MN-major A, m-contiguous C whose leading dimension TMA cannot address (ldc % 4 != 0), and unequal block counts
+    along m and n: the tcgen05 fit runs the problem transposed, the call falls through to SIMT, and the SIMT kernel must
+    index the tile grid the same way (columns n >= 256 were skipped). Whole range, then an odd partition."""
+    shape = ("(200,136):(1,208)", "(300,136):(1,304)", "(200,300):(1,201)")
+    assert _bf16_case(*shape, kat=True).startswith("simt")
+    assert _bf16_case(*shape, kat=False, seed=3).startswith("simt")
+    tiles = _tile_count(*shape)
+    assert tiles == 4
+    assert _bf16_case(*shape, kat=True, tile_ranges=[(0, 1), (1, 3), (3, tiles)]).startswith("simt")
+    big = ("(600,72):(1,608)", "(300,72):(1,304)", "(600,300):(1,601)")
+    tiles = _tile_count(*big)
+    assert _bf16_case(*big, kat=True, tile_ranges=[(0, 3), (3, 4), (4, tiles)]).startswith("simt")
 
 
 UMMA_SHAPES = [
