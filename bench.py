@@ -1,20 +1,26 @@
 #!/usr/bin/env python
 """Benchmark of the layout-driven hot path (BASELINE.json: "copy GB/s & GEMM TFLOP/s (% of B200 roofline)
-vs CPU ref").
+vs CPU ref, 1/2/4/8 GPUs").
 
     python bench.py --gpus N --steps K --warmup W            # our arm (libtlb.so, sm_100a)
     python bench.py --impl reference --gpus N ...            # the reference's own CPU implementation
 
 One JSON line on stdout (rank 0). The headline workload is BASELINE.json configs[1] (C2: bf16 4096^3 TN GEMM,
 fp32 accumulate); a "step" is one such GEMM per GPU (weak scaling: every rank owns one independent problem,
-no collective on the data path). The copy / index-map configs (C1, C3, C5) are timed in the same run and
-reported under "other_configs", each with its own HBM roofline.
+no collective on the data path). The copy / index-map configs (C1, C3, C5) and the batched GEMM (C4) are timed in
+the same run and reported under "other_configs", each with its own roofline, CPU baseline and end-to-end figure;
+at N > 1 they are the NAMED problem sharded by tile-coordinate ranges (strong scaling, paper_2603_02298_b200.shard).
+
+Launch: under torchrun (the driver's N > 1 command) RANK / LOCAL_RANK / WORLD_SIZE come from the environment. A plain
+`python bench.py --gpus N` with N > 1 re-launches itself under torch.distributed.run with N ranks (and fails loudly when
+the box has fewer than N GPUs), so both spellings measure the same thing.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -93,8 +99,34 @@ def dist_env():
     return rank, world, local
 
 
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> None:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start N ranks, one per GPU, and exit with their status."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}: launch one rank per GPU "
+                     f"(torchrun --nproc-per-node {args.gpus})")
+        return
+    if args.gpus <= 1 or args.impl == "reference":   # the CPU arm runs on rank 0 alone: nothing to spawn
+        return
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and not (args.share_gpu and have >= 1):
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but this box has {have} CUDA device(s); the multi-GPU path is "
+                 f"one process per GPU and is never emulated")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 # --------------------------------------------------------------------------------------------
-# reference arm: the reference's own CPU implementation (oracle/_ref when it was built, else the C port)
+# CPU legs: the reference's own implementation (oracle/_ref when it was built, else the C port)
 # --------------------------------------------------------------------------------------------
 def cpu_gemm_sample(m_rows: int, n_cols: int, K: int, threads: int):
     """tla::gemm (tensor.hpp:214) on an (m_rows*threads) x n_cols x K sub-problem of the TN workload, one row
@@ -126,6 +158,52 @@ def cpu_gemm_sample(m_rows: int, n_cols: int, K: int, threads: int):
         list(ex.map(work, range(threads)))
     dt = time.perf_counter() - t0
     return dt, m_rows * threads * n_cols * K, kind
+
+
+def cpu_copy_baseline(src: str, dst: str, elem_bytes: int, what: str):
+    """tla::copy (tensor.hpp:195-199) on a bounded slice of the workload: verbatim on 1 core and its loop body on all
+    host threads. GB/s counts 2 x elem_bytes per element, the GPU workload's bytes (the reference
+    itself moves 8-byte Int cells)."""
+    import numpy as np
+    import oracle_util as ou
+    from paper_2603_02298_b200 import L
+    n = L(src).size
+    threads = os.cpu_count() or 1
+    if ou.have_ref():
+        s1, c1 = ou.ref_copy_bench(src, dst, 1)
+        sn, cn = ou.ref_copy_bench(src, dst, threads)
+        assert c1 == cn, "1-core and N-thread reference copies disagree"
+        kind = "reference"
+    else:   # GPU box without the prebuilt reference: the C port, one core
+        a = np.arange(ou.cosize_of(src), dtype=np.int64) * 3 + 1
+        b = np.full(ou.cosize_of(dst), -1, dtype=np.int64)
+        t0 = time.perf_counter()
+        assert ou.orc_copy(src, a, dst, b) == 0
+        s1 = sn = time.perf_counter() - t0
+        threads_used = 1
+        kind = "port"
+    gb = 2.0 * elem_bytes * n / 1e9
+    return {"value": gb / sn, "unit": "GB/s", "cores": threads if kind == "reference" else 1, "kind": kind,
+            "one_core_value": gb / s1, "ns_per_element_one_core": s1 / n * 1e9,
+            "sample": f"tla::copy {'verbatim (unmodified reference headers)' if kind == 'reference' else '(C port)'} on {what}: "
+                      f"{n} elements, {s1:.2f} s on 1 core, {sn:.2f} s with the loop body on {threads if kind == 'reference' else 1} threads; "
+                      f"bytes counted as 2 x {elem_bytes} B per element"}
+
+
+def cpu_eval_baseline(layout: str, n: int):
+    import oracle_util as ou
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if ou.have_ref():
+        ou.ref_eval_range_mt(layout, 2**31, n, threads)
+        kind = "reference"
+    else:
+        ou.orc_eval_range(layout, 2**31, n)
+        threads, kind = 1, "port"
+    dt = time.perf_counter() - t0
+    return {"value": n * 8 / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": kind, "evals_per_s": n / dt,
+            "sample": f"tla::eval_int ({'unmodified reference' if kind == 'reference' else 'C port'}) on {n} consecutive indices "
+                      f"of the 2^32-element layout, {threads} host threads, {dt:.2f} s"}
 
 
 def run_reference(args):
@@ -167,6 +245,9 @@ def run_reference(args):
 # --------------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------------
+RED_DEV = "cuda"   # where the max-over-ranks reduction lives ("cpu" under --share-gpu: gloo)
+
+
 def timed(torch, dist, world, fn, steps, warmup):
     """W warm-up calls, then exactly K calls between barrier+synchronize, CUDA events on the launching stream,
     max over ranks. Returns seconds."""
@@ -186,20 +267,39 @@ def timed(torch, dist, world, fn, steps, warmup):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device=RED_DEV)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return ms / 1e3
 
 
+def wall_timed(torch, dist, world, fn, steps, warmup=2):
+    """Synchronous host-buffer calls (the e2e legs): wall clock around K calls, max over ranks. Returns seconds."""
+    for _ in range(warmup):
+        fn()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fn()
+    sec = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([sec], dtype=torch.float64, device=RED_DEV)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    return sec
+
+
 def traffic_for(config: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full capture of the
-    same workload (profiles/traffic.json, written by tools/ncu_summary.py); None when no capture exists."""
+    same workload (profiles/traffic.json, written by tools/ncu_summary.py: not measured in this run, the capture it
+    came from is named in traffic_source); None when no capture exists."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         e = json.loads(p.read_text()).get(config)
-        return e["dram_bytes_per_launch"] if e else None
-    return None
+        return (e["dram_bytes_per_launch"], e.get("source")) if e else (None, None)
+    return None, None
 
 
 def run_ours(args):
@@ -207,17 +307,30 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2603_02298_b200 import abi, host
+    from paper_2603_02298_b200 import abi, host, shard
 
     rank, world, local = dist_env()
     assert torch.cuda.is_available(), "bench.py needs a CUDA device: libtlb has no CPU fallback"
+    global RED_DEV
+    if args.share_gpu and world > 1:
+        # functional test of the N-rank code path on a box with fewer GPUs: every rank uses cuda:0, ranks talk over gloo
+        local = 0
+        RED_DEV = "cpu"
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    assert local < torch.cuda.device_count(), f"rank {rank}: LOCAL_RANK {local} has no GPU (one process per GPU)"
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and not args.share_gpu:
+        # communicator set-up is logged (NCCL INFO, INIT subsystem) so that the number of ranks is visible to whoever
+        # launched this; the data path below never uses the communicator
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     os.environ.setdefault("TLB_GEMM_CLOCK", "1")  # the GEMM kernels stamp {clock64, globaltimer}: SM clock under load
     lib = abi.load()
     pk = peaks()
     K, W = args.steps, args.warmup
+    only = set(args.only.split(",")) if args.only else None
 
     # ---- C2: bf16 4096^3 TN GEMM, fp32 accumulate (C += A B^T), one problem per rank -----------------
     M = N = Kd = 4096
@@ -267,8 +380,10 @@ def run_ours(args):
     burst = sec < 1.0
     peak = pk["bf16_tflops"] if burst else pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops / kernel_s / 1e12
+    tr, tr_src = traffic_for("C2")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic_for("C2"), "kernel": f"{'umma_wide_kernel' if plan.endswith('wide') else 'umma_gemm_kernel'} ({plan})",
+                "traffic": tr, "traffic_source": tr_src,
+                "kernel": f"{'umma_wide_kernel' if plan.endswith('wide') else 'umma_gemm_kernel'} ({plan})",
                 "peak_source": f"{pk['_source']} {'burst' if burst else 'sustained'} cuBLAS bf16",
                 "frac_of_nominal_2250": achieved / 2250.0, "algorithmic_flop_per_launch": flops}
 
@@ -280,23 +395,10 @@ def run_ours(args):
     etb = host.tensor_of(f"({N},{Kd}):({Kd},1)", hb, ranked=True)
     etc = host.tensor_of(f"({M},{N}):(1,{M})", hc, ranked=True)
     ke = max(3, min(K, 10))
-    for _ in range(3):
-        host.gemm_bf16_host(eta, etb, etc)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(ke):
-        host.gemm_bf16_host(eta, etb, etc)   # synchronous: returns after the D2H of C
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = wall_timed(torch, dist, world, lambda: host.gemm_bf16_host(eta, etb, etc), ke, 3)  # synchronous: returns after the D2H of C
     # verification gather (outside every timed region): one 64-bit checksum of C per rank over NCCL
-    from paper_2603_02298_b200 import shard
-    sums = shard.gather_checksums(shard.checksum64(sets[0][2][1][1]), device="cuda")
-    verify = {"collective": "all_gather of per-rank C checksums (nccl)" if world > 1 else "none (1 GPU)",
+    sums = shard.gather_checksums(shard.checksum64(sets[0][2][1][1]), device=RED_DEV)
+    verify = {"collective": f"all_gather of per-rank C checksums ({'gloo, shared GPU' if args.share_gpu else 'nccl'})" if world > 1 else "none (1 GPU)",
               "ranks_reporting": len(sums), "all_nonzero": all(x != 0 for x in sums)}
     e2e = {"value": flops * ke * world / e2e_s / 1e12, "unit": "TFLOP/s",
            "h2d_bytes_per_step": (M * Kd + N * Kd) * 2 + M * N * 4, "d2h_bytes_per_step": M * N * 4,
@@ -304,7 +406,7 @@ def run_ours(args):
     # context, not a target: the vendor library on the same box, same shape and timing recipe (cuBLAS writes bf16 C and
     # does not read it; this path reads and writes fp32 C), and torch's copy_ on the C1 footprint
     library = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not only:
         lsets = [[(torch.rand(M, Kd, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(2)] for _ in range(nsets)]
         lsec = timed(torch, dist, 1, lambda i: torch.matmul(lsets[i % nsets][0], lsets[i % nsets][1].t()), K, W)
         x_ = torch.empty(8192 * 8192, dtype=torch.float32, device="cuda")
@@ -318,9 +420,9 @@ def run_ours(args):
 
     other = []
     if not args.gemm_only:
-        other = other_configs(torch, dist, world, lib, host, pk, K, W)
+        other = other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, only)
 
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not only:
         # LAST, so that it does not pre-heat the other configs: an untimed half-second loop of the C2 step with nvidia-smi
         # sampling every 20 ms. Long enough for the samples to see the load (the timed region is not); it records the
         # power-capped operating point as context.
@@ -345,11 +447,12 @@ def run_ours(args):
         pc = probe.stop(p0 + 0.1, p1)
         clocks["sustained_probe"] = {"steps": n_probe, "seconds": round(psec, 3), "tflops": flops * n_probe / psec / 1e12,
                                      "sm_mhz": pc["sm_mhz"], "power_w": pc.get("power_w"), "reasons": pc["reasons"],
-                                     "samples": pc.get("samples")}
+                                     "samples": pc.get("samples"),
+                                     "frac_of_sustained_peak": flops * n_probe / psec / 1e12 / pk.get("bf16_tflops_sustained", pk["bf16_tflops"])}
         del psets
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         threads = os.cpu_count() or 1
         dt, macs, kind = cpu_gemm_sample(2, 16, 4096, threads)
         per_mac = dt * threads / macs
@@ -371,121 +474,201 @@ def run_ours(args):
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
             "verify": verify, "library_same_box": library, "other_configs": other,
         }
+        if args.share_gpu and world > 1:
+            line["shared_gpu"] = "all ranks on cuda:0 (functional test of the N-rank path; NOT a scaling measurement)"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def other_configs(torch, dist, world, lib, host, pk, K, W):
-    """C1 (8192^2 fp32 transpose), C3 (4 GiB hierarchical permute) and C5 (2^32 index map, 2^28-element chunks):
-    same timing rules, HBM roofline. Inputs exceed L2 (512 MiB / 8 GiB / 2 GiB per step)."""
+def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, only):
+    """C1 (8192^2 fp32 transpose), C3 (4 GiB hierarchical permute), C5 (2^32 index maps, 2^28-element chunks), two
+    fallback-plan copies, C2 with bf16 C and C4: same timing rules, own roofline. Inputs exceed L2 (512 MiB / 8 GiB /
+    2 GiB per step). At N > 1 the NAMED problem is sharded by coordinate ranges (strong scaling): every rank runs
+    tlb_copy / tlb_eval_range on its own range, value = whole-problem bytes / max-over-ranks time."""
     out = []
     hbm = pk["hbm_gbs"]
+    want = lambda name: only is None or name in only
+    cpu_ok = rank == 0 and not args.no_cpu
 
-    def entry(name, workload, bytes_per_step, sec, steps, plan, kernel, extra=None):
-        gbs = bytes_per_step * steps * world / sec / 1e9
-        per_gpu = bytes_per_step / (sec / steps) / 1e9
-        e = {"name": name, "metric": "copy_gbs" if name != "C5" else "index_map_gbs", "value": gbs, "unit": "GB/s",
+    def entry(name, metric, workload, bytes_per_step, sec, steps, plan, kernel, extra=None):
+        # bytes_per_step is the WHOLE problem's algorithmic bytes; at N > 1 each rank moved 1/N of them per step
+        gbs = bytes_per_step * steps / sec / 1e9
+        per_gpu = gbs / world
+        tr, tr_src = traffic_for(name)
+        e = {"name": name, "metric": metric, "value": gbs, "unit": "GB/s", "n_gpus": world,
+             "scaling": "strong" if world > 1 else "n/a (1 GPU)", "steps": steps,
              "ms_per_step": sec / steps * 1e3, "config": {"workload": workload, "plan": plan},
              "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": hbm, "unit": "GB/s", "frac": per_gpu / hbm,
-                          "traffic": traffic_for(name), "kernel": kernel, "peak_source": f"{pk['_source']} torch copy_",
-                          "frac_of_nominal_8000": per_gpu / 8000.0, "algorithmic_bytes_per_launch": bytes_per_step}}
+                          "traffic": tr, "traffic_source": tr_src, "kernel": kernel,
+                          "peak_source": f"{pk['_source']} torch copy_",
+                          "frac_of_nominal_8000": per_gpu / 8000.0, "algorithmic_bytes_per_launch": bytes_per_step / world}}
         if extra:
             e.update(extra)
         return e
 
+    def copy_config(name, s, d, eb, workload, kernel, steps, warm, cpu_sample=None, e2e_steps=0, dtype=torch.int32):
+        n = host.L(s).size
+        src = torch.empty(host.L(s).lower().max_offset + 1, dtype=dtype, device="cuda")
+        src.copy_(torch.arange(src.numel(), dtype=torch.int64, device="cuda").to(dtype)) if src.numel() < 2**31 else src.random_()
+        dst = torch.empty(host.L(d).lower().max_offset + 1, dtype=dtype, device="cuda")
+        a = host.tensor_of(s, src)
+        b = host.tensor_of(d, dst)
+        i0, i1 = shard.copy_range(s, world, rank) if world > 1 else (0, 2**64 - 1)
+        sec = timed(torch, dist, world, lambda i: host.copy(a, b, i0, i1), steps, warm)
+        plan = lib.tlb_last_plan().decode()
+        extra = {}
+        if world > 1:
+            extra["shard"] = {"rank0_range": list(shard.copy_range(s, world, 0)), "how": "shard.copy_range: whole slices of the outermost mode per rank"}
+        del src, dst
+        torch.cuda.empty_cache()
+        if e2e_steps:
+            hs = torch.empty(host.L(s).lower().max_offset + 1, dtype=dtype).pin_memory()
+            hs.random_(0, 2**31 - 1)
+            hd = torch.empty(host.L(d).lower().max_offset + 1, dtype=dtype).pin_memory()
+            ha_, hb_ = host.tensor_of(s, hs), host.tensor_of(d, hd)
+            esec = wall_timed(torch, dist, world, lambda: host.copy_host(ha_, hb_), e2e_steps, 1)
+            extra["e2e"] = {"value": 2.0 * eb * n * e2e_steps * world / esec / 1e9, "unit": "GB/s",
+                            "h2d_bytes_per_step": hs.numel() * eb, "d2h_bytes_per_step": hd.numel() * eb, "steps": e2e_steps,
+                            "ms_per_step": esec / e2e_steps * 1e3,
+                            "api": "tlb_copy_host (pinned host buffers; every rank copies the whole problem: weak)" if world > 1
+                                   else "tlb_copy_host (pinned host buffers)"}
+            del hs, hd
+        if cpu_ok and cpu_sample:
+            extra["cpu_baseline"] = cpu_copy_baseline(*cpu_sample)
+        out.append(entry(name, "copy_gbs", workload, 2 * n * eb, sec, steps, plan, kernel, extra))
+
     # C1
-    n = 8192
-    src = torch.arange(n * n, dtype=torch.int32, device="cuda")
-    dst = torch.empty(n * n, dtype=torch.int32, device="cuda")
-    a = host.tensor_of(f"({n},{n}):({n},1)", src)
-    b = host.tensor_of(f"({n},{n}):(1,{n})", dst)
-    sec = timed(torch, dist, world, lambda i: host.copy(a, b), K, W)
-    out.append(entry("C1", "fp32 8192x8192 transpose copy (8192,8192):(8192,1) -> (8192,8192):(1,8192) (configs[0])",
-                     2 * n * n * 4, sec, K, lib.tlb_last_plan().decode(), "tiled_kernel"))
-    del src, dst
+    if want("C1"):
+        n = 8192
+        copy_config("C1", f"({n},{n}):({n},1)", f"({n},{n}):(1,{n})", 4,
+                    "fp32 8192x8192 transpose copy (8192,8192):(8192,1) -> (8192,8192):(1,8192) (configs[0])", "tiled_kernel", K, W,
+                    cpu_sample=("(2048,2048):(8192,1)", "(2048,2048):(1,8192)", 4, "a 2048x2048 sub-block of C1 with the same strides (1/16 of the elements)"),
+                    e2e_steps=max(3, min(K, 5)))
     # C3
-    T = 4096
-    s = f"((8,128),(4,64),{T}):((1,2048),(8,32),262144)"
-    d = f"((8,128),(4,64),{T}):((128,1),(65536,1024),262144)"
-    src = torch.empty(262144 * T, dtype=torch.int32, device="cuda")
-    src.copy_(torch.arange(262144 * T, dtype=torch.int32, device="cuda"))
-    dst = torch.empty(262144 * T, dtype=torch.int32, device="cuda")
-    a = host.tensor_of(s, src)
-    b = host.tensor_of(d, dst)
-    k3 = max(3, K // 4)
-    sec = timed(torch, dist, world, lambda i: host.copy(a, b), k3, 3)
-    out.append(entry("C3", "hierarchical permute copy ((8,128),(4,64)) x 4096 tiles, 4 GiB tensors, Swizzle<3,4,3> smem staging (configs[2])",
-                     2 * 262144 * T * 4, sec, k3, lib.tlb_last_plan().decode(), "tiled_kernel", {"steps": k3}))
-    del src, dst
-    torch.cuda.empty_cache()
+    if want("C3"):
+        T = 4096
+        copy_config("C3", f"((8,128),(4,64),{T}):((1,2048),(8,32),262144)", f"((8,128),(4,64),{T}):((128,1),(65536,1024),262144)", 4,
+                    "hierarchical permute copy ((8,128),(4,64)) x 4096 tiles, 4 GiB tensors, Swizzle<3,4,3> smem staging (configs[2])",
+                    "tiled_kernel", max(3, K // 4), 3,
+                    cpu_sample=("((8,128),(4,64),8):((1,2048),(8,32),262144)", "((8,128),(4,64),8):((128,1),(65536,1024),262144)", 4,
+                                "8 of the 4096 tiles of C3 (1/512 of the elements)"),
+                    e2e_steps=0 if args.quick else 2)
+    # fallback plans: an Xor (swizzled) destination and a non-injective destination
+    if want("Cx"):
+        copy_config("Cx_xor_dst", "(128,8,65536):(1,128,1024)", "(128,8,65536):(f1,f144,f1024)", 4,
+                    "2^26 fp32 elements into a Swizzle<3,4,3>-per-KiB destination (128,8,65536):(f1,f144,f1024)", "gather_kernel (Xor strides)",
+                    max(3, K // 4), 3)
+        copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,0)", 4,
+                    "2^25 fp32 elements into a destination with a stride-0 mode (last writer wins, tensor.hpp:198)", "winner_kernel + ordered_kernel",
+                    max(3, K // 8), 2)
     # C5: index maps of the 2^32-element divided layout, materialised in 2^28-element chunks (2 GiB)
-    Lt = "((128,64),(512,1024)):((65536,1),(8388608,64))"
-    chunk = 2 ** 28
-    buf = torch.empty(chunk, dtype=torch.int64, device="cuda")
-    sec = timed(torch, dist, world, lambda i: host.eval_range(Lt, (i % 16) * chunk, chunk, buf), max(4, K // 2), 3)
-    steps5 = max(4, K // 2)
-    out.append(entry("C5", "crd2idx / index map of the 2^32-element zipped_divide layout, 2^28-element chunks, int64 out (configs[4])",
-                     chunk * 8, sec, steps5, "eval_range", "eval_warp_kernel",
-                     {"steps": steps5, "evals_per_s": chunk * steps5 * world / sec,
-                      "note": "write-only kernel: the denominator is the read+write copy peak, a pure write stream (torch fill_ "
-                              "of 2 GiB) measured 7533 GB/s on this pool, so frac may exceed 1"}))
-    del buf
-    torch.cuda.empty_cache()
+    if want("C5"):
+        Lt = "((128,64),(512,1024)):((65536,1),(8388608,64))"
+        Rt = "(64,1024,128,512):(128,4194304,1,8192)"
+        chunk = 2 ** 28
+        steps5 = max(4, K // 2)
+        c0, c1 = shard.even_split(chunk, world, rank, align=4096)    # this rank's slice of every chunk
+        cn = c1 - c0
+        buf = torch.empty(cn, dtype=torch.int64, device="cuda")
+        note = ("write-only kernel: the denominator is the read+write copy peak, a pure write stream (torch fill_ of 2 GiB) "
+                "measured 7533 GB/s on this pool, so frac may exceed 1")
+        sec = timed(torch, dist, world, lambda i: host.eval_range(Lt, (i % 16) * chunk + c0, cn, buf), steps5, 3)
+        extra = {"evals_per_s": chunk * steps5 / sec, "note": note}
+        if cpu_ok:
+            extra["cpu_baseline"] = cpu_eval_baseline(Lt, 2 ** 22)
+        if not args.quick:
+            hbuf = torch.empty(cn, dtype=torch.int64).pin_memory()
+            esec = wall_timed(torch, dist, world, lambda: host.eval_range_host(Lt, 3 * chunk + c0, cn, hbuf), 2, 1)
+            extra["e2e"] = {"value": chunk * 8 * 2 / esec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": cn * 8,
+                            "steps": 2, "ms_per_step": esec / 2 * 1e3, "api": "tlb_eval_range_host (pinned host output)"}
+            del hbuf
+        out.append(entry("C5", "index_map_gbs", "L(i): index map of the 2^32-element zipped_divide layout, 2^28-element chunks, int64 out (configs[4])",
+                         chunk * 8, sec, steps5, lib.tlb_last_plan().decode(), "eval_warp_kernel", extra))
+        sec = timed(torch, dist, world, lambda i: host.eval_range(Rt, (i % 16) * chunk + c0, cn, buf), steps5, 3)
+        out.append(entry("C5_rinv", "index_map_gbs", "R(k) = right_inverse(L)(k), 2^28-element chunks, int64 out (configs[4])",
+                         chunk * 8, sec, steps5, lib.tlb_last_plan().decode(), "eval_warp_kernel",
+                         {"evals_per_s": chunk * steps5 / sec, "note": note}))
+        del buf
+        # natural coordinates and back: idx2crd writes 4 leaves per index (32 B), crd2idx reads them and writes 8 B
+        n5 = 2 ** 26
+        q0, q1 = shard.even_split(n5, world, rank, align=4096)
+        qn = q1 - q0
+        crd = torch.empty(qn * 4, dtype=torch.int64, device="cuda")
+        idx = torch.empty(qn, dtype=torch.int64, device="cuda")
+        sec = timed(torch, dist, world, lambda i: host.idx2crd_range(Lt, (i % 64) * n5 + q0, qn, crd), steps5, 3)
+        out.append(entry("C5_idx2crd", "index_map_gbs", "idx2crd: natural coordinates (4 leaves) of 2^26 indices per step, int64 out",
+                         n5 * 32, sec, steps5, "idx2crd", "idx2crd_kernel<4>", {"evals_per_s": n5 * steps5 / sec}))
+        sec = timed(torch, dist, world, lambda i: host.crd2idx_range(Lt, crd, qn, idx), steps5, 3)
+        out.append(entry("C5_crd2idx", "index_map_gbs", "crd2idx of 2^26 natural coordinates per step (32 B read + 8 B written per index)",
+                         n5 * 40, sec, steps5, "crd2idx", "crd2idx_kernel", {"evals_per_s": n5 * steps5 / sec}))
+        del crd, idx
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        sec = timed(torch, dist, world, lambda i: host.rinv_check_range(Lt, Rt, (i % 16) * chunk + c0, cn, cnt), steps5, 3)
+        torch.cuda.synchronize()
+        out.append({"name": "C5_check", "metric": "checks_per_s", "value": chunk * steps5 / sec, "unit": "evaluations/s", "n_gpus": world,
+                    "steps": steps5, "ms_per_step": sec / steps5 * 1e3, "mismatches": int(cnt.item()),
+                    "config": {"workload": "L(R(k)) == k checked on device for 2^28 k per step (no output: compute bound)", "plan": "rinv_check"},
+                    "roofline": None})
+        torch.cuda.empty_cache()
     # C2 with C in the operands' type (bf16 C += A B^T, fp32 accumulation in TMEM, one rounding, bf16 reduction at L2): the
     # like-for-like workload of the cuBLAS bf16 -> bf16 figure that MEASURED_PEAKS.json and library_same_box quote
-    M2 = 4096
-    sets16 = []
-    g2 = torch.Generator(device="cuda").manual_seed(7)
-    for _ in range(3):
-        a16 = (torch.rand(M2 * M2, device="cuda", generator=g2) * 2 - 1).to(torch.bfloat16)
-        b16 = (torch.rand(M2 * M2, device="cuda", generator=g2) * 2 - 1).to(torch.bfloat16)
-        c16 = torch.zeros(M2 * M2, dtype=torch.bfloat16, device="cuda")
-        sets16.append((host.tensor_of(f"({M2},{M2}):({M2},1)", a16.view(torch.int16), ranked=True),
-                       host.tensor_of(f"({M2},{M2}):({M2},1)", b16.view(torch.int16), ranked=True),
-                       host.tensor_of(f"({M2},{M2}):(1,{M2})", c16.view(torch.int16), ranked=True)))
-    sec = timed(torch, dist, world, lambda i: host.gemm_bf16(*sets16[i % 3]), K, W)
-    tf16 = 2.0 * M2 ** 3 * K * world / sec / 1e12
-    per16 = 2.0 * M2 ** 3 / (sec / K) / 1e12
-    out.append({"name": "C2_bf16_c", "metric": "gemm_tflops", "value": tf16, "unit": "TFLOP/s", "ms_per_step": sec / K * 1e3,
-                "config": {"workload": "C2 shape with C in bf16 (C += A B^T, fp32 accumulation in TMEM, bf16 L2 reduction): the output "
-                                       "type of the cuBLAS figure the peak was measured with", "plan": lib.tlb_last_plan().decode()},
-                "roofline": {"bound": "tensor", "achieved": per16, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                             "frac": per16 / pk["bf16_tflops"], "traffic": None, "kernel": "umma_wide_kernel",
-                             "peak_source": f"{pk['_source']} burst cuBLAS bf16", "frac_of_nominal_2250": per16 / 2250.0,
-                             "algorithmic_flop_per_launch": 2.0 * M2 ** 3}})
-    del sets16
-    torch.cuda.empty_cache()
+    if want("C2_bf16_c"):
+        M2 = 4096
+        sets16 = []
+        g2 = torch.Generator(device="cuda").manual_seed(7)
+        for _ in range(3):
+            a16 = (torch.rand(M2 * M2, device="cuda", generator=g2) * 2 - 1).to(torch.bfloat16)
+            b16 = (torch.rand(M2 * M2, device="cuda", generator=g2) * 2 - 1).to(torch.bfloat16)
+            c16 = torch.zeros(M2 * M2, dtype=torch.bfloat16, device="cuda")
+            sets16.append((host.tensor_of(f"({M2},{M2}):({M2},1)", a16.view(torch.int16), ranked=True),
+                           host.tensor_of(f"({M2},{M2}):({M2},1)", b16.view(torch.int16), ranked=True),
+                           host.tensor_of(f"({M2},{M2}):(1,{M2})", c16.view(torch.int16), ranked=True)))
+        sec = timed(torch, dist, world, lambda i: host.gemm_bf16(*sets16[i % 3]), K, W)
+        tf16 = 2.0 * M2 ** 3 * K * world / sec / 1e12
+        per16 = 2.0 * M2 ** 3 / (sec / K) / 1e12
+        tr, tr_src = traffic_for("C2_bf16_c")
+        out.append({"name": "C2_bf16_c", "metric": "gemm_tflops", "value": tf16, "unit": "TFLOP/s", "ms_per_step": sec / K * 1e3,
+                    "n_gpus": world, "scaling": "weak",
+                    "config": {"workload": "C2 shape with C in bf16 (C += A B^T, fp32 accumulation in TMEM, bf16 L2 reduction): the output "
+                                           "type of the cuBLAS figure the peak was measured with", "plan": lib.tlb_last_plan().decode()},
+                    "roofline": {"bound": "tensor", "achieved": per16, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                                 "frac": per16 / pk["bf16_tflops"], "traffic": tr, "traffic_source": tr_src, "kernel": "umma_wide_kernel",
+                                 "peak_source": f"{pk['_source']} burst cuBLAS bf16", "frac_of_nominal_2250": per16 / 2250.0,
+                                 "algorithmic_flop_per_launch": 2.0 * M2 ** 3}})
+        del sets16
+        torch.cuda.empty_cache()
     # C4: batched bf16 GEMM 64 x 8192^3, sharded by whole batches (= tile-id ranges) across the ranks (strong
     # scaling of the 64 batches; every rank owns its batches' operands, no data-path collective)
-    from paper_2603_02298_b200 import shard
-    M = 8192
-    rank = dist.get_rank() if world > 1 else 0
-    b0, b1 = shard.batch_range(64, world, rank)
-    nb = b1 - b0
-    a = torch.empty(nb * M * M, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
-    b = torch.empty(nb * M * M, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
-    c = torch.zeros(nb * M * M, dtype=torch.float32, device="cuda")
-    ta = host.tensor_of(f"({M},{M}):({M},1)", a.view(torch.int16), ranked=True)
-    tb = host.tensor_of(f"({M},{M}):({M},1)", b.view(torch.int16), ranked=True)
-    tc = host.tensor_of(f"({M},{M}):(1,{M})", c, ranked=True)
-    k4 = 3
-    sec = timed(torch, dist, world, lambda i: host.gemm_bf16_batched(ta, tb, tc, M * M, M * M, M * M, 0, nb), k4, 3)
-    flops = 2.0 * M * M * M * 64
-    tf = flops * k4 / sec / 1e12
-    per_gpu = 2.0 * M * M * M * nb / (sec / k4) / 1e12
-    sustained = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    out.append({"name": "C4", "metric": "gemm_tflops", "value": tf, "unit": "TFLOP/s", "ms_per_step": sec / k4 * 1e3,
-                "steps": k4, "scaling": "strong",
-                "config": {"workload": "batched bf16 GEMM 64 x (8192^3), fp32 accumulate, batches sharded across ranks (configs[3])",
-                           "batches_this_rank": nb, "plan": lib.tlb_last_plan().decode()},
-                "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": sustained, "unit": "TFLOP/s",
-                             "frac": per_gpu / sustained, "traffic": traffic_for("C4"), "kernel": "umma_wide_kernel",
-                             "peak_source": f"{pk['_source']} sustained cuBLAS bf16 (step >= 50 ms)",
-                             "frac_of_nominal_2250": per_gpu / 2250.0,
-                             "algorithmic_flop_per_launch": 2.0 * M * M * M * nb}})
-    del a, b, c
-    torch.cuda.empty_cache()
+    if want("C4"):
+        M = 8192
+        b0, b1 = shard.batch_range(64, world, rank)
+        nb = b1 - b0
+        a = torch.empty(nb * M * M, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+        b = torch.empty(nb * M * M, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+        c = torch.zeros(nb * M * M, dtype=torch.float32, device="cuda")
+        ta = host.tensor_of(f"({M},{M}):({M},1)", a.view(torch.int16), ranked=True)
+        tb = host.tensor_of(f"({M},{M}):({M},1)", b.view(torch.int16), ranked=True)
+        tc = host.tensor_of(f"({M},{M}):(1,{M})", c, ranked=True)
+        k4 = 3
+        sec = timed(torch, dist, world, lambda i: host.gemm_bf16_batched(ta, tb, tc, M * M, M * M, M * M, 0, nb), k4, 3)
+        flops = 2.0 * M * M * M * 64
+        tf = flops * k4 / sec / 1e12
+        per_gpu = 2.0 * M * M * M * nb / (sec / k4) / 1e12
+        sustained = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        tr, tr_src = traffic_for("C4")
+        out.append({"name": "C4", "metric": "gemm_tflops", "value": tf, "unit": "TFLOP/s", "ms_per_step": sec / k4 * 1e3,
+                    "steps": k4, "scaling": "strong", "n_gpus": world,
+                    "config": {"workload": "batched bf16 GEMM 64 x (8192^3), fp32 accumulate, batches sharded across ranks (configs[3])",
+                               "batches_this_rank": nb, "plan": lib.tlb_last_plan().decode()},
+                    "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": sustained, "unit": "TFLOP/s",
+                                 "frac": per_gpu / sustained, "traffic": tr, "traffic_source": tr_src, "kernel": "umma_wide_kernel",
+                                 "peak_source": f"{pk['_source']} sustained cuBLAS bf16 (step >= 50 ms)",
+                                 "frac_of_nominal_2250": per_gpu / 2250.0,
+                                 "algorithmic_flop_per_launch": 2.0 * M * M * M * nb,
+                                 "traffic_note": "per 8192^3 batch (one of the launch's batches_this_rank)"}})
+        del a, b, c
+        torch.cuda.empty_cache()
     return out
 
 
@@ -496,10 +679,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gemm-path", default="auto", choices=["auto", "1sm", "2sm"])
-    ap.add_argument("--gemm-only", action="store_true", help="skip the C1/C3/C5 lines (profiling runs)")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
+    ap.add_argument("--gemm-only", action="store_true", help="skip the other_configs lines (profiling runs)")
+    ap.add_argument("--only", default="", help="comma-separated other_configs to run (C1,C3,Cx,C5,C2_bf16_c,C4): profiling runs")
+    ap.add_argument("--quick", action="store_true", help="skip the multi-GiB pinned-host e2e legs of C3 / C5")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs (profiling runs)")
+    ap.add_argument("--share-gpu", action="store_true", help="testing only: run the N ranks on cuda:0 over gloo when the box has fewer than N GPUs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    maybe_spawn(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -240,6 +240,9 @@ int tlb_gemm_clock_stats(double* median_mhz, double* median_us, uint32_t* launch
  * the library keeps per calling thread (grown on demand, with a private stream pair), copies in, runs, copies
  * the destination back, synchronises. */
 int tlb_copy_host(const tlb_tensor* src, const tlb_tensor* dst);
+/* tla::eval_int (layout.hpp:74) over [i0, i0 + n) into a HOST array: evaluated on the device in pieces whose download
+ * overlaps the next piece's evaluation. Synchronous. */
+int tlb_eval_range_host(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64_t* h_out);
 int tlb_gemm_bf16_host(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C);
 
 #ifdef __cplusplus

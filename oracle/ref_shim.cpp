@@ -11,6 +11,7 @@
 //
 // The product library (paper_2603_02298_b200/libtlb.so) never links or loads this.
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -297,6 +298,46 @@ int ref_copy_mt(const char* src_layout, const std::int64_t* src_cells, std::int6
         for (auto& th : pool) th.join();
         for (int s : status) if (s) throw bounds_error("copy failed in worker");
         std::memcpy(dst_cells, ds->data(), static_cast<std::size_t>(dst_len) * sizeof(Int));
+    });
+}
+
+// CPU baseline of the copy configs (bench.py): storage is allocated and filled here, and ONLY the copy is timed.
+// threads <= 1: tla::copy verbatim (tensor.hpp:195-199) on one core. threads > 1: the same loop body
+// dst.store(i, src(i)) over disjoint i-ranges on std::threads (race free for injective destinations).
+// *seconds = wall time of the copy alone, *checksum = sum of the destination cells (defeats dead-code elimination and
+// lets the caller check that the two variants agree).
+int ref_copy_bench(const char* src_layout, const char* dst_layout, int threads, double* seconds, std::uint64_t* checksum) {
+    return guarded([&] {
+        Layout ls = parse_layout(src_layout);
+        Layout ld = parse_layout(dst_layout);
+        auto ss = std::make_shared<std::vector<Int>>(static_cast<std::size_t>(cosize(ls)));
+        for (std::size_t i = 0; i < ss->size(); ++i) (*ss)[i] = static_cast<Int>(3 * i + 1);   // acceptance.cpp:289 fill
+        auto ds = std::make_shared<std::vector<Int>>(static_cast<std::size_t>(cosize(ld)), Int(-1));
+        Tensor src(Accessor::buffer(ss), ls);
+        Tensor dst(Accessor::buffer(ds), ld);
+        const auto t0 = std::chrono::steady_clock::now();
+        if (threads <= 1) {
+            copy(src, dst);
+        } else {
+            if (size(ls) != size(ld)) throw contract_error("copy requires equal sizes");
+            const Int n = size(ls);
+            std::vector<std::thread> pool;
+            std::vector<int> status(static_cast<std::size_t>(threads), 0);
+            for (int t = 0; t < threads; ++t) {
+                pool.emplace_back([&, t] {
+                    try {
+                        Int lo = n * t / threads, hi = n * (t + 1) / threads;
+                        for (Int i = lo; i < hi; ++i) dst.store(i, src(i));
+                    } catch (...) { status[static_cast<std::size_t>(t)] = 1; }
+                });
+            }
+            for (auto& th : pool) th.join();
+            for (int s2 : status) if (s2) throw bounds_error("copy failed in worker");
+        }
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::uint64_t sum = 0;
+        for (Int v : *ds) sum += static_cast<std::uint64_t>(v);
+        *checksum = sum;
     });
 }
 

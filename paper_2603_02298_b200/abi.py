@@ -81,6 +81,7 @@ SYMBOLS = {
     "tlb_gemm_set_path": (C.c_int, [C.c_int]),
     "tlb_gemm_clock_stats": (C.c_int, [_P(C.c_double), _P(C.c_double), _P(C.c_uint32)]),
     "tlb_copy_host": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor)]),
+    "tlb_eval_range_host": (C.c_int, [_P(tlb_layout_desc), C.c_uint64, C.c_uint64, C.c_void_p]),
     "tlb_gemm_bf16_host": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor)]),
 }
 

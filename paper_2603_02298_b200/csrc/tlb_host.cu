@@ -190,6 +190,29 @@ int tlb_copy_host(const tlb_tensor* src, const tlb_tensor* dst) {
     TLB_TRY(check_tensor(dst, "tlb_copy_host destination", true));
     TLB_TRY(require_device());
     HostCtx& ctx = g_host;
+    // Views of ONE host storage (tensor.hpp:29): when the two host buffers overlap they are staged as one device
+    // image, so that tlb_copy sees the same aliasing the reference would and resolves it to the serial result.
+    if (src->accessor == TLB_ACC_BUFFER && src->elem_bytes == dst->elem_bytes) {
+        const char* s0 = static_cast<const char*>(src->data);
+        const char* s1 = s0 + static_cast<size_t>(src->capacity) * src->elem_bytes;
+        char* d0 = static_cast<char*>(dst->data);
+        char* d1 = d0 + static_cast<size_t>(dst->capacity) * dst->elem_bytes;
+        if (s0 < d1 && d0 < s1) {
+            const char* lo = std::min<const char*>(s0, d0);
+            const char* hi = std::max<const char*>(s1, d1);
+            const size_t bytes = static_cast<size_t>(hi - lo);
+            TLB_TRY(ctx.begin((bytes + 255) & ~static_cast<size_t>(255)));
+            char* img = static_cast<char*>(ctx.take(bytes));
+            TLB_CUDA(cudaMemcpyAsync(img, lo, bytes, cudaMemcpyHostToDevice, ctx.s));
+            tlb_tensor ds = *src, dd = *dst;
+            ds.data = img + (s0 - lo);
+            dd.data = img + (d0 - lo);
+            TLB_TRY(copy_impl(&ds, &dd, 0, UINT64_MAX, ctx.s));
+            TLB_CUDA(cudaMemcpyAsync(d0, dd.data, static_cast<size_t>(d1 - d0), cudaMemcpyDeviceToHost, ctx.s));
+            TLB_CUDA(cudaStreamSynchronize(ctx.s));
+            return TLB_OK;
+        }
+    }
     TLB_TRY(ctx.begin(staged_bytes(*src) + staged_bytes(*dst)));
     tlb_tensor ds, dd;
     TLB_TRY(stage_in(*src, true, ctx, &ds));
@@ -198,6 +221,34 @@ int tlb_copy_host(const tlb_tensor* src, const tlb_tensor* dst) {
     TLB_CUDA(cudaMemcpyAsync(dst->data, dd.data, static_cast<size_t>(dst->capacity) * dst->elem_bytes,
                              cudaMemcpyDeviceToHost, ctx.s));
     TLB_CUDA(cudaStreamSynchronize(ctx.s));
+    return TLB_OK;
+}
+
+// eval_int over a range into HOST memory: the map is produced in 2^24-element pieces on stream s2 into a two-piece device
+// ring while the previous piece drains over PCIe on stream s (the download is the bottleneck: 8 B per evaluation).
+int tlb_eval_range_host(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64_t* h_out) {
+    if (!layout) return fail(TLB_ERR_CONTRACT, "tlb_eval_range_host: null layout");
+    if (n == 0) return TLB_OK;
+    if (!h_out) return fail(TLB_ERR_CONTRACT, "tlb_eval_range_host: null output");
+    TLB_TRY(require_device());
+    HostCtx& ctx = g_host;
+    const uint64_t piece = std::min<uint64_t>(n, 1ull << 24);
+    TLB_TRY(ctx.begin(2 * piece * sizeof(int64_t)));
+    int64_t* ring[2] = {static_cast<int64_t*>(ctx.take(piece * sizeof(int64_t))), static_cast<int64_t*>(ctx.take(piece * sizeof(int64_t)))};
+    int k = 0;
+    for (uint64_t done = 0; done < n; done += piece, ++k) {
+        const uint64_t cnt = std::min(piece, n - done);
+        const int slot = k & 1;
+        // the download that last used this slot (piece k - 2) must be finished before it is overwritten
+        if (k >= 2) TLB_CUDA(cudaStreamWaitEvent(ctx.s2, ctx.ev[2 + slot], 0));
+        TLB_TRY(tlb_eval_range(layout, i0 + done, cnt, ring[slot], ctx.s2));
+        TLB_CUDA(cudaEventRecord(ctx.ev[slot], ctx.s2));
+        TLB_CUDA(cudaStreamWaitEvent(ctx.s, ctx.ev[slot], 0));
+        TLB_CUDA(cudaMemcpyAsync(h_out + done, ring[slot], cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.s));
+        TLB_CUDA(cudaEventRecord(ctx.ev[2 + slot], ctx.s));
+    }
+    TLB_CUDA(cudaStreamSynchronize(ctx.s));
+    TLB_CUDA(cudaStreamSynchronize(ctx.s2));
     return TLB_OK;
 }
 

@@ -272,6 +272,14 @@ def eval_range(layout: Layout | str, i0: int, n: int, out, stream=None) -> None:
     abi.check(abi.load().tlb_eval_range(C.byref(d), i0, n, out.data_ptr(), _stream_ptr(stream)))
 
 
+def eval_range_host(layout: Layout | str, i0: int, n: int, out) -> None:
+    """tlb_eval_range_host: `out` is a HOST int64 tensor / array (pinned memory makes the download asynchronous)."""
+    lay = L(layout) if isinstance(layout, str) else layout
+    d = lay.lower()
+    ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+    abi.check(abi.load().tlb_eval_range_host(C.byref(d), i0, n, ptr))
+
+
 def idx2crd_range(layout: Layout | str, i0: int, n: int, out, stream=None) -> None:
     lay = L(layout) if isinstance(layout, str) else layout
     d = lay.lower()

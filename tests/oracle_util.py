@@ -204,6 +204,24 @@ def ref_eval_axes_range(text: str, n_axes: int, i0: int, n: int) -> np.ndarray:
     return out
 
 
+def ref_copy_bench(src_text: str, dst_text: str, threads: int):
+    """(seconds, checksum) of tla::copy on reference-owned storage: verbatim on one core (threads <= 1), or its loop
+    body over disjoint i-ranges on `threads` std::threads. Only the copy itself is timed."""
+    sec, chk = C.c_double(0), C.c_uint64(0)
+    st = ref().ref_copy_bench(src_text.encode(), dst_text.encode(), threads, C.byref(sec), C.byref(chk))
+    if st:
+        raise RuntimeError(f"reference status {st}: {ref().ref_last_error().decode()}")
+    return sec.value, chk.value
+
+
+def ref_eval_range_mt(text: str, i0: int, n: int, threads: int, which: int = 0) -> np.ndarray:
+    out = np.empty(n, dtype=np.int64)
+    st = ref().ref_eval_range_mt(text.encode(), C.c_int64(i0), C.c_int64(n), _p(out), which, threads)
+    if st:
+        raise RuntimeError(f"reference status {st}: {ref().ref_last_error().decode()}")
+    return out
+
+
 def ref_gemm(la: str, a: np.ndarray, lb: str, b: np.ndarray, lc: str, c: np.ndarray) -> int:
     return ref().ref_gemm(la.encode(), _p(a), C.c_int64(a.size), lb.encode(), _p(b), C.c_int64(b.size), lc.encode(),
                           _p(c), C.c_int64(c.size))

@@ -106,3 +106,18 @@ def test_two_rank_sharded_run_over_gloo():
     assert results.get("world") == 2
     assert results.get("copy_ok") is True
     assert results.get("gemm_ok") is True
+
+
+def test_bench_gpus_flag_is_never_silently_ignored():
+    """bench.py --gpus N: outside torchrun it must start N ranks or fail loudly (here: no GPU at all), and under
+    torchrun WORLD_SIZE must agree with --gpus."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    bench = str(Path(__file__).resolve().parent.parent / "bench.py")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    if not torch.cuda.is_available():
+        r = subprocess.run([sys.executable, bench, "--gpus", "2", "--steps", "3"], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode != 0 and "CUDA device(s)" in r.stderr and r.stdout.strip() == ""
+    r = subprocess.run([sys.executable, bench, "--gpus", "2"], capture_output=True, text=True, env=dict(env, WORLD_SIZE="4"), timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE=4" in r.stderr
