@@ -326,8 +326,8 @@ def run_ours(args):
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    os.environ.setdefault("TLB_GEMM_CLOCK", "1")  # the GEMM kernels stamp {clock64, globaltimer}: SM clock under load
     lib = abi.load()
+    host.config("GEMM_CLOCK", "1")  # the GEMM kernels stamp {clock64, globaltimer}: SM clock under load
     pk = peaks()
     K, W = args.steps, args.warmup
     only = set(args.only.split(",")) if args.only else None
@@ -509,8 +509,7 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
 
     def copy_config(name, s, d, eb, workload, kernel, steps, warm, cpu_sample=None, e2e_steps=0, dtype=torch.int32):
         n = host.L(s).size
-        src = torch.empty(host.L(s).lower().max_offset + 1, dtype=dtype, device="cuda")
-        src.copy_(torch.arange(src.numel(), dtype=torch.int64, device="cuda").to(dtype)) if src.numel() < 2**31 else src.random_()
+        src = torch.arange(host.L(s).lower().max_offset + 1, dtype=dtype, device="cuda")   # element-index bit patterns
         dst = torch.empty(host.L(d).lower().max_offset + 1, dtype=dtype, device="cuda")
         a = host.tensor_of(s, src)
         b = host.tensor_of(d, dst)

@@ -54,7 +54,8 @@ typedef enum tlb_status {
     TLB_ERR_OVERFLOW = 5,    /* tla::overflow_error   (common.hpp:101,107)        */
     TLB_ERR_CUDA = 6,        /* CUDA runtime / driver failure, or no device       */
     TLB_ERR_UNSUPPORTED = 7, /* valid request this build has no kernel for        */
-    TLB_ERR_INDEX = 8        /* tla::index_error                                  */
+    TLB_ERR_INDEX = 8,       /* tla::index_error                                  */
+    TLB_ERR_ADMISSIBILITY = 9 /* tla::admissibility_error (analysis.hpp:45,54)    */
 } tlb_status;
 
 /* Stride semimodule of a leaf (stride.hpp:16). */
@@ -117,6 +118,12 @@ uint64_t tlb_launch_count(void);
 /* Name of the plan the last tlb_copy / tlb_gemm_* / tlb_eval_range call on this thread selected ("vec", "tiled", "tiled_tma",
  * "gather", "ordered", "aliased", "umma_2sm_wide", "eval_warp32", ...). */
 const char* tlb_last_plan(void);
+
+/* Tuning / debugging knobs. The environment variables TLB_<NAME> are read once, at the first call into the library;
+ * afterwards a knob changes only through this call (value NULL or "" restores the default). `name` is the variable
+ * name with or without the TLB_ prefix, e.g. tlb_config_set("GEMM_WIDE", "1"). Unknown names: TLB_ERR_CONTRACT.
+ * Launch paths read knobs with one atomic load (no getenv). */
+int tlb_config_set(const char* name, const char* value);
 
 /* ---- (1) lowering: host layout -> device evaluator parameters --------- */
 /* Replaces the per-element call chain Tensor::operator() -> layout_eval -> eval_rec ->
@@ -207,6 +214,28 @@ int tlb_tensormap_fetch_tile(const void* tensormap_128B, int rank, const int32_t
  * rounding to bf16 / fp16, added to C in that type; tcgen05 wide plan or SIMT). */
 int tlb_gemm_bf16(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t tile_begin,
                   uint32_t tile_end, void* stream);
+/* The same GEMM partitioned by a caller-chosen tiler (local_tile(C, [bm, bn], (i, j)) is the tile of C a CTA
+ * or CTA pair owns, local_tile(A, [bm, bk], (i, k)) / local_tile(B, [bn, bk], (j, k)) its k-blocks). Every tensor map of the
+ * call is the tile mode of the corresponding zipped_divide (tlb_tensormap_from_divided's derivation), and the TiledMMA is
+ * the tcgen05.mma atom 128 x N x 16 (one CTA) or 256 x N x 16 (cta_group::2) with N = 128 or 256. Supported tilers, as rows
+ * x columns of C the way the plan runs it (an m-contiguous C runs transposed, so bm and bn swap roles):
+ * [128, 128|256, 64], [256, 128|256, 64] and [512, 256, 64]. Anything else, and layouts only the SIMT plan serves:
+ * TLB_ERR_UNSUPPORTED. Whole problems only; tlb_last_plan() names the kernel ("umma_1sm_n128", "umma_2sm", ...). */
+typedef struct tlb_gemm_tiler {
+    int32_t bm, bn, bk;
+} tlb_gemm_tiler;
+int tlb_gemm_bf16_tiled(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, const tlb_gemm_tiler* tiler,
+                        void* stream);
+/* tla::locate_offsets(A, T) (analysis.hpp:40-56): R = left_inverse(A) o T maps instruction coordinates to logical
+ * coordinates of the data layout A; admissible iff A(R(i)) == T(i) for every i < size(T). The host computes R for
+ * instruction leaves that each land inside one coalesced leaf of A (strided tiles: what TMEM accumulators are), the
+ * O(size(T)) admissibility loop runs on the device. Writes one flat mode of R per leaf of T into r_modes (room for
+ * TLB_MAX_MODES) and their count into *n_modes. TLB_ERR_ADMISSIBILITY when some offset of T is not in the image of A.
+ * Synchronous. The GEMM kernels' tcgen05.ld partition of their accumulators is derived through this call's host half. */
+int tlb_locate_offsets(const tlb_layout_desc* A, const tlb_layout_desc* T, tlb_mode* r_modes, int32_t* n_modes, void* stream);
+/* Hits / misses of the tensor-map cache since the library was loaded (diagnostics; either pointer may be NULL). */
+int tlb_tensormap_cache_stats(uint64_t* hits, uint64_t* misses);
+
 /* Number of output tiles of one problem under the plan tlb_gemm_bf16 would choose (host-only, no device
  * needed): shard [0, *tiles) across GPUs and pass each range as tile_begin / tile_end. */
 int tlb_gemm_tile_count(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t* tiles);

@@ -82,6 +82,15 @@ ALIAS_CASES = [
 ]
 
 
+LOCATE_CASES = [
+    # proj/tests/test_analysis.cpp:84-108 first, then TMEM-style tiles with the hardware lane stride (65536) and the paper's (16384)
+    ["(128,512):(16384,1)", "(1,128):(1,16384)"], ["(4,8):(1,4)", "5:7"], ["(4,8):(2,8)", "3:3"], ["(4,8):(1,5)", "2:4"],
+    ["(128,512):(65536,1)", "(32,32):(1,65536)"], ["(128,256):(65536,1)", "(32,32):(1,65536)"], ["(128,128):(65536,1)", "(32,32):(1,65536)"],
+    ["(128,512):(16384,1)", "(2,128):(1,16384)"], ["(128,512):(16384,1)", "(8,(16,4)):(1,(16384,524288))"],
+    ["(8,16):(16,1)", "(4,2):(1,32)"], ["(8,16):(16,1)", "(4,4):(2,16)"], ["(6,10):(10,1)", "(3,2):(2,10)"], ["(8,16):(32,1)", "3:16"],
+]
+
+
 def cosize(text):
     st, r = ou.ref_op("cosize", text)
     if st == 0:
@@ -184,6 +193,15 @@ def main():
         al.append({"src": s, "src_origin": so, "dst": d, "dst_origin": do, "cells": cells, "status": st,
                    "result": buf.tolist()})
     (OUT / "alias.json").write_text(json.dumps(al))
+    lo = []
+    for a, t in LOCATE_CASES:
+        st, r = ou.ref_op("locate_offsets", a, t)
+        row = {"A": a, "T": t, "status": st}
+        if st == 0:
+            row["R"] = r
+            row["R_values"] = ou.ref_eval_range(r, 0, int(ou.ref_op("size", t)[1])).tolist()
+        lo.append(row)
+    (OUT / "locate.json").write_text(json.dumps(lo))
     print("golden fixtures written to", OUT)
 
 

@@ -15,9 +15,9 @@ LIB_PATH = PKG / "libtlb.so"
 TLB_MAX_MODES = 16
 
 (TLB_OK, TLB_ERR_CONTRACT, TLB_ERR_BOUNDS, TLB_ERR_STRUCTURAL, TLB_ERR_SEMIMODULE, TLB_ERR_OVERFLOW, TLB_ERR_CUDA,
- TLB_ERR_UNSUPPORTED, TLB_ERR_INDEX) = range(9)
+ TLB_ERR_UNSUPPORTED, TLB_ERR_INDEX, TLB_ERR_ADMISSIBILITY) = range(10)
 STATUS_NAMES = ["ok", "contract_error", "bounds_error", "structural_error", "semimodule_error", "overflow_error",
-                "cuda_error", "unsupported", "index_error"]
+                "cuda_error", "unsupported", "index_error", "admissibility_error"]
 KIND_INT, KIND_BASIS, KIND_XOR = 0, 1, 2
 ACC_BUFFER, ACC_COUNTING = 0, 1
 LF_ALL_POW2, LF_HAS_NEG, LF_INJECTIVE = 1, 2, 4
@@ -38,6 +38,10 @@ class tlb_layout_desc(C.Structure):
     ]
 
 
+class tlb_gemm_tiler(C.Structure):
+    _fields_ = [("bm", C.c_int32), ("bn", C.c_int32), ("bk", C.c_int32)]
+
+
 class tlb_tensor(C.Structure):
     _fields_ = [("layout", C.POINTER(tlb_layout_desc)), ("data", C.c_void_p), ("origin", C.c_int64),
                 ("capacity", C.c_int64), ("elem_bytes", C.c_int32), ("accessor", C.c_int32)]
@@ -50,6 +54,7 @@ SYMBOLS = {
     "tlb_last_error": (C.c_char_p, []),
     "tlb_launch_count": (C.c_uint64, []),
     "tlb_last_plan": (C.c_char_p, []),
+    "tlb_config_set": (C.c_int, [C.c_char_p, C.c_char_p]),
     "tlb_layout_lower": (C.c_int, [_P(tlb_mode), C.c_int, _P(tlb_layout_desc)]),
     "tlb_layout_lower_ranked": (C.c_int, [_P(tlb_mode), C.c_int, _P(C.c_int32), C.c_int, _P(tlb_layout_desc)]),
     "tlb_eval_range": (C.c_int, [_P(tlb_layout_desc), C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
@@ -71,6 +76,9 @@ SYMBOLS = {
     "tlb_tensormap_fetch_tile": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_int32), C.c_uint32, C.c_int, C.c_void_p,
                                            C.c_void_p]),
     "tlb_gemm_bf16": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_uint32, C.c_uint32, C.c_void_p]),
+    "tlb_gemm_bf16_tiled": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_void_p, C.c_void_p]),
+    "tlb_locate_offsets": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(tlb_mode), _P(C.c_int32), C.c_void_p]),
+    "tlb_tensormap_cache_stats": (C.c_int, [_P(C.c_uint64), _P(C.c_uint64)]),
     "tlb_gemm_tile_count": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), _P(C.c_uint32)]),
     "tlb_gemm_bf16_batched": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_int64, C.c_int64, C.c_int64,
                                         C.c_int32, C.c_int32, C.c_void_p]),

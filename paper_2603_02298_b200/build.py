@@ -22,7 +22,7 @@ OBJ = PKG / "_obj"
 LIB = PKG / "libtlb.so"
 
 SOURCES = ["tlb_lower.cpp", "tlb_eval.cu", "tlb_tma.cu", "tlb_copy.cu", "tlb_gemm_simt.cu", "tlb_gemm_umma.cu", "tlb_gemm_umma_wide.cu",
-           "tlb_host.cu"]
+           "tlb_gemm_layout.cu", "tlb_host.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

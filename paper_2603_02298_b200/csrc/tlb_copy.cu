@@ -39,22 +39,13 @@ thread_local int g_copy_path = 0; // 0 auto, 1 gather, 2 tiled (LDG), 3 tiled TM
 thread_local bool g_dry_run = false; // tlb_copy_plan: run the planner, launch nothing
 
 // TLB_COPY_TMA=1 makes the TMA-fed tiled kernel the default for layouts that admit a tensor map.
-bool tma_default() {
-    static const bool on = [] {
-        const char* e = std::getenv("TLB_COPY_TMA");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
+bool tma_default() { return knob(K_COPY_TMA) == 1; }
 
 constexpr int kThreads = 256;
 
 // The tiled plan prefers 256-row tiles (1 KiB destination segments, 32 KiB of smem per CTA; C1 5.90 -> 6.09 TB/s);
 // TLB_COPY_LB256=0 caps the tile at 128 rows (A/B comparisons).
-bool lb256_enabled() {
-    const char* e = std::getenv("TLB_COPY_LB256");
-    return !(e && e[0] == '0');
-}
+bool lb256_enabled() { return knob(K_COPY_LB256) != 0; }
 
 // ---------------------------------------------------------------------------------------
 // device helpers

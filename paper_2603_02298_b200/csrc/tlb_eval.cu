@@ -325,13 +325,7 @@ int grid_for(uint64_t work_items) {
 }
 
 // TLB_EVAL_NO_WARP=1 keeps the per-thread grouped kernel only (A/B comparisons of the store pattern).
-bool eval_no_warp() {
-    static const bool on = [] {
-        const char* e = std::getenv("TLB_EVAL_NO_WARP");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
+bool eval_no_warp() { return knob(K_EVAL_NO_WARP) == 1; }
 
 int check_int_or_xor(const tlb_layout_desc* L, const char* who) {
     if (!L) return fail(TLB_ERR_CONTRACT, std::string(who) + ": null layout");

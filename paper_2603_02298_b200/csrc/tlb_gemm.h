@@ -27,6 +27,39 @@ __host__ __device__ inline uint32_t tile_of(const TileGrid& g, int64_t m, int64_
     return blk * 2u + half;
 }
 
+// ---- tensor maps derived from divided layouts (tlb_tma.cu) --------------------------------------------------
+// A GEMM operand is a rank-2 layout (rows, k) (+ a batch stride). The k-blocks a CTA loads are the tiles of
+// zipped_divide(operand, [box_rows, box_k]) (algebra.hpp:595): the PARENT layout's leaves become the TMA dimensions
+// (globalDim / globalStrides), the TILE mode's leaves become the box (boxDim). Modes may be hierarchical (GETT-style
+// folded modes): every leaf is its own TMA dimension, and the element index where a tile starts in
+// that dimension follows from the tile's 1-D coordinate in its mode by one division and one remainder.
+struct TmaCoord {
+    uint32_t src;      // which tile coordinate feeds this dimension: 0 = row index, 1 = k (or column) index, 2 = batch
+    uint32_t div, mod; // coordinate = (value / div) % mod; mod == 0: no remainder (outermost leaf of its mode)
+};
+struct TmaTileMap {
+    alignas(64) unsigned char desc[128];
+    int32_t rank;      // 3..5 (padded to 3 with unit dimensions)
+    TmaCoord c[5];
+};
+// Leaves of top-level mode `top` of `L`, coalesced in colex order (extent-1 leaves dropped). Returns the leaf count.
+int mode_leaves(const tlb_layout_desc& L, int top, int64_t* extent, int64_t* stride, int cap);
+struct TileDims {      // the derivation alone (pure host arithmetic, no driver call): what tlb_tensormap_describe reports
+    int32_t rank;
+    uint64_t dims[5], strides[5]; // extents and strides (elements), dimension 0 first
+    uint32_t box[5];
+    TmaCoord c[5];
+};
+int tile_dims_derive(const tlb_layout_desc& L, int inner_top, int outer_top, int64_t box_inner, int64_t box_outer,
+                     int inner_src, int outer_src, int batch, int64_t batch_stride, int elem_bytes, TileDims* out);
+// inner_top: the top-level mode whose first leaf has stride 1 (it becomes TMA dimension 0 and the inner box extent);
+// outer_top: the other mode. box_inner / box_outer: tile extents along them (elements of the modes' 1-D coordinates).
+// Fails with TLB_ERR_UNSUPPORTED (nothing written) when the layout is not TMA-addressable that way: no unit-stride
+// leaf, a stride that is not a multiple of 16 bytes, a tile that straddles leaf boundaries, more than 5 dimensions.
+int tensormap_for_tile(const tlb_layout_desc& L, int inner_top, int outer_top, int64_t box_inner, int64_t box_outer,
+                       int inner_src, int outer_src, const void* base, int batch, int64_t batch_stride, int elem_bytes,
+                       int is_float, int swizzle, int l2_promotion, TmaTileMap* out);
+
 struct UmmaProblem {
     const void* A;   // bf16, (M,K):(lda,1), or (M,K):(1,lda) when a_mn
     const void* B;   // bf16, (N,K):(ldb,1), or (N,K):(1,ldb) when b_mn
@@ -42,7 +75,21 @@ struct UmmaProblem {
     int32_t full_range;            // [tile_begin, tile_end) is every tile of every batch
     int32_t ab_f16;                // operands are IEEE fp16 instead of bf16 (instruction-descriptor formats 0 / 1)
     int32_t c_16;                  // C has the operands' 2-byte type (C points at 2-byte cells): wide plan only
+    // The layouts the tensor maps are derived from, as the plan runs them (A / B swapped when C is m-contiguous):
+    // top-level mode 0 = rows (m or n), mode 1 = k; for C: mode c_row_top = rows of the plan, the other = columns.
+    const tlb_layout_desc* la;
+    const tlb_layout_desc* lb;
+    const tlb_layout_desc* lc;
+    int32_t c_row_top;
+    int32_t bn;                    // UMMA N of the 128 x bn / 256 x bn plans (256 default, 128 from a tiler)
+    int32_t c_fold_tma;            // C has folded (hierarchical) modes that the reduce-add tensor map can address
+    int32_t force_wide;            // a tiler asked for the 512 x 256 plan / forbade it: 1 / -1 (0: planner decides)
 };
+int umma_operand_map(const UmmaProblem& p, int which /* 0 A, 1 B */, int box_rows, TmaTileMap* out);
+int umma_c_map(const UmmaProblem& p, int box_n, int box_m, int swizzle, TmaTileMap* out);
+// The tcgen05.ld partition of a 128-lane x bn-column accumulator (x halves), derived from the accumulator layout and the
+// instruction's offset layout (locate_offsets, analysis.hpp:40-56) and checked against the kernels' compile-time shape.
+int epilogue_partition_check(int bn, int halves);
 int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
 // Wide plan (tlb_gemm_umma_wide.cu): 512 x 256 pair tiles, chosen when the tile range is a whole number of them.
 bool umma_pdl_enabled();      // programmatic dependent launch (TLB_GEMM_PDL=0 turns it off)

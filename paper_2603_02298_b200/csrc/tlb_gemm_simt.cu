@@ -23,14 +23,12 @@ namespace tlb {
 namespace {
 
 thread_local int g_gemm_path = 0; // 0 auto, 1 SIMT, 2 tcgen05 cta_group::1, 3 tcgen05 cta_group::2
+thread_local const tlb_gemm_tiler* g_tiler = nullptr; // set for the duration of a tlb_gemm_*_tiled call
 
 constexpr int kThreads = 256;
 
 // TLB_GEMM_SPLIT_TAIL=0 keeps every C cell owned by one CTA (bitwise run-to-run reproducible sums).
-bool split_tail_enabled() {
-    const char* e = std::getenv("TLB_GEMM_SPLIT_TAIL");
-    return !(e && e[0] == '0');
-}
+bool split_tail_enabled() { return knob(K_GEMM_SPLIT_TAIL) != 0; }
 
 struct SimtArgs {
     int64_t a_origin, b_origin, c_origin;
@@ -197,34 +195,33 @@ struct UmmaFit {
 UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, const GemmDims& d, int64_t a_bs,
                  int64_t b_bs, int64_t c_bs, int batch_begin, int batch_end) {
     UmmaFit f;
-    int64_t eM, lda, eK, ska, eN, ldb, eKb, skb, eCm, csm, eCn, csn;
-    const bool flat = A->layout->kind == TLB_KIND_INT && B->layout->kind == TLB_KIND_INT &&
-                      C->layout->kind == TLB_KIND_INT && single_stride(*A->layout, 0, &eM, &lda) &&
-                      single_stride(*A->layout, 1, &eK, &ska) && single_stride(*B->layout, 0, &eN, &ldb) &&
-                      single_stride(*B->layout, 1, &eKb, &skb) && single_stride(*C->layout, 0, &eCm, &csm) &&
-                      single_stride(*C->layout, 1, &eCn, &csn);
-    if (!flat) return f;
+    if (A->layout->kind != TLB_KIND_INT || B->layout->kind != TLB_KIND_INT || C->layout->kind != TLB_KIND_INT) return f;
+    int64_t eCm, csm, eCn, csn;
+    if (!single_stride(*C->layout, 0, &eCm, &csm) || !single_stride(*C->layout, 1, &eCn, &csn)) return f;
     const bool batched = batch_end - batch_begin > 1 || batch_begin > 0;
-    // Operand majorness: K-major (k stride 1, the paper's "T" operands) or MN-major (m / n stride 1, the "N" operands of
-    // the NT / NTT rows). ld is the stride of the other mode.
-    auto major = [&](int64_t s_mn, int64_t s_k, int64_t e_mn, bool* mn, int64_t* ld) {
-        if (s_k == 1 || d.K == 1) {
-            *mn = false;
-            *ld = s_mn;
-            return s_mn > 0 || e_mn == 1;
-        }
-        if (s_mn == 1 || e_mn == 1) {
-            *mn = true;
-            *ld = s_k;
-            return s_k > 0;
-        }
-        return false;
+    // Operand majorness from the layout: K-major when the k mode starts with a unit-stride leaf (the paper's "T"
+    // operands), MN-major when the row mode does (the "N" operands of the NT / NTT rows). Modes may
+    // be hierarchical (GETT-style folded modes): the operand qualifies when the k-block tiles of
+    // zipped_divide(operand, [rows, 64]) are TMA boxes (tile_dims_derive: pure host arithmetic, nothing is encoded here).
+    auto operand = [&](const tlb_layout_desc& L, int64_t bs, bool* mn) {
+        int64_t e[4], st[4];
+        const int nk = mode_leaves(L, 1, e, st, 4);
+        if (nk < 0) return false;
+        const bool k_unit = nk == 0 || st[0] == 1;
+        const int nr = mode_leaves(L, 0, e, st, 4);
+        if (nr < 0) return false;
+        const bool r_unit = nr == 0 || st[0] == 1;
+        if (!k_unit && !r_unit) return false;
+        *mn = !k_unit;
+        TileDims td;
+        if (!*mn) return tile_dims_derive(L, 1, 0, 64, 256, 1, 0, batch_end, bs, 2, &td) == TLB_OK &&
+                         tile_dims_derive(L, 1, 0, 64, 128, 1, 0, batch_end, bs, 2, &td) == TLB_OK;
+        return tile_dims_derive(L, 0, 1, 64, 64, 0, 1, batch_end, bs, 2, &td) == TLB_OK;
     };
     bool a_mn = false, b_mn = false;
-    int64_t a_ld = 0, b_ld = 0;
-    bool ok = major(lda, ska, d.M, &a_mn, &a_ld) && major(ldb, skb, d.N, &b_mn, &b_ld) && a_ld > 0 && b_ld > 0 &&
-              a_ld % 8 == 0 && b_ld % 8 == 0 && csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) &&
-              (C->layout->flags & TLB_LF_INJECTIVE) && (!batched || (a_bs % 8 == 0 && b_bs % 8 == 0 && a_bs > 0 && b_bs > 0));
+    bool ok = operand(*A->layout, a_bs, &a_mn) && operand(*B->layout, b_bs, &b_mn) && csm >= 0 && csn >= 0 &&
+              (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) && (C->layout->flags & TLB_LF_INJECTIVE) &&
+              (!batched || (a_bs > 0 && b_bs > 0));
     const char* a_ptr = static_cast<const char*>(A->data) + A->origin * 2;
     const char* b_ptr = static_cast<const char*>(B->data) + B->origin * 2;
     ok = ok && (reinterpret_cast<uintptr_t>(a_ptr) % 16 == 0) && (reinterpret_cast<uintptr_t>(b_ptr) % 16 == 0);
@@ -236,8 +233,11 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
     p.B = f.swapped ? a_ptr : b_ptr;
     p.C = reinterpret_cast<float*>(static_cast<char*>(C->data) + C->origin * C->elem_bytes);
     p.c_16 = C->elem_bytes == 2 ? 1 : 0;
-    p.lda = f.swapped ? b_ld : a_ld;
-    p.ldb = f.swapped ? a_ld : b_ld;
+    p.la = f.swapped ? B->layout : A->layout;
+    p.lb = f.swapped ? A->layout : B->layout;
+    p.lc = C->layout;
+    p.c_row_top = f.swapped ? 1 : 0;
+    p.bn = 256;
     p.a_mn = (f.swapped ? b_mn : a_mn) ? 1 : 0;
     p.b_mn = (f.swapped ? a_mn : b_mn) ? 1 : 0;
     p.cs_m = f.swapped ? csn : csm;
@@ -295,6 +295,17 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
         if (t0 >= t1) return TLB_OK;
     }
 
+    if (g_tiler) {
+        // A caller-chosen tiler [bm, bn, bk]: the CTA (pair) tile of zipped_divide(C, [bm, bn]) and the k-block. The
+        // TiledMMA atoms are tcgen05.mma 128 x N x 16 (one CTA) and 256 x N x 16 (cta_group::2), N = 128 or 256, so the
+        // tile is one or two atoms high; bk is the 64-element (128-byte) swizzle row.
+        if (i64 || !fit.ok) return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm_*_tiled: these layouts run on the SIMT plan, which takes no tiler");
+        if (tile_begin != 0 || tile_end != UINT32_MAX) return fail(TLB_ERR_CONTRACT, "tlb_gemm_*_tiled: tile ranges refer to the default tiling");
+        const int tm = fit.swapped ? g_tiler->bn : g_tiler->bm, tn = fit.swapped ? g_tiler->bm : g_tiler->bn;
+        if (g_tiler->bk != 64 || (tn != 128 && tn != 256) || (tm != 128 && tm != 256 && !(tm == 512 && tn == 256)))
+            return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm_*_tiled: supported tilers are [128|256, 128|256, 64] and [512, 256, 64] "
+                                             "(rows x columns of C as the plan runs it: transposed for an m-contiguous C)");
+    }
     if (!i64 && g_gemm_path != 1) {
         if (fit.ok) {
             UmmaProblem& p = fit.p;
@@ -305,6 +316,13 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
             p.cta_group = g_gemm_path == 2 ? 1 : g_gemm_path == 3 ? 2 : (even ? 2 : 1);
             p.full_range = (t0 == 0 && t1 == tpb * static_cast<uint64_t>(batch_end)) ? 1 : 0;
             p.ab_f16 = f16 ? 1 : 0;
+            if (g_tiler) {
+                const int tm = fit.swapped ? g_tiler->bn : g_tiler->bm, tn = fit.swapped ? g_tiler->bm : g_tiler->bn;
+                p.bn = tn;
+                p.cta_group = tm == 128 ? 1 : 2;
+                p.force_wide = tm == 512 ? 1 : -1;
+                if (!p.full_range) return fail(TLB_ERR_CONTRACT, "tlb_gemm_*_tiled: whole problems only");
+            }
             const bool mn_major = p.a_mn || p.b_mn;
             if ((!mn_major && !p.c_16) || umma_wide_applies(p)) {
                 if (p.cta_group == 2 && !even)
@@ -426,6 +444,15 @@ int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
     if (st != TLB_OK) return st;
     if (h == TLB_ERR_OVERFLOW) return tlb::fail(TLB_ERR_OVERFLOW, "integer overflow in gemm accumulation");
     return TLB_OK;
+}
+
+int tlb_gemm_bf16_tiled(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, const tlb_gemm_tiler* tiler,
+                        void* stream) {
+    if (!tiler) return tlb::fail(TLB_ERR_CONTRACT, "tlb_gemm_bf16_tiled: null tiler");
+    tlb::g_tiler = tiler;
+    const int st = tlb::run_gemm(A, B, C, false, 0, 0, 0, 0, 1, 0, UINT32_MAX, nullptr, static_cast<cudaStream_t>(stream));
+    tlb::g_tiler = nullptr;
+    return st;
 }
 
 int tlb_gemm_tile_count(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, uint32_t* tiles) {

@@ -22,6 +22,7 @@
 // slices that run first and combine through the same reduce-add epilogue (tail-wave balancing).
 // No CUTLASS / CuTe: descriptors are encoded by hand below.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -37,7 +38,7 @@ namespace tlb {
 namespace {
 
 constexpr int BM = 128;      // rows of C per CTA
-constexpr int BN = 256;      // columns of C per CTA (UMMA N)
+// columns of C per CTA / CTA pair (UMMA N) are the template parameter BN: 256 (default plans) or 128 (from a tiler)
 constexpr int BK = 64;       // k-block: 64 bf16 = one 128-byte swizzle row
 constexpr int UMMA_K = 16;
 constexpr int kEpiWarps = 8; // two warps per TMEM lane quadrant, 128 columns each
@@ -54,7 +55,7 @@ constexpr uint32_t kTmemCols = 512; // two 256-column fp32 accumulators
 enum { EPI_REGS = 0, EPI_TMA = 1 };
 constexpr uint32_t kEpiChunkBytes = BM * 32 * 4; // 16 KiB
 
-template <int CG, int EPI> struct Cfg {
+template <int CG, int EPI, int BN> struct Cfg {
     static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : 1; // staging buffers per column half
     static constexpr int kStages = CG == 1 ? 4 : 6; // even: smem stages are released in pairs
     static constexpr int kPairs = kStages / 2;
@@ -69,7 +70,7 @@ template <int CG, int EPI> struct Cfg {
 using namespace umma;
 
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N = 256, M = 128 * CG.
-template <int CG> __device__ __forceinline__ constexpr uint32_t make_idesc() {
+template <int CG, int BN> __device__ __forceinline__ constexpr uint32_t make_idesc() {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
            (static_cast<uint32_t>((BM * CG) >> 4) << 24);
 }
@@ -78,7 +79,7 @@ struct UmmaArgs {
     float* C;
     int64_t cs_m, cs_n, c_bs;
     int32_t M, N, K;
-    uint32_t mb, nb;               // 256x256 blocks along m and n
+    uint32_t mb, nb;               // blocks of 256 rows x BN columns along m and n
     uint32_t group_m;              // m-blocks per rasterisation group (L2 reuse of the A panel)
     uint32_t unit_begin, unit_end; // CG=1: 128x256 tile ids; CG=2: 256x256 block ids (all batches)
     uint32_t n_split_units;        // the LAST n_split_units units of the range are split along K ...
@@ -93,6 +94,9 @@ struct UmmaArgs {
     long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
     uint32_t ab_f16;               // operands are fp16 (A / B format fields of the instruction descriptor = 0)
     long long* clk;                // optional (TLB_GEMM_CLOCK=1): CTA 0 stamps {clock64, globaltimer} at entry and exit
+    // how a tile's (row, k | column, batch) start turns into the coordinates of the layout-derived tensor maps
+    int32_t rank_a, rank_b, rank_c;
+    TmaCoord ca[5], cb[5], cc[5];
 };
 constexpr int kTraceSlots = 128;
 #define TLB_TRACE(slot)                                                                                    \
@@ -136,11 +140,11 @@ __device__ __forceinline__ void decode_unit(const UmmaArgs& a, uint32_t unit, ui
     *n_blk = rem / gm;
 }
 
-template <int CG, int EPI>
+template <int CG, int EPI, int BN>
 __global__ void __launch_bounds__(kUmmaThreads, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const __grid_constant__ UmmaArgs args) {
-    using C = Cfg<CG, EPI>;
+    using C = Cfg<CG, EPI, BN>;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     const uint32_t epi_base = smem_base + C::kStages * C::kStageBytes; // 1 KiB aligned (stage sizes are)
@@ -235,33 +239,30 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
                     } else if constexpr (CG == 1) {
                         mbar_expect_tx(full_bar(stage), C::kStageBytes);
+                        int ta[5], tb[5];
+                        tile_coords(args.ca, args.rank_a, m0, kb * BK, batch, ta);
+                        tile_coords(args.cb, args.rank_b, n0, kb * BK, batch, tb);
                         if (hint_ab) {
-                            tma_load_3d_hint(a_stage(stage), &map_a, full_bar(stage), kb * BK, m0, batch, pol_ab);
-                            tma_load_3d_hint(b_stage(stage), &map_b, full_bar(stage), kb * BK, n0, batch, pol_ab);
+                            tma_load_tile_hint<false>(a_stage(stage), &map_a, full_bar(stage), args.rank_a, ta, pol_ab);
+                            tma_load_tile_hint<false>(b_stage(stage), &map_b, full_bar(stage), args.rank_b, tb, pol_ab);
                         } else {
-                            tma_load_3d(a_stage(stage), &map_a, full_bar(stage), kb * BK, m0, batch);
-                            tma_load_3d(b_stage(stage), &map_b, full_bar(stage), kb * BK, n0, batch);
+                            tma_load_tile<false>(a_stage(stage), &map_a, full_bar(stage), args.rank_a, ta);
+                            tma_load_tile<false>(b_stage(stage), &map_b, full_bar(stage), args.rank_b, tb);
                         }
                     } else {
                         // The leader's barrier expects the bytes of BOTH CTAs; the peer's TMA may complete before
                         // this expect_tx is issued (tx-count goes transiently negative, as with multicast).
                         const uint32_t lbar = lbar0 + 8u * stage;
-                        if ((args.debug & 16u) && (kb & 1)) {
-                            // timing experiment: 25 % less operand traffic (B reloaded every other k-block only)
-                            if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kABytes);
-                            tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
-                            __syncwarp();
-                            if (stage == C::kStages - 1) ring_filled = true;
-                            if (++stage == C::kStages) { stage = 0; phase ^= 1u; ring_wrapped = true; }
-                            continue;
-                        }
+                        int ta[5], tb[5];
+                        tile_coords(args.ca, args.rank_a, m0, kb * BK, batch, ta);
+                        tile_coords(args.cb, args.rank_b, n0, kb * BK, batch, tb);
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
                         if (hint_ab) {
-                            tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
-                            tma_load_3d_2sm_hint(b_stage(stage), &map_b, lbar, kb * BK, n0, batch, pol_ab);
+                            tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, args.rank_a, ta, pol_ab);
+                            tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, args.rank_b, tb, pol_ab);
                         } else {
-                            tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
-                            tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, n0, batch);
+                            tma_load_tile<true>(a_stage(stage), &map_a, lbar, args.rank_a, ta);
+                            tma_load_tile<true>(b_stage(stage), &map_b, lbar, args.rank_b, tb);
                         }
                     }
                 }
@@ -276,7 +277,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         // lane issues the MMAs and the commits (tcgen05.commit tracks the MMAs of the issuing thread). =====
         if (leader) {
             // A / B format fields (bits 7-9, 10-12): 1 = bf16, 0 = fp16
-            const uint32_t idesc = args.ab_f16 ? (make_idesc<CG>() & ~((1u << 7) | (1u << 10))) : make_idesc<CG>();
+            const uint32_t idesc = args.ab_f16 ? (make_idesc<CG, BN>() & ~((1u << 7) | (1u << 10))) : make_idesc<CG, BN>();
             const uint32_t a_lo0 = desc_lo(a_stage(0)), b_lo0 = desc_lo(b_stage(0));
             int stage = 0;
             uint32_t phase = 0, acc = 0, acc_phase = 0;
@@ -374,8 +375,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     fence_async_smem();
                     named_bar(bar_id, 128);
                     if (issuer && !(args.debug & (2u | 8u))) {
-                        if (hint_c) tma_reduce_add_3d_hint(&map_c, buf, nbase + ci * 32, m0, batch, pol_c);
-                        else tma_reduce_add_3d(&map_c, buf, nbase + ci * 32, m0, batch);
+                        int tc[5];
+                        tile_coords(args.cc, args.rank_c, m0, nbase + ci * 32, batch, tc);
+                        if (hint_c && args.rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
+                        else tma_reduce_add_tile(&map_c, buf, args.rank_c, tc);
                         bulk_commit();
                     }
                 }
@@ -485,7 +488,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 constexpr int kClkSlots = 4096;
 long long* g_clk_host = nullptr;
 long long* g_clk_dev = nullptr;
-unsigned g_clk_next = 0;
+std::atomic<unsigned> g_clk_next{0};
 void clk_fetch() {
     cudaDeviceSynchronize();
     cudaMemcpy(g_clk_host, g_clk_dev, kClkSlots * 4 * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -509,8 +512,7 @@ void clk_report() {
 }
 long long* clk_slot() {
     static const bool on = [] {
-        const char* e = std::getenv("TLB_GEMM_CLOCK");
-        if (!(e && e[0] == '1')) return false;
+        if (knob(K_GEMM_CLOCK) != 1) return false;
         // device memory, fetched on demand: stamps in mapped host memory would put a PCIe round trip into every
         // kernel's completion (measured: about +4 us per launch)
         const size_t bytes = kClkSlots * 4 * sizeof(long long);
@@ -522,49 +524,53 @@ long long* clk_slot() {
         return true;
     }();
     if (!on) return nullptr;
-    return g_clk_dev + 4 * (g_clk_next++ % kClkSlots);
+    return g_clk_dev + 4 * (g_clk_next.fetch_add(1, std::memory_order_relaxed) % kClkSlots);
 }
 
-int encode_operand_map(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch,
-                       int box_rows) {
-    const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(rows), static_cast<uint64_t>(batch)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(ld) * 2,
-                                 static_cast<uint64_t>(batch > 1 ? batch_stride : ld * static_cast<int64_t>(rows)) * 2};
-    const uint32_t box[3] = {BK, static_cast<uint32_t>(box_rows), 1};
-    return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
+} // namespace
+
+// Tensor maps of the plans, derived from the operand layouts (tlb_tma.cu: tensormap_for_tile): the k-blocks are the tiles
+// of zipped_divide(operand, [box_rows, 64]); K-major operands put k in dimension 0, MN-major ones the rows (staged as
+// chunks of 64 rows x 64 k); C tiles are zipped_divide(C, [box_m, box_n]) with the contiguous (column) mode innermost.
+int umma_operand_map(const UmmaProblem& p, int which, int box_rows, TmaTileMap* out) {
+    const tlb_layout_desc& L = which == 0 ? *p.la : *p.lb;
+    const bool mn = which == 0 ? p.a_mn != 0 : p.b_mn != 0;
+    const void* base = which == 0 ? p.A : p.B;
+    const int64_t bs = which == 0 ? p.a_bs : p.b_bs;
+    if (!mn) return tensormap_for_tile(L, 1, 0, BK, box_rows, 1, 0, base, p.batch, bs, 2, 1, TMA_SW_128, 256, out);
+    return tensormap_for_tile(L, 0, 1, 64, BK, 0, 1, base, p.batch, bs, 2, 1, TMA_SW_128, 256, out);
+}
+int umma_c_map(const UmmaProblem& p, int box_n, int box_m, int swizzle, TmaTileMap* out) {
+    const int cb = p.c_16 ? 2 : 4;
+    return tensormap_for_tile(*p.lc, 1 - p.c_row_top, p.c_row_top, box_n, box_m, 1, 0, p.C, p.batch, p.c_bs, cb,
+                              p.c_16 && p.ab_f16 ? 2 : 1, swizzle, 0, out);
 }
 
-// Tensor map of an n-contiguous C for the reduce-add epilogue: fp32, dims (N, M, batch), box 32 x 128.
-int encode_c_map(TmaDesc* out, const UmmaProblem& p) {
-    const uint64_t dims[3] = {static_cast<uint64_t>(p.N), static_cast<uint64_t>(p.M), static_cast<uint64_t>(p.batch)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * 4,
-                                 static_cast<uint64_t>(p.batch > 1 ? p.c_bs : p.cs_m * static_cast<int64_t>(p.M)) * 4};
-    const uint32_t box[3] = {32u, static_cast<uint32_t>(BM), 1};
-    return tma_encode(out, 4, true, 3, p.C, dims, strides, box, TMA_SW_128, 0);
-}
+namespace {
 
 int pick_epilogue(const UmmaProblem& p) {
-    if (const char* e = std::getenv("TLB_GEMM_EPILOGUE"))
-        if (e[0] == 'r') return EPI_REGS; // "regs": keep C in registers (profiling / A-B comparisons)
+    if (knob(K_GEMM_EPILOGUE) == 1) return EPI_REGS; // "regs": keep C in registers (profiling / A-B comparisons)
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
     if (base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N) return EPI_TMA;
+    if (base_ok && p.c_fold_tma) return EPI_TMA; // folded C modes with a unit-stride column leaf (GETT-style C)
     return EPI_REGS;
 }
 
-template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream) {
-    using C = Cfg<CG, EPI>;
-    static bool attr_set[64] = {false};
+template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t stream) {
+    using C = Cfg<CG, EPI, BN>;
+    static std::atomic<bool> attr_set[64];   // per device; setting the attribute twice from two threads is harmless
     int dev = 0;
     TLB_CUDA(cudaGetDevice(&dev));
-    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-        TLB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<CG, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr_set[dev] = true;
+    if (dev >= 0 && dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
+        TLB_CUDA((cudaFuncSetAttribute(umma_gemm_kernel<CG, EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem)));
+        attr_set[dev].store(true, std::memory_order_release);
     }
-    TmaDesc ma, mb, mc;
-    TLB_TRY(encode_operand_map(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BM));
-    TLB_TRY(encode_operand_map(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, C::kBRows));
-    if (EPI != EPI_REGS) TLB_TRY(encode_c_map(&mc, p));
+    TmaTileMap ma, mb, mc;
+    TLB_TRY(umma_operand_map(p, 0, BM, &ma));
+    TLB_TRY(umma_operand_map(p, 1, C::kBRows, &mb));
+    if (EPI != EPI_REGS) TLB_TRY(umma_c_map(p, 32, BM, TMA_SW_128, &mc));
     else mc = ma; // unused by the register epilogue
+    TLB_TRY(epilogue_partition_check(BN, 1)); // tcgen05.ld partition derived from the accumulator layout (tlb_gemm_layout.cu)
     UmmaArgs a;
     std::memset(&a, 0, sizeof(a));
     a.C = p.C;
@@ -576,13 +582,22 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
     a.K = p.K;
     a.ab_f16 = p.ab_f16 ? 1u : 0u;
     a.mb = (p.M + 255) / 256;
-    a.nb = (p.N + 255) / 256;
-    {
-        const char* e = std::getenv("TLB_GEMM_GROUP_M");
-        a.group_m = e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : static_cast<uint32_t>(kGemmGroupM);
+    a.nb = (p.N + BN - 1) / BN;
+    a.rank_a = ma.rank;
+    a.rank_b = mb.rank;
+    a.rank_c = mc.rank;
+    for (int d = 0; d < 5; ++d) {
+        a.ca[d] = ma.c[d];
+        a.cb[d] = mb.c[d];
+        a.cc[d] = mc.c[d];
     }
+    a.group_m = static_cast<uint32_t>(std::max(1, knob(K_GEMM_GROUP_M)));
     a.unit_begin = CG == 1 ? p.tile_begin : p.tile_begin / 2;
     a.unit_end = CG == 1 ? p.tile_end : p.tile_end / 2;
+    if (p.full_range) { // tile ids are 128 x 256 tiles; with a 128-column tiler the units are counted from the blocks
+        a.unit_begin = 0;
+        a.unit_end = a.mb * a.nb * static_cast<uint32_t>(std::max(p.batch, 1)) * (CG == 1 ? 2u : 1u);
+    }
     a.c_vec = (p.cs_n == 1 && p.cs_m % 4 == 0 && p.c_bs % 4 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0) ? 1 : 0;
     const uint32_t units = a.unit_end - a.unit_begin;
     if (units == 0) return TLB_OK;
@@ -604,14 +619,9 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
         a.n_split_units = split > 1 ? tail : 0;
         a.work_end = a.unit_begin + (units - a.n_split_units) + a.n_split_units * split;
     }
-    {
-        const char* e = std::getenv("TLB_GEMM_BACKOFF_NS");
-        a.backoff_ns = e ? static_cast<uint32_t>(std::atoi(e)) : 100u;
-        const char* d = std::getenv("TLB_GEMM_DEBUG");
-        a.debug = d ? static_cast<uint32_t>(std::atoi(d)) : 0u;
-        const char* h = std::getenv("TLB_GEMM_HINTS");
-        a.hints = h ? static_cast<uint32_t>(std::atoi(h)) : 0u;
-    }
+    a.backoff_ns = static_cast<uint32_t>(knob(K_GEMM_BACKOFF_NS));
+    a.debug = static_cast<uint32_t>(knob(K_GEMM_DEBUG));
+    a.hints = static_cast<uint32_t>(knob(K_GEMM_HINTS));
     a.clk = clk_slot();
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
@@ -638,20 +648,21 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;
     CUtensorMap tma, tmb, tmc;
-    std::memcpy(&tma, ma.bytes, 128);
-    std::memcpy(&tmb, mb.bytes, 128);
-    std::memcpy(&tmc, mc.bytes, 128);
+    std::memcpy(&tma, ma.desc, 128);
+    std::memcpy(&tmb, mb.desc, 128);
+    std::memcpy(&tmc, mc.desc, 128);
     // Debug timeline: TLB_GEMM_TRACE=<file> makes this launch synchronous and dumps per-CTA clock64 stamps.
-    const char* trace_path = std::getenv("TLB_GEMM_TRACE");
+    static const char* const trace_path = std::getenv("TLB_GEMM_TRACE"); // debug timeline: read once per process
     const size_t trace_bytes = static_cast<size_t>(cfg.gridDim.x) * kTraceSlots * sizeof(long long);
     if (trace_path && trace_path[0]) {
         TLB_CUDA(cudaMalloc(reinterpret_cast<void**>(&a.trace), trace_bytes));
         TLB_CUDA(cudaMemset(a.trace, 0, trace_bytes));
     }
-    TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_gemm_kernel<CG, EPI>, tma, tmb, tmc, a));
+    TLB_CUDA((cudaLaunchKernelEx(&cfg, umma_gemm_kernel<CG, EPI, BN>, tma, tmb, tmc, a)));
     count_launch();
-    static const char* const names[2][2] = {{"umma_1sm_regs", "umma_1sm"}, {"umma_2sm_regs", "umma_2sm"}};
-    set_plan(names[CG - 1][EPI]);
+    static const char* const names[2][2][2] = {{{"umma_1sm_regs", "umma_1sm"}, {"umma_2sm_regs", "umma_2sm"}},
+                                               {{"umma_1sm_n128_regs", "umma_1sm_n128"}, {"umma_2sm_n128_regs", "umma_2sm_n128"}}};
+    set_plan(names[BN == 128 ? 1 : 0][CG - 1][EPI]);
     if (a.trace) {
         std::vector<long long> h(trace_bytes / sizeof(long long));
         TLB_CUDA(cudaStreamSynchronize(stream));
@@ -668,18 +679,16 @@ template <int CG, int EPI> int launch(const UmmaProblem& p, cudaStream_t stream)
 }
 
 template <int CG> int launch_cg(const UmmaProblem& p, cudaStream_t stream) {
-    if (pick_epilogue(p) == EPI_TMA) return launch<CG, EPI_TMA>(p, stream);
-    return launch<CG, EPI_REGS>(p, stream);
+    const bool tma = pick_epilogue(p) == EPI_TMA;
+    if (p.bn == 128) return tma ? launch<CG, EPI_TMA, 128>(p, stream) : launch<CG, EPI_REGS, 128>(p, stream);
+    return tma ? launch<CG, EPI_TMA, 256>(p, stream) : launch<CG, EPI_REGS, 256>(p, stream);
 }
 
 } // namespace
 
 long long* umma_clk_slot() { return clk_slot(); }
 // TLB_GEMM_PDL=0 turns programmatic dependent launch off (A/B comparisons).
-bool umma_pdl_enabled() {
-    const char* e = std::getenv("TLB_GEMM_PDL");
-    return !(e && e[0] == '0');
-}
+bool umma_pdl_enabled() { return knob(K_GEMM_PDL) != 0; }
 
 } // namespace tlb
 

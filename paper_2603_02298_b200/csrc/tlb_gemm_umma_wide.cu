@@ -28,6 +28,7 @@
 // (every tile a range touches is one more epilogue), and run FIRST; whole tiles follow round-robin. Partial tiles
 // combine through the same reduce-add epilogue. The prologue overlaps the previous kernel's tail (griddepcontrol).
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -81,6 +82,9 @@ struct WideArgs {
     uint32_t sk_cut[kMaxWorkers + 1]; // k-range [sk_cut[w], sk_cut[w+1]) of the stream-K tiles owned by worker w
     long long* clk;
     long long* cta_times;     // optional (TLB_GEMM_CTA_TIMES=<file>): {globaltimer at entry, at exit} of every CTA
+    // how a tile's (row, k | column, batch) start turns into the coordinates of the layout-derived tensor maps
+    int32_t rank_a, rank_b, rank_c;
+    TmaCoord ca[5], cb[5], cc[5];
 };
 
 struct Item {
@@ -250,23 +254,30 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         const uint32_t lbar = lbar0 + 8u * stage;
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * kStageBytes);
                         const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
+                        int tc[5];
                         if (!args.a_mn) {
                             // K-major A: one box of 256 rows x 64 k (rows of 128 B)
-                            if (args.hints & 1u) tma_load_3d_2sm_hint(a_stage(stage), &map_a, lbar, kb * BK, m0, batch, pol_ab);
-                            else tma_load_3d_2sm(a_stage(stage), &map_a, lbar, kb * BK, m0, batch);
+                            tile_coords(args.ca, args.rank_a, m0, kb * BK, batch, tc);
+                            if (args.hints & 1u) tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, args.rank_a, tc, pol_ab);
+                            else tma_load_tile<true>(a_stage(stage), &map_a, lbar, args.rank_a, tc);
                         } else {
                             // MN-major A: four chunks of 64 rows, each [64 k][64 m] (the map's dimension 0 is m)
 #pragma unroll
-                            for (int c = 0; c < BMC / 64; ++c)
-                                tma_load_3d_2sm(a_stage(stage) + c * 8192, &map_a, lbar, m0 + c * 64, kb * BK, batch);
+                            for (int c = 0; c < BMC / 64; ++c) {
+                                tile_coords(args.ca, args.rank_a, m0 + c * 64, kb * BK, batch, tc);
+                                tma_load_tile<true>(a_stage(stage) + c * 8192, &map_a, lbar, args.rank_a, tc);
+                            }
                         }
                         if (!args.b_mn) {
-                            if (args.hints & 1u) tma_load_3d_2sm_hint(b_stage(stage), &map_b, lbar, kb * BK, nb0, batch, pol_ab);
-                            else tma_load_3d_2sm(b_stage(stage), &map_b, lbar, kb * BK, nb0, batch);
+                            tile_coords(args.cb, args.rank_b, nb0, kb * BK, batch, tc);
+                            if (args.hints & 1u) tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, args.rank_b, tc, pol_ab);
+                            else tma_load_tile<true>(b_stage(stage), &map_b, lbar, args.rank_b, tc);
                         } else {
 #pragma unroll
-                            for (int c = 0; c < BN / 2 / 64; ++c)
-                                tma_load_3d_2sm(b_stage(stage) + c * 8192, &map_b, lbar, nb0 + c * 64, kb * BK, batch);
+                            for (int c = 0; c < BN / 2 / 64; ++c) {
+                                tile_coords(args.cb, args.rank_b, nb0 + c * 64, kb * BK, batch, tc);
+                                tma_load_tile<true>(b_stage(stage) + c * 8192, &map_b, lbar, args.rank_b, tc);
+                            }
                         }
                     }
                 }
@@ -407,7 +418,9 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         fence_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            tma_reduce_add_3d(&map_c, buf, n0 + ci * 64, m0 + h * BMH, static_cast<int>(batch));
+                            int tc[5];
+                            tile_coords(args.cc, args.rank_c, m0 + h * BMH, n0 + ci * 64, batch, tc);
+                            tma_reduce_add_tile(&map_c, buf, args.rank_c, tc);
                             bulk_commit();
                         }
                     }
@@ -444,13 +457,15 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         __syncwarp();
                         if (et) et[3] = clock64();
                         if (lane == 0 && !(args.debug & 8u)) {
-                            if (args.debug & 4u)  // timing experiment: plain store instead of the L2 reduction
+                            int tc[5];
+                            tile_coords(args.cc, args.rank_c, m0 + h * BMH, n0 + ci * 32, batch, tc);
+                            if ((args.debug & 4u) && args.rank_c == 3)  // timing experiment: plain store instead of the L2 reduction
                                 asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&map_c),
-                                             "r"(buf), "r"(n0 + ci * 32), "r"(m0 + h * BMH), "r"(static_cast<int>(batch)) : "memory");
-                            else if (args.hints & 2u)
-                                tma_reduce_add_3d_hint(&map_c, buf, n0 + ci * 32, m0 + h * BMH, static_cast<int>(batch), pol_c);
+                                             "r"(buf), "r"(tc[0]), "r"(tc[1]), "r"(tc[2]) : "memory");
+                            else if ((args.hints & 2u) && args.rank_c == 3)
+                                tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
                             else
-                                tma_reduce_add_3d(&map_c, buf, n0 + ci * 32, m0 + h * BMH, static_cast<int>(batch));
+                                tma_reduce_add_tile(&map_c, buf, args.rank_c, tc);
                             bulk_commit();
                             if (et) et[4] = clock64();
                         }
@@ -485,14 +500,14 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 constexpr int kCtaRing = 64, kCtaSlots = 2 * 160 + 64; // + 64: epilogue step stamps of CTA 0 / warp 0 (debug)
 long long* g_cta_host = nullptr;
 long long* g_cta_dev = nullptr;
-unsigned g_cta_next = 0;
+std::atomic<unsigned> g_cta_next{0};
 void cta_times_dump() {
     const char* path = std::getenv("TLB_GEMM_CTA_TIMES");
     if (!g_cta_host || !path) return;
     cudaDeviceSynchronize();
     cudaMemcpy(g_cta_host, g_cta_dev, static_cast<size_t>(kCtaRing) * kCtaSlots * sizeof(long long), cudaMemcpyDeviceToHost);
     if (FILE* f = std::fopen(path, "wb")) {
-        const long long hdr[4] = {kCtaRing, kCtaSlots, static_cast<long long>(g_cta_next), 0};
+        const long long hdr[4] = {kCtaRing, kCtaSlots, static_cast<long long>(g_cta_next.load()), 0};
         std::fwrite(hdr, sizeof(hdr), 1, f);
         std::fwrite(g_cta_host, sizeof(long long), static_cast<size_t>(kCtaRing) * kCtaSlots, f);
         std::fclose(f);
@@ -512,33 +527,7 @@ long long* cta_times_slot() {
         return true;
     }();
     if (!on) return nullptr;
-    return g_cta_dev + static_cast<size_t>(g_cta_next++ % kCtaRing) * kCtaSlots;
-}
-
-int encode_operand(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch, int box_rows) {
-    const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(rows), static_cast<uint64_t>(batch)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(ld) * 2,
-                                 static_cast<uint64_t>(batch > 1 ? batch_stride : ld * static_cast<int64_t>(rows)) * 2};
-    const uint32_t box[3] = {BK, static_cast<uint32_t>(box_rows), 1};
-    return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
-}
-
-// MN-major operand (r, k) at r + k * ld: dimension 0 is the row index, box = 64 rows x 64 k (one staged chunk).
-int encode_operand_mn(TmaDesc* out, const void* base, int64_t ld, int64_t batch_stride, int rows, int K, int batch) {
-    const uint64_t dims[3] = {static_cast<uint64_t>(rows), static_cast<uint64_t>(K), static_cast<uint64_t>(batch)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(ld) * 2,
-                                 static_cast<uint64_t>(batch > 1 ? batch_stride : ld * static_cast<int64_t>(K)) * 2};
-    const uint32_t box[3] = {64, BK, 1};
-    return tma_encode(out, 2, true, 3, const_cast<void*>(base), dims, strides, box, TMA_SW_128, 256);
-}
-
-int encode_c(TmaDesc* out, const UmmaProblem& p, uint32_t box_n, uint32_t box_m, int swizzle) {
-    const uint64_t cb = p.c_16 ? 2 : 4;
-    const uint64_t dims[3] = {static_cast<uint64_t>(p.N), static_cast<uint64_t>(p.M), static_cast<uint64_t>(p.batch)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(p.cs_m) * cb,
-                                 static_cast<uint64_t>(p.batch > 1 ? p.c_bs : p.cs_m * static_cast<int64_t>(p.M)) * cb};
-    const uint32_t box[3] = {box_n, box_m, 1};
-    return tma_encode(out, static_cast<int>(cb), p.c_16 && p.ab_f16 ? 2 : 1, 3, p.C, dims, strides, box, swizzle, 0);
+    return g_cta_dev + static_cast<size_t>(g_cta_next.fetch_add(1, std::memory_order_relaxed) % kCtaRing) * kCtaSlots;
 }
 
 } // namespace
@@ -588,8 +577,8 @@ void stream_k_cuts(uint32_t sk_units, uint32_t kblocks, uint32_t W, uint32_t epi
 }
 
 bool umma_wide_applies(const UmmaProblem& p) {
-    if (const char* e = std::getenv("TLB_GEMM_WIDE"))
-        if (e[0] == '0') return false;
+    const int wide_knob = p.force_wide ? (p.force_wide > 0 ? 1 : 0) : knob(K_GEMM_WIDE);
+    if (wide_knob == 0 || p.bn != 256) return false;
     if (p.cta_group != 2) return false;
     // A range of 128 x 256 tile ids selects whole pair tiles when ceil(M/256) is even (pair tile g = tiles 4g .. 4g+3);
     // the full range of a problem does for any M (the last pair tile is clipped by the TMA bounds).
@@ -601,36 +590,35 @@ bool umma_wide_applies(const UmmaProblem& p) {
         const uint64_t nb = static_cast<uint64_t>((p.N + 255) / 256);
         const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
                                                  : (p.tile_end - p.tile_begin) / 4;
-        const char* e = std::getenv("TLB_GEMM_WIDE");
-        if (!(e && e[0] == '1') && pair_tiles < 48) return false;
+        if (wide_knob != 1 && pair_tiles < 48) return false;
     }
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
+    if (p.c_fold_tma) return base_ok && (!p.c_16 || p.batch <= 1 || p.c_bs % 8 == 0);
     return base_ok && p.cs_n == 1 && p.cs_m % (p.c_16 ? 8 : 4) == 0 && p.cs_m >= p.N &&   // TMA reduce-add epilogue only
            (!p.c_16 || p.batch <= 1 || p.c_bs % 8 == 0);
 }
 
 
 int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
-    static bool attr_set[64] = {false};
+    static std::atomic<bool> attr_set[64];
     int dev = 0;
     TLB_CUDA(cudaGetDevice(&dev));
-    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    if (dev >= 0 && dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
         TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
-        attr_set[dev] = true;
+        attr_set[dev].store(true, std::memory_order_release);
     }
-    TmaDesc ma, mb, mc, mcp;
-    if (p.a_mn) TLB_TRY(encode_operand_mn(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch));
-    else TLB_TRY(encode_operand(&ma, p.A, p.lda, p.a_bs, p.M, p.K, p.batch, BMC));
-    if (p.b_mn) TLB_TRY(encode_operand_mn(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch));
-    else TLB_TRY(encode_operand(&mb, p.B, p.ldb, p.b_bs, p.N, p.K, p.batch, BN / 2));
-    TLB_TRY(encode_c(&mc, p, p.c_16 ? 64 : 32, 32, TMA_SW_128));
+    // tensor maps = the divided layouts: zipped_divide(A, [256, 64]), zipped_divide(B, [128, 64]) (64 x 64 chunks for
+    // MN-major operands), zipped_divide(C, [32, 32 | 64])
+    TmaTileMap ma, mb, mc, mcp;
+    TLB_TRY(umma_operand_map(p, 0, BMC, &ma));
+    TLB_TRY(umma_operand_map(p, 1, BN / 2, &mb));
+    TLB_TRY(umma_c_map(p, p.c_16 ? 64 : 32, 32, TMA_SW_128, &mc));
+    TLB_TRY(epilogue_partition_check(BN, 2)); // tcgen05.ld partition derived from the accumulator layout (tlb_gemm_layout.cu)
     WideArgs a;
     std::memset(&a, 0, sizeof(a));
     // C prefetch into L2 is off by default: measured, it evicts operand lines and costs 1.5 % (8192^3) to 7 % (4096^3).
-    a.prefetch_c = 0;
-    if (const char* e = std::getenv("TLB_GEMM_PREFETCH_C"))
-        if (e[0] == '1') a.prefetch_c = 1;
-    if (a.prefetch_c && (p.c_16 || encode_c(&mcp, p, 256, BMH, TMA_SW_NONE) != TLB_OK)) a.prefetch_c = 0;
+    a.prefetch_c = knob(K_GEMM_PREFETCH_C) == 1 ? 1u : 0u;
+    if (a.prefetch_c && (p.c_16 || umma_c_map(p, 256, BMH, TMA_SW_NONE, &mcp) != TLB_OK || mcp.rank != 3)) a.prefetch_c = 0;
     if (!a.prefetch_c) mcp = mc;
     a.M = p.M;
     a.N = p.N;
@@ -641,20 +629,22 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     a.c_16 = p.c_16 ? 1u : 0u;
     a.a_mn = p.a_mn ? 1u : 0u;
     a.b_mn = p.b_mn ? 1u : 0u;
-    {
-        const char* e = std::getenv("TLB_GEMM_GROUP_M");
-        const uint32_t group_m = e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : static_cast<uint32_t>(kGemmGroupM);
-        a.group_w = std::max(1u, group_m / 2);
-        const char* d = std::getenv("TLB_GEMM_DEBUG");
-        a.debug = d ? static_cast<uint32_t>(std::atoi(d)) : 0u;
-        const char* h = std::getenv("TLB_GEMM_HINTS");
-        a.hints = h ? static_cast<uint32_t>(std::atoi(h)) : 0u;
+    a.rank_a = ma.rank;
+    a.rank_b = mb.rank;
+    a.rank_c = mc.rank;
+    for (int d = 0; d < 5; ++d) {
+        a.ca[d] = ma.c[d];
+        a.cb[d] = mb.c[d];
+        a.cc[d] = mc.c[d];
     }
+    a.group_w = std::max(1u, static_cast<uint32_t>(std::max(1, knob(K_GEMM_GROUP_M))) / 2);
+    a.debug = static_cast<uint32_t>(knob(K_GEMM_DEBUG));
+    a.hints = static_cast<uint32_t>(knob(K_GEMM_HINTS));
     a.unit_begin = p.full_range ? 0u : p.tile_begin / 4;
     const uint32_t units = p.full_range ? a.mbw * a.nb * static_cast<uint32_t>(std::max(p.batch, 1)) : p.tile_end / 4 - a.unit_begin;
     if (units == 0) return TLB_OK;
     uint32_t W = static_cast<uint32_t>(sm_count() / 2);
-    if (const char* e = std::getenv("TLB_GEMM_WORKERS")) W = std::max(1u, std::min(W, static_cast<uint32_t>(std::atoi(e))));
+    if (const int cap = knob(K_GEMM_WORKERS); cap > 0) W = std::max(1u, std::min(W, static_cast<uint32_t>(cap)));
     const int kblocks = (p.K + BK - 1) / BK;
     // Tail balancing: the (units mod W) tiles of the partial wave become one k-range per worker (run first). With
     // split_tail off (TLB_GEMM_SPLIT_TAIL=0) every tile is summed by one CTA pair in k order: bitwise reproducible.
@@ -662,11 +652,10 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     // tiles would leave more than TLB_GEMM_SK_PCT % (default 4) of the CTA pairs idle in the last wave.
     // (2-byte C: every partial tile would be one more rounding step at L2, so the partial wave is not cut unless
     // TLB_GEMM_C16_SK=1 asks for it: 4096^3 1449 -> 1486 TFLOP/s)
-    const bool c16_sk = [] { const char* e = std::getenv("TLB_GEMM_C16_SK"); return e && e[0] == '1'; }();
+    const bool c16_sk = knob(K_GEMM_C16_SK) == 1;
     a.sk_units = (p.split_tail && (!p.c_16 || c16_sk) && kblocks >= 2 * kMinSeg) ? units % W : 0;
     if (a.sk_units && units > W) {
-        int pct = 4;
-        if (const char* e = std::getenv("TLB_GEMM_SK_PCT")) pct = std::atoi(e);
+        const int pct = knob(K_GEMM_SK_PCT);
         const uint32_t waves = (units + W - 1) / W;
         const double idle = 1.0 - static_cast<double>(units) / (static_cast<double>(waves) * W);
         if (idle * 100.0 <= pct) a.sk_units = 0;
@@ -677,8 +666,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
         a.dp_units = units;
     }
     if (a.sk_units) {
-        uint32_t epi = 10;
-        if (const char* e = std::getenv("TLB_GEMM_EPI_KB")) epi = static_cast<uint32_t>(std::max(0, std::atoi(e)));
+        const uint32_t epi = static_cast<uint32_t>(std::max(0, knob(K_GEMM_EPI_KB)));
         stream_k_cuts(a.sk_units, static_cast<uint32_t>(kblocks), W, epi, a.sk_cut);
     }
     const uint32_t workers = a.sk_units ? W : std::min(units, W);
@@ -699,10 +687,10 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     cfg.dynamicSmemBytes = kSmemW;
     cfg.stream = stream;
     CUtensorMap tma, tmb, tmc, tmcp;
-    std::memcpy(&tma, ma.bytes, 128);
-    std::memcpy(&tmb, mb.bytes, 128);
-    std::memcpy(&tmc, mc.bytes, 128);
-    std::memcpy(&tmcp, mcp.bytes, 128);
+    std::memcpy(&tma, ma.desc, 128);
+    std::memcpy(&tmb, mb.desc, 128);
+    std::memcpy(&tmc, mc.desc, 128);
+    std::memcpy(&tmcp, mcp.desc, 128);
     TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel, tma, tmb, tmc, tmcp, a));
     count_launch();
     set_plan("umma_2sm_wide");

@@ -96,8 +96,7 @@ bool covers_buffer(const tlb_tensor& t) {
 // Returns false (nothing enqueued) when the problem does not have that shape.
 bool gemm_host_pipelined(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, HostCtx& ctx, int* status) {
     *status = TLB_OK;
-    if (const char* e = std::getenv("TLB_HOST_PIPELINE"))
-        if (e[0] == '0') return false;
+    if (knob(K_HOST_PIPELINE) == 0) return false;
     GemmFlat f;
     if (C->elem_bytes != 4 || !gemm_flat_view(A, B, C, &f)) return false;
     if (f.a_sk != 1 || f.b_sk != 1 || f.a_sm < f.K || f.b_sn < f.K) return false;
@@ -105,8 +104,8 @@ bool gemm_host_pipelined(const tlb_tensor* A, const tlb_tensor* B, const tlb_ten
     const bool c_n_contig = f.c_sn == 1 && f.c_sm >= f.N;         // C (M,N):(ldc,1): slice along m (A and C panels)
     if (!c_m_contig && !c_n_contig) return false;
     const bool slice_n = c_m_contig;
-    int64_t panel = 1024; // measured on C2: 3.03 ms with 1024-row panels, 3.09 with 512, 3.22 with 2048, 3.76 unpipelined
-    if (const char* e = std::getenv("TLB_HOST_PANEL")) panel = std::max(512, std::atoi(e) / 512 * 512);
+    // measured on C2: 3.03 ms with 1024-row panels (the default), 3.09 with 512, 3.22 with 2048, 3.76 unpipelined
+    const int64_t panel = std::max(512, knob(K_HOST_PANEL) / 512 * 512);
     const int64_t rows = slice_n ? f.N : f.M;
     const int64_t n_panels = (rows + panel - 1) / panel;
     if (n_panels < 2 || n_panels > kMaxPanels) return false;

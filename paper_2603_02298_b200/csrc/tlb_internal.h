@@ -32,6 +32,36 @@ void count_launch(uint64_t n = 1);              // bumps tlb_launch_count()
         if (s__ != TLB_OK) return s__; \
     } while (0)
 
+// ---- configuration knobs ---------------------------------------------------------
+// Every tuning / debugging switch of the library. The environment (TLB_<NAME>) is read ONCE, at the first use of any
+// knob; after that a knob only changes through tlb_config_set(). Reading a knob on a launch path is one relaxed atomic
+// load: no getenv, no locks, no allocation.
+enum KnobId {
+    K_GEMM_WIDE,        // -1 auto, 0 never, 1 always take the 512 x 256 plan when it applies
+    K_GEMM_SPLIT_TAIL,  // 1: cut the partial wave into k-ranges (default), 0: bitwise reproducible sums
+    K_GEMM_EPILOGUE,    // 0 auto, 1 "regs": register epilogue
+    K_GEMM_GROUP_M,     // rasterisation group (m-blocks)
+    K_GEMM_BACKOFF_NS,
+    K_GEMM_DEBUG,       // timing experiments (garbage results)
+    K_GEMM_HINTS,       // L2 hints
+    K_GEMM_PDL,         // programmatic dependent launch of the GEMM kernels
+    K_GEMM_PREFETCH_C,
+    K_GEMM_WORKERS,     // cap on CTA pairs (0 = all)
+    K_GEMM_C16_SK,
+    K_GEMM_SK_PCT,
+    K_GEMM_EPI_KB,
+    K_GEMM_CLOCK,       // record {clock64, globaltimer} per launch
+    K_PDL,              // programmatic stream serialisation of the copy / eval kernels
+    K_COPY_TMA,         // TMA-fed tiled copy as the default
+    K_COPY_LB256,
+    K_COPY_PERSIST,     // persistent ring variant of the tiled copy
+    K_EVAL_NO_WARP,
+    K_HOST_PIPELINE,
+    K_HOST_PANEL,
+    K_COUNT
+};
+int knob(KnobId id);
+
 // One device is required; there is no CPU fallback anywhere in this library.
 int require_device();
 int sm_count();
@@ -69,10 +99,7 @@ bool gemm_flat_view(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* 
 // drains. Kernels launched this way execute pdl_wait() before their first global-memory access, which blocks until
 // that previous kernel has completed and flushed; without the attribute pdl_wait() is a no-op. Hides the 2-4 us of
 // launch latency and scheduling ramp between back-to-back kernels (TLB_PDL=0 turns it off).
-inline bool pdl_enabled() {
-    const char* e = std::getenv("TLB_PDL");
-    return !(e && e[0] == '0');
-}
+inline bool pdl_enabled() { return knob(K_PDL) != 0; }
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -116,9 +143,14 @@ struct TmaDesc {
 };
 enum TmaSwizzle { TMA_SW_NONE = 0, TMA_SW_32 = 1, TMA_SW_64 = 2, TMA_SW_128 = 3 };
 // dtype_bytes: 1,2,4,8; is_float: 0 unsigned integers, 1 bf16 / fp32, 2 fp16 (the element type matters to TMA reductions).
+// Served from a mutex-guarded cache keyed by (device, base, dtype, rank, dims, strides, box, swizzle, promotion).
 int tma_encode(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base, const uint64_t* dims,
                const uint64_t* strides_bytes /* rank-1 entries, dims 1.. */, const uint32_t* box,
                int swizzle, int l2_promotion_bytes);
+int tma_encode_uncached(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base, const uint64_t* dims,
+                        const uint64_t* strides_bytes, const uint32_t* box, int swizzle, int l2_promotion_bytes);
+uint64_t tma_cache_hits();
+uint64_t tma_cache_misses();
 
 } // namespace tlb
 

@@ -3,8 +3,10 @@
 // stand in for the reference's per-access checks (tensor.hpp:99, common.hpp:99-109).
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "tlb_internal.h"
@@ -30,6 +32,39 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 void set_plan(const char* name) { g_plan = name; }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+struct KnobDef {
+    const char* name;
+    int def;
+};
+// index = KnobId
+const KnobDef kKnobDefs[K_COUNT] = {
+    {"GEMM_WIDE", -1}, {"GEMM_SPLIT_TAIL", 1}, {"GEMM_EPILOGUE", 0}, {"GEMM_GROUP_M", 8}, {"GEMM_BACKOFF_NS", 100},
+    {"GEMM_DEBUG", 0}, {"GEMM_HINTS", 0}, {"GEMM_PDL", 1}, {"GEMM_PREFETCH_C", 0}, {"GEMM_WORKERS", 0},
+    {"GEMM_C16_SK", 0}, {"GEMM_SK_PCT", 4}, {"GEMM_EPI_KB", 10}, {"GEMM_CLOCK", 0}, {"PDL", 1},
+    {"COPY_TMA", 0}, {"COPY_LB256", 1}, {"COPY_PERSIST", 1}, {"EVAL_NO_WARP", 0}, {"HOST_PIPELINE", 1}, {"HOST_PANEL", 1024},
+};
+std::atomic<int> g_knobs[K_COUNT];
+std::once_flag g_knobs_once;
+
+int parse_knob(int id, const char* v) {
+    if (!v || !v[0]) return kKnobDefs[id].def;
+    if (id == K_GEMM_EPILOGUE) return v[0] == 'r' ? 1 : std::atoi(v);
+    return std::atoi(v);
+}
+void load_knobs() {
+    for (int i = 0; i < K_COUNT; ++i) {
+        const std::string env = std::string("TLB_") + kKnobDefs[i].name;
+        g_knobs[i].store(parse_knob(i, std::getenv(env.c_str())), std::memory_order_relaxed);
+    }
+}
+} // namespace
+
+int knob(KnobId id) {
+    std::call_once(g_knobs_once, load_knobs);
+    return g_knobs[id].load(std::memory_order_relaxed);
+}
 
 int require_device() {
     int n = 0;
@@ -297,6 +332,18 @@ int tlb_abi_version(void) { return TLB_ABI_VERSION; }
 const char* tlb_last_error(void) { return tlb::g_error.c_str(); }
 uint64_t tlb_launch_count(void) { return tlb::g_launches.load(std::memory_order_relaxed); }
 const char* tlb_last_plan(void) { return tlb::g_plan; }
+
+int tlb_config_set(const char* name, const char* value) {
+    if (!name) return tlb::fail(TLB_ERR_CONTRACT, "tlb_config_set: null name");
+    (void)tlb::knob(tlb::K_PDL); // make sure the environment has been read first
+    const char* n = std::strncmp(name, "TLB_", 4) == 0 ? name + 4 : name;
+    for (int i = 0; i < tlb::K_COUNT; ++i)
+        if (std::strcmp(n, tlb::kKnobDefs[i].name) == 0) {
+            tlb::g_knobs[i].store(tlb::parse_knob(i, value), std::memory_order_relaxed);
+            return TLB_OK;
+        }
+    return tlb::fail(TLB_ERR_CONTRACT, std::string("tlb_config_set: unknown knob ") + name);
+}
 
 int tlb_layout_lower(const tlb_mode* modes, int n_modes, tlb_layout_desc* out) {
     return tlb::lower_impl(modes, n_modes, nullptr, 0, out);

@@ -5,12 +5,15 @@
 // cuTensorMapEncodeTiled is resolved through cudaGetDriverEntryPoint so libtlb.so carries no
 // link-time dependency on libcuda (it must load on the GPU-less build host).
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include <cuda.h>
 
 #include "tlb_internal.h"
+#include "tlb_gemm.h"
 
 namespace tlb {
 
@@ -33,8 +36,70 @@ EncodeTiledFn encode_fn() {
 }
 } // namespace
 
+namespace {
+// Cache of encoded tensor maps, keyed by everything that goes into cuTensorMapEncodeTiled plus the device: a GEMM or a
+// TMA-fed copy issued again on the same buffers (the steady state of a training / serving loop, and every step of
+// bench.py) reuses its maps instead of re-encoding three of them per call. Mutex-guarded; 256 entries, round-robin
+// replacement; the only state the library shares between host threads besides the launch counter and the knobs.
+struct MapKey {
+    int32_t device, dtype_bytes, is_float, rank, swizzle, l2;
+    uint64_t base;
+    uint64_t dims[5];
+    uint64_t strides[4];
+    uint32_t box[5];
+    uint32_t pad_;
+};
+struct MapEntry {
+    MapKey key;
+    TmaDesc desc;
+};
+constexpr int kMapCache = 256;
+std::mutex g_map_mu;
+std::vector<MapEntry> g_map_cache;
+unsigned g_map_next = 0;
+std::atomic<uint64_t> g_map_hits{0}, g_map_misses{0};
+} // namespace
+
+uint64_t tma_cache_hits() { return g_map_hits.load(std::memory_order_relaxed); }
+uint64_t tma_cache_misses() { return g_map_misses.load(std::memory_order_relaxed); }
+
 int tma_encode(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base, const uint64_t* dims,
                const uint64_t* strides_bytes, const uint32_t* box, int swizzle, int l2_promotion_bytes) {
+    if (rank < 1 || rank > 5) return fail(TLB_ERR_UNSUPPORTED, "TMA tensor maps have rank 1..5");
+    MapKey key;
+    std::memset(&key, 0, sizeof(key));
+    if (cudaGetDevice(&key.device) != cudaSuccess) key.device = -1;
+    key.dtype_bytes = dtype_bytes;
+    key.is_float = is_float;
+    key.rank = rank;
+    key.swizzle = swizzle;
+    key.l2 = l2_promotion_bytes;
+    key.base = reinterpret_cast<uint64_t>(base);
+    for (int d = 0; d < rank; ++d) {
+        key.dims[d] = dims[d];
+        key.box[d] = box[d];
+        if (d > 0) key.strides[d - 1] = strides_bytes[d - 1];
+    }
+    {
+        std::lock_guard<std::mutex> lock(g_map_mu);
+        for (const MapEntry& e : g_map_cache)
+            if (std::memcmp(&e.key, &key, sizeof(key)) == 0) {
+                *out = e.desc;
+                g_map_hits.fetch_add(1, std::memory_order_relaxed);
+                return TLB_OK;
+            }
+    }
+    const int st = tma_encode_uncached(out, dtype_bytes, is_float, rank, base, dims, strides_bytes, box, swizzle, l2_promotion_bytes);
+    if (st != TLB_OK) return st;
+    g_map_misses.fetch_add(1, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    if (g_map_cache.size() < static_cast<size_t>(kMapCache)) g_map_cache.push_back({key, *out});
+    else g_map_cache[g_map_next++ % kMapCache] = {key, *out};
+    return TLB_OK;
+}
+
+int tma_encode_uncached(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base, const uint64_t* dims,
+                        const uint64_t* strides_bytes, const uint32_t* box, int swizzle, int l2_promotion_bytes) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(TLB_ERR_CUDA, "cuTensorMapEncodeTiled is not available from this driver");
     if (rank < 1 || rank > 5) return fail(TLB_ERR_UNSUPPORTED, "TMA tensor maps have rank 1..5");
@@ -72,6 +137,122 @@ int tma_encode(TmaDesc* out, int dtype_bytes, int is_float, int rank, void* base
     CUresult r = fn(reinterpret_cast<CUtensorMap*>(out->bytes), dt, static_cast<cuuint32_t>(rank), base, gdim, gstr,
                     bdim, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(TLB_ERR_CUDA, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string(int(r)));
+    return TLB_OK;
+}
+
+} // namespace tlb
+
+namespace tlb {
+
+int mode_leaves(const tlb_layout_desc& L, int top, int64_t* extent, int64_t* stride, int cap) {
+    int n = 0;
+    for (int r = L.top_start[top]; r < L.top_start[top + 1]; ++r) {
+        if (L.extent[r] == 1) continue;
+        if (n > 0 && stride[n - 1] * extent[n - 1] == L.stride[r]) {
+            extent[n - 1] *= L.extent[r]; // coalesce (layout.hpp:206): the two leaves walk one stride chain
+            continue;
+        }
+        if (n == cap) return -1;
+        extent[n] = L.extent[r];
+        stride[n] = L.stride[r];
+        ++n;
+    }
+    return n;
+}
+
+// The tensor map of the tiles of zipped_divide(L, [box_inner, box_outer]) (see tlb_gemm.h). Dimension order: the leaves of
+// the inner mode, the leaves of the outer mode, the batch; so a box lands in shared memory as [outer tile][inner tile] with
+// both tiles in the colex order of their modes, which is the order the UMMA descriptors and the epilogue expect.
+int tile_dims_derive(const tlb_layout_desc& L, int inner_top, int outer_top, int64_t box_inner, int64_t box_outer,
+                     int inner_src, int outer_src, int batch, int64_t batch_stride, int elem_bytes, TileDims* out) {
+    if (L.kind != TLB_KIND_INT) return fail(TLB_ERR_UNSUPPORTED, "tensor maps require integer strides");
+    const int64_t align = 16 / elem_bytes; // strides of dimensions 1.. must be multiples of 16 bytes
+    uint64_t* dims = out->dims;
+    uint64_t* strides = out->strides;
+    uint32_t* box = out->box;
+    TmaCoord* cc = out->c;
+    int rank = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int top = pass == 0 ? inner_top : outer_top;
+        int64_t e[4], st[4];
+        int n = mode_leaves(L, top, e, st, 4);
+        if (n < 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: a mode folds into more than 4 leaves");
+        if (n == 0) { // extent-1 mode: a unit dimension
+            n = 1;
+            e[0] = 1;
+            st[0] = pass == 0 ? 1 : align;
+        }
+        if (pass == 0 && st[0] != 1 && !(n == 1 && e[0] == 1))
+            return fail(TLB_ERR_UNSUPPORTED, "tensor map: the inner mode does not start with a unit-stride leaf");
+        int64_t t = pass == 0 ? box_inner : box_outer;
+        uint64_t prefix = 1;
+        for (int j = 0; j < n; ++j) {
+            if (rank == 4) return fail(TLB_ERR_UNSUPPORTED, "tensor map: layout needs more than 5 TMA dimensions");
+            if (st[j] <= 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: strides must be positive");
+            if (!(pass == 0 && j == 0) && (st[j] % align != 0 && e[j] > 1))
+                return fail(TLB_ERR_UNSUPPORTED, "tensor map: strides must be multiples of 16 bytes");
+            if (e[j] >= (1ll << 32)) return fail(TLB_ERR_UNSUPPORTED, "tensor map: extent exceeds 2^32");
+            const bool last = j + 1 == n;
+            int64_t b;
+            if (t == 1) b = 1;
+            else if (last) b = t; // ragged / short outermost leaf: the TMA unit clips and zero-fills
+            else if (t <= e[j]) {
+                if (e[j] % t != 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: tile straddles a leaf boundary");
+                b = t;
+            } else {
+                if (t % e[j] != 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: tile straddles a leaf boundary");
+                b = e[j];
+            }
+            // the swizzled staging layouts need the whole inner tile in ONE dimension (rows of box_inner elements)
+            if (pass == 0 && j == 0 && b != box_inner && !(last))
+                return fail(TLB_ERR_UNSUPPORTED, "tensor map: the inner tile does not fit the unit-stride leaf");
+            if (b > 256) return fail(TLB_ERR_UNSUPPORTED, "tensor map: box extents must be 1..256");
+            t = t == 1 ? 1 : (last ? 1 : (t <= e[j] ? 1 : t / e[j]));
+            dims[rank] = static_cast<uint64_t>(e[j]);
+            strides[rank] = static_cast<uint64_t>(st[j]);
+            box[rank] = static_cast<uint32_t>(b);
+            cc[rank].src = static_cast<uint32_t>(pass == 0 ? inner_src : outer_src);
+            cc[rank].div = static_cast<uint32_t>(prefix);
+            cc[rank].mod = last ? 0u : static_cast<uint32_t>(e[j]);
+            prefix *= static_cast<uint64_t>(e[j]);
+            ++rank;
+        }
+    }
+    // batch: the last dimension (a unit dimension for a single problem)
+    dims[rank] = static_cast<uint64_t>(std::max(batch, 1));
+    if (batch > 1) {
+        if (batch_stride <= 0 || batch_stride % align != 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: batch stride must be a positive multiple of 16 bytes");
+        strides[rank] = static_cast<uint64_t>(batch_stride);
+    } else {
+        uint64_t span = 1;
+        for (int d = 0; d < rank; ++d) span = std::max<uint64_t>(span, strides[d] * dims[d]);
+        strides[rank] = (span + align - 1) / align * align;
+    }
+    box[rank] = 1;
+    cc[rank] = {2u, 1u, 0u};
+    ++rank;
+    out->rank = rank;
+    for (int d = rank; d < 5; ++d) {
+        dims[d] = 1;
+        strides[d] = 0;
+        box[d] = 1;
+        cc[d] = TmaCoord{2u, 1u, 0u};
+    }
+    return TLB_OK;
+}
+
+int tensormap_for_tile(const tlb_layout_desc& L, int inner_top, int outer_top, int64_t box_inner, int64_t box_outer,
+                       int inner_src, int outer_src, const void* base, int batch, int64_t batch_stride, int elem_bytes,
+                       int is_float, int swizzle, int l2_promotion, TmaTileMap* out) {
+    TileDims td;
+    TLB_TRY(tile_dims_derive(L, inner_top, outer_top, box_inner, box_outer, inner_src, outer_src, batch, batch_stride, elem_bytes, &td));
+    uint64_t sb[4];
+    for (int d = 1; d < td.rank; ++d) sb[d - 1] = td.strides[d] * static_cast<uint64_t>(elem_bytes);
+    TmaDesc tmp;
+    TLB_TRY(tma_encode(&tmp, elem_bytes, is_float, td.rank, const_cast<void*>(base), td.dims, sb, td.box, swizzle, l2_promotion));
+    std::memcpy(out->desc, tmp.bytes, 128);
+    out->rank = td.rank;
+    for (int d = 0; d < 5; ++d) out->c[d] = td.c[d];
     return TLB_OK;
 }
 
@@ -207,6 +388,12 @@ extern "C" int tlb_tensormap_from_divided(const tlb_layout_desc* parent, const t
     TmaDesc tmp;
     TLB_TRY(tma_encode(&tmp, elem_bytes, false, static_cast<int>(dims.size()), d_base, gd, gs, bx, swizzle, 128));
     std::memcpy(out_tensormap_128B, tmp.bytes, 128);
+    return TLB_OK;
+}
+
+extern "C" int tlb_tensormap_cache_stats(uint64_t* hits, uint64_t* misses) {
+    if (hits) *hits = tma_cache_hits();
+    if (misses) *misses = tma_cache_misses();
     return TLB_OK;
 }
 

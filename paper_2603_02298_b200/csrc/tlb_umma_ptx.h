@@ -6,6 +6,8 @@
 
 #include <cuda.h>
 
+#include "tlb_gemm.h"
+
 namespace tlb {
 namespace umma {
 
@@ -200,6 +202,66 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
 // Shared-memory matrix descriptor of a K-major bf16 tile staged with the 128-byte swizzle: rows of 128 B,
 // 8-row groups 1024 B apart (SBO), sm_100 descriptor version 1, layout type 2 (SWIZZLE_128B). Only the low
 // word depends on the tile address; advancing K by 16 elements inside the swizzle row adds 32 B (+2).
+// ---- tiles of layout-derived tensor maps (TmaTileMap, tlb_gemm.h) --------------------------------------------------
+// TMA coordinates of the tile that starts at (row0, k0, batch) of its operand: one division and one remainder per
+// dimension that belongs to a folded mode, nothing for plain (rows, k, batch) maps.
+__device__ __forceinline__ void tile_coords(const TmaCoord* tc, int rank, uint32_t row0, uint32_t k0, uint32_t batch, int* c) {
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        if (d < rank) {
+            const uint32_t v = tc[d].src == 0u ? row0 : (tc[d].src == 1u ? k0 : batch);
+            uint32_t q = tc[d].div == 1u ? v : v / tc[d].div;
+            if (tc[d].mod) q %= tc[d].mod;
+            c[d] = static_cast<int>(q);
+        } else {
+            c[d] = 0;
+        }
+    }
+}
+// cp.async.bulk.tensor of rank 3..5; CG2: cta_group::2 form (transaction bytes complete on the leader's barrier).
+template <bool CG2>
+__device__ __forceinline__ void tma_load_tile(uint32_t dst, const void* map, uint32_t bar, int rank, const int* c) {
+    if (rank == 3) {
+        if constexpr (CG2) tma_load_3d_2sm(dst, map, bar, c[0], c[1], c[2]);
+        else tma_load_3d(dst, map, bar, c[0], c[1], c[2]);
+    } else if (rank == 4) {
+        if constexpr (CG2)
+            asm volatile("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+                         "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+        else
+            asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+                         "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+    } else {
+        if constexpr (CG2)
+            asm volatile("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+                         "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+        else
+            asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+                         "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+    }
+}
+template <bool CG2>
+__device__ __forceinline__ void tma_load_tile_hint(uint32_t dst, const void* map, uint32_t bar, int rank, const int* c, uint64_t pol) {
+    if (rank == 3) {
+        if constexpr (CG2) tma_load_3d_2sm_hint(dst, map, bar, c[0], c[1], c[2], pol);
+        else tma_load_3d_hint(dst, map, bar, c[0], c[1], c[2], pol);
+    } else {
+        tma_load_tile<CG2>(dst, map, bar, rank, c); // folded modes: no hinted form
+    }
+}
+// C += staged chunk through a rank 3..5 map.
+__device__ __forceinline__ void tma_reduce_add_tile(const void* map, uint32_t src, int rank, const int* c) {
+    if (rank == 3) {
+        tma_reduce_add_3d(map, src, c[0], c[1], c[2]);
+    } else if (rank == 4) {
+        asm volatile("cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+                     "r"(src), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+    } else {
+        asm volatile("cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(map),
+                     "r"(src), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+    }
+}
+
 constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
 __device__ __forceinline__ uint32_t desc_lo(uint32_t smem_addr) { return ((smem_addr >> 4) & 0x3fffu) | (1u << 16); }
 __device__ __forceinline__ uint64_t make_desc(uint32_t lo) { return (static_cast<uint64_t>(kDescHi) << 32) | lo; }

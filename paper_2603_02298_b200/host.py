@@ -171,6 +171,11 @@ def L(text: str) -> Layout:
     return Layout.parse(text)
 
 
+def config(name: str, value: str | None) -> None:
+    """tlb_config_set: change a library knob (the TLB_* environment is only read once, at first use)."""
+    abi.check(abi.load().tlb_config_set(name.encode(), None if value is None else str(value).encode()))
+
+
 def make_tensor(desc: abi.tlb_layout_desc, data_ptr: int | None, capacity: int, elem_bytes: int, origin: int = 0,
                 counting: bool = False) -> abi.tlb_tensor:
     t = abi.tlb_tensor()
@@ -240,6 +245,30 @@ def gemm_f16(a, b, c, tile_begin: int = 0, tile_end: int = 2**32 - 1, stream=Non
     lib = abi.load()
     abi.check(lib.tlb_gemm_f16(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), tile_begin, tile_end, _stream_ptr(stream)))
     return lib.tlb_last_plan().decode()
+
+
+def gemm_bf16_tiled(a, b, c, tiler, stream=None) -> str:
+    """tlb_gemm_bf16_tiled: tiler = (bm, bn, bk), the CTA (pair) tile of zipped_divide(C, [bm, bn]) and the k-block."""
+    lib = abi.load()
+    t = abi.tlb_gemm_tiler(*tiler)
+    abi.check(lib.tlb_gemm_bf16_tiled(C.byref(a[0]), C.byref(b[0]), C.byref(c[0]), C.addressof(t), _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
+def locate_offsets(a: Layout | str, t: Layout | str, stream=None) -> list:
+    """tlb_locate_offsets: flat modes [(extent, stride), ...] of R = left_inverse(A) o T; raises admissibility_error."""
+    da = (L(a) if isinstance(a, str) else a).lower()
+    dt = (L(t) if isinstance(t, str) else t).lower()
+    modes = (abi.tlb_mode * abi.TLB_MAX_MODES)()
+    n = C.c_int32(0)
+    abi.check(abi.load().tlb_locate_offsets(C.byref(da), C.byref(dt), modes, C.byref(n), _stream_ptr(stream)))
+    return [(modes[i].extent, modes[i].stride) for i in range(n.value)]
+
+
+def tensormap_cache_stats():
+    h, m = C.c_uint64(0), C.c_uint64(0)
+    abi.check(abi.load().tlb_tensormap_cache_stats(C.byref(h), C.byref(m)))
+    return h.value, m.value
 
 
 def gemm_tile_count(a, b, c) -> int:

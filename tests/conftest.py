@@ -30,6 +30,22 @@ def _built():
     yield
 
 
+@pytest.fixture
+def tlb_config():
+    """Set library knobs for one test (tlb_config_set: the TLB_* environment is read only once per process); every knob
+    the test touched goes back to its default afterwards."""
+    from paper_2603_02298_b200 import host
+    touched = []
+
+    def set_knob(name, value):
+        touched.append(name)
+        host.config(name, value)
+
+    yield set_knob
+    for name in touched:
+        host.config(name, None)
+
+
 def has_cuda() -> bool:
     try:
         import torch

@@ -222,10 +222,10 @@ def test_c2_gemm_4096_full_size_exact(cg):
 
 
 @pytest.fixture
-def force_wide(monkeypatch):
-    """K-major problems below 48 pair tiles default to the 256 x 256 plan; TLB_GEMM_WIDE=1 keeps the small parity shapes
+def force_wide(tlb_config):
+    """K-major problems below 48 pair tiles default to the 256 x 256 plan; GEMM_WIDE=1 keeps the small parity shapes
     on the wide kernel."""
-    monkeypatch.setenv("TLB_GEMM_WIDE", "1")
+    tlb_config("GEMM_WIDE", "1")
 
 
 WIDE_SHAPES = [
@@ -277,11 +277,11 @@ def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape):
     (WIDE_SHAPES[1], 0, "umma_2sm_wide"), (WIDE_SHAPES[2], 0, "umma_2sm_wide"), (MN_MAJOR_SHAPES[0], 0, "umma_2sm_wide"),
     (("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)"), 0, "simt_f16"),
 ])
-def test_gemm_f16_operands(shape, path, plan, monkeypatch):
+def test_gemm_f16_operands(shape, path, plan, tlb_config):
     """tlb_gemm_f16: IEEE fp16 operands on every plan (instruction-descriptor formats 0 instead of 1), exact on the
     reference's integer fills and within the stated tolerance on random data."""
     if plan.endswith("wide"):
-        monkeypatch.setenv("TLB_GEMM_WIDE", "1")
+        tlb_config("GEMM_WIDE", "1")
     assert _bf16_case(*shape, kat=True, path=path, f16=True) == plan
     assert _bf16_case(*shape, kat=False, seed=17, path=path, f16=True) == plan
 
@@ -354,19 +354,19 @@ def test_gemm_wide_plan_takes_large_problems_with_an_odd_number_of_row_blocks():
     assert _bf16_case("(1280,64):(64,1)", "(4096,64):(64,1)", "(1280,4096):(4096,1)", kat=True) == "umma_2sm_wide"
 
 
-def test_gemm_wide_plan_falls_back_when_it_does_not_apply(monkeypatch):
+def test_gemm_wide_plan_falls_back_when_it_does_not_apply(tlb_config):
     # ceil(M/256) odd: no m-adjacent block pairs -> 256 x 256 plan
     assert _bf16_case("(768,128):(128,1)", "(256,128):(128,1)", "(768,256):(256,1)", kat=True, path=3) == "umma_2sm"
     assert _bf16_case(*WIDE_SHAPES[1], kat=True, path=3) == "umma_2sm"          # 2 pair tiles: too small for the wide plan
-    monkeypatch.setenv("TLB_GEMM_WIDE", "0")
+    tlb_config("GEMM_WIDE", "0")
     assert _bf16_case("(2048,64):(64,1)", "(4096,64):(64,1)", "(2048,4096):(4096,1)", kat=True, path=3) == "umma_2sm"
 
 
-def test_gemm_wide_plan_without_k_split_is_reproducible(monkeypatch):
+def test_gemm_wide_plan_without_k_split_is_reproducible(tlb_config):
     """TLB_GEMM_SPLIT_TAIL=0: every tile is summed by one CTA pair in k order, so two runs agree bit for bit (with the
     k-range cut of the partial wave the partial sums meet in L2 in arrival order)."""
-    monkeypatch.setenv("TLB_GEMM_SPLIT_TAIL", "0")
-    monkeypatch.setenv("TLB_GEMM_WIDE", "1")
+    tlb_config("GEMM_SPLIT_TAIL", "0")
+    tlb_config("GEMM_WIDE", "1")
     assert _bf16_case(*WIDE_SHAPES[4], kat=False, seed=5, path=3) == "umma_2sm_wide"
     M, N, K = 2048, 2304, 512                                            # 36 pair tiles on 74 CTA pairs
     g = torch.Generator(device="cuda").manual_seed(9)
@@ -386,8 +386,8 @@ def test_gemm_wide_plan_without_k_split_is_reproducible(monkeypatch):
     assert torch.allclose(outs[0].view(M, N), ref, rtol=1e-3, atol=1e-2)
 
 
-def test_gemm_register_epilogue_matches_tma_epilogue(monkeypatch):
-    monkeypatch.setenv("TLB_GEMM_EPILOGUE", "regs")
+def test_gemm_register_epilogue_matches_tma_epilogue(tlb_config):
+    tlb_config("GEMM_EPILOGUE", "regs")
     assert _bf16_case(*UMMA_SHAPES[1], kat=True, path=2) == "umma_1sm_regs"
     assert _bf16_case(*UMMA_SHAPES[2], kat=False, seed=3, path=3) == "umma_2sm_regs"
     _flat_tn_check(4096, 4096, 1024, 2)
@@ -471,10 +471,10 @@ def test_gemm_host_entry_point():
 
 
 @pytest.mark.parametrize("lc_kind", ["m_contiguous", "n_contiguous"])
-def test_gemm_host_entry_point_pipelined_panels(lc_kind, monkeypatch):
+def test_gemm_host_entry_point_pipelined_panels(lc_kind, tlb_config):
     """tlb_gemm_bf16_host on a problem with several 512-row panels (ragged last panel, padded leading dimensions): the
     upload / compute / download pipeline must produce exactly what the one-shot path does, and the oracle's cells."""
-    monkeypatch.setenv("TLB_HOST_PANEL", "512")
+    tlb_config("HOST_PANEL", "512")
     M, N, K = 1300, 1400, 72
     lda, ldb = 80, 88
     rng = np.random.default_rng(21)
@@ -494,7 +494,7 @@ def test_gemm_host_entry_point_pipelined_panels(lc_kind, monkeypatch):
     assert st == 0
     outs = []
     for pipe in ("1", "0"):
-        monkeypatch.setenv("TLB_HOST_PIPELINE", pipe)
+        tlb_config("HOST_PIPELINE", pipe)
         ha, hb, hc = (torch.from_numpy(x.copy()) for x in (ab.view(np.int16), bb.view(np.int16), c0))
         ta, ka = host.tensor_of(la, ha, ranked=True)
         tb, kb = host.tensor_of(lb, hb, ranked=True)
@@ -531,3 +531,113 @@ def test_c4_batched_8192_two_batches_exact():
     want = np.ones((N, M), dtype=np.float32)
     ou.orc_gemm_bf16_tn_flat(an.ravel(), K, bn.ravel(), K, want.ravel(), M, M, N, K, 4096, 4104, 8000, 8008)
     assert (c[1].cpu().numpy()[8000:8008, 4096:4104] == want[8000:8008, 4096:4104]).all()
+
+
+# ---- layout-driven tiling (north_star: "tiled GEMM partitioned by local_tile / local_partition / TiledMMA") ----------------
+TILERS = [(128, 128, 64), (128, 256, 64), (256, 128, 64), (256, 256, 64), (512, 256, 64)]
+TILER_PLANS = {(128, 128): "umma_1sm_n128", (128, 256): "umma_1sm", (256, 128): "umma_2sm_n128", (256, 256): "umma_2sm",
+               (512, 256): "umma_2sm_wide"}
+
+
+def _tiled_case(la, lb, lc, tiler, kat=True, seed=0):
+    M, N, K = _dims(la, lb)
+    na, nb, nc = ou.cosize_of(la), ou.cosize_of(lb), ou.cosize_of(lc)
+    rng = np.random.default_rng(seed)
+    ao = ou.orc_eval_range(la, 0, M * K).reshape(K, M).T
+    bo = ou.orc_eval_range(lb, 0, N * K).reshape(K, N).T
+    a, b = np.zeros(na, dtype=np.float32), np.zeros(nb, dtype=np.float32)
+    if kat:
+        i, p = np.meshgrid(np.arange(M), np.arange(K), indexing="ij")
+        a[ao] = (i * 7 + p * 3 + 1) % 11
+        j, p = np.meshgrid(np.arange(N), np.arange(K), indexing="ij")
+        b[bo] = (j * 5 + p * 2 + 2) % 13
+        c0 = (np.arange(nc) % 5 - 2).astype(np.float32)
+    else:
+        a[ao] = rng.uniform(-1, 1, (M, K))
+        b[bo] = rng.uniform(-1, 1, (N, K))
+        c0 = rng.uniform(-1, 1, nc).astype(np.float32)
+    ab, bb = ou.f32_to_bf16_bits(a), ou.f32_to_bf16_bits(b)
+    want = c0.copy()
+    st, sabs = ou.orc_gemm_bf16(la, ab, lb, bb, lc, want, want_abs=True)
+    assert st == 0
+    ta_, tb_, tc_ = dev(ab.view(np.int16)), dev(bb.view(np.int16)), dev(c0)
+    ta, tb, tc = (host.tensor_of(t, buf, ranked=True) for t, buf in ((la, ta_), (lb, tb_), (lc, tc_)))
+    plan = host.gemm_bf16_tiled(ta, tb, tc, tiler)
+    torch.cuda.synchronize()
+    got = tc_.cpu().numpy()
+    if kat:
+        assert (got == want).all(), f"{plan} tiler {tiler}: {int((got != want).sum())} of {got.size} cells differ"
+    else:
+        touched = sabs > 0
+        assert (np.abs(got - want)[touched] <= (RTOL * sabs + ATOL)[touched]).all()
+        assert (got[~touched] == want[~touched]).all()
+    return plan
+
+
+@pytest.mark.parametrize("tiler", TILERS)
+@pytest.mark.parametrize("shape", [
+    ("(512,256):(256,1)", "(768,256):(256,1)", "(512,768):(768,1)"),      # n-contiguous C: the tiler applies as given
+    ("(1000,200):(200,1)", "(300,200):(200,1)", "(1000,300):(300,1)"),    # ragged M, N, K
+    ("(1024,520):(528,1)", "(768,520):(536,1)", "(1024,768):(800,1)"),    # padded leading dimensions
+])
+def test_gemm_partitioned_by_a_caller_chosen_tiler(shape, tiler):
+    """tlb_gemm_bf16_tiled: the CTA tile, the k-block boxes and the UMMA atom all follow from the tiler [bm, bn, bk]
+    (zipped_divide tile modes -> tensor maps; 128 x N x 16 or 256 x N x 16 atoms): every tiler gives the exact result."""
+    assert _tiled_case(*shape, tiler, kat=True) == TILER_PLANS[tiler[:2]]
+    _tiled_case(*shape, tiler, kat=False, seed=23)
+
+
+@pytest.mark.parametrize("tiler", TILERS)
+def test_gemm_tiler_on_the_papers_tn_layout(tiler):
+    """TN: C is m-contiguous, the plan runs C^T, so the caller's [bm, bn] becomes [bn, bm] rows x columns."""
+    shape = ("(768,256):(256,1)", "(512,256):(256,1)", "(768,512):(1,768)")
+    user = (tiler[1], tiler[0], 64)                                     # chosen so that the plan's tile is `tiler`
+    assert _tiled_case(*shape, user, kat=True) == TILER_PLANS[tiler[:2]]
+
+
+def test_gemm_tiler_contracts():
+    shape = ("(512,256):(256,1)", "(768,256):(256,1)", "(512,768):(768,1)")
+    for bad in [(64, 128, 64), (128, 64, 64), (128, 128, 32), (512, 128, 64), (192, 256, 64)]:
+        with pytest.raises(TlbError) as e:
+            _tiled_case(*shape, bad)
+        assert e.value.status == abi.TLB_ERR_UNSUPPORTED
+    with pytest.raises(TlbError) as e:                                  # BLIS strides: SIMT plan, no tiler
+        _tiled_case("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)", (128, 128, 64))
+    assert e.value.status == abi.TLB_ERR_UNSUPPORTED
+
+
+def test_gemm_tensor_maps_come_from_the_divided_layouts_and_are_cached():
+    """The tensor maps of a GEMM call are derived from zipped_divide tile modes (tlb_tensormap_describe shows the same
+    dimensions) and encoded once: a second call on the same buffers is served from the mutex-guarded cache."""
+    rank, dims, strides, box = host.tensormap_describe("(4096,4096):(4096,1)", "(256,64):(4096,1)")
+    assert (rank, dims, strides, box) == (2, [4096, 4096], [1, 4096], [64, 256])      # A k-blocks of the wide plan
+    M = 1024
+    a = torch.zeros(M * M, dtype=torch.int16, device="cuda")
+    c = torch.zeros(M * M, dtype=torch.float32, device="cuda")
+    ta = host.tensor_of(f"({M},{M}):({M},1)", a, ranked=True)
+    tc = host.tensor_of(f"({M},{M}):({M},1)", c, ranked=True)
+    host.gemm_bf16(ta, ta, tc)
+    h0, m0 = host.tensormap_cache_stats()
+    for _ in range(5):
+        host.gemm_bf16(ta, ta, tc)
+    torch.cuda.synchronize()
+    h1, m1 = host.tensormap_cache_stats()
+    assert m1 == m0 and h1 - h0 >= 10                                    # 5 calls x (A = B map, C map), no new encode
+
+
+def test_locate_offsets_matches_the_reference():
+    """tlb_locate_offsets vs tla::locate_offsets (analysis.hpp:40-56): the reference's own goldens (test_analysis.cpp:84-108),
+    the tcgen05.ld 32x32b partition of TMEM accumulators, and inadmissible offsets."""
+    for row in ou.golden("locate.json"):
+        if row["status"] != 0:
+            with pytest.raises(TlbError) as e:
+                host.locate_offsets(row["A"], row["T"])
+            assert e.value.status == abi.TLB_ERR_ADMISSIBILITY, (row["A"], row["T"])
+            continue
+        modes = host.locate_offsets(row["A"], row["T"])
+        n = len(row["R_values"])
+        text = (f"{modes[0][0]}:{modes[0][1]}" if len(modes) == 1 else
+                "(" + ",".join(str(e) for e, _ in modes) + "):(" + ",".join(str(s) for _, s in modes) + ")")
+        assert ou.orc_eval_range(text, 0, n).tolist() == row["R_values"], (row["A"], row["T"], text)
+    # the partition the kernels use: 32 lanes x 32 columns per tcgen05.ld.32x32b.x32 of a (128, N):(65536, 1) accumulator
+    assert host.locate_offsets("(128,512):(65536,1)", "(32,32):(1,65536)") == [(32, 128), (32, 1)]
