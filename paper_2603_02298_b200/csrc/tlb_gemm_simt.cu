@@ -107,6 +107,104 @@ gemm_simt_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_consta
     }
 }
 
+// ---- tiled SIMT plan for 2-byte operands --------------------------------------------------------------------------------
+// Every layout family the tcgen05 plans do not take (BLIS strides, Xor strides, strides TMA cannot address, folded modes
+// whose tiles straddle leaves): the offset of A(m, k) is f(m) (+|^) g(k) with f and g the evaluations of the two top-level
+// modes, so a CTA evaluates the layouts ONCE per row / column / k of its tile (offset tables in shared memory) instead of
+// twice per MAC, stages 64 x 16 and 64 x 16 operand tiles as fp32 in shared memory, and every thread accumulates a 4 x 4
+// block of C with k ascending: the reference's summation order (tensor.hpp:223-231), hence bit-exact against the
+// sequential fp32 restatement (products of bf16 / fp16 pairs are exact in fp32).
+constexpr int TS_M = 64, TS_N = 64, TS_K = 16;
+
+__global__ void __launch_bounds__(kThreads)
+gemm_simt_tiled_kernel(const __grid_constant__ tlb_layout_desc LA, const __grid_constant__ tlb_layout_desc LB,
+                       const __grid_constant__ tlb_layout_desc LC, const uint16_t* __restrict__ A, const uint16_t* __restrict__ B,
+                       void* C, const __grid_constant__ SimtArgs p, int a_k_fast, int b_k_fast) {
+    __shared__ __align__(16) float sa[TS_K][TS_M + 4];
+    __shared__ __align__(16) float sb[TS_K][TS_N + 4];
+    __shared__ int64_t off_am[TS_M], off_bn[TS_N], off_ak[TS_K], off_bk[TS_K];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const uint32_t tiles_m = static_cast<uint32_t>((p.M + TS_M - 1) / TS_M);
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x % tiles_m) * TS_M, n0 = static_cast<int64_t>(blockIdx.x / tiles_m) * TS_N;
+    const int64_t batch = p.batch_begin + blockIdx.y;
+    const uint16_t* a = A + batch * p.a_bs;
+    const uint16_t* b = B + batch * p.b_bs;
+    auto cvt = [&](uint16_t v) { return p.ab_f16 ? __half2float(__ushort_as_half(v)) : __uint_as_float(static_cast<uint32_t>(v) << 16); };
+    if (tid < TS_M) off_am[tid] = m0 + tid < p.M ? dev_eval_top(LA, 0, static_cast<uint64_t>(m0 + tid)) : 0;
+    else if (tid < TS_M + TS_N) off_bn[tid - TS_M] = n0 + tid - TS_M < p.N ? dev_eval_top(LB, 0, static_cast<uint64_t>(n0 + tid - TS_M)) : 0;
+    // this thread's 4 x 4 block of C: positions, tile membership, starting accumulators
+    const uint32_t tpb = tiles_per_batch(p.grid);
+    int64_t cpos[4][4];
+    bool live[4][4];
+    float acc[4][4];
+    float* c32 = static_cast<float*>(C);
+    uint16_t* c16 = static_cast<uint16_t*>(C);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t m = m0 + ty * 4 + i;
+        const int64_t cm = m < p.M ? dev_eval_top(LC, 0, static_cast<uint64_t>(m)) : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t n = n0 + tx * 4 + j;
+            live[i][j] = m < p.M && n < p.N;
+            acc[i][j] = 0.f;
+            if (live[i][j]) {
+                const uint64_t tile = static_cast<uint64_t>(batch) * tpb + (p.swapped ? tile_of(p.grid, n, m) : tile_of(p.grid, m, n));
+                live[i][j] = tile >= p.tile_begin && tile < p.tile_end;
+            }
+            if (live[i][j]) {
+                cpos[i][j] = dev_position(LC, p.c_origin, combine(LC.kind, cm, dev_eval_top(LC, 1, static_cast<uint64_t>(n)))) + batch * p.c_bs;
+                acc[i][j] = p.c_16 ? cvt(c16[cpos[i][j]]) : c32[cpos[i][j]];
+            }
+        }
+    }
+    for (int64_t k0 = 0; k0 < p.K; k0 += TS_K) {
+        if (tid < TS_K) off_ak[tid] = k0 + tid < p.K ? dev_eval_top(LA, 1, static_cast<uint64_t>(k0 + tid)) : 0;
+        else if (tid < 2 * TS_K) off_bk[tid - TS_K] = k0 + tid - TS_K < p.K ? dev_eval_top(LB, 1, static_cast<uint64_t>(k0 + tid - TS_K)) : 0;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < TS_M * TS_K / kThreads; ++u) {
+            const int idx = tid + u * kThreads;
+            // consecutive threads walk the operand's faster mode (coalescing where the layout allows it)
+            const int am = a_k_fast ? idx / TS_K : idx % TS_M, ak = a_k_fast ? idx % TS_K : idx / TS_M;
+            const int bn = b_k_fast ? idx / TS_K : idx % TS_N, bk = b_k_fast ? idx % TS_K : idx / TS_N;
+            float va = 0.f, vb = 0.f;
+            if (m0 + am < p.M && k0 + ak < p.K) va = cvt(a[dev_position(LA, p.a_origin, combine(LA.kind, off_am[am], off_ak[ak]))]);
+            if (n0 + bn < p.N && k0 + bk < p.K) vb = cvt(b[dev_position(LB, p.b_origin, combine(LB.kind, off_bn[bn], off_bk[bk]))]);
+            sa[ak][am] = va;
+            sb[bk][bn] = vb;
+        }
+        __syncthreads();
+        const int kmax = static_cast<int>(min(static_cast<int64_t>(TS_K), p.K - k0)); // no padded k: -0 + 0 would flip a sign bit
+        for (int kk = 0; kk < kmax; ++kk) {
+            const float4 a4 = *reinterpret_cast<const float4*>(&sa[kk][ty * 4]);
+            const float4 b4 = *reinterpret_cast<const float4*>(&sb[kk][tx * 4]);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (live[i][j]) {
+                if (p.c_16) c16[cpos[i][j]] = p.ab_f16 ? __half_as_ushort(__float2half_rn(acc[i][j])) : __bfloat16_as_ushort(__float2bfloat16_rn(acc[i][j]));
+                else c32[cpos[i][j]] = acc[i][j];
+            }
+}
+
+// Smallest |stride| among the leaves of a top-level mode (which of an operand's two modes walks memory faster).
+int64_t min_abs_stride(const tlb_layout_desc& L, int t) {
+    int64_t best = INT64_MAX;
+    for (int r = L.top_start[t]; r < L.top_start[t + 1]; ++r)
+        if (L.extent[r] > 1) best = std::min<int64_t>(best, std::llabs(L.stride[r]));
+    return best;
+}
+
 int64_t top_size(const tlb_layout_desc& L, int t) {
     int64_t s = 1;
     for (int r = L.top_start[t]; r < L.top_start[t + 1]; ++r) s *= L.extent[r];
@@ -196,9 +294,27 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
                  int64_t b_bs, int64_t c_bs, int batch_begin, int batch_end) {
     UmmaFit f;
     if (A->layout->kind != TLB_KIND_INT || B->layout->kind != TLB_KIND_INT || C->layout->kind != TLB_KIND_INT) return f;
-    int64_t eCm, csm, eCn, csn;
-    if (!single_stride(*C->layout, 0, &eCm, &csm) || !single_stride(*C->layout, 1, &eCn, &csn)) return f;
+    int64_t eCm = 0, csm = 0, eCn = 0, csn = 0;
+    const bool c_flat = single_stride(*C->layout, 0, &eCm, &csm) && single_stride(*C->layout, 1, &eCn, &csn);
     const bool batched = batch_end - batch_begin > 1 || batch_begin > 0;
+    // C with hierarchical modes (a GETT-style folded m or n): the reduce-add epilogue addresses it through
+    // a rank-4/5 tensor map when the mode that runs along the accumulator's columns starts with a unit-stride leaf.
+    int c_col_top = -1;
+    if (!c_flat) {
+        const int cb = C->elem_bytes;
+        for (int top = 1; top >= 0 && c_col_top < 0; --top) {
+            int64_t e[4], st[4];
+            const int n = mode_leaves(*C->layout, top, e, st, 4);
+            TileDims td;
+            if (n > 0 && st[0] == 1 &&
+                tile_dims_derive(*C->layout, top, 1 - top, cb == 2 ? 64 : 32, 32, 1, 0, batch_end, c_bs, cb, &td) == TLB_OK &&
+                tile_dims_derive(*C->layout, top, 1 - top, 32, 128, 1, 0, batch_end, c_bs, cb, &td) == TLB_OK)
+                c_col_top = top;
+        }
+        if (c_col_top < 0) return f;
+        // no register epilogue for folded C: the tensor-map path must apply (16-byte aligned base)
+        if ((reinterpret_cast<uintptr_t>(static_cast<char*>(C->data) + C->origin * cb) & 15) != 0) return f;
+    }
     // Operand majorness from the layout: K-major when the k mode starts with a unit-stride leaf (the paper's "T"
     // operands), MN-major when the row mode does (the "N" operands of the NT / NTT rows). Modes may
     // be hierarchical (GETT-style folded modes): the operand qualifies when the k-block tiles of
@@ -219,16 +335,17 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
         return tile_dims_derive(L, 0, 1, 64, 64, 0, 1, batch_end, bs, 2, &td) == TLB_OK;
     };
     bool a_mn = false, b_mn = false;
-    bool ok = operand(*A->layout, a_bs, &a_mn) && operand(*B->layout, b_bs, &b_mn) && csm >= 0 && csn >= 0 &&
-              (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1) && (C->layout->flags & TLB_LF_INJECTIVE) &&
-              (!batched || (a_bs > 0 && b_bs > 0));
+    bool ok = operand(*A->layout, a_bs, &a_mn) && operand(*B->layout, b_bs, &b_mn) &&
+              (!c_flat || (csm >= 0 && csn >= 0 && (csm > 0 || d.M == 1) && (csn > 0 || d.N == 1))) &&
+              (C->layout->flags & TLB_LF_INJECTIVE) && (!batched || (a_bs > 0 && b_bs > 0));
     const char* a_ptr = static_cast<const char*>(A->data) + A->origin * 2;
     const char* b_ptr = static_cast<const char*>(B->data) + B->origin * 2;
     ok = ok && (reinterpret_cast<uintptr_t>(a_ptr) % 16 == 0) && (reinterpret_cast<uintptr_t>(b_ptr) % 16 == 0);
     if (!ok) return f;
     UmmaProblem& p = f.p;
     std::memset(&p, 0, sizeof(p));
-    f.swapped = csm == 1 && csn != 1;
+    f.swapped = c_flat ? (csm == 1 && csn != 1) : (c_col_top == 0);
+    p.c_fold_tma = c_flat ? 0 : 1;
     p.A = f.swapped ? b_ptr : a_ptr;
     p.B = f.swapped ? a_ptr : b_ptr;
     p.C = reinterpret_cast<float*>(static_cast<char*>(C->data) + C->origin * C->elem_bytes);
@@ -366,8 +483,15 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
     const int gridx = static_cast<int>(std::max<uint64_t>(blocks, 1));
     if (i64)
         gemm_simt_kernel<true><<<gridx, kThreads, 0, stream>>>(*A->layout, *B->layout, *C->layout, A->data, B->data, C->data, p, d_status);
-    else
-        gemm_simt_kernel<false><<<gridx, kThreads, 0, stream>>>(*A->layout, *B->layout, *C->layout, A->data, B->data, C->data, p, nullptr);
+    else {
+        const uint64_t tiles = static_cast<uint64_t>((d.M + TS_M - 1) / TS_M) * static_cast<uint64_t>((d.N + TS_N - 1) / TS_N);
+        const int nbatch = batch_end - batch_begin;
+        if (tiles > 0x7fffffffull || nbatch > 65535) return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: too many tiles for the SIMT plan");
+        gemm_simt_tiled_kernel<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(nbatch)), kThreads, 0, stream>>>(
+            *A->layout, *B->layout, *C->layout, static_cast<const uint16_t*>(A->data), static_cast<const uint16_t*>(B->data), C->data, p,
+            min_abs_stride(*A->layout, 1) < min_abs_stride(*A->layout, 0) ? 1 : 0,
+            min_abs_stride(*B->layout, 1) < min_abs_stride(*B->layout, 0) ? 1 : 0);
+    }
     count_launch();
     TLB_CUDA(cudaGetLastError());
     set_plan(i64 ? "simt_i64" : f16 ? "simt_f16" : "simt_bf16");

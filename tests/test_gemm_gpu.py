@@ -641,3 +641,48 @@ def test_locate_offsets_matches_the_reference():
         assert ou.orc_eval_range(text, 0, n).tolist() == row["R_values"], (row["A"], row["T"], text)
     # the partition the kernels use: 32 lanes x 32 columns per tcgen05.ld.32x32b.x32 of a (128, N):(65536, 1) accumulator
     assert host.locate_offsets("(128,512):(65536,1)", "(32,32):(1,65536)") == [(32, 128), (32, 1)]
+
+
+# ---- folded (GETT) and strided (BLIS) operand families at scale (test_tensor.cpp:187-189) ---------------
+GETT_SHAPES = [
+    # A[(m0,m1),(k0,k1)] K-major with folded rows AND folded k, B[n,(k0,k1)], plain C: rank-5 / rank-4 operand maps
+    ("((128,8),(64,8)):((64,65536),(1,8192))", "(512,(64,8)):(64,(1,32768))", "(1024,512):(512,1)"),
+    # the same contraction with the paper's TN output
+    ("((128,8),(64,8)):((64,65536),(1,8192))", "(512,(64,8)):(64,(1,32768))", "(1024,512):(1,1024)"),
+    # A[(m0,m1),k] m0-contiguous (MN-major, folded m), C[(m0,m1),n] folded the same way: the epilogue's reduce-add map is rank 4
+    ("((64,16),512):((1,32768),64)", "(768,512):(512,1)", "((64,16),768):((1,49152),64)"),
+    # folded n on B and on C's columns, ragged K
+    ("(512,200):(200,1)", "((64,8),200):((200,16000),1)", "(512,(64,8)):(1024,(1,128))"),
+]
+
+
+@pytest.mark.parametrize("shape", GETT_SHAPES)
+def test_gemm_gett_folded_modes_on_tensor_cores(shape):
+    """GETT: modes folded into several leaves. Each leaf is a TMA dimension of a rank-4/5 tensor map derived from the
+    divided layout; the producer decomposes a tile's 1-D coordinate into per-leaf coordinates. Exact on the reference's
+    integer fills, within tolerance on random data."""
+    assert _bf16_case(*shape, kat=True).startswith("umma_2sm")
+    assert _bf16_case(*shape, kat=False, seed=29).startswith("umma_2sm")
+
+
+def test_gemm_gett_folded_modes_on_every_tensor_core_plan(tlb_config):
+    shape = GETT_SHAPES[0]
+    assert _bf16_case(*shape, kat=True, path=2) == "umma_1sm"
+    assert _bf16_case(*shape, kat=True, path=3) == "umma_2sm"
+    tlb_config("GEMM_WIDE", "1")
+    assert _bf16_case(*shape, kat=True, path=3) == "umma_2sm_wide"
+    assert _tiled_case(*shape, (128, 128, 64)) == "umma_1sm_n128"
+
+
+@pytest.mark.parametrize("shape", [
+    ("(512,256):(3,1549)", "(384,256):(2,771)", "(512,384):(5,2563)"),                       # BLIS: no unit stride anywhere
+    ("((2,256),256):((1,512),2)", "(384,256):(256,1)", "((2,256),384):((1,2),512)"),           # the reference's GETT row scaled: k stride 2
+    ("(300,200):(f1,f512)", "(100,200):(200,1)", "(300,100):(1,300)"),                       # Xor-strided operand
+    ("(333,77):(77,1)", "(129,77):(1,129)", "(333,129):(129,1)"),                            # odd extents, unaligned leading dimensions
+])
+def test_gemm_simt_tiled_plan_is_exact_on_strided_families(shape):
+    """Layouts TMA cannot address (no unit-stride leaf, strides that are not multiples of 16 bytes, Xor strides) run on the
+    tiled SIMT plan: offset tables per tile, fp32 staging in shared memory, k ascending per output -> bit-exact."""
+    assert _bf16_case(*shape, kat=True).startswith("simt")
+    assert _bf16_case(*shape, kat=False, seed=31).startswith("simt")
+    assert _bf16_case(*shape, kat=False, seed=37, f16=True).startswith("simt")
