@@ -637,6 +637,41 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
                                  "algorithmic_flop_per_launch": 2.0 * M2 ** 3}})
         del sets16
         torch.cuda.empty_cache()
+    # The other operand families of the paper's GEMM table: GETT-folded modes on tcgen05 through
+    # rank-4/5 tensor maps, and BLIS strides (no unit stride: not TMA-addressable) on the tiled SIMT plan
+    if want("Cg"):
+        def gemm_family(name, la, lb, lc, workload, steps, kernel):
+            Lx = host.L
+            M_ = 1
+            for e, *_ in Lx(la).modes[:Lx(la).top_leaves[0]]:
+                M_ *= e
+            N_ = 1
+            for e, *_ in Lx(lb).modes[:Lx(lb).top_leaves[0]]:
+                N_ *= e
+            K_ = Lx(la).size // M_
+            fsets = []
+            for _ in range(2):
+                a_ = torch.empty(Lx(la).lower().max_offset + 1, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+                b_ = torch.empty(Lx(lb).lower().max_offset + 1, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+                c_ = torch.zeros(Lx(lc).lower().max_offset + 1, dtype=torch.float32, device="cuda")
+                fsets.append((host.tensor_of(la, a_.view(torch.int16), ranked=True), host.tensor_of(lb, b_.view(torch.int16), ranked=True),
+                              host.tensor_of(lc, c_, ranked=True)))
+            sec = timed(torch, dist, world, lambda i: host.gemm_bf16(*fsets[i % 2]), steps, 3)
+            fl = 2.0 * M_ * N_ * K_
+            per = fl / (sec / steps) / 1e12
+            out.append({"name": name, "metric": "gemm_tflops", "value": fl * steps * world / sec / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+                        "scaling": "weak", "steps": steps, "ms_per_step": sec / steps * 1e3,
+                        "config": {"workload": workload, "A": la, "B": lb, "C": lc, "plan": lib.tlb_last_plan().decode()},
+                        "roofline": {"bound": "tensor", "achieved": per, "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": per / pk["bf16_tflops"],
+                                     "traffic": None, "kernel": kernel, "peak_source": f"{pk['_source']} burst cuBLAS bf16",
+                                     "frac_of_nominal_2250": per / 2250.0, "algorithmic_flop_per_launch": fl}})
+            del fsets
+            torch.cuda.empty_cache()
+        gemm_family("Cg_gett_folded", "((128,32),(64,64)):((64,524288),(1,8192))", "((128,32),(64,64)):((64,524288),(1,8192))",
+                    "(4096,4096):(1,4096)", "GETT: 4096^3 with m, n and k each folded into two leaves (rank-5 tensor maps), TN output", K,
+                    "umma_wide_kernel")
+        gemm_family("Cg_blis_strided", "(2048,2048):(3,6151)", "(2048,2048):(2,4099)", "(2048,2048):(5,10243)",
+                    "BLIS: 2048^3 with general strides on every mode (no unit stride anywhere)", max(3, K // 8), "gemm_simt_tiled_kernel")
     # C4: batched bf16 GEMM 64 x 8192^3, sharded by whole batches (= tile-id ranges) across the ranks (strong
     # scaling of the 64 batches; every rank owns its batches' operands, no data-path collective)
     if want("C4"):
@@ -679,7 +714,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gemm-path", default="auto", choices=["auto", "1sm", "2sm"])
     ap.add_argument("--gemm-only", action="store_true", help="skip the other_configs lines (profiling runs)")
-    ap.add_argument("--only", default="", help="comma-separated other_configs to run (C1,C3,Cx,C5,C2_bf16_c,C4): profiling runs")
+    ap.add_argument("--only", default="", help="comma-separated other_configs to run (C1,C3,Cx,C5,C2_bf16_c,Cg,C4): profiling runs")
     ap.add_argument("--quick", action="store_true", help="skip the multi-GiB pinned-host e2e legs of C3 / C5")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs (profiling runs)")
     ap.add_argument("--share-gpu", action="store_true", help="testing only: run the N ranks on cuda:0 over gloo when the box has fewer than N GPUs")

@@ -158,6 +158,12 @@ int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uin
  * detail::verify_distributed (algebra.hpp:211) re-checks on the host in O(size(B)). */
 int tlb_compose_check_range(const tlb_layout_desc* A, const tlb_layout_desc* B, const tlb_layout_desc* R,
                             uint64_t i0, uint64_t n, unsigned long long* d_mismatch, void* stream);
+/* The whole check in one synchronous call: *mismatches = #{ i < size(B) : A(B(i)) != R(i) }. This is what lets
+ * tla::compose skip its O(size(B)) host loop (detail::verify_distributed, algebra.hpp:211-228: about 18 s for the
+ * 8192 x 8192 transpose map of config C1): include/tla/device.hpp's compose_device() runs the reference's own
+ * per-leaf composition and verifies the result here in milliseconds. */
+int tlb_compose_check(const tlb_layout_desc* A, const tlb_layout_desc* B, const tlb_layout_desc* R, uint64_t* mismatches,
+                      void* stream);
 /* Per-axis evaluation of a Basis (coordinate) layout: d_out[k*n_axes + a] (layout_eval_axes, layout.hpp:103). */
 int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t i0, uint64_t n,
                         int64_t* d_out, void* stream);
@@ -172,6 +178,11 @@ int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uin
  * the plan it would pick is then available from tlb_last_plan(). Pointers are only inspected for
  * alignment. (Xor-kind bounds that need the exact device scan are assumed to pass.) */
 int tlb_copy_plan(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end);
+/* tla::max_common_vector(a, b) (analysis.hpp:18-28): the number of leading offsets 0 .. K-1 both layouts reach from the
+ * same integral coordinates, i.e. how many elements can move as one vector. Host only. Computed from the common
+ * refinement the copy planner works on (it is what bounds the "vec" plan's vector width); layouts the reference cannot
+ * right-invert give the scalar answer 1, as there. */
+int tlb_max_common_vector(const tlb_layout_desc* a, const tlb_layout_desc* b, int64_t* k);
 /* Planner knobs for tlb_copy on the calling thread: force one path (testing / profiling).
  * 0 = auto, 1 = gather only, 2 = tiled (LDG-fed), 3 = tiled TMA-fed. Returns the previous value. */
 int tlb_copy_set_path(int path);

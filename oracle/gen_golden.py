@@ -193,6 +193,23 @@ def main():
         al.append({"src": s, "src_origin": so, "dst": d, "dst_origin": do, "cells": cells, "status": st,
                    "result": buf.tolist()})
     (OUT / "alias.json").write_text(json.dumps(al))
+    # max_common_vector (analysis.hpp:18-28): Table-1 pairs, gaps, broadcasts and 60 random stride permutations of (2,4,3,8)
+    mc = [["8:1", "8:1"], ["(8,2,3):(1,16,32)", "(8,2,3):(1,16,32)"], ["(2,3,2):(42,1,128)", "12:1"], ["12:1", "(2,3,2):(42,1,128)"],
+          ["(8,3):(1,8)", "(8,3):(3,1)"], ["(8,(3,5)):(1,(57,8))", "(8,15):(1,8)"], ["(64,64):(64,1)", "(64,64):(1,64)"],
+          ["(4,8):(8,1)", "(4,8):(8,1)"], ["(4,8):(1,4)", "32:1"], ["(4,8):(1,8)", "(4,8):(1,8)"], ["(4,8):(1,8)", "(4,8):(1,4)"],
+          ["7:0", "7:1"], ["(4,6):(1,4)", "(4,6):(0,1)"], ["(8192,8192):(8192,1)", "(8192,8192):(1,8192)"]]
+    rng2 = np.random.default_rng(0)
+    shp = [2, 4, 3, 8]
+    for _ in range(60):
+        def build(perm):
+            st_, run = [0] * 4, 1
+            for i in perm:
+                st_[i] = run
+                run *= shp[i]
+            return "(" + ",".join(map(str, shp)) + "):(" + ",".join(map(str, st_)) + ")"
+        mc.append([build(rng2.permutation(4)), build(rng2.permutation(4))])
+    (OUT / "mcv.json").write_text(json.dumps([{"a": a, "b": b, "k": int(ou.ref_op("max_common_vector", a, b)[1])} for a, b in mc]))
+
     lo = []
     for a, t in LOCATE_CASES:
         st, r = ou.ref_op("locate_offsets", a, t)

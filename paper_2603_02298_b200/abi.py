@@ -65,9 +65,11 @@ SYMBOLS = {
                                        C.c_void_p]),
     "tlb_compose_check_range": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(tlb_layout_desc), C.c_uint64,
                                           C.c_uint64, C.c_void_p, C.c_void_p]),
+    "tlb_compose_check": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(tlb_layout_desc), _P(C.c_uint64), C.c_void_p]),
     "tlb_eval_axes_range": (C.c_int, [_P(tlb_mode), C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
     "tlb_copy": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), C.c_uint64, C.c_uint64, C.c_void_p]),
     "tlb_copy_plan": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), C.c_uint64, C.c_uint64]),
+    "tlb_max_common_vector": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(C.c_int64)]),
     "tlb_copy_set_path": (C.c_int, [C.c_int]),
     "tlb_tensormap_from_divided": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p]),

@@ -1215,6 +1215,33 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
 
 extern "C" {
 
+// tla::max_common_vector (analysis.hpp:18-28) from the common refinement: the reference takes the stride-1 identity prefix
+// of coalesce(B o right_inverse(A)), i.e. the longest run of offsets 0 .. K-1 that both layouts reach from the same
+// coordinates. In the refinement that is the chain of modes whose source AND destination strides are 1, e_0, e_0 e_1, ...
+int tlb_max_common_vector(const tlb_layout_desc* a, const tlb_layout_desc* b, int64_t* k) {
+    if (!a || !b || !k) return tlb::fail(TLB_ERR_CONTRACT, "tlb_max_common_vector: null argument");
+    if (a->size != b->size) return tlb::fail(TLB_ERR_CONTRACT, "max_common_vector requires equal sizes");
+    *k = 1; // "any inadmissible step falls back to the always-correct scalar answer 1"
+    if (a->kind != TLB_KIND_INT || b->kind != TLB_KIND_INT) return TLB_OK;
+    std::vector<tlb::JM> modes;
+    if (!tlb::refine_modes(*a, *b, &modes)) return TLB_OK;
+    std::vector<bool> used(modes.size(), false);
+    int64_t K = 1;
+    for (;;) {
+        int hit = -1;
+        for (size_t r = 0; r < modes.size(); ++r)
+            if (!used[r] && modes[r].e > 1 && modes[r].ss == K && modes[r].ds == K) {
+                hit = static_cast<int>(r);
+                break;
+            }
+        if (hit < 0) break;
+        used[hit] = true;
+        K *= modes[hit].e;
+    }
+    *k = K;
+    return TLB_OK;
+}
+
 int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, void* stream) {
     return tlb::copy_impl(src, dst, i_begin, i_end, static_cast<cudaStream_t>(stream));
 }

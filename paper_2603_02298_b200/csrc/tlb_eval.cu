@@ -509,6 +509,27 @@ int tlb_compose_check_range(const tlb_layout_desc* A, const tlb_layout_desc* B, 
     return TLB_OK;
 }
 
+int tlb_compose_check(const tlb_layout_desc* A, const tlb_layout_desc* B, const tlb_layout_desc* R, uint64_t* mismatches,
+                      void* stream) {
+    if (!A || !B || !R || !mismatches) return fail(TLB_ERR_CONTRACT, "tlb_compose_check: null argument");
+    *mismatches = 0;
+    if (B->size != R->size) return fail(TLB_ERR_CONTRACT, "tlb_compose_check: size(B) != size(R)");
+    TLB_TRY(require_device());
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long* d = nullptr;
+    unsigned long long h = 0;
+    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), s));
+    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(h), s);
+    int st = TLB_OK;
+    if (e == cudaSuccess) st = tlb_compose_check_range(A, B, R, 0, static_cast<uint64_t>(B->size), d, stream);
+    if (e == cudaSuccess && st == TLB_OK) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && st == TLB_OK) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(d, s);
+    TLB_CUDA(e);
+    *mismatches = h;
+    return st;
+}
+
 int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t i0, uint64_t n, int64_t* d_out,
                         void* stream) {
     if (!modes || n_modes < 1 || n_modes > TLB_MAX_MODES) return fail(TLB_ERR_CONTRACT, "tlb_eval_axes_range: bad modes");

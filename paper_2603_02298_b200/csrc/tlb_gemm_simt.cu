@@ -273,7 +273,9 @@ bool byte_range(const tlb_tensor& t, int64_t bs, int b0, int b1, uintptr_t* lo, 
     Span sp;
     if (position_span(*t.layout, t.origin, &sp) != TLB_OK) return false;
     const int64_t first = bs * b0, last = bs * (b1 - 1);
-    const int64_t plo = sp.lo + std::min(first, last), phi = sp.hi + std::max(first, last);
+    // the bounds pre-flight has passed: every access lies inside [0, capacity) (Xor spans are OR-bounds, possibly loose)
+    const int64_t plo = std::max<int64_t>(sp.lo + std::min(first, last), 0);
+    const int64_t phi = std::min<int64_t>(sp.hi + std::max(first, last), t.capacity - 1);
     const uintptr_t base = reinterpret_cast<uintptr_t>(t.data);
     *lo = base + static_cast<uintptr_t>(plo) * static_cast<uintptr_t>(t.elem_bytes);
     *hi = base + (static_cast<uintptr_t>(phi) + 1) * static_cast<uintptr_t>(t.elem_bytes);

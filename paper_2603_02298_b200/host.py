@@ -231,6 +231,14 @@ def copy_plan(src_layout, dst_layout, elem_bytes: int, i_begin: int = 0, i_end: 
     return lib.tlb_last_plan().decode()
 
 
+def max_common_vector(a: Layout | str, b: Layout | str) -> int:
+    da = (L(a) if isinstance(a, str) else a).lower()
+    db = (L(b) if isinstance(b, str) else b).lower()
+    k = C.c_int64(0)
+    abi.check(abi.load().tlb_max_common_vector(C.byref(da), C.byref(db), C.byref(k)))
+    return k.value
+
+
 def copy_host(src, dst) -> None:
     abi.check(abi.load().tlb_copy_host(C.byref(src[0]), C.byref(dst[0])))
 

@@ -10,11 +10,13 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <typeinfo>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "tla/tla.hpp"
+#include "helpers.hpp" // proj/tests/helpers.hpp of the reference: slice-coordinate text
 #include "tla/device.hpp"
 
 using namespace tla;
@@ -79,6 +81,46 @@ static void copy_pairs() {
     CHECK(threw);
 }
 
+// Fig. 7 slice rows (test_tensor.cpp:42-60) on DEVICE tensors: slice() of a DeviceTensor is the reference's own slice on
+// the view, so origin and layout must be the goldens of the reference's test, and copying the sliced device view into a
+// compact buffer must give exactly what the reference's slice of the same host tensor holds.
+static SliceCoord SC(const char* s) { return tlatest::SC(s); } // the reference's own test helper (proj/tests/helpers.hpp)
+
+static void fig7_slices_on_device() {
+    Layout full = L("((3,2),((2,3),2)):((4,1),((2,15),100))");
+    auto store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(full)));
+    std::iota(store->begin(), store->end(), 1000);
+    Tensor host(Accessor::buffer(store), full);
+    DevBuf<Int> dbuf(*store);
+    DeviceTensor dev(dbuf.p, Int(dbuf.n), 8, full);
+    struct Row { const char* sc; Int offset; const char* layout; };
+    for (Row row : {Row{"(2,_)", 8, "((2,3),2):((2,15),100)"}, Row{"(_,5)", 32, "(3,2):(4,1)"},
+                    Row{"(2,((0,_),_))", 8, "(3,2):(15,100)"}, Row{"((_,1),(_,0))", 1, "(3,(2,3)):(4,(2,15))"},
+                    Row{"((_,0),((0,_),1))", 100, "(3,3):(4,15)"}, Row{"((1,_),((_,0),_))", 4, "(2,(2,2)):(1,(2,100))"}}) {
+        DeviceTensor ds = slice(dev, SC(row.sc));
+        CHECK(ds.origin() == row.offset);
+        CHECK(format_layout(ds.layout()) == row.layout);
+        Tensor hs = slice(host, SC(row.sc));                                                  // reference
+        Int n = size(hs.layout());
+        Layout compact = Layout(Shape(n), Stride(StrideElem(1)));
+        DevBuf<Int> out(std::vector<Int>(static_cast<size_t>(n), -1));
+        copy(ds, DeviceTensor(out.p, n, 8, compact));                                         // device
+        cudaDeviceSynchronize();
+        std::vector<Int> got = out.get();
+        bool same = true;
+        for (Int i = 0; i < n; ++i) same = same && got[static_cast<size_t>(i)] == hs(i);
+        CHECK(same);
+    }
+    // slicing errors are the reference's own (test_tensor.cpp:80-84)
+    DeviceTensor small(dbuf.p, Int(dbuf.n), 8, L("(4,8):(1,4)"));
+    bool threw = false;
+    try { slice(small, SC("(4,_)")); } catch (const index_error&) { threw = true; }
+    CHECK(threw);
+    threw = false;
+    try { slice(small, SC("(_,_,_)")); } catch (const structural_error&) { threw = true; }
+    CHECK(threw);
+}
+
 // local_tile: slice(Tensor(acc, zipped_divide(L, tiler)), (_, blk)) (partition_demo.cpp) on device:
 // copy tile (3,5) of a 512x512 row-major matrix into a compact tile buffer and compare with the reference copy.
 static void local_tile_copy() {
@@ -87,8 +129,6 @@ static void local_tile_copy() {
     auto store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(full)));
     std::iota(store->begin(), store->end(), 7);
     Tensor whole(Accessor::buffer(store), divided);
-    std::size_t pos = 0;
-    (void)pos;
     std::vector<SliceCoord> blk{fix(3), fix(5)};
     std::vector<SliceCoord> sc{keep(), SliceCoord(blk)};
     Tensor tile = slice(whole, SliceCoord(sc));
@@ -96,10 +136,95 @@ static void local_tile_copy() {
     auto out = std::make_shared<std::vector<Int>>(128 * 64, -1);
     copy(tile, Tensor(Accessor::buffer(out), compact));                                                // reference
     DevBuf<Int> dsrc(*store), ddst(std::vector<Int>(128 * 64, -1));
-    copy(DeviceTensor(dsrc.p, Int(dsrc.n), 8, tile.layout(), tile.accessor().position()),
-         DeviceTensor(ddst.p, 128 * 64, 8, compact));                                                  // device
+    DeviceTensor dtile = local_tile(DeviceTensor(dsrc.p, Int(dsrc.n), 8, full), parse_tiler("[128,64]"), SliceCoord(blk));
+    CHECK(dtile.origin() == tile.accessor().position());
+    CHECK(format_layout(dtile.layout()) == format_layout(tile.layout()));
+    copy(dtile, DeviceTensor(ddst.p, 128 * 64, 8, compact));                                           // device
     cudaDeviceSynchronize();
     CHECK(ddst.get() == *out);
+}
+
+// GEMM on local_tile-sliced operands: C_tile(128 x 256) += A_tile(128 x 64) * B_tile(256 x 64)^T where the three tiles are
+// local_tile views of larger matrices (tile (1,2) of A, (0,2) of B, (1,0) of C); checked against tla::gemm on the same
+// slices of host tensors, cell by cell, for the checked-int64 path and for bf16 on tcgen05 (and with a caller-chosen tiler).
+static void gemm_on_local_tiles() {
+    Layout la = L("(256,256):(256,1)"), lb = L("(512,256):(256,1)"), lc = L("(256,512):(512,1)");
+    auto a = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(la)));
+    auto b = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(lb)));
+    auto c = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(lc)), 2);
+    for (size_t i = 0; i < a->size(); ++i) (*a)[i] = Int(i * 7 + 1) % 11;
+    for (size_t i = 0; i < b->size(); ++i) (*b)[i] = Int(i * 5 + 2) % 13;
+    auto tile_of = [](const std::shared_ptr<std::vector<Int>>& st, const Layout& l, const char* tiler, Int i, Int j) {
+        std::vector<SliceCoord> blk{fix(i), fix(j)};
+        std::vector<SliceCoord> sc{keep(), SliceCoord(blk)};
+        return slice(Tensor(Accessor::buffer(st), zipped_divide(l, parse_tiler(tiler))), SliceCoord(sc));
+    };
+    std::vector<Int> c0 = *c;
+    Tensor ta = tile_of(a, la, "[128,64]", 1, 2), tb = tile_of(b, lb, "[256,64]", 0, 2), tc = tile_of(c, lc, "[128,256]", 1, 0);
+    gemm(ta, tb, tc);                                                                                   // reference
+    auto blk = [](Int i, Int j) { std::vector<SliceCoord> v{fix(i), fix(j)}; return SliceCoord(v); };
+    {
+        DevBuf<Int> da(*a), db(*b), dc(c0);
+        gemm(local_tile(DeviceTensor(da.p, Int(da.n), 8, la), parse_tiler("[128,64]"), blk(1, 2)),
+             local_tile(DeviceTensor(db.p, Int(db.n), 8, lb), parse_tiler("[256,64]"), blk(0, 2)),
+             local_tile(DeviceTensor(dc.p, Int(dc.n), 8, lc), parse_tiler("[128,256]"), blk(1, 0)));
+        CHECK(dc.get() == *c);
+    }
+    std::vector<uint16_t> ha(a->size()), hb(b->size());
+    for (size_t i = 0; i < ha.size(); ++i) ha[i] = to_bf16(float((*a)[i]));
+    for (size_t i = 0; i < hb.size(); ++i) hb[i] = to_bf16(float((*b)[i]));
+    std::vector<float> hc(c0.size());
+    for (size_t i = 0; i < hc.size(); ++i) hc[i] = float(c0[i]);
+    for (int tiled = 0; tiled < 2; ++tiled) {
+        DevBuf<uint16_t> fa(ha), fb(hb);
+        DevBuf<float> fc(hc);
+        DeviceTensor xa = local_tile(DeviceTensor(fa.p, Int(fa.n), 2, la), parse_tiler("[128,64]"), blk(1, 2));
+        DeviceTensor xb = local_tile(DeviceTensor(fb.p, Int(fb.n), 2, lb), parse_tiler("[256,64]"), blk(0, 2));
+        DeviceTensor xc = local_tile(DeviceTensor(fc.p, Int(fc.n), 4, lc), parse_tiler("[128,256]"), blk(1, 0));
+        if (tiled) gemm(xa, xb, xc, tlb_gemm_tiler{128, 128, 64});
+        else gemm(xa, xb, xc);
+        cudaDeviceSynchronize();
+        CHECK(std::string(tlb_last_plan()).rfind("umma", 0) == 0);                                      // tensor cores, not SIMT
+        std::vector<float> got = fc.get();
+        bool same = true;
+        for (size_t i = 0; i < got.size(); ++i) same = same && (Int(got[i]) == (*c)[i]) && (float(Int(got[i])) == got[i]);
+        CHECK(same);
+    }
+}
+
+// compose with the O(size(B)) verification on the device (compose_device) vs tla::compose: same layouts, same exceptions;
+// and config C1's 2^26-element transpose map through the boundary, which costs the reference ~18 s of host loop.
+static void compose_on_device() {
+    struct Row { const char* a; const char* b; };
+    for (Row row : {Row{"(2048,2048):(1,2048)", "(2048,2048):(2048,1)"}, Row{"(4,8):(1,4)", "(2,4):(4,1)"}, Row{"(6,4):(4,1)", "(3,2):(2,9)"},
+                    Row{"((2,2),(4,2)):((1,8),(2,16))", "(4,4):(1,8)"}, Row{"(8,8):(f1,f9)", "(4,2):(2,16)"}, Row{"(4,6):(1,5)", "(2,3):(3,7)"}}) {
+        std::string want, got;
+        try { want = format_layout(compose(L(row.a), L(row.b))); } catch (const error& e) { want = std::string("!") + typeid(e).name(); }
+        try { got = format_layout(compose_device(L(row.a), L(row.b))); } catch (const error& e) { got = std::string("!") + typeid(e).name(); }
+        if (want != got) std::printf("compose(%s, %s): reference %s, device-checked %s\n", row.a, row.b, want.c_str(), got.c_str());
+        CHECK(want == got);
+    }
+    Layout src = L("(8192,8192):(8192,1)"), dst = L("(8192,8192):(1,8192)");
+    Layout r = compose_device(src, right_inverse(dst));                       // src o rinv(dst): SURVEY.md 8(a), config C1
+    CHECK(format_layout(coalesce(r)) == "(8192,8192):(8192,1)");
+}
+
+// locate_offsets (analysis.hpp:40-56) with the admissibility loop on the device vs the reference's own function.
+static void locate_offsets_on_device() {
+    struct Row { const char* a; const char* t; };
+    for (Row row : {Row{"(128,512):(16384,1)", "(1,128):(1,16384)"}, Row{"(4,8):(1,4)", "5:7"}, Row{"(128,256):(65536,1)", "(32,32):(1,65536)"},
+                    Row{"(4,8):(2,8)", "3:3"}, Row{"(4,8):(1,5)", "2:4"}}) {
+        bool ref_ok = true, dev_ok = true;
+        Layout want = L("1:0"), got = L("1:0");
+        try { want = locate_offsets(L(row.a), L(row.t)); } catch (const admissibility_error&) { ref_ok = false; }
+        try { got = locate_offsets_device(L(row.a), L(row.t)); } catch (const admissibility_error&) { dev_ok = false; }
+        CHECK(ref_ok == dev_ok);
+        if (ref_ok && dev_ok) {
+            bool same = true;
+            for (Int i = 0; i < size(L(row.t)); ++i) same = same && eval_int(want, i) == eval_int(got, i);
+            CHECK(same);
+        }
+    }
 }
 
 static void gemm_family(const Layout& la, const Layout& lb, const Layout& lc, bool also_bf16) {
@@ -197,8 +322,12 @@ int main() {
     int ndev = 0;
     CUDA_OK(cudaGetDeviceCount(&ndev));
     copy_pairs();
+    fig7_slices_on_device();
     local_tile_copy();
     gemm_families();
+    gemm_on_local_tiles();
+    locate_offsets_on_device();
+    compose_on_device();
     index_maps();
     if (g_fail) std::printf("dropin: %d check(s) FAILED\n", g_fail);
     else std::printf("dropin: all checks passed (launches=%llu)\n", (unsigned long long)tlb_launch_count());

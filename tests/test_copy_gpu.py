@@ -392,3 +392,28 @@ def test_tensormap_from_divided_fetches_the_tile_the_layout_names():
     torch.cuda.synchronize()
     want = (2 * 262144 + 64 + np.arange(32)[None, :] + 2048 * np.arange(128)[:, None]).astype(np.int32)
     assert (got.cpu().numpy().view(np.int32).reshape(128, 32) == want).all()
+
+
+def test_tma_coordinates_come_from_the_tiled_coordinate_identity():
+    """TMA coordinates are produced from tiled identity tensors. coordinate_identity((96,192)) =
+    (96,192):(e0,e1) (layout.hpp:253); zipped_divide by [32,32] gives ((32,32),(3,6)):((e0,e1),(32*e0,32*e1)), whose rest
+    mode evaluated ON THE DEVICE (tlb_eval_axes_range over the tile index) is the (row, column) where each tile starts.
+    Those per-axis coordinates, reversed to TMA order (dimension 0 = the stride-1 column axis), fetch every tile of the
+    divided layout through the tensor map; each box must hold exactly the cells the divided layout addresses (oracle)."""
+    parent = "(96,192):(192,1)"
+    buf = torch.arange(96 * 192, dtype=torch.int32, device="cuda") * 3 + 1
+    hbuf = buf.cpu().numpy()
+    rest = "(3,6):(32*e0,32*e1)"                                   # rest mode of the divided coordinate identity
+    crd = torch.empty(18, 2, dtype=torch.int64, device="cuda")
+    host.eval_axes_range(rest, 2, 0, 18, crd)
+    torch.cuda.synchronize()
+    coords = crd.cpu().numpy()
+    assert (coords == ou.orc_eval_axes_range(rest, 2, 0, 18)).all()
+    tile = "(32,32):(192,1)"
+    tile_off = ou.orc_eval_range(tile, 0, 32 * 32).reshape(32, 32)   # [col][row]
+    for t in range(18):
+        row0, col0 = int(coords[t, 0]), int(coords[t, 1])
+        got = host.tensormap_fetch(parent, tile, buf, (col0, row0), swizzle=3)
+        torch.cuda.synchronize()
+        want = hbuf[row0 * 192 + col0 + tile_off].T
+        assert (got.cpu().numpy().view(np.int32).reshape(32, 32) == want).all(), t

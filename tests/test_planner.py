@@ -85,3 +85,23 @@ def test_cli_plan_and_exit_codes(capsys):
     assert main(["plan", "8:1", "4:1"]) == 1            # contract_error: sizes differ
     assert main(["plan", "8:1", "(4"]) == 2             # parse error
     assert main(["nonsense"]) == 2                      # usage
+
+
+def test_max_common_vector_matches_the_reference():
+    """tlb_max_common_vector (host only) vs tla::max_common_vector (analysis.hpp:18-28) on the reference's answers for
+    Table-1 pairs, gapped / broadcast layouts, config C1 and 60 random stride permutations (tests/golden/mcv.json)."""
+    import oracle_util as ou
+    from paper_2603_02298_b200 import host
+    rows = ou.golden("mcv.json")
+    assert len(rows) >= 70
+    for row in rows:
+        assert host.max_common_vector(row["a"], row["b"]) == row["k"], (row["a"], row["b"])
+    assert host.max_common_vector("(8192,8192):(8192,1)", "(8192,8192):(1,8192)") == 1      # SURVEY.md 8(a): C1 has no common vector
+
+
+def test_vec_plan_width_is_bounded_by_the_common_vector():
+    """The vec plan moves min(max_common_vector, 16 bytes) cells per access when the common vector starts the layouts."""
+    from paper_2603_02298_b200 import host
+    assert host.max_common_vector("(64,32):(1,64)", "(64,32):(1,128)") == 64
+    assert host.copy_plan("(64,32):(1,64)", "(64,32):(1,128)", 4) == "vec"
+    assert host.max_common_vector("(63,5):(1,63)", "(63,5):(1,64)") == 63
