@@ -140,7 +140,7 @@ __device__ __forceinline__ void decode_unit(const UmmaArgs& a, uint32_t unit, ui
     *n_blk = rem / gm;
 }
 
-template <int CG, int EPI, int BN>
+template <int CG, int EPI, int BN, bool PLAIN>
 __global__ void __launch_bounds__(kUmmaThreads, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const __grid_constant__ UmmaArgs args) {
@@ -158,6 +158,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const uint32_t tmem_slot = bar_base + 8u * (2 * C::kStages + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank_a = PLAIN ? 3 : args.rank_a, rank_b = PLAIN ? 3 : args.rank_b, rank_c = PLAIN ? 3 : args.rank_c;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
     const bool leader = rank == 0;
     const uint32_t n_workers = CG == 2 ? gridDim.x / 2 : gridDim.x;
@@ -227,6 +228,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             const int n0 = n_blk * BN + (CG == 2 ? rank * (BN / 2) : 0);
             const int item = static_cast<int>((w - args.unit_begin) / n_workers);
             if (lane == 0) TLB_TRACE(8 + item * 10 + 0);
+            // row / batch coordinates of this tile's operand boxes: once per tile, k refreshed per k-block
+            int ta[5], tb[5];
+            tile_coords_t<PLAIN>(args.ca, rank_a, false, m0, 0, batch, ta);
+            tile_coords_t<PLAIN>(args.cb, rank_b, false, n0, 0, batch, tb);
             for (int kb = kb0; kb < kb1; ++kb) {
                 // Stages are released in pairs (one commit per 8 MMAs). The MMA thread commits on the LEADER's
                 // barrier only; the leader's producer relays each release to the peer CTA's barrier.
@@ -239,30 +244,28 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
                     } else if constexpr (CG == 1) {
                         mbar_expect_tx(full_bar(stage), C::kStageBytes);
-                        int ta[5], tb[5];
-                        tile_coords(args.ca, args.rank_a, m0, kb * BK, batch, ta);
-                        tile_coords(args.cb, args.rank_b, n0, kb * BK, batch, tb);
+                        tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, ta);
+                        tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tb);
                         if (hint_ab) {
-                            tma_load_tile_hint<false>(a_stage(stage), &map_a, full_bar(stage), args.rank_a, ta, pol_ab);
-                            tma_load_tile_hint<false>(b_stage(stage), &map_b, full_bar(stage), args.rank_b, tb, pol_ab);
+                            tma_load_tile_hint<false>(a_stage(stage), &map_a, full_bar(stage), rank_a, ta, pol_ab);
+                            tma_load_tile_hint<false>(b_stage(stage), &map_b, full_bar(stage), rank_b, tb, pol_ab);
                         } else {
-                            tma_load_tile<false>(a_stage(stage), &map_a, full_bar(stage), args.rank_a, ta);
-                            tma_load_tile<false>(b_stage(stage), &map_b, full_bar(stage), args.rank_b, tb);
+                            tma_load_tile<false>(a_stage(stage), &map_a, full_bar(stage), rank_a, ta);
+                            tma_load_tile<false>(b_stage(stage), &map_b, full_bar(stage), rank_b, tb);
                         }
                     } else {
                         // The leader's barrier expects the bytes of BOTH CTAs; the peer's TMA may complete before
                         // this expect_tx is issued (tx-count goes transiently negative, as with multicast).
                         const uint32_t lbar = lbar0 + 8u * stage;
-                        int ta[5], tb[5];
-                        tile_coords(args.ca, args.rank_a, m0, kb * BK, batch, ta);
-                        tile_coords(args.cb, args.rank_b, n0, kb * BK, batch, tb);
+                        tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, ta);
+                        tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tb);
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
                         if (hint_ab) {
-                            tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, args.rank_a, ta, pol_ab);
-                            tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, args.rank_b, tb, pol_ab);
+                            tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, rank_a, ta, pol_ab);
+                            tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, rank_b, tb, pol_ab);
                         } else {
-                            tma_load_tile<true>(a_stage(stage), &map_a, lbar, args.rank_a, ta);
-                            tma_load_tile<true>(b_stage(stage), &map_b, lbar, args.rank_b, tb);
+                            tma_load_tile<true>(a_stage(stage), &map_a, lbar, rank_a, ta);
+                            tma_load_tile<true>(b_stage(stage), &map_b, lbar, rank_b, tb);
                         }
                     }
                 }
@@ -376,9 +379,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     named_bar(bar_id, 128);
                     if (issuer && !(args.debug & (2u | 8u))) {
                         int tc[5];
-                        tile_coords(args.cc, args.rank_c, m0, nbase + ci * 32, batch, tc);
-                        if (hint_c && args.rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
-                        else tma_reduce_add_tile(&map_c, buf, args.rank_c, tc);
+                        tile_coords_t<PLAIN>(args.cc, rank_c, false, m0, nbase + ci * 32, batch, tc);
+                        if (hint_c && rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
+                        else tma_reduce_add_tile(&map_c, buf, rank_c, tc);
                         bulk_commit();
                     }
                 }
@@ -558,11 +561,14 @@ int pick_epilogue(const UmmaProblem& p) {
 
 template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t stream) {
     using C = Cfg<CG, EPI, BN>;
+    auto* const kern_plain = umma_gemm_kernel<CG, EPI, BN, true>;
+    auto* const kern_any = umma_gemm_kernel<CG, EPI, BN, false>;
     static std::atomic<bool> attr_set[64];   // per device; setting the attribute twice from two threads is harmless
     int dev = 0;
     TLB_CUDA(cudaGetDevice(&dev));
     if (dev >= 0 && dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
-        TLB_CUDA((cudaFuncSetAttribute(umma_gemm_kernel<CG, EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem)));
+        TLB_CUDA((cudaFuncSetAttribute(kern_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem)));
+        TLB_CUDA((cudaFuncSetAttribute(kern_any, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem)));
         attr_set[dev].store(true, std::memory_order_release);
     }
     TmaTileMap ma, mb, mc;
@@ -658,7 +664,9 @@ template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t
         TLB_CUDA(cudaMalloc(reinterpret_cast<void**>(&a.trace), trace_bytes));
         TLB_CUDA(cudaMemset(a.trace, 0, trace_bytes));
     }
-    TLB_CUDA((cudaLaunchKernelEx(&cfg, umma_gemm_kernel<CG, EPI, BN>, tma, tmb, tmc, a)));
+    // plain (unfolded) operands and C: the coordinates of every map are the kernel's loop variables (tile_coords_t)
+    const bool plain = tma_map_is_plain(ma, false) && tma_map_is_plain(mb, false) && (EPI == EPI_REGS || tma_map_is_plain(mc, false));
+    TLB_CUDA((cudaLaunchKernelEx(&cfg, plain ? kern_plain : kern_any, tma, tmb, tmc, a)));
     count_launch();
     static const char* const names[2][2][2] = {{{"umma_1sm_regs", "umma_1sm"}, {"umma_2sm_regs", "umma_2sm"}},
                                                {{"umma_1sm_n128_regs", "umma_1sm_n128"}, {"umma_2sm_n128_regs", "umma_2sm_n128"}}};

@@ -166,6 +166,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
 
 constexpr uint32_t kIdescW = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
 
+// PLAIN (tile_coords_t, tlb_umma_ptx.h): all three tensor maps are rank 3 with identity coordinates (unfolded operands, the
+// common case): the general rank 3..5 decomposition is compiled out of the producer's and the epilogue's loops.
+template <bool PLAIN>
 __global__ void __launch_bounds__(kThreadsW, 1)
 umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_cp,
@@ -187,6 +190,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const bool leader = rank == 0;
     const uint32_t n_workers = gridDim.x / 2, worker = blockIdx.x / 2;
     const int kblocks = (args.K + BK - 1) / BK;
+    const int rank_a = PLAIN ? 3 : args.rank_a, rank_b = PLAIN ? 3 : args.rank_b, rank_c = PLAIN ? 3 : args.rank_c;
     if (threadIdx.x == 0 && args.cta_times) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -244,6 +248,11 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 // this CTA's 256 x 256 cells of C -> L2 (two 128-row boxes), long before the reductions need them
                 tma_prefetch_3d(&map_cp, n0, m0 + lane * BMH, static_cast<int>(batch));
             }
+            // row / batch coordinates of this tile's K-major operand boxes: once per tile, k refreshed per k-block
+            const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
+            int tca[5], tcb[5];
+            if (!args.a_mn) tile_coords_t<PLAIN>(args.ca, rank_a, false, m0, 0, batch, tca);
+            if (!args.b_mn) tile_coords_t<PLAIN>(args.cb, rank_b, false, nb0, 0, batch, tcb);
             for (int kb = it.kb0; kb < it.kb1; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1u, 64);
                 if (elect_one()) {
@@ -253,30 +262,29 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     } else {
                         const uint32_t lbar = lbar0 + 8u * stage;
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * kStageBytes);
-                        const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
                         int tc[5];
                         if (!args.a_mn) {
                             // K-major A: one box of 256 rows x 64 k (rows of 128 B)
-                            tile_coords(args.ca, args.rank_a, m0, kb * BK, batch, tc);
-                            if (args.hints & 1u) tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, args.rank_a, tc, pol_ab);
-                            else tma_load_tile<true>(a_stage(stage), &map_a, lbar, args.rank_a, tc);
+                            tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, tca);
+                            if (args.hints & 1u) tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, rank_a, tca, pol_ab);
+                            else tma_load_tile<true>(a_stage(stage), &map_a, lbar, rank_a, tca);
                         } else {
                             // MN-major A: four chunks of 64 rows, each [64 k][64 m] (the map's dimension 0 is m)
 #pragma unroll
                             for (int c = 0; c < BMC / 64; ++c) {
-                                tile_coords(args.ca, args.rank_a, m0 + c * 64, kb * BK, batch, tc);
-                                tma_load_tile<true>(a_stage(stage) + c * 8192, &map_a, lbar, args.rank_a, tc);
+                                tile_coords_t<PLAIN>(args.ca, rank_a, true, m0 + c * 64, kb * BK, batch, tc);
+                                tma_load_tile<true>(a_stage(stage) + c * 8192, &map_a, lbar, rank_a, tc);
                             }
                         }
                         if (!args.b_mn) {
-                            tile_coords(args.cb, args.rank_b, nb0, kb * BK, batch, tc);
-                            if (args.hints & 1u) tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, args.rank_b, tc, pol_ab);
-                            else tma_load_tile<true>(b_stage(stage), &map_b, lbar, args.rank_b, tc);
+                            tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tcb);
+                            if (args.hints & 1u) tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, rank_b, tcb, pol_ab);
+                            else tma_load_tile<true>(b_stage(stage), &map_b, lbar, rank_b, tcb);
                         } else {
 #pragma unroll
                             for (int c = 0; c < BN / 2 / 64; ++c) {
-                                tile_coords(args.cb, args.rank_b, nb0 + c * 64, kb * BK, batch, tc);
-                                tma_load_tile<true>(b_stage(stage) + c * 8192, &map_b, lbar, args.rank_b, tc);
+                                tile_coords_t<PLAIN>(args.cb, rank_b, true, nb0 + c * 64, kb * BK, batch, tc);
+                                tma_load_tile<true>(b_stage(stage) + c * 8192, &map_b, lbar, rank_b, tc);
                             }
                         }
                     }
@@ -419,8 +427,8 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         __syncwarp();
                         if (lane == 0) {
                             int tc[5];
-                            tile_coords(args.cc, args.rank_c, m0 + h * BMH, n0 + ci * 64, batch, tc);
-                            tma_reduce_add_tile(&map_c, buf, args.rank_c, tc);
+                            tile_coords_t<PLAIN>(args.cc, rank_c, false, m0 + h * BMH, n0 + ci * 64, batch, tc);
+                            tma_reduce_add_tile(&map_c, buf, rank_c, tc);
                             bulk_commit();
                         }
                     }
@@ -458,14 +466,14 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         if (et) et[3] = clock64();
                         if (lane == 0 && !(args.debug & 8u)) {
                             int tc[5];
-                            tile_coords(args.cc, args.rank_c, m0 + h * BMH, n0 + ci * 32, batch, tc);
-                            if ((args.debug & 4u) && args.rank_c == 3)  // timing experiment: plain store instead of the L2 reduction
+                            tile_coords_t<PLAIN>(args.cc, rank_c, false, m0 + h * BMH, n0 + ci * 32, batch, tc);
+                            if ((args.debug & 4u) && rank_c == 3)  // timing experiment: plain store instead of the L2 reduction
                                 asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&map_c),
                                              "r"(buf), "r"(tc[0]), "r"(tc[1]), "r"(tc[2]) : "memory");
-                            else if ((args.hints & 2u) && args.rank_c == 3)
+                            else if ((args.hints & 2u) && rank_c == 3)
                                 tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
                             else
-                                tma_reduce_add_tile(&map_c, buf, args.rank_c, tc);
+                                tma_reduce_add_tile(&map_c, buf, rank_c, tc);
                             bulk_commit();
                             if (et) et[4] = clock64();
                         }
@@ -604,7 +612,8 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     int dev = 0;
     TLB_CUDA(cudaGetDevice(&dev));
     if (dev >= 0 && dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
-        TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
+        TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
+        TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
         attr_set[dev].store(true, std::memory_order_release);
     }
     // tensor maps = the divided layouts: zipped_divide(A, [256, 64]), zipped_divide(B, [128, 64]) (64 x 64 chunks for
@@ -691,7 +700,10 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     std::memcpy(&tmb, mb.desc, 128);
     std::memcpy(&tmc, mc.desc, 128);
     std::memcpy(&tmcp, mcp.desc, 128);
-    TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel, tma, tmb, tmc, tmcp, a));
+    // plain (unfolded) operands and C: the coordinates of every map are the kernel's loop variables
+    const bool plain = tma_map_is_plain(ma, p.a_mn != 0) && tma_map_is_plain(mb, p.b_mn != 0) && tma_map_is_plain(mc, false);
+    if (plain) TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<true>, tma, tmb, tmc, tmcp, a));
+    else TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<false>, tma, tmb, tmc, tmcp, a));
     count_launch();
     set_plan("umma_2sm_wide");
     return TLB_OK;

@@ -211,9 +211,9 @@ int tile_dims_derive(const tlb_layout_desc& L, int inner_top, int outer_top, int
             dims[rank] = static_cast<uint64_t>(e[j]);
             strides[rank] = static_cast<uint64_t>(st[j]);
             box[rank] = static_cast<uint32_t>(b);
-            cc[rank].src = static_cast<uint32_t>(pass == 0 ? inner_src : outer_src);
-            cc[rank].div = static_cast<uint32_t>(prefix);
-            cc[rank].mod = last ? 0u : static_cast<uint32_t>(e[j]);
+            if (prefix >= (1ull << 31)) return fail(TLB_ERR_UNSUPPORTED, "tensor map: mode extent exceeds 2^31");
+            cc[rank] = tma_coord(static_cast<uint32_t>(pass == 0 ? inner_src : outer_src), static_cast<uint32_t>(prefix),
+                                 last ? 0u : static_cast<uint32_t>(e[j]));
             prefix *= static_cast<uint64_t>(e[j]);
             ++rank;
         }
@@ -229,14 +229,14 @@ int tile_dims_derive(const tlb_layout_desc& L, int inner_top, int outer_top, int
         strides[rank] = (span + align - 1) / align * align;
     }
     box[rank] = 1;
-    cc[rank] = {2u, 1u, 0u};
+    cc[rank] = tma_coord(2u, 1u, 0u);
     ++rank;
     out->rank = rank;
     for (int d = rank; d < 5; ++d) {
         dims[d] = 1;
         strides[d] = 0;
         box[d] = 1;
-        cc[d] = TmaCoord{2u, 1u, 0u};
+        cc[d] = tma_coord(2u, 1u, 0u);
     }
     return TLB_OK;
 }
