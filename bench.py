@@ -671,7 +671,13 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
                     "(4096,4096):(1,4096)", "GETT: 4096^3 with m, n and k each folded into two leaves (rank-5 tensor maps), TN output", K,
                     "umma_wide_kernel")
         gemm_family("Cg_blis_strided", "(2048,2048):(3,6151)", "(2048,2048):(2,4099)", "(2048,2048):(5,10243)",
-                    "BLIS: 2048^3 with general strides on every mode (no unit stride anywhere)", max(3, K // 8), "gemm_simt_tiled_kernel")
+                    "BLIS: 2048^3 with general strides on every mode (no unit stride anywhere): packed by tlb_copy, tcgen05 on the "
+                    "packed panels, C scattered back (the step times all five kernels)", max(3, K // 2), "copy kernels + umma_gemm_kernel")
+        # CONV: fprop as a GEMM whose A is the im2col LAYOUT of the NHWC activations (no im2col buffer):
+        # rows (q, p, n), k (c, s, r); 32 x 34 x 34 x 128 input, 3 x 3 filters, 1024 output channels
+        gemm_family("Cg_conv_im2col", "((32,32,32),(128,3,3)):((128,4352,147968),(1,128,4352))", "(1024,1152):(1152,1)",
+                    "(32768,1024):(1024,1)", "CONV fprop: 32x34x34x128 NHWC input, 3x3 filters, 1024 output channels, as a GEMM over the "
+                    "im2col layout of the input (rank-5 tensor map: leaves q, p, n | c s, r), M 32768, N 1024, K 1152", K, "umma_wide_kernel")
     # C4: batched bf16 GEMM 64 x 8192^3, sharded by whole batches (= tile-id ranges) across the ranks (strong
     # scaling of the 64 batches; every rank owns its batches' operands, no data-path collective)
     if want("C4"):

@@ -445,11 +445,12 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
 // ---------------------------------------------------------------------------------------
 // tiled, TMA-fed: phase 1 is a cp.async.bulk.tensor load through a tensor map derived from the source layout
 // (tlb_tensormap_describe: parent = the source's refined modes, tile = the A and B runs) with the hardware
-// 128-byte swizzle, which is the staging layout phase 2 already expects. Each CTA walks kTmaTilesPerCta
-// consecutive tiles through a ring of kTmaStages staged tiles, so loads run several tiles ahead of the stores.
+// 128-byte swizzle, which is the staging layout phase 2 already expects. PERSISTENT: a few CTAs per SM, CTA c walks the
+// tiles c, c + grid, c + 2 grid, ... through a ring of staged tiles, so loads run `stages` tiles ahead of the stores and
+// the CTAs that run together read NEIGHBOURING tiles (consecutive tile ids are adjacent 128-byte pieces of the same
+// source rows: walking consecutive tiles inside one CTA instead touches every DRAM page at eight different times).
 // ---------------------------------------------------------------------------------------
-constexpr int kTmaStages = 4;
-constexpr int kTmaTilesPerCta = 8;
+constexpr int kTmaMaxStages = 8;
 
 struct TmaTileParams {
     TileParams t;
@@ -477,22 +478,22 @@ __device__ __forceinline__ void tma_issue_tile(const CUtensorMap* map, uint32_t 
 
 template <int EB, int LB>
 __global__ void __launch_bounds__(kThreads)
-tiled_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ TmaTileParams P, char* __restrict__ dst) {
+tiled_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ TmaTileParams P, char* __restrict__ dst, int stages) {
     constexpr int LA = 128 / EB;
     constexpr uint32_t kTileBytes = LB * 128;
     extern __shared__ unsigned char smem_dyn[];
     __shared__ int64_t s_offA[LA];
-    __shared__ int64_t s_base_d[kTmaStages];
-    __shared__ __align__(8) unsigned long long s_bar[kTmaStages];
+    __shared__ int64_t s_base_d[kTmaMaxStages];
+    __shared__ __align__(8) unsigned long long s_bar[kTmaMaxStages];
     const uint32_t smem0 = (static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn)) + 1023u) & ~1023u;
     unsigned char* tiles = smem_dyn + (smem0 - static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn)));
-    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kTmaTilesPerCta;
-    const int count = static_cast<int>(min(static_cast<uint64_t>(kTmaTilesPerCta), P.t.n_tiles - t0));
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    const int count = first < P.t.n_tiles ? static_cast<int>((P.t.n_tiles - first + step - 1) / step) : 0;
 
-    auto issue = [&](int i) { // thread 0 only: tile t0 + i -> stage i % kTmaStages
-        const int stage = i % kTmaStages;
+    auto issue = [&](int i) { // thread 0 only: tile first + i * step -> stage i % stages
+        const int stage = i % stages;
         int64_t base_s, base_d;
-        dev_joint(P.t.rest, t0 + i, &base_s, &base_d);
+        dev_joint(P.t.rest, first + static_cast<uint64_t>(i) * step, &base_s, &base_d);
         s_base_d[stage] = base_d;
         int c[5];
         int64_t off = base_s;
@@ -508,10 +509,9 @@ tiled_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant_
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTmaStages; ++s)
+        for (int s = 0; s < stages; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[s]))) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < min(count, kTmaStages); ++i) issue(i);
     }
     for (int t = threadIdx.x; t < LA; t += kThreads) {
         uint32_t i = t;
@@ -524,11 +524,15 @@ tiled_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant_
         }
         s_offA[t] = acc;
     }
+    // everything above overlaps the previous kernel's tail; no global access before this point
+    pdl_wait();
+    if (threadIdx.x == 0)
+        for (int i = 0; i < min(count, stages); ++i) issue(i);
     __syncthreads();
 
     for (int i = 0; i < count; ++i) {
-        const int stage = i % kTmaStages;
-        const uint32_t parity = (i / kTmaStages) & 1;
+        const int stage = i % stages;
+        const uint32_t parity = (i / stages) & 1;
         const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[stage]));
         const long long t_start = clock64();
         for (;;) {
@@ -539,7 +543,7 @@ tiled_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant_
         }
         tile_phase2<EB, LB>(tiles + stage * kTileBytes, s_offA, dst, s_base_d[stage]);
         __syncthreads(); // every lane is done reading this stage
-        if (threadIdx.x == 0 && i + kTmaStages < count) issue(i + kTmaStages);
+        if (threadIdx.x == 0 && i + stages < count) issue(i + stages);
     }
 }
 
@@ -1016,12 +1020,17 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
                     for (int d2 = 0; d2 < 5; ++d2) TP.dim_stride[d2] = d2 < rank ? static_cast<int64_t>(strides[d2]) : 1;
                     CUtensorMap map;
                     std::memcpy(&map, mapbytes, 128);
-                    const unsigned grid_tma = static_cast<unsigned>((tiles + kTmaTilesPerCta - 1) / kTmaTilesPerCta);
-                    const size_t smem = static_cast<size_t>(kTmaStages) * Lb * 128 + 1024;
+                    // persistent grid: ctas CTAs per SM (as many as the ring's shared memory lets co-reside), tiles dealt round-robin
+                    int stages = std::max(2, std::min(kTmaMaxStages, knob(K_COPY_TMA_STAGES)));
+                    while (stages > 2 && static_cast<size_t>(stages) * Lb * 128 + 2048 > 227u * 1024u) --stages;
+                    const size_t smem = static_cast<size_t>(stages) * Lb * 128 + 1024;
+                    const int fit = std::max(1, static_cast<int>((227u * 1024u) / (smem + 1024)));
+                    const int ctas = std::max(1, std::min(fit, knob(K_COPY_TMA_CTAS)));
+                    const unsigned grid_tma = static_cast<unsigned>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * ctas));
 #define TLB_TILED_TMA(EB, LB)                                                                                          \
     do {                                                                                                               \
         TLB_CUDA(cudaFuncSetAttribute(tiled_tma_kernel<EB, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
-        tiled_tma_kernel<EB, LB><<<grid_tma, kThreads, smem, c.stream>>>(map, TP, db);                                 \
+        TLB_CUDA(launch_pdl(tiled_tma_kernel<EB, LB>, dim3(grid_tma), dim3(kThreads), smem, c.stream, map, TP, db, stages)); \
     } while (0)
                     if (eb == 4) {
                         if (Lb == 256) TLB_TILED_TMA(4, 256); else if (Lb == 128) TLB_TILED_TMA(4, 128); else if (Lb == 64) TLB_TILED_TMA(4, 64); else TLB_TILED_TMA(4, 32);

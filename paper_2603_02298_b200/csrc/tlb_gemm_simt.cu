@@ -10,7 +10,9 @@
 // (bf16 x bf16 is exact in fp32, hence fma(a, b, acc) == acc + a*b).
 #include <algorithm>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include <cuda_bf16.h>
@@ -374,7 +376,60 @@ UmmaFit fit_umma(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
 
 int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool i64, int64_t a_bs, int64_t b_bs,
              int64_t c_bs, int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, int* d_status,
-             cudaStream_t stream, uint32_t* count_only = nullptr, bool f16 = false) {
+             cudaStream_t stream, uint32_t* count_only = nullptr, bool f16 = false);
+
+// ---- packed plan ------------------------------------------------------------------------------------------------
+// Operands or a C that no tensor map can address (BLIS-style general strides on every mode, test_tensor.cpp:187 and
+// PAPER.md:1769; Xor strides; leading dimensions that are not multiples of 16 bytes) still run on the tensor cores: the
+// layout-driven copy (tlb_copy, any layout pair) PACKS A and B into K-major panels and C into an n-contiguous fp32 (or
+// 2-byte) tile buffer, the tcgen05 plan runs on the packed tensors, and the copy scatters C back through its layout.
+// This is BLIS's own recipe (pack, then a fixed-layout micro-kernel) with the packing expressed as tla::copy between two
+// layouts. C += A B^T is preserved (packed C starts as a copy of C); the workspace lives on the stream
+// (cudaMallocAsync / cudaFreeAsync). Copies cost O(MK + NK + MN) against O(MNK) of math: 2048^3 with no unit stride
+// anywhere ran at 7 TFLOP/s on the SIMT plan.
+thread_local bool g_in_packed = false;
+thread_local std::string g_packed_plan;
+
+int lower_rowmajor(int64_t rows, int64_t cols, int64_t ld, tlb_layout_desc* out) {
+    const tlb_mode m[2] = {{rows, ld, TLB_KIND_INT, 0}, {cols, 1, TLB_KIND_INT, 0}};
+    const int32_t tops[2] = {1, 1};
+    return tlb_layout_lower_ranked(m, 2, tops, 2, out);
+}
+
+int run_packed(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, const GemmDims& d, bool f16, cudaStream_t stream) {
+    const int cb = C->elem_bytes;
+    const int64_t Kp = (d.K + 7) / 8 * 8, Np = (d.N + 16 / cb - 1) / (16 / cb) * (16 / cb); // 16-byte rows
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t bytes_a = up(static_cast<size_t>(d.M) * Kp * 2), bytes_b = up(static_cast<size_t>(d.N) * Kp * 2),
+                 bytes_c = up(static_cast<size_t>(d.M) * Np * cb);
+    tlb_layout_desc la, lb, lc;
+    TLB_TRY(lower_rowmajor(d.M, d.K, Kp, &la));
+    TLB_TRY(lower_rowmajor(d.N, d.K, Kp, &lb));
+    TLB_TRY(lower_rowmajor(d.M, d.N, Np, &lc));
+    char* ws = nullptr;
+    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes_a + bytes_b + bytes_c, stream));
+    const tlb_tensor pa{&la, ws, 0, d.M * Kp, 2, TLB_ACC_BUFFER}, pb{&lb, ws + bytes_a, 0, d.N * Kp, 2, TLB_ACC_BUFFER},
+        pc{&lc, ws + bytes_a + bytes_b, 0, d.M * Np, cb, TLB_ACC_BUFFER};
+    int st = tlb_copy(A, &pa, 0, static_cast<uint64_t>(d.M) * d.K, stream);
+    if (st == TLB_OK) st = tlb_copy(B, &pb, 0, static_cast<uint64_t>(d.N) * d.K, stream);
+    if (st == TLB_OK) st = tlb_copy(C, &pc, 0, static_cast<uint64_t>(d.M) * d.N, stream);
+    if (st == TLB_OK) {
+        g_in_packed = true;
+        st = run_gemm(&pa, &pb, &pc, false, 0, 0, 0, 0, 1, 0, UINT32_MAX, nullptr, stream, nullptr, f16);
+        g_in_packed = false;
+    }
+    if (st == TLB_OK) {
+        g_packed_plan = std::string("packed+") + tlb_last_plan();
+        st = tlb_copy(&pc, C, 0, static_cast<uint64_t>(d.M) * d.N, stream);
+    }
+    cudaFreeAsync(ws, stream);
+    if (st == TLB_OK) set_plan(g_packed_plan.c_str());
+    return st;
+}
+
+int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool i64, int64_t a_bs, int64_t b_bs,
+             int64_t c_bs, int batch_begin, int batch_end, uint32_t tile_begin, uint32_t tile_end, int* d_status,
+             cudaStream_t stream, uint32_t* count_only, bool f16) {
     GemmDims d;
     TLB_TRY(check_gemm(A, B, C, i64 ? 8 : 2, i64 ? 8 : 4, &d));
     if (batch_begin < 0 || batch_end < batch_begin) return fail(TLB_ERR_CONTRACT, "tlb_gemm: bad batch range");
@@ -456,9 +511,14 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
         }
     }
 
-    // ---- SIMT plan
     if (!(C->layout->flags & TLB_LF_INJECTIVE))
         return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: C must be injective (aliased accumulators are order-dependent)");
+    // ---- packed plan: whole single problems that are large enough for three packing copies and one scatter to pay
+    if (!i64 && g_gemm_path == 0 && !g_in_packed && !g_tiler && knob(K_GEMM_PACK) != 0 && batch_begin == 0 && batch_end == 1 &&
+        tile_begin == 0 && tile_end == UINT32_MAX && A->accessor == TLB_ACC_BUFFER && B->accessor == TLB_ACC_BUFFER &&
+        static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K) >= std::ldexp(1.0, knob(K_GEMM_PACK_MIN)))
+        return run_packed(A, B, C, d, f16, stream);
+    // ---- SIMT plan
     SimtArgs p;
     std::memset(&p, 0, sizeof(p));
     p.a_origin = A->origin;

@@ -58,6 +58,10 @@ enum KnobId {
     K_EVAL_NO_WARP,
     K_HOST_PIPELINE,
     K_HOST_PANEL,
+    K_COPY_TMA_STAGES,  // staged tiles per CTA of the TMA-fed tiled copy
+    K_COPY_TMA_CTAS,    // its CTAs per SM
+    K_GEMM_PACK,        // 1: operands / C that no tensor map can address are packed and run on tcgen05 (default), 0: SIMT plan
+    K_GEMM_PACK_MIN,    // log2 of the smallest M*N*K that takes the packed plan
     K_COUNT
 };
 int knob(KnobId id);

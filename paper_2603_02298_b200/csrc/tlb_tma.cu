@@ -187,7 +187,9 @@ int tile_dims_derive(const tlb_layout_desc& L, int inner_top, int outer_top, int
         int64_t t = pass == 0 ? box_inner : box_outer;
         uint64_t prefix = 1;
         for (int j = 0; j < n; ++j) {
-            if (rank == 4) return fail(TLB_ERR_UNSUPPORTED, "tensor map: layout needs more than 5 TMA dimensions");
+            // five dimensions in all: a single problem may spend the batch dimension on a fifth leaf (im2col operands:
+            // three row leaves (q, p, n) and two k leaves (c s, r))
+            if (rank == (batch > 1 ? 4 : 5)) return fail(TLB_ERR_UNSUPPORTED, "tensor map: layout needs more than 5 TMA dimensions");
             if (st[j] <= 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: strides must be positive");
             if (!(pass == 0 && j == 0) && (st[j] % align != 0 && e[j] > 1))
                 return fail(TLB_ERR_UNSUPPORTED, "tensor map: strides must be multiples of 16 bytes");
@@ -218,7 +220,11 @@ int tile_dims_derive(const tlb_layout_desc& L, int inner_top, int outer_top, int
             ++rank;
         }
     }
-    // batch: the last dimension (a unit dimension for a single problem)
+    // batch: the last dimension (a unit dimension for a single problem, dropped when the leaves need all five)
+    if (rank == 5) {
+        out->rank = rank;
+        return TLB_OK;
+    }
     dims[rank] = static_cast<uint64_t>(std::max(batch, 1));
     if (batch > 1) {
         if (batch_stride <= 0 || batch_stride % align != 0) return fail(TLB_ERR_UNSUPPORTED, "tensor map: batch stride must be a positive multiple of 16 bytes");

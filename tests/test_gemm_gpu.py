@@ -686,3 +686,56 @@ def test_gemm_simt_tiled_plan_is_exact_on_strided_families(shape):
     assert _bf16_case(*shape, kat=True).startswith("simt")
     assert _bf16_case(*shape, kat=False, seed=31).startswith("simt")
     assert _bf16_case(*shape, kat=False, seed=37, f16=True).startswith("simt")
+
+
+PACKED_SHAPES = [
+    ("(512,256):(3,1549)", "(384,256):(2,771)", "(512,384):(5,2563)"),                       # BLIS: no unit stride anywhere
+    ("((2,256),256):((1,512),2)", "(384,256):(256,1)", "((2,256),384):((1,2),512)"),           # GETT row with k stride 2
+    ("(300,200):(f1,f512)", "(100,200):(200,1)", "(300,100):(1,300)"),                       # Xor-strided operand
+    ("(333,77):(77,1)", "(129,77):(1,129)", "(333,129):(129,1)"),                            # unaligned leading dimensions
+    ("(4,8):(3,13)", "(6,8):(2,17)", "(4,6):(5,23)"),                                        # test_tensor.cpp:187 verbatim
+]
+
+
+@pytest.mark.parametrize("shape", PACKED_SHAPES)
+def test_gemm_packed_plan_runs_unaddressable_layouts_on_tensor_cores(shape, tlb_config):
+    """Layouts no tensor map can address take the packed plan once the problem is large enough: tlb_copy packs A, B
+    (K-major) and C (n-contiguous), the tcgen05 plan runs on the packed tensors, tlb_copy scatters C back. Forced here
+    on small shapes (GEMM_PACK_MIN = 0) so the oracle stays cheap: exact on the reference's integer fills, within the
+    GEMM tolerance on random data, C += semantics kept (c_init)."""
+    tlb_config("GEMM_PACK_MIN", "0")
+    assert _bf16_case(*shape, kat=True).startswith("packed+umma")
+    assert _bf16_case(*shape, kat=False, seed=41).startswith("packed+umma")
+    assert _bf16_case(*shape, kat=False, seed=43, f16=True).startswith("packed+umma")
+    tlb_config("GEMM_PACK", "0")
+    assert _bf16_case(*shape, kat=True).startswith("simt")
+
+
+def test_gemm_packed_plan_default_threshold_and_size():
+    """Default knobs: a 1024 x 768 x 512 BLIS-strided problem (2^28.6 MACs) is packed; partial tile ranges and the
+    forced SIMT path are not. C cells outside the layout's image stay untouched (cosize > size)."""
+    shape = ("(1024,512):(3,3079)", "(768,512):(2,1543)", "(1024,768):(5,5123)")
+    assert _bf16_case(*shape, kat=True) == "packed+umma_2sm_wide" or _bf16_case(*shape, kat=True).startswith("packed+umma")
+    assert _bf16_case(*shape, kat=True, path=1).startswith("simt")
+    tiles = _tile_count(*shape)
+    assert _bf16_case(*shape, kat=True, tile_ranges=[(0, 2), (2, tiles)]).startswith("simt")
+
+
+def _im2col(n, h, w, c, r, s, kout):
+    """NHWC activations, stride 1, no padding: A = ((Q,P,N),(C,S,R)) over the input buffer, B = filters (Kout, C S R),
+    C = NHWC output. A is non-injective (windows overlap): it is only read."""
+    p, q = h - r + 1, w - s + 1
+    la = f"(({q},{p},{n}),({c},{s},{r})):(({c},{w * c},{h * w * c}),(1,{c},{w * c}))"
+    lb = f"({kout},{c * s * r}):({c * s * r},1)"
+    lc = f"({q * p * n},{kout}):({kout},1)"
+    return la, lb, lc
+
+
+@pytest.mark.parametrize("dims", [(2, 18, 18, 64, 3, 3, 128), (1, 34, 34, 64, 3, 3, 256), (4, 10, 18, 64, 3, 3, 64)])
+def test_gemm_conv_im2col_layout_on_tensor_cores(dims):
+    """CONV row of the paper's GEMM table: fprop as C(m, kout) += A(m, k) B(kout, k) with A the im2col
+    LAYOUT of the input (five leaves -> a rank-5 tensor map without a batch dimension), no im2col buffer is materialised.
+    Exact on the reference's integer fills against the oracle's evaluation of the same layouts."""
+    shape = _im2col(*dims)
+    assert _bf16_case(*shape, kat=True).startswith("umma_")
+    assert _bf16_case(*shape, kat=False, seed=47).startswith("umma_")

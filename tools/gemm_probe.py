@@ -15,12 +15,13 @@ import os
 lib = abi.load()
 sets = []
 nsets = int(os.environ.get('PROBE_SETS', 3 if batch == 1 else 1))
+LD = int(os.environ.get('PROBE_LD', K))  # leading dimension of A and B (elements); > K pads the rows
 for s in range(nsets):
-    a = torch.empty(batch * M * K, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
-    b = torch.empty(batch * N * K, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+    a = torch.empty(batch * M * LD, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+    b = torch.empty(batch * N * LD, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
     c = torch.zeros(batch * M * N, dtype=torch.bfloat16 if os.environ.get('PROBE_C16') else torch.float32, device="cuda")
-    sets.append((host.tensor_of(f"({M},{K}):({K},1)", a.view(torch.int16), ranked=True),
-                 host.tensor_of(f"({N},{K}):({K},1)", b.view(torch.int16), ranked=True),
+    sets.append((host.tensor_of(f"({M},{K}):({LD},1)", a.view(torch.int16), ranked=True),
+                 host.tensor_of(f"({N},{K}):({LD},1)", b.view(torch.int16), ranked=True),
                  host.tensor_of(f"({M},{N}):(1,{M})", c.view(torch.int16) if c.dtype == torch.bfloat16 else c, ranked=True)))
 
 
@@ -29,7 +30,7 @@ def step(i):
     if batch == 1:
         host.gemm_bf16(ta, tb, tc)
     else:
-        host.gemm_bf16_batched(ta, tb, tc, M * K, N * K, M * N, 0, batch)
+        host.gemm_bf16_batched(ta, tb, tc, M * LD, N * LD, M * N, 0, batch)
 
 
 import subprocess, threading, time
