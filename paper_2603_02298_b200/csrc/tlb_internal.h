@@ -60,6 +60,7 @@ enum KnobId {
     K_HOST_PANEL,
     K_COPY_TMA_STAGES,  // staged tiles per CTA of the TMA-fed tiled copy
     K_COPY_TMA_CTAS,    // its CTAs per SM
+    K_GEMM_CHUNK_WAVES, // waves of pair tiles per launch of the wide plan (0: one launch whatever the range)
     K_GEMM_PACK,        // 1: operands / C that no tensor map can address are packed and run on tcgen05 (default), 0: SIMT plan
     K_GEMM_PACK_MIN,    // log2 of the smallest M*N*K that takes the packed plan
     K_COUNT

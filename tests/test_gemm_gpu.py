@@ -739,3 +739,35 @@ def test_gemm_conv_im2col_layout_on_tensor_cores(dims):
     shape = _im2col(*dims)
     assert _bf16_case(*shape, kat=True).startswith("umma_")
     assert _bf16_case(*shape, kat=False, seed=47).startswith("umma_")
+
+
+def test_gemm_wide_plan_chunked_launches_are_exact(tlb_config):
+    """Long tile ranges are cut into several launches of a few waves each (the workers of a persistent launch drift apart
+    and stop sharing operand panels in L2: DESIGN.md 3.3). Forced here with one wave per launch on a 5-batch problem whose
+    launch boundaries fall inside batches: same exact result as one launch, more launches counted."""
+    M, N, K, B = 2048, 2048, 256, 5
+    i = torch.arange(M, device="cuda").view(M, 1)
+    p = torch.arange(K, device="cuda").view(1, K)
+    a1 = ((i * 7 + p * 3 + 1) % 11).to(torch.bfloat16)
+    b1 = ((i * 5 + p * 2 + 2) % 13).to(torch.bfloat16)
+    a = torch.stack([a1.roll(bi, 0) for bi in range(B)]).contiguous()
+    b = torch.stack([b1.roll(-bi, 0) for bi in range(B)]).contiguous()
+    ta = host.make_tensor(L(f"({M},{K}):({K},1)").lower(ranked=True), a.data_ptr(), a.numel(), 2)
+    tb = host.make_tensor(L(f"({N},{K}):({K},1)").lower(ranked=True), b.data_ptr(), b.numel(), 2)
+    lib = abi.load()
+    tlb_config("GEMM_WIDE", "1")
+    results, launches = [], []
+    for waves in ("0", "1"):
+        tlb_config("GEMM_CHUNK_WAVES", waves)
+        c = torch.ones(B, N, M, dtype=torch.float32, device="cuda")
+        tc = host.make_tensor(L(f"({M},{N}):(1,{M})").lower(ranked=True), c.data_ptr(), c.numel(), 4)
+        n0 = lib.tlb_launch_count()
+        assert host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 0, B) == "umma_2sm_wide"
+        torch.cuda.synchronize()
+        launches.append(int(lib.tlb_launch_count() - n0))
+        results.append(c)
+    assert launches[0] == 1 and launches[1] >= 2
+    for bi in range(B):
+        ref = (a[bi].double() @ b[bi].double().t()).t() + 1.0
+        assert torch.equal(results[0][bi].double(), ref)
+        assert torch.equal(results[1][bi].double(), ref)

@@ -1,18 +1,14 @@
 #!/bin/bash
-# Scratch: DRAM / L2 traffic of the wide GEMM at 8192^3 against cuBLAS, for padded leading dimensions and rasterisation groups.
-M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,lts__t_sectors_srcunit_tex.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"
+# Scratch: DRAM traffic per batch of the batched wide GEMM as the launch gets longer (worker drift?), and throughput at equal total work.
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct"
 show() { echo "$1: $(grep -E 'dram__bytes_read|dram__bytes_write|gpu__time|hit_rate|tensor' $2 | awk -F'","' '{printf "%s=%s%s ", $(NF-2), $NF, $(NF-1)}' | tr -d '"\n')"; }
-ncu --metrics $M --clock-control none -k regex:'gemm|nvjet|cutlass|sm100' -s 3 -c 1 --csv --log-file gpurun_out/nt_cublas.csv python tools/cublas_point.py 8192 3 > /dev/null 2>&1
-show cublas gpurun_out/nt_cublas.csv
-for ld in 8192 8256 8320; do
-  PROBE_LD=$ld ncu --metrics $M --clock-control none -k regex:umma_ -s 3 -c 1 --csv --log-file gpurun_out/nt_ld$ld.csv python tools/gemm_probe.py 8192 8192 8192 3 > /dev/null 2>&1
-  show "ours ld=$ld" gpurun_out/nt_ld$ld.csv
+for b in 1 2 4 8 16 64; do
+  ncu --metrics $M --clock-control none -k regex:umma_ -s 3 -c 1 --csv --log-file gpurun_out/nt_b$b.csv python tools/gemm_probe.py 8192 8192 8192 2 $b > /dev/null 2>&1
+  show "batch=$b" gpurun_out/nt_b$b.csv
 done
-for g in 2 4 16 32; do
-  TLB_GEMM_GROUP_M=$g ncu --metrics $M --clock-control none -k regex:umma_ -s 3 -c 1 --csv --log-file gpurun_out/nt_g$g.csv python tools/gemm_probe.py 8192 8192 8192 3 > /dev/null 2>&1
-  show "ours group_m=$g" gpurun_out/nt_g$g.csv
+for rep in 1 2; do
+python tools/gemm_probe.py 8192 8192 8192 6 64 2>&1 | tail -1
+python tools/gemm_probe.py 8192 8192 8192 48 8 2>&1 | tail -1
+python tools/gemm_probe.py 8192 8192 8192 384 1 2>&1 | tail -1
 done
-for ld in 8192 8256; do
-echo "timing ld=$ld:"; PROBE_LD=$ld python tools/gemm_probe.py 8192 8192 8192 20 2>&1 | tail -1
-echo "sustained ld=$ld:"; PROBE_LD=$ld python tools/gemm_probe.py 8192 8192 8192 20 8 2>&1 | tail -1
-done
+python tools/cublas_point.py 8192 384 2>&1 | tail -1

@@ -1,14 +1,17 @@
 #!/bin/bash
-# Scratch: TMA-fed persistent copy sweep + new GEMM tests
-echo "== LDG tiled"; python tools/copy_probe.py c1 c3 2>&1 | tail -2
-for st in 2 3 4 6; do for ct in 1 2 3 4; do
-  echo "== TMA stages=$st ctas=$ct"; TLB_COPY_TMA=1 TLB_COPY_TMA_STAGES=$st TLB_COPY_TMA_CTAS=$ct python tools/copy_probe.py c1 c3 2>&1 | tail -2
-done; done
-echo "== LB128"; TLB_COPY_LB256=0 TLB_COPY_TMA=1 TLB_COPY_TMA_STAGES=4 TLB_COPY_TMA_CTAS=3 python tools/copy_probe.py c1 c3 2>&1 | tail -2
-TLB_COPY_LB256=0 TLB_COPY_TMA=1 TLB_COPY_TMA_STAGES=6 TLB_COPY_TMA_CTAS=2 python tools/copy_probe.py c1 c3 2>&1 | tail -2
-python -m pytest tests/test_gemm_gpu.py -x -q -m gpu -k "packed or conv or gett" 2>&1 | tail -5
-python bench.py --only Cg --no-cpu --steps 20 --gemm-only > gpurun_out/b_cg.json 2>gpurun_out/b_cg.err; python - <<'PY'
+python -m pytest tests/test_gemm_gpu.py -x -q -m gpu -k "chunked or c4_batched or batched" 2>&1 | tail -3
+for rep in 1 2; do
+python tools/gemm_probe.py 8192 8192 8192 6 64 2>&1 | tail -1
+TLB_GEMM_CHUNK_WAVES=0 python tools/gemm_probe.py 8192 8192 8192 6 64 2>&1 | tail -1
+TLB_GEMM_CHUNK_WAVES=4 python tools/gemm_probe.py 8192 8192 8192 6 64 2>&1 | tail -1
+TLB_GEMM_CHUNK_WAVES=16 python tools/gemm_probe.py 8192 8192 8192 6 64 2>&1 | tail -1
+done
+python tools/gemm_probe.py 16384 16384 16384 6 1 2>&1 | tail -1
+TLB_GEMM_CHUNK_WAVES=0 python tools/gemm_probe.py 16384 16384 16384 6 1 2>&1 | tail -1
+python tools/cublas_point.py 16384 6 2>&1 | tail -1
+python bench.py --only C4 --no-cpu --steps 20 > gpurun_out/b_c4.json 2>gpurun_out/b_c4.err; python -c "
 import json
-d=json.load(open('gpurun_out/b_cg.json'))
-for e in d['other_configs']: print(e['name'], e['value'], e['config'].get('plan'))
-PY
+d=json.load(open('gpurun_out/b_c4.json'))
+print('C2', d['value'], d['clocks'])
+for e in d['other_configs']: print(e['name'], round(e['value'],1), e['ms_per_step'], e['config'].get('plan'), e['roofline']['frac'])
+"
