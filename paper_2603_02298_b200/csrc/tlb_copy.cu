@@ -94,6 +94,25 @@ gather_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__
     }
 }
 
+// gather, vectorised: when both layouts keep V consecutive integral coordinates in V consecutive cells (the low run of
+// tla::max_common_vector, analysis.hpp:18-28, here also for Xor layouts: leaf 0 is the identity on the low bits and no
+// other leaf touches them) a thread evaluates both layouts ONCE per vector and moves VB = V * elem_bytes bytes.
+template <int VB>
+__global__ void __launch_bounds__(kThreads)
+gather_vec_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__ tlb_layout_desc D,
+                  const char* __restrict__ src, char* __restrict__ dst, int64_t s_origin, int64_t d_origin, uint64_t i0,
+                  uint64_t n_vec, int v_elems, int elem_bytes) {
+    using T = typename Cell<VB>::type;
+    pdl_wait();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n_vec; k += stride) {
+        const uint64_t i = i0 + k * static_cast<uint64_t>(v_elems);
+        const int64_t sp = dev_position(S, s_origin, dev_eval(S, i));
+        const int64_t dp = dev_position(D, d_origin, dev_eval(D, i));
+        *reinterpret_cast<T*>(dst + dp * elem_bytes) = *reinterpret_cast<const T*>(src + sp * elem_bytes);
+    }
+}
+
 // gather over the common refinement: one peel yields both offsets (half the index arithmetic of two evaluations), and,
 // the destination being injective, the refined modes may be walked in any order: the host sorts them by destination
 // stride so that consecutive threads store to neighbouring cells.
@@ -671,19 +690,66 @@ struct CopyCall {
     cudaStream_t stream;
 };
 
+// Largest power-of-two V (elements) such that every aligned block of V consecutive integral coordinates lands in V
+// consecutive cells of the tensor: leaf 0 is the identity on the low coordinate bits (Int stride 1 / Xor mask 1, extent a
+// multiple of V), no other leaf reaches below V (Int stride a multiple of V, Xor mask without bits below V), and the
+// origin and the base pointer are V-aligned.
+int low_run(const tlb_tensor& t, int vmax) {
+    const tlb_layout_desc& L = *t.layout;
+    if (L.kind != TLB_KIND_INT && L.kind != TLB_KIND_XOR) return 1;
+    int lead = 0;
+    while (lead < L.n_modes && L.extent[lead] == 1) ++lead;
+    if (lead == L.n_modes || L.stride[lead] != 1) return 1;
+    int v = vmax;
+    while (v > 1) {
+        bool ok = L.extent[lead] % v == 0 && t.origin % v == 0 &&
+                  reinterpret_cast<uintptr_t>(t.data) % (static_cast<uintptr_t>(v) * t.elem_bytes) == 0;
+        for (int r = lead + 1; ok && r < L.n_modes; ++r) {
+            if (L.extent[r] == 1) continue;
+            ok = L.kind == TLB_KIND_INT ? (L.stride[r] % v == 0) : ((L.stride[r] & (v - 1)) == 0);
+        }
+        if (ok) break;
+        v >>= 1;
+    }
+    return v;
+}
+
 int launch_gather(const CopyCall& c) {
     const tlb_layout_desc& S = *c.src->layout;
     const tlb_layout_desc& D = *c.dst->layout;
     const int counting = c.src->accessor == TLB_ACC_COUNTING;
+    const int eb = c.dst->elem_bytes;
+    int V = 1;
+    if (!counting && eb < 16 && c.src->data) {
+        V = std::min(low_run(*c.src, 16 / eb), low_run(*c.dst, 16 / eb));
+        while (V > 1 && (c.i0 % V != 0 || c.n % V != 0)) V >>= 1;
+    }
     if (g_dry_run) {
-        set_plan("gather");
+        set_plan(V > 1 ? "gather_vec" : "gather");
+        return TLB_OK;
+    }
+    if (V > 1) {
+        const uint64_t n_vec = c.n / V;
+        const int gridv = launch_grid(n_vec, kThreads, 8);
+        const char* sb = static_cast<const char*>(c.src->data);
+        char* db = static_cast<char*>(c.dst->data);
+#define TLB_GV(VB) TLB_CUDA(launch_pdl(gather_vec_kernel<VB>, dim3(gridv), dim3(kThreads), 0, c.stream, S, D, sb, db, c.src->origin, c.dst->origin, c.i0, n_vec, V, eb))
+        switch (V * eb) {
+        case 2: TLB_GV(2); break;
+        case 4: TLB_GV(4); break;
+        case 8: TLB_GV(8); break;
+        default: TLB_GV(16); break;
+        }
+#undef TLB_GV
+        count_launch();
+        set_plan("gather_vec");
         return TLB_OK;
     }
     const int grid = launch_grid(c.n, kThreads, 8);
 #define TLB_GATHER(EB)                                                                                        \
     gather_kernel<EB><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
                                                        c.i0, c.n, counting)
-    switch (c.dst->elem_bytes) {
+    switch (eb) {
     case 1: TLB_GATHER(1); break;
     case 2: TLB_GATHER(2); break;
     case 4: TLB_GATHER(4); break;

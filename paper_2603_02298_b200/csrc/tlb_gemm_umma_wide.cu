@@ -169,7 +169,13 @@ constexpr uint32_t kIdescW = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<u
 
 // PLAIN (tile_coords_t, tlb_umma_ptx.h): all three tensor maps are rank 3 with identity coordinates (unfolded operands, the
 // common case): the general rank 3..5 decomposition is compiled out of the producer's and the epilogue's loops.
-template <bool PLAIN>
+// MC (clusters of 4 = two CTA pairs on n-adjacent pair tiles, K-major plain operands): the two pairs need the same 512
+// rows of A, so every CTA loads only a QUARTER of them (128 rows x 64 k, 16 KiB) and multicasts it to its counterpart in
+// the other pair: L2 -> SM requests per CTA and k-block drop from 48 KiB to 32 KiB (the cluster tile is 512 x 512). A
+// stage is then written by CTAs of BOTH pairs, so it is released only when both pairs' MMAs have consumed it: the MMA
+// thread commits on its leader's `done` barrier, the leader's producer relays that to the `empty` barrier (count 2) of
+// all four CTAs.
+template <bool PLAIN, bool MC>
 __global__ void __launch_bounds__(kThreadsW, 1)
 umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_cp,
@@ -185,11 +191,16 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     auto tfull_bar = [&](int h) { return bar_base + 8u * (2 * kStages + h); };
     auto tempty_bar = [&](int h) { return bar_base + 8u * (2 * kStages + 2 + h); };
     const uint32_t tmem_slot = bar_base + 8u * (2 * kStages + 4);
+    auto done_bar = [&](int s) { return bar_base + 8u * (2 * kStages + 5 + s); };   // MC only, pair leaders
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t crank = cluster_rank();           // 0..3 with MC, 0..1 otherwise
+    const uint32_t pair = MC ? crank >> 1 : 0u;      // which CTA pair of the cluster
+    const uint32_t rank = crank & 1u;                // position inside the pair
+    const uint32_t lead_cta = pair * 2u;             // cluster rank of this pair's leader
     const bool leader = rank == 0;
-    const uint32_t n_workers = gridDim.x / 2, worker = blockIdx.x / 2;
+    constexpr uint32_t kCluster = MC ? 4u : 2u;
+    const uint32_t n_workers = gridDim.x / kCluster, worker = blockIdx.x / kCluster;
     const int kblocks = (args.K + BK - 1) / BK;
     const int rank_a = PLAIN ? 3 : args.rank_a, rank_b = PLAIN ? 3 : args.rank_b, rank_c = PLAIN ? 3 : args.rank_c;
     if (threadIdx.x == 0 && args.cta_times) {
@@ -204,7 +215,8 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
         for (int s = 0; s < kStages; ++s) {
             mbar_init(full_bar(s), 1);  // the leader's producer arrive; the TMA bytes of both CTAs complete the phase
-            mbar_init(empty_bar(s), 1); // one tcgen05.commit (leader) / one relayed arrive (peer)
+            mbar_init(empty_bar(s), MC ? 2 : 1); // one tcgen05.commit (leader) / one relayed arrive (peer); MC: one relay per pair
+            if (MC) mbar_init(done_bar(s), 1);   // this pair's tcgen05.commit
         }
         for (int h = 0; h < 2; ++h) {
             mbar_init(tfull_bar(h), 1);              // one multicast tcgen05.commit
@@ -236,13 +248,18 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         int stage = 0;
         uint32_t phase = 0;
         bool ring_wrapped = false;
-        const uint32_t peer_empty0 = map_to_cta(empty_bar(0), 1);
-        const uint32_t lbar0 = map_to_cta(full_bar(0), 0);
+        const uint32_t peer_empty0 = map_to_cta(empty_bar(0), lead_cta + 1);
+        const uint32_t lbar0 = map_to_cta(full_bar(0), lead_cta);
+        uint32_t all_empty0[4] = {0, 0, 0, 0};
+        if constexpr (MC)
+            for (uint32_t c = 0; c < 4; ++c) all_empty0[c] = map_to_cta(empty_bar(0), c);
+        const uint16_t a_mask = static_cast<uint16_t>((1u << crank) | (1u << (crank ^ 2u))); // this CTA and its counterpart
         const uint64_t pol_ab = policy_evict_last();
         Item it;
         while (sched.next(args, kblocks, &it)) {
             uint32_t batch, m_tile, n_blk;
             decode_pair_tile(args, it.unit, &batch, &m_tile, &n_blk);
+            if constexpr (MC) n_blk = n_blk * 2 + pair;   // units are 512 x 512 cluster tiles
             const int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC;
             const int n0 = static_cast<int>(n_blk) * BN;
             if (args.prefetch_c && lane < 2) {
@@ -255,16 +272,30 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             if (!args.a_mn) tile_coords_t<PLAIN>(args.ca, rank_a, false, m0, 0, batch, tca);
             if (!args.b_mn) tile_coords_t<PLAIN>(args.cb, rank_b, false, nb0, 0, batch, tcb);
             for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                if constexpr (MC) {
+                    if (leader && ring_wrapped) {
+                        mbar_wait(done_bar(stage), phase ^ 1u, 64);   // this pair's MMAs have consumed the stage ...
+                        if (elect_one()) {
+#pragma unroll
+                            for (uint32_t c = 0; c < 4; ++c) mbar_arrive_cluster(all_empty0[c] + 8u * stage); // ... tell all four CTAs
+                        }
+                        __syncwarp();
+                    }
+                }
                 mbar_wait(empty_bar(stage), phase ^ 1u, 64);
                 if (elect_one()) {
-                    if (leader && ring_wrapped) mbar_arrive_cluster(peer_empty0 + 8u * stage); // relay the release
+                    if (!MC && leader && ring_wrapped) mbar_arrive_cluster(peer_empty0 + 8u * stage); // relay the release
                     if ((args.debug & 1u) && ring_wrapped) {
                         if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
                     } else {
                         const uint32_t lbar = lbar0 + 8u * stage;
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * kStageBytes);
                         int tc[5];
-                        if (!args.a_mn) {
+                        if constexpr (MC) {
+                            // this CTA's quarter of the cluster's A rows -> the same half slot of this CTA and of its counterpart
+                            tma_load_3d_2sm_mc(a_stage(stage) + pair * (BMH * BK * 2), &map_a, lbar, kb * BK, m0 + static_cast<int>(pair) * BMH,
+                                               static_cast<int>(batch), a_mask);
+                        } else if (!args.a_mn) {
                             // K-major A: one box of 256 rows x 64 k (rows of 128 B)
                             tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, tca);
                             if (args.hints & 1u) tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, rank_a, tca, pol_ab);
@@ -299,6 +330,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         if (leader) {
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
+            const uint16_t pair_mask = static_cast<uint16_t>(3u << lead_cta); // both CTAs of THIS pair
             // 4 UMMAs of k-block `kb` in ring slot s into accumulator half h
             // Descriptors: K-major tiles are rows of 128 B with 8-row groups 1024 B apart (SBO), a k-step of 16 advances
             // the start by 32 B; MN-major tiles are 64-row chunks of [64 k][128 B]: 8-k groups 1024 B apart (SBO), chunks
@@ -331,7 +363,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         tc_fence_after();
                         if (elect_one()) {
                             issue_half(s, 0, j == 0);
-                            if (j == n - 1) umma_commit<2>(tfull_bar(0));
+                            if (j == n - 1) umma_commit<2>(tfull_bar(0), pair_mask);
                         }
                         __syncwarp();
                         if (++s == kStages) { s = 0; ph ^= 1u; }
@@ -342,8 +374,8 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 for (int j = 0; j < pre; ++j) {
                     if (elect_one()) {
                         issue_half(stage, 1, j == 0);
-                        umma_commit_local<2>(empty_bar(stage)); // both halves of this stage are consumed
-                        if (j == n - 1) umma_commit<2>(tfull_bar(1));
+                        umma_commit_local<2>(MC ? done_bar(stage) : empty_bar(stage)); // both halves of this stage are consumed
+                        if (j == n - 1) umma_commit<2>(tfull_bar(1), pair_mask);
                     }
                     __syncwarp();
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -354,10 +386,10 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     tc_fence_after();
                     if (elect_one()) {
                         issue_half(stage, 0, false);
-                        if (j == n - 1) umma_commit<2>(tfull_bar(0)); // half 0 complete: its epilogue starts a k-block early
+                        if (j == n - 1) umma_commit<2>(tfull_bar(0), pair_mask); // half 0 complete: its epilogue starts a k-block early
                         issue_half(stage, 1, false);
-                        umma_commit_local<2>(empty_bar(stage));
-                        if (j == n - 1) umma_commit<2>(tfull_bar(1));
+                        umma_commit_local<2>(MC ? done_bar(stage) : empty_bar(stage));
+                        if (j == n - 1) umma_commit<2>(tfull_bar(1), pair_mask);
                     }
                     __syncwarp();
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -371,7 +403,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         const uint32_t colh = static_cast<uint32_t>(warp) >> 2; // which 128 columns of a half
         const uint32_t buf0 = epi_base + static_cast<uint32_t>(warp) * kEpiBufs * kEpiWarpBytes;
         uint32_t chunk_no = 0;
-        const uint32_t tempty_leader = map_to_cta(tempty_bar(0), 0);
+        const uint32_t tempty_leader = map_to_cta(tempty_bar(0), lead_cta);
         const uint64_t pol_c = policy_evict_first();
         const uint32_t row = lane;
         uint32_t acc_phase = 0;
@@ -379,6 +411,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         while (sched.next(args, kblocks, &it)) {
             uint32_t batch, m_tile, n_blk;
             decode_pair_tile(args, it.unit, &batch, &m_tile, &n_blk);
+            if constexpr (MC) n_blk = n_blk * 2 + pair;
             int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC + static_cast<int>(quad) * 32;
             int n0 = static_cast<int>(n_blk) * BN + static_cast<int>(colh) * (BN / 2);
             if (args.debug & 32u) {  // timing experiment: every CTA reduces into the first tile (L2-resident, no DRAM traffic)
@@ -609,7 +642,7 @@ bool umma_wide_applies(const UmmaProblem& p) {
 
 
 // One launch over `units` pair tiles starting at a.unit_begin: partial-wave cut, grid, cluster and PDL attributes.
-static int launch_units(const UmmaProblem& p, WideArgs& a, uint32_t units, uint32_t W, int kblocks, bool plain, const CUtensorMap& tma,
+static int launch_units(const UmmaProblem& p, WideArgs& a, uint32_t units, uint32_t W, int kblocks, bool plain, bool mc, const CUtensorMap& tma,
                  const CUtensorMap& tmb, const CUtensorMap& tmc, const CUtensorMap& tmcp, cudaStream_t stream) {
     // Tail balancing: the (units mod W) tiles of the partial wave become one k-range per worker (run first). With
     // split_tail off (TLB_GEMM_SPLIT_TAIL=0) every tile is summed by one CTA pair in k order: bitwise reproducible.
@@ -637,9 +670,9 @@ static int launch_units(const UmmaProblem& p, WideArgs& a, uint32_t units, uint3
     const uint32_t workers = a.sk_units ? W : std::min(units, W);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
-    cfg.gridDim = dim3(2 * workers);
+    cfg.gridDim = dim3((mc ? 4 : 2) * workers);
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = mc ? 4 : 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -649,25 +682,52 @@ static int launch_units(const UmmaProblem& p, WideArgs& a, uint32_t units, uint3
     cfg.blockDim = dim3(kThreadsW);
     cfg.dynamicSmemBytes = kSmemW;
     cfg.stream = stream;
-    if (plain) TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<true>, tma, tmb, tmc, tmcp, a));
-    else TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<false>, tma, tmb, tmc, tmcp, a));
+    if (mc) TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<true, true>, tma, tmb, tmc, tmcp, a));
+    else if (plain) TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<true, false>, tma, tmb, tmc, tmcp, a));
+    else TLB_CUDA(cudaLaunchKernelEx(&cfg, umma_wide_kernel<false, false>, tma, tmb, tmc, tmcp, a));
     count_launch();
     return TLB_OK;
 }
+
+static std::atomic<int> g_clusters4[64]; // co-resident clusters of 4 of the multicast kernel, per device
 
 int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     static std::atomic<bool> attr_set[64];
     int dev = 0;
     TLB_CUDA(cudaGetDevice(&dev));
     if (dev >= 0 && dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
-        TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
-        TLB_CUDA(cudaFuncSetAttribute(umma_wide_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW));
+        TLB_CUDA((cudaFuncSetAttribute(umma_wide_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW)));
+        TLB_CUDA((cudaFuncSetAttribute(umma_wide_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW)));
+        TLB_CUDA((cudaFuncSetAttribute(umma_wide_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemW)));
+        // how many clusters of 4 fit (GPCs whose SM count is not a multiple of 4 leave SMs over: 132 of 148 on B200)
+        cudaLaunchConfig_t qc = {};
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = 4;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.gridDim = dim3(4 * 64);
+        qc.blockDim = dim3(kThreadsW);
+        qc.dynamicSmemBytes = kSmemW;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int n4 = 0;
+        if (cudaOccupancyMaxActiveClusters(&n4, umma_wide_kernel<true, true>, &qc) != cudaSuccess) n4 = 0;
+        (void)cudaGetLastError();
+        g_clusters4[dev].store(n4, std::memory_order_relaxed);
         attr_set[dev].store(true, std::memory_order_release);
     }
     // tensor maps = the divided layouts: zipped_divide(A, [256, 64]), zipped_divide(B, [128, 64]) (64 x 64 chunks for
     // MN-major operands), zipped_divide(C, [32, 32 | 64])
+    // Multicast plan (clusters of 4, A quarters shared between two n-adjacent pair tiles): K-major unfolded operands, whole
+    // problems, an even number of 256-column blocks. GEMM_MCAST: 0 never, 1 when it applies, -1 auto (see below).
+    const uint32_t nb_all = static_cast<uint32_t>((p.N + 255) / 256);
+    const int n4 = (dev >= 0 && dev < 64) ? g_clusters4[dev].load(std::memory_order_relaxed) : 0;
+    const int mc_knob = knob(K_GEMM_MCAST);
+    bool use_mc = mc_knob != 0 && n4 > 0 && !p.a_mn && !p.b_mn && p.full_range && nb_all % 2 == 0 && nb_all >= 2;
+    if (use_mc && mc_knob < 0) use_mc = static_cast<uint64_t>((p.M + 511) / 512) * (nb_all / 2) * static_cast<uint64_t>(std::max(p.batch, 1)) >= static_cast<uint64_t>(n4);
     TmaTileMap ma, mb, mc, mcp;
-    TLB_TRY(umma_operand_map(p, 0, BMC, &ma));
+    TLB_TRY(umma_operand_map(p, 0, use_mc ? BMH : BMC, &ma));
     TLB_TRY(umma_operand_map(p, 1, BN / 2, &mb));
     TLB_TRY(umma_c_map(p, p.c_16 ? 64 : 32, 32, TMA_SW_128, &mc));
     TLB_TRY(epilogue_partition_check(BN, 2)); // tcgen05.ld partition derived from the accumulator layout (tlb_gemm_layout.cu)
@@ -681,7 +741,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     a.N = p.N;
     a.K = p.K;
     a.mbw = static_cast<uint32_t>((p.M + 511) / 512);
-    a.nb = static_cast<uint32_t>((p.N + 255) / 256);
+    a.nb = nb_all;
     a.ab_f16 = p.ab_f16 ? 1u : 0u;
     a.c_16 = p.c_16 ? 1u : 0u;
     a.a_mn = p.a_mn ? 1u : 0u;
@@ -712,6 +772,19 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     std::memcpy(&tmcp, mcp.desc, 128);
     // plain (unfolded) operands and C: the coordinates of every map are the kernel's loop variables
     const bool plain = tma_map_is_plain(ma, p.a_mn != 0) && tma_map_is_plain(mb, p.b_mn != 0) && tma_map_is_plain(mc, false);
+    if (use_mc && !plain) { // folded operands keep the pair plan (the A map goes back to 256-row boxes)
+        use_mc = false;
+        TLB_TRY(umma_operand_map(p, 0, BMC, &ma));
+        std::memcpy(&tma, ma.desc, 128);
+        a.rank_a = ma.rank;
+        for (int d = 0; d < 5; ++d) a.ca[d] = ma.c[d];
+    }
+    if (use_mc) {
+        a.nb = nb_all / 2;   // units are 512 x 512 cluster tiles; pair p of a cluster takes column block 2 n + p
+        W = static_cast<uint32_t>(n4);
+        if (const int cap = knob(K_GEMM_WORKERS); cap > 0) W = std::max(1u, std::min(W, static_cast<uint32_t>(cap)));
+    }
+    const uint32_t units_total = use_mc ? a.mbw * a.nb * static_cast<uint32_t>(std::max(p.batch, 1)) : units_all;
 
     // One launch covers at most ~GEMM_CHUNK_WAVES waves of pair tiles. The workers of a persistent launch are only
     // synchronised at its start: every tile boundary adds a little jitter, after some tens of tiles the CTAs that share an
@@ -725,7 +798,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     {
         const uint32_t waves = static_cast<uint32_t>(std::max(0, knob(K_GEMM_CHUNK_WAVES)));
         const uint32_t per_batch = a.mbw * a.nb;
-        if (waves > 0 && units_all > (waves + waves / 2) * W) {
+        if (waves > 0 && units_total > (waves + waves / 2) * W) {
             // boundaries at whole batches when a batch holds at least a wave, else anywhere; single problems at whole
             // rasterisation groups
             uint32_t align = 1;
@@ -733,16 +806,16 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
             else if (p.full_range) align = a.group_w * a.nb;
             const uint32_t target = waves * W;
             const uint32_t step = align >= target ? align : std::max(1u, target / align) * align;
-            for (uint32_t u = step; u + step / 2 < units_all; u += step) cuts.push_back(u);
+            for (uint32_t u = step; u + step / 2 < units_total; u += step) cuts.push_back(u);
         }
-        cuts.push_back(units_all);
+        cuts.push_back(units_total);
     }
     for (size_t ci = 0; ci + 1 < cuts.size(); ++ci) {
         a.unit_begin = unit_begin + cuts[ci];
         const uint32_t units = cuts[ci + 1] - cuts[ci];
-        TLB_TRY(launch_units(p, a, units, W, kblocks, plain, tma, tmb, tmc, tmcp, stream));
+        TLB_TRY(launch_units(p, a, units, W, kblocks, plain, use_mc, tma, tmb, tmc, tmcp, stream));
     }
-    set_plan("umma_2sm_wide");
+    set_plan(use_mc ? "umma_2sm_wide_mc" : "umma_2sm_wide");
     return TLB_OK;
 }
 

@@ -61,6 +61,7 @@ enum KnobId {
     K_COPY_TMA_STAGES,  // staged tiles per CTA of the TMA-fed tiled copy
     K_COPY_TMA_CTAS,    // its CTAs per SM
     K_GEMM_CHUNK_WAVES, // waves of pair tiles per launch of the wide plan (0: one launch whatever the range)
+    K_GEMM_MCAST,       // wide plan in clusters of 4 with A multicast between two pair tiles: 0 never, 1 when it applies, -1 auto
     K_GEMM_PACK,        // 1: operands / C that no tensor map can address are packed and run on tcgen05 (default), 0: SIMT plan
     K_GEMM_PACK_MIN,    // log2 of the smallest M*N*K that takes the packed plan
     K_COUNT

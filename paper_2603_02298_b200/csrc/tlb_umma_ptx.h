@@ -75,6 +75,14 @@ __device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const void* map, u
         "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// cta_group::2 + multicast: the box lands at the same offset in every CTA of `mask` and each destination's bytes complete
+// on the barrier at leader_bar's offset in THAT destination's pair leader (measured: tools/probes/mcast_probe.cu).
+__device__ __forceinline__ void tma_load_3d_2sm_mc(uint32_t dst, const void* map, uint32_t leader_bar, int c0, int c1, int c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+        : "memory");
+}
 // L2 eviction-priority policies for the per-tensor cache hints.
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
@@ -165,11 +173,11 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint
     }
 }
 // tcgen05.commit: the barrier is arrived on when every MMA previously issued by this thread has finished.
-template <int CG> __device__ __forceinline__ void umma_commit(uint32_t bar) {
+template <int CG> __device__ __forceinline__ void umma_commit(uint32_t bar, uint16_t mask = 3) {
     if constexpr (CG == 1) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
     } else {
-        const uint16_t mask = 3; // both CTAs of the pair, same barrier offset in each
+        // mask: both CTAs of the pair (cluster ranks; 3 for the first pair of a cluster), same barrier offset in each
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
             "h"(mask)

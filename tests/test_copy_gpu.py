@@ -187,6 +187,20 @@ def test_copy_xor_layouts():
     assert (tdst.cpu().numpy() == want).all()
 
 
+@pytest.mark.parametrize("eb,plan", [(1, "gather_vec"), (2, "gather_vec"), (4, "gather_vec"), (8, "gather_vec"), (16, "gather")])
+def test_copy_xor_layouts_vectorised(eb, plan):
+    """Swizzled (Xor) layouts keep the low coordinate bits contiguous (leaf 0 is f1, the other masks start at bit 4): the
+    gather evaluates both layouts once per 16-byte vector (max_common_vector, analysis.hpp:18-28, extended to Xor leaves).
+    Both directions, an Xor layout on both sides, origins (Xor acts on the absolute position, tensor.hpp:57) and a range
+    that is not a whole number of vectors (falls back to one cell per thread)."""
+    sw, flat = "(128,8,32):(f1,f144,f1024)", "(128,8,32):(1,128,1024)"
+    assert run_copy_case(flat, sw, eb) == plan
+    assert run_copy_case(sw, flat, eb, seed=1) == plan
+    assert run_copy_case(sw, "(128,8,32):(f1,f160,f1024)", eb, seed=2) == plan   # two different swizzles
+    assert run_copy_case(flat, sw, eb, src_origin=16, dst_origin=32768, seed=3) == plan
+    assert run_copy_case(flat, sw, eb, src_origin=1, dst_origin=32768, seed=4) in ("gather", "gather_vec")   # unaligned source
+
+
 def test_copy_non_injective_destination_last_writer_wins():
     """7:0 -> 7:0 makes dst[0] = src(6) (test_tensor.cpp:98); larger aliasing cases vs the oracle."""
     assert run_copy_case("7:1", "7:0", 8) == "ordered"

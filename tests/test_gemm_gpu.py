@@ -771,3 +771,38 @@ def test_gemm_wide_plan_chunked_launches_are_exact(tlb_config):
         ref = (a[bi].double() @ b[bi].double().t()).t() + 1.0
         assert torch.equal(results[0][bi].double(), ref)
         assert torch.equal(results[1][bi].double(), ref)
+
+
+@pytest.mark.parametrize("dims", [(512, 1024, 128), (1000, 1024, 200), (768, 512, 72)])
+def test_gemm_wide_multicast_plan_matches_the_oracle(dims, tlb_config):
+    """Clusters of 4: two CTA pairs on n-adjacent pair tiles share the A rows, every CTA loads a quarter and multicasts it
+    to its counterpart (cta_group::2 + multicast TMA; stage release needs both pairs). Exact on the integer fills against
+    the oracle, incl. a ragged M and a K that is not a multiple of 64; random data within the GEMM tolerance."""
+    M, N, K = dims
+    tlb_config("GEMM_WIDE", "1")
+    tlb_config("GEMM_MCAST", "1")
+    la, lb, lc = f"({M},{K}):({K},1)", f"({N},{K}):({K},1)", f"({M},{N}):({N},1)"
+    assert _bf16_case(la, lb, lc, kat=True) == "umma_2sm_wide_mc"
+    assert _bf16_case(la, lb, lc, kat=False, seed=53) == "umma_2sm_wide_mc"
+    # m-contiguous C (the paper's TN row) runs transposed: the columns of the plan are then m
+    assert _bf16_case(la, lb, f"({M},{N}):(1,{M})", kat=True) == ("umma_2sm_wide_mc" if ((M + 255) // 256) % 2 == 0 else "umma_2sm_wide")
+
+
+def test_gemm_wide_multicast_plan_stream_k_exact(tlb_config):
+    """64 cluster tiles on the 33 co-resident clusters of 4: the partial wave is cut into k-ranges that BOTH pairs of a
+    cluster walk in lockstep. Exact against an fp64 product of the integer fills."""
+    M = N = 4096
+    K = 1024
+    i = torch.arange(M, device="cuda").view(M, 1)
+    p = torch.arange(K, device="cuda").view(1, K)
+    a = ((i * 7 + p * 3 + 1) % 11).to(torch.bfloat16).contiguous()
+    b = ((i * 5 + p * 2 + 2) % 13).to(torch.bfloat16).contiguous()
+    ref = a.double() @ b.double().t() + 1.0
+    ta = host.make_tensor(L(f"({M},{K}):({K},1)").lower(ranked=True), a.data_ptr(), a.numel(), 2)
+    tb = host.make_tensor(L(f"({N},{K}):({K},1)").lower(ranked=True), b.data_ptr(), b.numel(), 2)
+    tlb_config("GEMM_MCAST", "1")
+    c = torch.ones(M, N, dtype=torch.float32, device="cuda")
+    tc = host.make_tensor(L(f"({M},{N}):({N},1)").lower(ranked=True), c.data_ptr(), c.numel(), 4)
+    assert host.gemm_bf16((ta, None), (tb, None), (tc, None)) == "umma_2sm_wide_mc"
+    torch.cuda.synchronize()
+    assert torch.equal(c.double(), ref)
