@@ -556,11 +556,25 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
     # fallback plans: an Xor (swizzled) destination and a non-injective destination
     if want("Cx"):
         copy_config("Cx_xor_dst", "(128,8,65536):(1,128,1024)", "(128,8,65536):(f1,f144,f1024)", 4,
-                    "2^26 fp32 elements into a Swizzle<3,4,3>-per-KiB destination (128,8,65536):(f1,f144,f1024)", "gather_kernel (Xor strides)",
+                    "2^26 fp32 elements into a Swizzle<3,4,3>-per-KiB destination (128,8,65536):(f1,f144,f1024)", "gather_vec_kernel (Xor strides, 16-byte vectors)",
                     max(3, K // 4), 3)
-        copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,0)", 4,
-                    "2^25 fp32 elements into a destination with a stride-0 mode (last writer wins, tensor.hpp:198)", "winner_kernel + ordered_kernel",
-                    max(3, K // 8), 2)
+        copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,8191)", 4,
+                    "2^25 fp32 elements into a destination whose columns overlap by one cell (stride 8191 < 8192: last writer wins, tensor.hpp:198)",
+                    "winner_kernel + ordered_kernel", max(3, K // 8), 2)
+        # a stride-0 (broadcast) destination mode: only the slice at its last coordinate survives, so the call is an 8192-element
+        # copy; reported as elements of the reference's loop retired per second, not as bandwidth
+        n_b = 8192 * 4096
+        src_b = torch.arange(n_b, dtype=torch.int32, device="cuda")
+        dst_b = torch.empty(8192, dtype=torch.int32, device="cuda")
+        ab, bb = host.tensor_of("(8192,4096):(1,8192)", src_b), host.tensor_of("(8192,4096):(1,0)", dst_b)
+        kb = max(3, K // 2)
+        sec_b = timed(torch, dist, world, lambda i: host.copy(ab, bb), kb, 3)
+        out.append({"name": "Cx_broadcast_dst", "metric": "copy_elements_per_s", "value": n_b * kb * world / sec_b, "unit": "elements/s", "n_gpus": world,
+                    "scaling": "weak", "steps": kb, "ms_per_step": sec_b / kb * 1e3,
+                    "config": {"workload": "2^25 fp32 elements into (8192,4096):(1,0): 4096 writers per cell, the last one wins (tensor.hpp:198); "
+                                           "runs as the injective copy of the last column", "plan": lib.tlb_last_plan().decode()},
+                    "roofline": None})
+        del src_b, dst_b
     # C5: index maps of the 2^32-element divided layout, materialised in 2^28-element chunks (2 GiB)
     if want("C5"):
         Lt = "((128,64),(512,1024)):((65536,1),(8388608,64))"

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include <cuda.h>
@@ -1241,6 +1242,58 @@ int check_tensor(const tlb_tensor* t, const char* who, bool writable) {
     return TLB_OK;
 }
 
+int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, cudaStream_t stream);
+
+// Non-injective destination whose only aliasing comes from stride-0 (broadcast) modes: every destination cell is written
+// once per coordinate of those modes and the LAST writer in ascending i (tensor.hpp:198) is the one whose broadcast
+// coordinates are all maximal (i grows with every coordinate). The copy therefore equals the injective copy of the slice
+// that fixes those modes at their last coordinate, which the ordinary plans run: nothing else is read. Worked on the
+// common refinement (a broadcast mode of the destination may cut across source modes).
+thread_local std::string g_lw_plan;
+int try_last_writer_slice(const CopyCall& c, bool* done) {
+    *done = false;
+    const tlb_layout_desc& S = *c.src->layout;
+    const tlb_layout_desc& D = *c.dst->layout;
+    if (g_copy_path != 0 || S.kind != TLB_KIND_INT || D.kind != TLB_KIND_INT) return TLB_OK;
+    if (c.i0 != 0 || c.n != static_cast<uint64_t>(S.size)) return TLB_OK;
+    std::vector<JM> modes;
+    if (!refine_modes(S, D, &modes)) return TLB_OK;
+    std::vector<tlb_mode> sm, dm;
+    int64_t shift = 0;
+    bool any = false;
+    for (const JM& m : modes) {
+        if (m.e == 1) continue;
+        if (m.ds == 0) {
+            int64_t t;
+            if (!mul_ok(m.e - 1, m.ss, &t) || __builtin_add_overflow(shift, t, &shift)) return TLB_OK;
+            any = true;
+            continue;
+        }
+        sm.push_back({m.e, m.ss, TLB_KIND_INT, 0});
+        dm.push_back({m.e, m.ds, TLB_KIND_INT, 0});
+    }
+    if (!any || sm.size() > TLB_MAX_MODES) return TLB_OK;
+    if (sm.empty()) {
+        sm.push_back({1, 0, TLB_KIND_INT, 0});
+        dm.push_back({1, 0, TLB_KIND_INT, 0});
+    }
+    tlb_layout_desc ls, ld;
+    if (tlb_layout_lower(sm.data(), static_cast<int>(sm.size()), &ls) != TLB_OK) return TLB_OK;
+    if (tlb_layout_lower(dm.data(), static_cast<int>(dm.size()), &ld) != TLB_OK) return TLB_OK;
+    if (!(ld.flags & TLB_LF_INJECTIVE)) return TLB_OK; // other modes overlap as well: winner election
+    tlb_tensor s2 = *c.src, d2 = *c.dst;
+    s2.layout = &ls;
+    d2.layout = &ld;
+    s2.origin += shift;
+    const int st = copy_impl(&s2, &d2, 0, static_cast<uint64_t>(ls.size), c.stream);
+    if (st == TLB_OK) {
+        g_lw_plan = std::string("last_writer+") + tlb_last_plan();
+        set_plan(g_lw_plan.c_str());
+    }
+    *done = true;
+    return st;
+}
+
 int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, cudaStream_t stream) {
     TLB_TRY(check_tensor(src, "tlb_copy source", false));
     TLB_TRY(check_tensor(dst, "tlb_copy destination", true));
@@ -1273,7 +1326,12 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
         const uintptr_t d1 = reinterpret_cast<uintptr_t>(dst->data) + (static_cast<uintptr_t>(dspan.hi) + 1) * eb;
         if (s0 < d1 && d0 < s1) return launch_aliased(c, dspan, (D.flags & TLB_LF_INJECTIVE) != 0);
     }
-    if (!(D.flags & TLB_LF_INJECTIVE)) return launch_ordered(c, dspan);
+    if (!(D.flags & TLB_LF_INJECTIVE)) {
+        bool sliced = false;
+        const int st = try_last_writer_slice(c, &sliced);
+        if (sliced) return st;
+        return launch_ordered(c, dspan);
+    }
     if (g_copy_path != 1) {
         bool done = false;
         Refined refined;

@@ -192,23 +192,35 @@ __global__ void __launch_bounds__(kThreads) idx2crd_kernel(const __grid_constant
 // detects wrapping through checked_mul / checked_add (common.hpp:99-109); so does this kernel: a wrapped element
 // is not written and *d_status (when given) becomes TLB_ERR_OVERFLOW. The prefix products themselves are proven to
 // fit on the host (the lowering rejects shapes whose size overflows).
+// NM > 0: the coordinate vectors have NM (even) entries and are read with 16-byte streaming loads (a thread's NM int64
+// are contiguous: scalar loads would touch every 32-byte sector NM / 4 times per warp instruction); NM == 0: any length.
+template <int NM>
 __global__ void __launch_bounds__(kThreads) crd2idx_kernel(const __grid_constant__ tlb_layout_desc S,
                                                            const int64_t* __restrict__ crd, uint64_t n,
                                                            int64_t* __restrict__ out, int* d_status) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const int nm = S.n_modes;
+    const int nm = NM > 0 ? NM : S.n_modes;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
         const int64_t* c = crd + k * nm;
         int64_t idx = 0, scale = 1;
         bool ovf = false;
-        for (int r = 0; r < nm; ++r) {
-            const int64_t x = c[r];
+        auto step = [&](int r, int64_t x) {
             const int64_t lo = static_cast<int64_t>(static_cast<uint64_t>(x) * static_cast<uint64_t>(scale));
             ovf |= __mul64hi(x, scale) != (lo >> 63);
             const int64_t sum = static_cast<int64_t>(static_cast<uint64_t>(idx) + static_cast<uint64_t>(lo));
             ovf |= ((idx ^ sum) & (lo ^ sum)) < 0;
             idx = sum;
             scale *= S.extent[r];
+        };
+        if constexpr (NM > 0) {
+            int64_t x[NM];
+#pragma unroll
+            for (int r = 0; r < NM; r += 2)
+                asm volatile("ld.global.nc.L1::no_allocate.v2.s64 {%0, %1}, [%2];" : "=l"(x[r]), "=l"(x[r + 1]) : "l"(c + r));
+#pragma unroll
+            for (int r = 0; r < NM; ++r) step(r, x[r]);
+        } else {
+            for (int r = 0; r < nm; ++r) step(r, c[r]);
         }
         if (ovf) {
             if (d_status) atomicExch(d_status, TLB_ERR_OVERFLOW);
@@ -463,7 +475,13 @@ int tlb_crd2idx_range_checked(const tlb_layout_desc* shape, const int64_t* d_crd
     // lowering has already proven that the full product fits (shape->size), so no prefix product can wrap.
     if (shape->size < 1) return fail(TLB_ERR_OVERFLOW, "integer overflow in multiplication");
     TLB_TRY(require_device());
-    crd2idx_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*shape, d_crd, n, d_out, d_status);
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    const bool al16 = (reinterpret_cast<uintptr_t>(d_crd) & 15) == 0;
+    if (al16 && shape->n_modes == 2) crd2idx_kernel<2><<<grid_for(n), kThreads, 0, cs>>>(*shape, d_crd, n, d_out, d_status);
+    else if (al16 && shape->n_modes == 4) crd2idx_kernel<4><<<grid_for(n), kThreads, 0, cs>>>(*shape, d_crd, n, d_out, d_status);
+    else if (al16 && shape->n_modes == 6) crd2idx_kernel<6><<<grid_for(n), kThreads, 0, cs>>>(*shape, d_crd, n, d_out, d_status);
+    else if (al16 && shape->n_modes == 8) crd2idx_kernel<8><<<grid_for(n), kThreads, 0, cs>>>(*shape, d_crd, n, d_out, d_status);
+    else crd2idx_kernel<0><<<grid_for(n), kThreads, 0, cs>>>(*shape, d_crd, n, d_out, d_status);
     count_launch();
     TLB_CUDA(cudaGetLastError());
     return TLB_OK;

@@ -76,7 +76,7 @@ struct WideArgs {
     uint32_t unit_begin;      // first 512 x 256 pair tile of the range (all batches)
     uint32_t dp_units;        // whole tiles, dealt round-robin
     uint32_t sk_units;        // the tiles after them, cut into one k-range per worker
-    uint32_t prefetch_c;      // 1: map_cp is valid
+    uint32_t prefetch_c;      // > 0: map_cp is valid; 1: prefetch this tile's C cells into L2 at the tile's start, n > 1: n k-blocks before its end
     uint32_t hints;           // L2 hints: 1 = operand loads evict_last, 2 = C reductions evict_first
     uint32_t debug;           // TLB_GEMM_DEBUG timing experiments (garbage results): 1 = no TMA loads once the ring is
                               // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only, 32 = all reductions into the first tile
@@ -262,7 +262,7 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             if constexpr (MC) n_blk = n_blk * 2 + pair;   // units are 512 x 512 cluster tiles
             const int m0 = static_cast<int>(m_tile) * BMH + static_cast<int>(rank) * BMC;
             const int n0 = static_cast<int>(n_blk) * BN;
-            if (args.prefetch_c && lane < 2) {
+            if (args.prefetch_c == 1 && lane < 2) {
                 // this CTA's 256 x 256 cells of C -> L2 (two 128-row boxes), long before the reductions need them
                 tma_prefetch_3d(&map_cp, n0, m0 + lane * BMH, static_cast<int>(batch));
             }
@@ -271,7 +271,11 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             int tca[5], tcb[5];
             if (!args.a_mn) tile_coords_t<PLAIN>(args.ca, rank_a, false, m0, 0, batch, tca);
             if (!args.b_mn) tile_coords_t<PLAIN>(args.cb, rank_b, false, nb0, 0, batch, tcb);
+            const int kb_pf = args.prefetch_c > 1 ? max(it.kb0, it.kb1 - static_cast<int>(args.prefetch_c)) : -1;
             for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                // late prefetch: the tile's C cells reach L2 shortly before the reduce-add epilogue needs them (the L2
+                // then adds in place instead of fetching each line from DRAM under the atomics)
+                if (kb == kb_pf && lane < 2) tma_prefetch_3d(&map_cp, n0, m0 + lane * BMH, static_cast<int>(batch));
                 if constexpr (MC) {
                     if (leader && ring_wrapped) {
                         mbar_wait(done_bar(stage), phase ^ 1u, 64);   // this pair's MMAs have consumed the stage ...
@@ -734,7 +738,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     WideArgs a;
     std::memset(&a, 0, sizeof(a));
     // C prefetch into L2 is off by default: measured, it evicts operand lines and costs 1.5 % (8192^3) to 7 % (4096^3).
-    a.prefetch_c = knob(K_GEMM_PREFETCH_C) == 1 ? 1u : 0u;
+    a.prefetch_c = static_cast<uint32_t>(std::max(0, knob(K_GEMM_PREFETCH_C)));
     if (a.prefetch_c && (p.c_16 || umma_c_map(p, 256, BMH, TMA_SW_NONE, &mcp) != TLB_OK || mcp.rank != 3)) a.prefetch_c = 0;
     if (!a.prefetch_c) mcp = mc;
     a.M = p.M;

@@ -203,10 +203,16 @@ def test_copy_xor_layouts_vectorised(eb, plan):
 
 def test_copy_non_injective_destination_last_writer_wins():
     """7:0 -> 7:0 makes dst[0] = src(6) (test_tensor.cpp:98); larger aliasing cases vs the oracle."""
-    assert run_copy_case("7:1", "7:0", 8) == "ordered"
-    assert run_copy_case("(64,64):(1,64)", "(64,64):(1,0)", 4) == "ordered"
-    assert run_copy_case("(64,64):(64,1)", "(64,64):(0,1)", 4) == "ordered"
+    # stride-0 (broadcast) destination modes: the copy equals the injective copy of the slice at their last coordinate
+    assert run_copy_case("7:1", "7:0", 8) == "last_writer+gather"
+    assert run_copy_case("(64,64):(1,64)", "(64,64):(1,0)", 4) == "last_writer+vec"
+    assert run_copy_case("(64,64):(64,1)", "(64,64):(0,1)", 4).startswith("last_writer+")
+    assert run_copy_case("(256,128,3):(128,1,32768)", "(256,128,3):(1,256,0)", 4) == "last_writer+tiled"   # a transpose under a broadcast
+    assert run_copy_case("(6,35):(1,6)", "((2,3),(5,7)):((0,2),(6,0))", 8).startswith("last_writer+")       # broadcast leaves inside both modes
+    assert run_copy_case("(64,64):(1,64)", "(64,64):(1,0)", 4, path=1) == "ordered"                          # forced fallback keeps the election
+    # genuinely overlapping strides: winner election (atomicMax of i per cell, then only the winners store)
     assert run_copy_case("(32,32,4):(1,32,1024)", "(32,32,4):(1,31,3)", 8) == "ordered"
+    assert run_copy_case("(16,16,4):(1,16,256)", "(16,16,4):(1,15,0)", 4) == "ordered"                       # broadcast AND overlap
 
 
 def _alias_case(s, d, so, do, cells_n, eb=8, seed=0):

@@ -18,7 +18,7 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(64,8,4):(1,256,64)", "(64,8,4):(1,64,512)", 2, "vec"),
     # the Table-1 rows (test_tensor.cpp:93-100)
     ("8:1", "8:1", 8, "vec"), ("(8,2,3):(1,16,32)", "(8,2,3):(1,16,32)", 8, "vec"),
-    ("(2,3,2):(42,1,128)", "12:1", 8, "gather"), ("7:0", "7:1", 8, "gather"), ("7:0", "7:0", 8, "ordered"),
+    ("(2,3,2):(42,1,128)", "12:1", 8, "gather"), ("7:0", "7:1", 8, "gather"), ("7:0", "7:0", 8, "last_writer+gather"),
     ("(8,3):(1,8)", "(8,3):(3,1)", 8, "gather"),
     # Xor strides, interleaved runs, ragged rows, aliasing destinations
     ("(8,8):(f1,f9)", "64:1", 8, "gather"),
@@ -27,7 +27,10 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(128,8,64):(f1,f144,f1024)", "(128,8,64):(1,128,1024)", 2, "gather_vec"),
     ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, "gather"),
     ("(96,160):(160,1)", "(96,160):(1,96)", 2, "gather"),
-    ("(64,64):(1,64)", "(64,64):(1,0)", 4, "ordered"),
+    # stride-0 destination modes: only the slice at their last coordinate survives (last writer wins), an injective copy
+    ("(64,64):(1,64)", "(64,64):(1,0)", 4, "last_writer+vec"),
+    # genuinely overlapping destination strides: winner election
+    ("(32,32,4):(1,32,1024)", "(32,32,4):(1,31,3)", 8, "ordered"),
 ])
 def test_plan_selection(s, d, eb, plan):
     assert host.copy_plan(s, d, eb) == plan
