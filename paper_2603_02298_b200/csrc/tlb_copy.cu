@@ -131,29 +131,33 @@ gather_joint_kernel(const __grid_constant__ JointDesc J, const char* __restrict_
 }
 
 // ordered pass 1: winner[dp - lo] = max(i + 1) over the i that store to dp
+// W: 32-bit winners (k + 1, relative to the call's range) when the range has fewer than 2^32 - 1 elements (half the winner
+// traffic), 64-bit otherwise and for the aliased plan's writer table.
+template <typename W>
 __global__ void __launch_bounds__(kThreads)
 winner_kernel(const __grid_constant__ tlb_layout_desc D, int64_t d_origin, int64_t lo, uint64_t i0, uint64_t n,
-              unsigned long long* __restrict__ winner) {
+              W* __restrict__ winner) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
         const uint64_t i = i0 + k;
         const int64_t dp = dev_position(D, d_origin, dev_eval(D, i));
-        atomicMax(winner + (dp - lo), static_cast<unsigned long long>(i + 1));
+        if constexpr (sizeof(W) == 4) atomicMax(winner + (dp - lo), static_cast<unsigned int>(k + 1));
+        else atomicMax(winner + (dp - lo), static_cast<unsigned long long>(i + 1));
     }
 }
 
 // ordered pass 2: only the last writer of each destination cell stores
-template <int EB>
+template <int EB, typename W>
 __global__ void __launch_bounds__(kThreads)
 ordered_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__ tlb_layout_desc D,
                const void* __restrict__ src, void* __restrict__ dst, int64_t s_origin, int64_t d_origin, int64_t lo,
-               uint64_t i0, uint64_t n, int counting, const unsigned long long* __restrict__ winner) {
+               uint64_t i0, uint64_t n, int counting, const W* __restrict__ winner) {
     using T = typename Cell<EB>::type;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += stride) {
         const uint64_t i = i0 + k;
         const int64_t dp = dev_position(D, d_origin, dev_eval(D, i));
-        if (winner[dp - lo] != i + 1) continue;
+        if (static_cast<uint64_t>(winner[dp - lo]) != (sizeof(W) == 4 ? k + 1 : i + 1)) continue;
         const int64_t sp = dev_position(S, s_origin, dev_eval(S, i));
         if constexpr (EB == 8) {
             if (counting) {
@@ -807,14 +811,21 @@ int launch_ordered(const CopyCall& c, Span dspan) {
         set_plan("ordered");
         return TLB_OK;
     }
-    unsigned long long* winner = nullptr;
-    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&winner), cells * sizeof(unsigned long long), c.stream));
-    TLB_CUDA(cudaMemsetAsync(winner, 0, cells * sizeof(unsigned long long), c.stream));
+    const bool w32 = c.n < 0xffffffffull;
+    const size_t wbytes = w32 ? 4 : 8;
+    void* winner = nullptr;
+    TLB_CUDA(ws_malloc(&winner, cells * wbytes, c.stream));
+    TLB_CUDA(cudaMemsetAsync(winner, 0, cells * wbytes, c.stream));
     const int grid = launch_grid(c.n, kThreads, 8);
-    winner_kernel<<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, winner);
+    if (w32) winner_kernel<unsigned int><<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, static_cast<unsigned int*>(winner));
+    else winner_kernel<unsigned long long><<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, static_cast<unsigned long long*>(winner));
 #define TLB_ORDERED(EB)                                                                                         \
-    ordered_kernel<EB><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
-                                                        dspan.lo, c.i0, c.n, counting, winner)
+    do {                                                                                                        \
+        if (w32) ordered_kernel<EB, unsigned int><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
+                                                        dspan.lo, c.i0, c.n, counting, static_cast<const unsigned int*>(winner)); \
+        else ordered_kernel<EB, unsigned long long><<<grid, kThreads, 0, c.stream>>>(S, D, c.src->data, c.dst->data, c.src->origin, c.dst->origin, \
+                                                        dspan.lo, c.i0, c.n, counting, static_cast<const unsigned long long*>(winner)); \
+    } while (0)
     switch (c.dst->elem_bytes) {
     case 1: TLB_ORDERED(1); break;
     case 2: TLB_ORDERED(2); break;
@@ -867,14 +878,14 @@ int launch_aliased(const CopyCall& c, Span dspan, bool injective) {
     const uint64_t cells = static_cast<uint64_t>(dspan.hi - dspan.lo) + 1;
     unsigned long long *writer = nullptr, *root = nullptr;
     void* vals = nullptr;
-    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&writer), cells * 8, c.stream));
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&root), c.n * 8, c.stream);
-    if (e == cudaSuccess) e = cudaMallocAsync(&vals, c.n * static_cast<uint64_t>(eb), c.stream);
+    TLB_CUDA(ws_malloc(reinterpret_cast<void**>(&writer), cells * 8, c.stream));
+    cudaError_t e = ws_malloc(reinterpret_cast<void**>(&root), c.n * 8, c.stream);
+    if (e == cudaSuccess) e = ws_malloc(&vals, c.n * static_cast<uint64_t>(eb), c.stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(writer, 0, cells * 8, c.stream);
     int launches = 0;
     if (e == cudaSuccess) {
         const int grid = launch_grid(c.n, kThreads, 8);
-        winner_kernel<<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, writer);
+        winner_kernel<unsigned long long><<<grid, kThreads, 0, c.stream>>>(D, c.dst->origin, dspan.lo, c.i0, c.n, writer);
         alias_pred_kernel<<<grid, kThreads, 0, c.stream>>>(S, c.src->origin, static_cast<int64_t>(delta / eb), dspan.lo, dspan.hi,
                                                            c.i0, c.n, writer, root);
         launches = 2;
@@ -1193,7 +1204,7 @@ int bounds_preflight(const tlb_tensor& t, uint64_t i0, uint64_t n, const char* w
             !g_dry_run) {
             long long h[2] = {INT64_MAX, INT64_MIN};
             long long* d = nullptr;
-            TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), stream));
+            TLB_CUDA(ws_malloc(reinterpret_cast<void**>(&d), sizeof(h), stream));
             TLB_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, stream));
             span_kernel<<<launch_grid(n, kThreads, 8), kThreads, 0, stream>>>(L, t.origin, i0, n, d);
             count_launch();
@@ -1208,7 +1219,7 @@ int bounds_preflight(const tlb_tensor& t, uint64_t i0, uint64_t n, const char* w
         if ((sp.lo < 0 || sp.hi >= t.capacity) && t.accessor == TLB_ACC_BUFFER && t.origin >= 0 && !g_dry_run) {
             long long h[2] = {INT64_MAX, INT64_MIN};
             long long* d = nullptr;
-            TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), stream));
+            TLB_CUDA(ws_malloc(reinterpret_cast<void**>(&d), sizeof(h), stream));
             TLB_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, stream));
             span_kernel<<<launch_grid(n, kThreads, 8), kThreads, 0, stream>>>(L, t.origin, i0, n, d);
             count_launch();

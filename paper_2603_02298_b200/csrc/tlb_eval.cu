@@ -536,7 +536,7 @@ int tlb_compose_check(const tlb_layout_desc* A, const tlb_layout_desc* B, const 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     unsigned long long* d = nullptr;
     unsigned long long h = 0;
-    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(h), s));
+    TLB_CUDA(ws_malloc(reinterpret_cast<void**>(&d), sizeof(h), s));
     cudaError_t e = cudaMemsetAsync(d, 0, sizeof(h), s);
     int st = TLB_OK;
     if (e == cudaSuccess) st = tlb_compose_check_range(A, B, R, 0, static_cast<uint64_t>(B->size), d, stream);

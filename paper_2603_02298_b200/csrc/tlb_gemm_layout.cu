@@ -126,7 +126,7 @@ extern "C" int tlb_locate_offsets(const tlb_layout_desc* A, const tlb_layout_des
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     unsigned long long* d_bad = nullptr;
     unsigned long long h_bad = 0;
-    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(unsigned long long), s));
+    TLB_CUDA(ws_malloc(reinterpret_cast<void**>(&d_bad), sizeof(unsigned long long), s));
     cudaError_t e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
     int st = TLB_OK;
     if (e == cudaSuccess) st = tlb_compose_check_range(A, &R, T, 0, static_cast<uint64_t>(T->size), d_bad, stream);

@@ -407,7 +407,7 @@ int run_packed(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, co
     TLB_TRY(lower_rowmajor(d.N, d.K, Kp, &lb));
     TLB_TRY(lower_rowmajor(d.M, d.N, Np, &lc));
     char* ws = nullptr;
-    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes_a + bytes_b + bytes_c, stream));
+    TLB_CUDA(ws_malloc(reinterpret_cast<void**>(&ws), bytes_a + bytes_b + bytes_c, stream));
     const tlb_tensor pa{&la, ws, 0, d.M * Kp, 2, TLB_ACC_BUFFER}, pb{&lb, ws + bytes_a, 0, d.N * Kp, 2, TLB_ACC_BUFFER},
         pc{&lc, ws + bytes_a + bytes_b, 0, d.M * Np, cb, TLB_ACC_BUFFER};
     int st = tlb_copy(A, &pa, 0, static_cast<uint64_t>(d.M) * d.K, stream);
@@ -620,7 +620,7 @@ int tlb_gemm_i64(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, 
     uint32_t tiles = 0;
     TLB_TRY(tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, nullptr, nullptr, &tiles)); // contracts first, no device needed
     if (tlb::require_device() != TLB_OK) return TLB_ERR_CUDA;
-    TLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int32_t), s));
+    TLB_CUDA(tlb::ws_malloc(reinterpret_cast<void**>(&d), sizeof(int32_t), s));
     cudaError_t e = cudaMemsetAsync(d, 0, sizeof(int32_t), s);
     int st = e == cudaSuccess ? tlb::run_gemm(A, B, C, true, 0, 0, 0, 0, 1, 0, UINT32_MAX, d, s) : TLB_OK;
     if (e == cudaSuccess && st == TLB_OK) e = cudaMemcpyAsync(&h, d, sizeof(int32_t), cudaMemcpyDeviceToHost, s);

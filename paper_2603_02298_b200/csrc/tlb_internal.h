@@ -70,6 +70,11 @@ int knob(KnobId id);
 
 // One device is required; there is no CPU fallback anywhere in this library.
 int require_device();
+// Stream-ordered workspace (winner arrays, packed GEMM panels, status words): cudaMallocFromPoolAsync on a per-device pool
+// of the library's own whose release threshold is unlimited, so a call that allocates the same workspace every time (a
+// copy in a loop) reuses the pool's memory instead of returning it to the driver at every synchronisation. Freed with
+// cudaFreeAsync. The process's default pool is left alone.
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t stream);
 int sm_count();
 
 // ---- host helpers over descriptors -------------------------------------------
