@@ -307,6 +307,8 @@ struct TileParams {
     int64_t eB[kMaxPieces]; // B pieces: extents (product = Lb) ...
     int64_t sB[kMaxPieces]; // ... and SOURCE strides
     int32_t La, Lb;         // elements; La * EB = 128 bytes (one swizzle row), Lb rows
+    int32_t ua, ub;         // element stride of the A run on the source / of the B run on the destination (1: contiguous;
+                            // > 1: "tiled_s", runs along the smallest-stride modes of layouts without a unit stride)
     uint64_t n_tiles;
 };
 
@@ -318,7 +320,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return (r << 7
 // transpose, 128-bit stores along B (lanes sharing a chunk cover 32 consecutive b).
 // 16 staged bytes -> global: one 128-bit store when the layouts guarantee 16-byte alignment (AL), V cell-sized stores
 // otherwise (unaligned bases / leading dimensions: the L2 merges them into full sectors before they reach HBM).
-template <int EB, bool AL> __device__ __forceinline__ void store_vec(char* p, const uint4& v) {
+template <int EB, bool AL> __device__ __forceinline__ void store_vec(char* p, const uint4& v, int ub = 1) {
     if constexpr (AL) {
         stg_stream(p, v);
     } else {
@@ -326,13 +328,13 @@ template <int EB, bool AL> __device__ __forceinline__ void store_vec(char* p, co
         union { uint4 v; T e[16 / EB]; } u;
         u.v = v;
 #pragma unroll
-        for (int k = 0; k < 16 / EB; ++k) reinterpret_cast<T*>(p)[k] = u.e[k];
+        for (int k = 0; k < 16 / EB; ++k) reinterpret_cast<T*>(p)[static_cast<int64_t>(k) * ub] = u.e[k];
     }
 }
 
 template <int EB, int LB, bool AL = true>
 __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int64_t* s_offA, char* __restrict__ dst,
-                                            int64_t base_d) {
+                                            int64_t base_d, int ub = 1) {
     using T = typename Cell<EB>::type;
     constexpr int V = 16 / EB;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -364,7 +366,7 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
             for (int i = 0; i < V; ++i) {
 #pragma unroll
                 for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
-                store_vec<EB, AL>(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+                store_vec<EB, AL>(dst + (base_d + s_offA[c * V + i] + static_cast<int64_t>(r0) * ub) * EB, out.v, ub);
             }
         }
         return;
@@ -398,7 +400,7 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
         for (int i = 0; i < V; ++i) {
 #pragma unroll
             for (int j = 0; j < V; ++j) out.e[j] = in[j].e[i];
-            store_vec<EB, AL>(dst + (base_d + s_offA[c * V + i] + r0) * EB, out.v);
+            store_vec<EB, AL>(dst + (base_d + s_offA[c * V + i] + static_cast<int64_t>(r0) * ub) * EB, out.v, ub);
         }
     }
 }
@@ -441,14 +443,14 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
         const int v = threadIdx.x + u * kThreads;
         if (NVEC % kThreads == 0 || v < NVEC) {
             const int c = v & 7, b = v >> 3;
-            const char* gp = src + (base_s + s_offB[b] + c * V) * EB;
             if constexpr (AL) {
-                stage[u] = ldg_stream(gp);
+                stage[u] = ldg_stream(src + (base_s + s_offB[b] + c * V) * EB);
             } else {
                 using T = typename Cell<EB>::type;
+                const char* gp = src + (base_s + s_offB[b] + static_cast<int64_t>(c * V) * P.ua) * EB;
                 union { uint4 v; T e[V]; } t;
 #pragma unroll
-                for (int k = 0; k < V; ++k) t.e[k] = reinterpret_cast<const T*>(gp)[k];
+                for (int k = 0; k < V; ++k) t.e[k] = reinterpret_cast<const T*>(gp)[static_cast<int64_t>(k) * P.ua];
                 stage[u] = t.v;
             }
         }
@@ -463,7 +465,7 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
     }
     __syncthreads();
 
-    tile_phase2<EB, LB, AL>(tile, s_offA, dst, base_d);
+    tile_phase2<EB, LB, AL>(tile, s_offA, dst, base_d, AL ? 1 : P.ub);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -659,8 +661,8 @@ int fill_joint(const std::vector<JM>& m, JointDesc* J) {
 // Takes a run of total length L (elements) along the stride chain of one side, starting at the
 // mode whose stride on that side is 1. Pieces are split off `modes` (partial modes leave their
 // outer part behind). `src_side` selects which stride forms the chain.
-bool take_run(std::vector<JM>* modes, bool src_side, int64_t L, std::vector<JM>* pieces) {
-    int64_t want = L, next = 1;
+bool take_run(std::vector<JM>* modes, bool src_side, int64_t L, std::vector<JM>* pieces, int64_t unit = 1) {
+    int64_t want = L, next = unit;
     while (want > 1) {
         int hit = -1;
         for (size_t r = 0; r < modes->size(); ++r)
@@ -954,11 +956,32 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         if (modes[r].ss == 1 && ia < 0) ia = static_cast<int>(r);
         if (modes[r].ds == 1 && ib < 0) ib = static_cast<int>(r);
     }
-    if (ia < 0 || ib < 0) return TLB_OK;
+    // Layouts without a unit stride on one side (BLIS-style general strides, every second element, ...) still take the
+    // staged plan: the run then follows the mode with the SMALLEST positive stride on that side ("tiled_s", cell-sized
+    // strided accesses: a 3-element stride reads a third of every sector instead of one cell per sector).
+    int64_t ua = 1, ub = 1;
+    if (ia < 0 || ib < 0) {
+        if (g_copy_path == 3) return TLB_OK;
+        auto smallest = [&](bool src_side, int* idx) {
+            int64_t best = 0;
+            for (size_t r = 0; r < modes.size(); ++r) {
+                const int64_t st = src_side ? modes[r].ss : modes[r].ds;
+                if (modes[r].e > 1 && st > 0 && (best == 0 || st < best)) {
+                    best = st;
+                    *idx = static_cast<int>(r);
+                }
+            }
+            return best;
+        };
+        if (ia < 0) ua = smallest(true, &ia);
+        if (ib < 0) ub = smallest(false, &ib);
+        if (ia < 0 || ib < 0 || ua > 64 || ub > 64) return TLB_OK; // far-apart cells gain nothing from staging
+    }
+    const bool strided_runs = ua != 1 || ub != 1;
     const char* sp = static_cast<const char*>(s.data);
     char* dp = static_cast<char*>(d.data);
 
-    if (ia == ib && g_copy_path != 2 && g_copy_path != 3) {
+    if (ia == ib && !strided_runs && g_copy_path != 2 && g_copy_path != 3) {
         // ---- vec plan: widest power-of-two vector that divides the run and every other stride
         int vb = 16;
         auto fits = [&](int bytes) {
@@ -1021,10 +1044,10 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         if (eb == 1 && (Lb < 128 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 1-byte cells: LDG-staged, 128+ rows
         if (eb == 16 && (Lb == 64 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 16-byte cells: LDG-staged, 256 / 128 / 32 rows
         std::vector<JM> work = modes, A, B;
-        if (!take_run(&work, true, La, &A)) break; // the A run does not depend on Lb
-        if (!take_run(&work, false, Lb, &B)) continue;
+        if (!take_run(&work, true, La, &A, ua)) break; // the A run does not depend on Lb
+        if (!take_run(&work, false, Lb, &B, ub)) continue;
         if (A.size() > kMaxPieces || B.size() > kMaxPieces) continue;
-        bool ok = base_al;
+        bool ok = base_al && !strided_runs;
         for (const JM& m : A) ok = ok && (m.ds % V == 0);
         for (const JM& m : B) ok = ok && (m.ss % V == 0);
         std::vector<JM> rest;
@@ -1049,6 +1072,8 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         for (size_t r = 0; r < B.size(); ++r) { P.eB[r] = B[r].e; P.sB[r] = B[r].ss; }
         P.La = static_cast<int>(La);
         P.Lb = static_cast<int>(Lb);
+        P.ua = static_cast<int32_t>(ua);
+        P.ub = static_cast<int32_t>(ub);
         uint64_t tiles = 1;
         for (const JM& m : rest) tiles *= static_cast<uint64_t>(m.e);
         P.n_tiles = tiles;
@@ -1129,7 +1154,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
             if (g_copy_path == 3) continue; // this |B| has no tensor map: a shorter B run may have one
         }
         if (g_dry_run) {
-            set_plan(unaligned ? "tiled_u" : "tiled");
+            set_plan(strided_runs ? "tiled_s" : unaligned ? "tiled_u" : "tiled");
             *done = true;
             return TLB_OK;
         }
@@ -1147,7 +1172,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
             }
             count_launch();
             TLB_CUDA(cudaGetLastError());
-            set_plan("tiled_u");
+            set_plan(strided_runs ? "tiled_s" : "tiled_u");
             *done = true;
             return TLB_OK;
         }

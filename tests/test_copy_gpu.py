@@ -201,6 +201,20 @@ def test_copy_xor_layouts_vectorised(eb, plan):
     assert run_copy_case(flat, sw, eb, src_origin=1, dst_origin=32768, seed=4) in ("gather", "gather_vec")   # unaligned source
 
 
+@pytest.mark.parametrize("eb", [2, 4, 8])
+def test_copy_strided_runs_take_the_staged_plan(eb):
+    """No unit stride on one side (BLIS-style general strides): the staged plan runs along the smallest-stride mode with
+    cell-sized strided accesses ("tiled_s"). Packing a strided matrix into rows, scattering rows into a strided matrix,
+    strided on both sides, a reversed outer mode, and the cases that must stay on the gather (same mode fastest on both
+    sides, strides too far apart)."""
+    assert run_copy_case("(256,128):(3,779)", "(256,128):(128,1)", eb) == "tiled_s"            # pack: m stride 3 -> rows
+    assert run_copy_case("(256,128):(128,1)", "(256,128):(5,1291)", eb, seed=1) == "tiled_s"   # scatter: rows -> m stride 5
+    assert run_copy_case("(256,256):(3,779)", "(256,256):(1543,2)", eb, seed=2) == "tiled_s"   # strided on both sides
+    assert run_copy_case("(256,128):(3,-779)", "(256,128):(128,1)", eb, src_origin=779 * 127, slack=779 * 127, seed=3) == "tiled_s"
+    assert run_copy_case("(256,128):(3,779)", "(256,128):(2,515)", eb, seed=4) in ("gather", "gather_vec")  # same fastest mode
+    assert run_copy_case("(64,64):(100,6400)", "(64,64):(64,1)", eb, seed=5) in ("gather", "gather_vec")    # stride 100: no gain
+
+
 def test_copy_non_injective_destination_last_writer_wins():
     """7:0 -> 7:0 makes dst[0] = src(6) (test_tensor.cpp:98); larger aliasing cases vs the oracle."""
     # stride-0 (broadcast) destination modes: the copy equals the injective copy of the slice at their last coordinate

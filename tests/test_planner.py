@@ -27,6 +27,9 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(128,8,64):(f1,f144,f1024)", "(128,8,64):(1,128,1024)", 2, "gather_vec"),
     ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, "gather"),
     ("(96,160):(160,1)", "(96,160):(1,96)", 2, "gather"),
+    # no unit stride on the source: the staged plan runs along the smallest-stride mode
+    ("(2048,2048):(3,6151)", "(2048,2048):(2048,1)", 2, "tiled_s"),
+    ("(2048,2048):(2048,1)", "(2048,2048):(5,10243)", 4, "tiled_s"),
     # stride-0 destination modes: only the slice at their last coordinate survives (last writer wins), an injective copy
     ("(64,64):(1,64)", "(64,64):(1,0)", 4, "last_writer+vec"),
     # genuinely overlapping destination strides: winner election
