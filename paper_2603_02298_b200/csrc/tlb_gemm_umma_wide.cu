@@ -77,6 +77,7 @@ struct WideArgs {
     uint32_t dp_units;        // whole tiles, dealt round-robin
     uint32_t sk_units;        // the tiles after them, cut into one k-range per worker
     uint32_t prefetch_c;      // > 0: map_cp is valid; 1: prefetch this tile's C cells into L2 at the tile's start, n > 1: n k-blocks before its end
+    uint32_t early_release;   // fp32 C: drain a half to registers and release its TMEM before the reductions (GEMM_EARLY_RELEASE)
     uint32_t hints;           // L2 hints: 1 = operand loads evict_last, 2 = C reductions evict_first
     uint32_t debug;           // TLB_GEMM_DEBUG timing experiments (garbage results): 1 = no TMA loads once the ring is
                               // full, 2 = epilogue without staging / reductions, 4 = plain TMA store instead of reduce-add, 8 = staging only, 32 = all reductions into the first tile
@@ -472,6 +473,41 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     }
                     continue;
                 }
+                if (args.early_release) {
+                    // The warp's whole share of this half (32 lanes x 128 columns) goes to REGISTERS first (4 x 32 fp32 per
+                    // thread: the epilogue warps have the budget, 1 CTA per SM), the half is handed back to the MMA warp
+                    // at once, and only then do the four chunks trickle through the staging tile at the pace of the L2
+                    // reductions. TMEM is free ~0.5 k cycles after the half completes instead of after three reductions.
+                    uint32_t v[4][32];
+                    const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + h * BN + colh * (BN / 2);
+#pragma unroll
+                    for (int ci = 0; ci < 4; ++ci) tmem_ld32(taddr + ci * 32, v[ci]);
+                    tmem_ld_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader + 8u * h);
+#pragma unroll
+                    for (int ci = 0; ci < 4; ++ci, ++chunk_no) {
+                        const uint32_t buf = buf0 + (chunk_no % kEpiBufs) * kEpiWarpBytes;
+                        if (lane == 0) bulk_wait_read<kEpiBufs - 1>(); // the reduction that last used this staging tile has read it
+                        __syncwarp();
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + row * 128u + ((c ^ (row & 7u)) << 4)),
+                                         "r"(v[ci][4 * c + 0]), "r"(v[ci][4 * c + 1]), "r"(v[ci][4 * c + 2]), "r"(v[ci][4 * c + 3])
+                                         : "memory");
+                        fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            int tc[5];
+                            tile_coords_t<PLAIN>(args.cc, rank_c, false, m0 + h * BMH, n0 + ci * 32, batch, tc);
+                            if ((args.hints & 2u) && rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
+                            else tma_reduce_add_tile(&map_c, buf, rank_c, tc);
+                            bulk_commit();
+                        }
+                    }
+                    continue;
+                }
 #pragma unroll 1
                 for (int ci = 0; ci < 4; ++ci, ++chunk_no) {
                     const uint32_t buf = buf0 + (chunk_no % kEpiBufs) * kEpiWarpBytes;
@@ -761,6 +797,7 @@ int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream) {
     a.group_w = std::max(1u, static_cast<uint32_t>(std::max(1, knob(K_GEMM_GROUP_M))) / 2);
     a.debug = static_cast<uint32_t>(knob(K_GEMM_DEBUG));
     a.hints = static_cast<uint32_t>(knob(K_GEMM_HINTS));
+    a.early_release = knob(K_GEMM_EARLY_RELEASE) != 0 ? 1u : 0u;
     const uint32_t unit_begin = p.full_range ? 0u : p.tile_begin / 4;
     const uint32_t units_all = p.full_range ? a.mbw * a.nb * static_cast<uint32_t>(std::max(p.batch, 1)) : p.tile_end / 4 - unit_begin;
     if (units_all == 0) return TLB_OK;

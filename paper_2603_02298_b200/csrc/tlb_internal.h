@@ -62,6 +62,7 @@ enum KnobId {
     K_COPY_TMA_CTAS,    // its CTAs per SM
     K_GEMM_CHUNK_WAVES, // waves of pair tiles per launch of the wide plan (0: one launch whatever the range)
     K_GEMM_MCAST,       // wide plan in clusters of 4 with A multicast between two pair tiles: 0 never, 1 when it applies, -1 auto
+    K_GEMM_EARLY_RELEASE, // wide plan, fp32 C: accumulator halves go to registers and are released before their reductions
     K_GEMM_PACK,        // 1: operands / C that no tensor map can address are packed and run on tcgen05 (default), 0: SIMT plan
     K_GEMM_PACK_MIN,    // log2 of the smallest M*N*K that takes the packed plan
     K_COUNT
