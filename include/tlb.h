@@ -119,7 +119,9 @@ uint64_t tlb_launch_count(void);
  * "gather", "ordered", "aliased", "umma_2sm_wide", "eval_warp32", ...). */
 const char* tlb_last_plan(void);
 
-/* Tuning / debugging knobs. The environment variables TLB_<NAME> are read once, at the first call into the library;
+/* Tuning / debugging knobs (GEMM_WIDE, GEMM_SPLIT_TAIL, GEMM_CHUNK_WAVES, GEMM_MCAST, GEMM_EARLY_RELEASE, GEMM_PACK,
+ * GEMM_PACK_MIN, COPY_TMA, COPY_TMA_STAGES, COPY_TMA_CTAS, PDL, HOST_PANEL, ...: the table is in csrc/tlb_lower.cpp).
+ * The environment variables TLB_<NAME> are read once, at the first call into the library;
  * afterwards a knob changes only through this call (value NULL or "" restores the default). `name` is the variable
  * name with or without the TLB_ prefix, e.g. tlb_config_set("GEMM_WIDE", "1"). Unknown names: TLB_ERR_CONTRACT.
  * Launch paths read knobs with one atomic load (no getenv). */
@@ -172,7 +174,16 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
 /* tla::copy(src, dst) (tensor.hpp:195-199): for i in [i_begin, i_end) ascending,
  * dst(i) = src(i). Pass i_begin = 0, i_end = UINT64_MAX for the whole domain. Last-writer-wins
  * order is preserved for non-injective destinations. Sizes must agree (contract_error).
- * The planner picks contiguous / tiled (swizzled smem staging, optionally TMA-fed) / gather kernels. */
+ * The planner works on the common refinement of the two layouts and picks (tlb_last_plan()):
+ *   "vec"           one refined mode contiguous on both sides: <= 16-byte vectors
+ *   "tiled"         transposes / permutes: 128-byte swizzle-staged tiles (Swizzle<3,4,3>), 128-bit accesses both ways;
+ *                   "tiled_u" with cell-sized accesses for unaligned bases / leading dimensions, "tiled_s" along the
+ *                   smallest-stride modes of layouts WITHOUT a unit stride, "tiled_tma" the TMA-fed persistent variant
+ *   "gather_vec"    anything else whose low run (max_common_vector, also for Xor layouts) is >= 2 cells: one evaluation
+ *                   of both layouts per <= 16-byte vector;  "gather": one cell per thread
+ *   "last_writer+P" non-injective destination whose aliasing is only stride-0 (broadcast) modes: the injective copy
+ *                   (plan P) of the slice at their last coordinates;  "ordered": overlapping strides, winner election
+ *   "aliased" / "serial"  source and destination overlap in memory (see Aliasing above). */
 int tlb_copy(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, void* stream);
 /* Runs the contract checks and the planner of tlb_copy without a device and without launching anything;
  * the plan it would pick is then available from tlb_last_plan(). Pointers are only inspected for
@@ -215,10 +226,16 @@ int tlb_tensormap_fetch_tile(const void* tensormap_128B, int rank, const int32_t
  * aligned to 4 tiles keep the wide (512 x 256) tcgen05 plan, ranges aligned to 2 the 256 x 256 plan. The ids
  * refer to the tiling of the plan the library selects, which runs the problem transposed when C is
  * m-contiguous; every range partition of [0, count) covers C exactly once.
- * Operands whose modes coalesce to one stride each with either mode contiguous (K-major "T" or MN-major "N":
- * the TN, NT and NTT rows of PAPER.md:1766-1771) and an M- or N-contiguous C run on tcgen05 (TMA -> swizzled
- * smem -> UMMA -> TMEM -> TMA reduce-add); every other layout family (BLIS strides, GETT folded modes, Xor,
- * leading dimensions TMA cannot address) runs on the layout-evaluating SIMT kernel.
+ * Every operand family of PAPER.md:1766-1771 runs on tcgen05 (TMA -> swizzled smem -> UMMA -> TMEM -> TMA reduce-add):
+ * K-major "T" and MN-major "N" operands (TN, NT, NTT rows) with an M- or N-contiguous C directly; hierarchical modes
+ * (GETT-folded operands and C, CONV as a GEMM over the im2col LAYOUT of the input) through rank-4/5 tensor maps derived
+ * from the divided layouts; layouts no tensor map can address (BLIS strides on every mode, Xor strides, rows that are not
+ * multiples of 16 bytes) through the PACKED plan: tlb_copy packs A, B and C into TMA-addressable panels on a stream-ordered
+ * workspace, the tcgen05 plan runs on them, tlb_copy scatters C back ("packed+<plan>"; whole single problems of at least
+ * 2^GEMM_PACK_MIN MACs). Small problems of that kind, tile ranges of them and the int64 value type run on the
+ * layout-evaluating SIMT kernel.
+ * Long tile ranges are cut into several launches of about GEMM_CHUNK_WAVES waves (tlb_launch_count counts them): the
+ * workers of one persistent launch drift apart and stop sharing operand panels in L2.
  * Partial tiles of the last wave are summed by several CTA pairs through L2 reductions, so fp32 sums are not
  * bitwise reproducible from run to run unless TLB_GEMM_SPLIT_TAIL=0 is set in the environment.
  * A.elem_bytes = B.elem_bytes = 2; C.elem_bytes = 4 (fp32 C) or 2 (C in the operands' type: fp32 accumulation, one
