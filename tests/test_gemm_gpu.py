@@ -806,3 +806,41 @@ def test_gemm_wide_multicast_plan_stream_k_exact(tlb_config):
     assert host.gemm_bf16((ta, None), (tb, None), (tc, None)) == "umma_2sm_wide_mc"
     torch.cuda.synchronize()
     assert torch.equal(c.double(), ref)
+
+
+def test_c4_full_size_64_batches_by_linearity():
+    """Config C4 at BASELINE's full size: 64 x (8192 x 8192 x 8192), batch strides, TN with m-contiguous C, one call (cut into
+    one launch per batch by the library). The oracle cannot run 7e13 MACs, so the check is a size-independent property of
+    the exact integer fills (every partial sum < 2^24, fp32 accumulation exact in any order): for every batch,
+    row sums and column sums of C - C0 equal the matrix-vector products with the operands' column sums (linearity),
+    computed exactly in fp64 / int64. A wrong, missing or doubled tile changes at least one row sum and one column sum."""
+    M = N = K = 8192
+    B = 64
+    i = torch.arange(M, device="cuda").view(M, 1)
+    p = torch.arange(K, device="cuda").view(1, K)
+    a = torch.empty(B, M, K, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty(B, N, K, dtype=torch.bfloat16, device="cuda")
+    for bi in range(B):
+        a[bi] = ((i * 7 + p * 3 + 1 + bi) % 11).to(torch.bfloat16)
+        b[bi] = ((i * 5 + p * 2 + 2 + 3 * bi) % 13).to(torch.bfloat16)
+    c = torch.ones(B, N, M, dtype=torch.float32, device="cuda")           # C(m, n) at m + M n: stored as [n][m]
+    ta = host.make_tensor(L(f"({M},{K}):({K},1)").lower(ranked=True), a.data_ptr(), a.numel(), 2)
+    tb = host.make_tensor(L(f"({N},{K}):({K},1)").lower(ranked=True), b.data_ptr(), b.numel(), 2)
+    tc = host.make_tensor(L(f"({M},{N}):(1,{M})").lower(ranked=True), c.data_ptr(), c.numel(), 4)
+    lib = abi.load()
+    n0 = lib.tlb_launch_count()
+    assert host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 0, B) == "umma_2sm_wide"
+    torch.cuda.synchronize()
+    assert lib.tlb_launch_count() - n0 == B                                 # one launch per batch (GEMM_CHUNK_WAVES)
+    for bi in range(B):
+        ad, bd = a[bi].double(), b[bi].double()
+        cd = c[bi].double() - 1.0                                           # [n][m]
+        # sum over n of C(m, n) = sum_k A(m, k) * colsum_B(k); sum over m of C(m, n) = sum_k B(n, k) * colsum_A(k)
+        assert torch.equal(cd.sum(dim=0), ad @ bd.sum(dim=0)), f"batch {bi}: row sums"
+        assert torch.equal(cd.sum(dim=1), bd @ ad.sum(dim=0)), f"batch {bi}: column sums"
+    # and one sampled tile of the last batch against the flat restatement
+    an = a[B - 1].view(torch.int16).cpu().numpy().view(np.uint16)
+    bn = b[B - 1].view(torch.int16).cpu().numpy().view(np.uint16)
+    want = np.ones((N, M), dtype=np.float32)
+    ou.orc_gemm_bf16_tn_flat(an.ravel(), K, bn.ravel(), K, want.ravel(), M, M, N, K, 512, 520, 7680, 7688)
+    assert (c[B - 1].cpu().numpy()[7680:7688, 512:520] == want[7680:7688, 512:520]).all()
