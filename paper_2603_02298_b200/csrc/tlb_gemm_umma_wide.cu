@@ -673,6 +673,11 @@ bool umma_wide_applies(const UmmaProblem& p) {
         const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
                                                  : (p.tile_end - p.tile_begin) / 4;
         if (wide_knob != 1 && pair_tiles < 48) return false;
+        // short k-loops: a 512 x 256 tile flushes 256 KiB per CTA after only K / 64 k-blocks and cannot hide it (TMEM is
+        // full), the 256 x 256 plan overlaps its flush with the next tile. Measured crossover (round 2, 4096^2 and 8192^2
+        // outputs): K = 2048 the 256 x 256 plan is 13 % ahead, K = 3072 0-3 %, K = 4096 a tie, from K = 5120 the wide plan
+        // leads (6144^3 +4 %, 3072^2 x 8192 +7 %).
+        if (wide_knob != 1 && (p.K + BK - 1) / BK < 64) return false;
     }
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
     if (p.c_fold_tma) return base_ok && (!p.c_16 || p.batch <= 1 || p.c_bs % 8 == 0);

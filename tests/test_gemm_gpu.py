@@ -348,10 +348,27 @@ def test_gemm_wide_plan_tile_ranges_partition_the_output(force_wide):
     assert abi.load().tlb_last_plan().decode() == "umma_2sm_wide"
 
 
-def test_gemm_wide_plan_takes_large_problems_with_an_odd_number_of_row_blocks():
-    """ceil(M/256) odd: the full range of a large problem still runs 512 x 256 pair tiles (the last one is clipped by the
-    TMA bounds); 3 x 16 = 48 pair tiles."""
+def test_gemm_wide_plan_takes_large_problems_with_an_odd_number_of_row_blocks(force_wide):
+    """ceil(M/256) odd: the full range of a problem still runs 512 x 256 pair tiles (the last one is clipped by the
+    TMA bounds); 3 x 16 = 48 pair tiles. (Forced: with K = 64 the planner would keep the 256 x 256 plan.)"""
     assert _bf16_case("(1280,64):(64,1)", "(4096,64):(64,1)", "(1280,4096):(4096,1)", kat=True) == "umma_2sm_wide"
+
+
+def test_gemm_plan_selection_by_k_and_size():
+    """The planner's crossover (measured, tlb_gemm_umma_wide.cu): the 512 x 256 plan needs at least 48 pair tiles AND 64
+    k-blocks (K >= 4096); shorter k-loops keep the 256 x 256 plan, whose flush overlaps the next tile. Host-side decision,
+    checked through tlb_last_plan on zero-filled operands (nothing to compare: the parity tests cover both kernels)."""
+    def plan(M, N, K):
+        a = torch.zeros(M * K, dtype=torch.bfloat16, device="cuda")
+        b = torch.zeros(N * K, dtype=torch.bfloat16, device="cuda")
+        c = torch.zeros(M * N, dtype=torch.float32, device="cuda")
+        return host.gemm_bf16(host.tensor_of(f"({M},{K}):({K},1)", a.view(torch.int16), ranked=True),
+                              host.tensor_of(f"({N},{K}):({K},1)", b.view(torch.int16), ranked=True),
+                              host.tensor_of(f"({M},{N}):({N},1)", c, ranked=True))
+    assert plan(4096, 4096, 4096) == "umma_2sm_wide"
+    assert plan(4096, 4096, 2048) == "umma_2sm"
+    assert plan(2048, 2048, 8192) == "umma_2sm"          # 32 pair tiles
+    assert plan(3072, 4096, 4096) == "umma_2sm_wide"     # 96 pair tiles
 
 
 def test_gemm_wide_plan_falls_back_when_it_does_not_apply(tlb_config):
@@ -801,6 +818,7 @@ def test_gemm_wide_multicast_plan_stream_k_exact(tlb_config):
     ta = host.make_tensor(L(f"({M},{K}):({K},1)").lower(ranked=True), a.data_ptr(), a.numel(), 2)
     tb = host.make_tensor(L(f"({N},{K}):({K},1)").lower(ranked=True), b.data_ptr(), b.numel(), 2)
     tlb_config("GEMM_MCAST", "1")
+    tlb_config("GEMM_WIDE", "1")
     c = torch.ones(M, N, dtype=torch.float32, device="cuda")
     tc = host.make_tensor(L(f"({M},{N}):({N},1)").lower(ranked=True), c.data_ptr(), c.numel(), 4)
     assert host.gemm_bf16((ta, None), (tb, None), (tc, None)) == "umma_2sm_wide_mc"
