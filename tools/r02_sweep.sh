@@ -1,7 +1,10 @@
 #!/bin/bash
-for s in "4096 4096 2048" "4096 4096 3072" "4096 4096 4096" "4096 4096 5120" "8192 8192 2048" "8192 8192 3072" "8192 8192 4096" "8192 4096 4096" "2048 2048 8192" "3072 3072 8192"; do
-  set -- $s
-  echo "== $s"
-  TLB_GEMM_WIDE=1 timeout 120 python tools/gemm_probe.py $1 $2 $3 50 2>&1 | tail -1
-  TLB_GEMM_WIDE=0 timeout 120 python tools/gemm_probe.py $1 $2 $3 50 2>&1 | tail -1
-done
+timeout 1500 python -m pytest tests -m gpu -q --durations=25 2>&1 | tail -45
+echo "== bench --gpus 2 on a 1-GPU box must fail loudly"
+timeout 300 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --quick > gpurun_out/b_2gpu.json 2> gpurun_out/b_2gpu.err; echo "exit $?"; tail -3 gpurun_out/b_2gpu.err
+echo "== bench --gpus 2 --share-gpu (functional)"
+timeout 600 python bench.py --gpus 2 --share-gpu --steps 3 --warmup 3 --no-cpu --quick --only C1,C5 > gpurun_out/b_2share.json 2> gpurun_out/b_2share.err; echo "exit $?"; python -c "
+import json
+d=json.load(open('gpurun_out/b_2share.json'))
+print(d['n_gpus'], d['verify'], [ (e['name'], e['n_gpus'], round(e['value'],1)) for e in d['other_configs']])
+"
