@@ -862,3 +862,50 @@ def test_c4_full_size_64_batches_by_linearity():
     want = np.ones((N, M), dtype=np.float32)
     ou.orc_gemm_bf16_tn_flat(an.ravel(), K, bn.ravel(), K, want.ravel(), M, M, N, K, 512, 520, 7680, 7688)
     assert (c[B - 1].cpu().numpy()[7680:7688, 512:520] == want[7680:7688, 512:520]).all()
+
+
+def _fuzz_gemm_case(rng):
+    """One random GEMM problem over the layout families of test_tensor.cpp:176-195: K- or MN-major operands with padded
+    (aligned or unaligned) leading dimensions, optionally a mode folded into two leaves (GETT) or strided (BLIS), C m- or
+    n-contiguous."""
+    M, N, K = int(rng.integers(1, 18)) * 64, int(rng.integers(1, 14)) * 64, int(rng.integers(1, 40)) * 16
+    if rng.random() < 0.3:
+        M, N, K = M - int(rng.integers(0, 60)), N - int(rng.integers(0, 60)), K - int(rng.integers(0, 15))
+
+    def operand(rows, k):
+        kind = rng.choice(["k_major", "mn_major", "folded", "strided"], p=[0.4, 0.3, 0.2, 0.1])
+        pad = int(rng.choice([0, 8, 24, 3]))
+        if kind == "k_major":
+            return f"({rows},{k}):({k + pad},1)"
+        if kind == "mn_major":
+            return f"({rows},{k}):(1,{rows + pad})"
+        if kind == "folded" and rows % 128 == 0 and k % 64 == 0:
+            r0, k0 = 64, 32                                  # rows = (r0, rows / r0), k = (k0, k / k0): four leaves
+            return f"(({r0},{rows // r0}),({k0},{k // k0})):(({k0},{k0 * r0 * (k // k0)}),(1,{k0 * r0}))"
+        if kind == "strided":
+            return f"({rows},{k}):(3,{3 * rows + 5})"
+        return f"({rows},{k}):({k + pad},1)"
+
+    la, lb = operand(M, K), operand(N, K)
+    pad = int(rng.choice([0, 4, 12, 1]))
+    lc = f"({M},{N}):({N + pad},1)" if rng.random() < 0.5 else f"({M},{N}):(1,{M + pad})"
+    return la, lb, lc
+
+
+_FUZZ_PLANS = set()
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_gemm_fuzz_layout_families_against_the_oracle(seed):
+    """Differential fuzz through every GEMM plan the planner may pick (tcgen05 1-CTA / 2-CTA / wide, register and TMA
+    epilogues, rank-4/5 tensor maps, packed, SIMT): 8 random problems per seed against the sequential-k restatement,
+    bf16 and fp16, exact where the plan keeps the reference's order, within the stated tolerance elsewhere."""
+    rng = np.random.default_rng(1000 + seed)
+    plans = set()
+    for _ in range(8):
+        la, lb, lc = _fuzz_gemm_case(rng)
+        plans.add(_bf16_case(la, lb, lc, kat=bool(rng.random() < 0.3), seed=int(rng.integers(1 << 30)), f16=bool(rng.random() < 0.3)))
+    _FUZZ_PLANS.update(plans)
+    if seed == 19:   # the fuzz must actually reach the tensor-core plans, the packed plan and the SIMT plan
+        kinds = {p.split("+")[0].replace("_regs", "") for p in _FUZZ_PLANS}
+        assert {"umma_2sm", "umma_2sm_wide", "packed"} <= kinds and any(k.startswith("simt") for k in kinds), _FUZZ_PLANS
