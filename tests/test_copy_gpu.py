@@ -170,6 +170,61 @@ def test_copy_random_layout_pairs_vs_oracle():
         done += 1
 
 
+def _structured_pair(rng):
+    """A (source, destination) pair over one shape of 3-5 power-of-two modes: each side assigns compact strides in its own
+    random mode order (permutes / transposes), optionally scaled (no unit stride), padded, with a reversed mode, a
+    broadcast (stride-0) destination mode, or a swizzled (Xor) destination. Returns (src, dst, src_origin, dst_origin, slack)."""
+    if rng.random() < 0.15:
+        r = int(rng.choice([2, 8, 32]))
+        order = rng.permutation(3)
+        ext = [128, 8, r]
+        st = [0, 0, 0]
+        acc = 1
+        for m in order:
+            st[m] = acc
+            acc *= ext[m]
+        return f"(128,8,{r}):({st[0]},{st[1]},{st[2]})", f"(128,8,{r}):(f1,f144,f1024)", 0, 0, 0
+    nm = int(rng.integers(2, 5))
+    ext = [int(rng.choice([4, 16, 32, 64, 128, 256])) for _ in range(nm)]
+    while np.prod(ext) > (1 << 18):
+        ext[int(np.argmax(ext))] //= 2
+    def side(scale_choices, allow_zero):
+        order = rng.permutation(nm)
+        scale = int(rng.choice(scale_choices))
+        st = [0] * nm
+        acc = scale
+        for k, m in enumerate(order):
+            st[m] = acc
+            acc *= ext[m]
+            if k == nm - 2 and rng.random() < 0.3:
+                acc += int(rng.choice([1, 4, 8])) * scale          # padded outermost mode
+        origin = 0
+        if rng.random() < 0.12:                                    # one reversed mode
+            m = int(rng.integers(nm))
+            origin = (ext[m] - 1) * st[m]
+            st[m] = -st[m]
+        if allow_zero and rng.random() < 0.15:
+            st[int(rng.integers(nm))] = 0
+        return st, origin
+    ss, so = side([1, 1, 1, 2, 3], False)
+    ds, do = side([1, 1, 1, 1, 5], True)
+    shape = ",".join(str(e) for e in ext)
+    mk = lambda st: f"({shape}):({','.join(str(x) for x in st)})"
+    return mk(ss), mk(ds), so, do, max(so, do)
+
+
+def test_copy_structured_fuzz_reaches_every_plan():
+    """Differential fuzz over permutes / transposes / strided / padded / reversed / broadcast / swizzled layout pairs large
+    enough for the staged plans, all cell sizes, against the oracle; the run must reach every family of plans."""
+    rng = np.random.default_rng(11)
+    plans = set()
+    for case in range(220):
+        s, d, so, do, slack = _structured_pair(rng)
+        plans.add(run_copy_case(s, d, int(rng.choice([1, 2, 4, 8, 16])), src_origin=so, dst_origin=do, slack=slack, seed=case))
+    kinds = {p.split("+")[0] for p in plans}
+    assert {"vec", "tiled", "gather", "gather_vec", "last_writer"} <= kinds and kinds & {"tiled_u", "tiled_s"}, plans
+
+
 def test_copy_xor_layouts():
     run_copy_case("(8,8):(f1,f9)", "64:1", 8)
     run_copy_case("64:1", "(8,8):(f1,f9)", 4)
