@@ -127,6 +127,11 @@ const char* tlb_last_plan(void);
  * Launch paths read knobs with one atomic load (no getenv). */
 int tlb_config_set(const char* name, const char* value);
 
+/* Workspaces (winner arrays of the "ordered" copy plan, packed GEMM panels, status words) come from a stream-ordered
+ * memory pool the library owns per device; freed blocks stay in the pool so that a call repeated in a loop does not go
+ * back to the driver. This releases the pool's unused memory down to keep_bytes (cudaMemPoolTrimTo) on the current device. */
+int tlb_workspace_trim(uint64_t keep_bytes);
+
 /* ---- (1) lowering: host layout -> device evaluator parameters --------- */
 /* Replaces the per-element call chain Tensor::operator() -> layout_eval -> eval_rec ->
  * idx2crd/eval_leaf (tensor.hpp:119, layout.hpp:49-74) with a one-time flattening

@@ -76,6 +76,7 @@ int require_device();
 // copy in a loop) reuses the pool's memory instead of returning it to the driver at every synchronisation. Freed with
 // cudaFreeAsync. The process's default pool is left alone.
 cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t stream);
+cudaError_t ws_trim(size_t keep_bytes);
 int sm_count();
 
 // ---- host helpers over descriptors -------------------------------------------

@@ -77,9 +77,23 @@ int require_device() {
     return TLB_OK;
 }
 
+namespace {
+std::mutex g_ws_mu;
+cudaMemPool_t g_ws_pools[64] = {};
+} // namespace
+
+cudaError_t ws_trim(size_t keep_bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaSuccess;
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    return g_ws_pools[dev] ? cudaMemPoolTrimTo(g_ws_pools[dev], keep_bytes) : cudaSuccess;
+}
+
 cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t stream) {
-    static std::mutex mu;
-    static cudaMemPool_t pools[64] = {};
+    std::mutex& mu = g_ws_mu;
+    cudaMemPool_t* pools = g_ws_pools;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -363,6 +377,12 @@ int tlb_abi_version(void) { return TLB_ABI_VERSION; }
 const char* tlb_last_error(void) { return tlb::g_error.c_str(); }
 uint64_t tlb_launch_count(void) { return tlb::g_launches.load(std::memory_order_relaxed); }
 const char* tlb_last_plan(void) { return tlb::g_plan; }
+
+int tlb_workspace_trim(uint64_t keep_bytes) {
+    if (tlb::require_device() != TLB_OK) return TLB_ERR_CUDA;
+    TLB_CUDA(tlb::ws_trim(static_cast<size_t>(keep_bytes)));
+    return TLB_OK;
+}
 
 int tlb_config_set(const char* name, const char* value) {
     if (!name) return tlb::fail(TLB_ERR_CONTRACT, "tlb_config_set: null name");
