@@ -720,7 +720,7 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
                                  "peak_source": f"{pk['_source']} sustained cuBLAS bf16 (step >= 50 ms)",
                                  "frac_of_nominal_2250": per_gpu / 2250.0,
                                  "algorithmic_flop_per_launch": 2.0 * M * M * M * nb,
-                                 "traffic_note": "per 8192^3 batch (one of the launch's batches_this_rank)"}})
+                                 "traffic_note": "per 8192^3 batch = per launch (the call is cut into one launch per batch)"}})
         del a, b, c
         torch.cuda.empty_cache()
     return out
