@@ -705,7 +705,9 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
         tb = host.tensor_of(f"({M},{M}):({M},1)", b.view(torch.int16), ranked=True)
         tc = host.tensor_of(f"({M},{M}):(1,{M})", c, ranked=True)
         k4 = 3
+        n_l0 = lib.tlb_launch_count()
         sec = timed(torch, dist, world, lambda i: host.gemm_bf16_batched(ta, tb, tc, M * M, M * M, M * M, 0, nb), k4, 3)
+        launches_c4 = int(lib.tlb_launch_count() - n_l0) // (k4 + 3)   # the call is cut into launches of ~8 waves (one per batch)
         flops = 2.0 * M * M * M * 64
         tf = flops * k4 / sec / 1e12
         per_gpu = 2.0 * M * M * M * nb / (sec / k4) / 1e12
@@ -719,7 +721,7 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
                                  "frac": per_gpu / sustained, "traffic": tr, "traffic_source": tr_src, "kernel": "umma_wide_kernel",
                                  "peak_source": f"{pk['_source']} sustained cuBLAS bf16 (step >= 50 ms)",
                                  "frac_of_nominal_2250": per_gpu / 2250.0,
-                                 "algorithmic_flop_per_launch": 2.0 * M * M * M * nb,
+                                 "algorithmic_flop_per_launch": 2.0 * M * M * M, "launches_per_step": launches_c4,
                                  "traffic_note": "per 8192^3 batch = per launch (the call is cut into one launch per batch)"}})
         del a, b, c
         torch.cuda.empty_cache()
