@@ -1,10 +1,10 @@
 #!/bin/bash
-timeout 1500 python -m pytest tests -m gpu -q --durations=25 2>&1 | tail -45
-echo "== bench --gpus 2 on a 1-GPU box must fail loudly"
-timeout 300 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --quick > gpurun_out/b_2gpu.json 2> gpurun_out/b_2gpu.err; echo "exit $?"; tail -3 gpurun_out/b_2gpu.err
-echo "== bench --gpus 2 --share-gpu (functional)"
-timeout 600 python bench.py --gpus 2 --share-gpu --steps 3 --warmup 3 --no-cpu --quick --only C1,C5 > gpurun_out/b_2share.json 2> gpurun_out/b_2share.err; echo "exit $?"; python -c "
-import json
-d=json.load(open('gpurun_out/b_2share.json'))
-print(d['n_gpus'], d['verify'], [ (e['name'], e['n_gpus'], round(e['value'],1)) for e in d['other_configs']])
-"
+for rep in 1 2; do
+for o in 0 1; do
+  echo "== SK_ORDER=$o"
+  TLB_GEMM_SK_ORDER=$o timeout 120 python tools/gemm_probe.py 4096 4096 4096 50 2>&1 | tail -1
+  TLB_GEMM_SK_ORDER=$o timeout 120 python tools/gemm_probe.py 8192 8192 8192 20 2>&1 | tail -1
+  TLB_GEMM_SK_ORDER=$o timeout 120 python tools/gemm_probe.py 4096 4096 4096 3000 2>&1 | tail -1
+done
+done
+TLB_GEMM_SK_ORDER=1 timeout 600 python -m pytest tests/test_gemm_gpu.py -m gpu -q -x -k "wide_plan_kat or c2 or chunked or fuzz" 2>&1 | tail -3
