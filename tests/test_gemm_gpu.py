@@ -909,3 +909,21 @@ def test_gemm_fuzz_layout_families_against_the_oracle(seed):
     if seed == 19:   # the fuzz must actually reach the tensor-core plans, the packed plan and the SIMT plan
         kinds = {p.split("+")[0].replace("_regs", "") for p in _FUZZ_PLANS}
         assert {"umma_2sm", "umma_2sm_wide", "packed"} <= kinds and any(k.startswith("simt") for k in kinds), _FUZZ_PLANS
+
+
+@pytest.mark.parametrize("shape", [
+    ("(1,64):(64,1)", "(256,64):(64,1)", "(1,256):(256,1)"),        # one row of C
+    ("(256,64):(64,1)", "(1,64):(64,1)", "(256,1):(1,256)"),        # one column of C
+    ("(128,1):(1,128)", "(128,1):(1,128)", "(128,128):(128,1)"),    # K = 1: an outer product
+    ("(1,1):(1,1)", "(1,1):(1,1)", "(1,1):(1,1)"),                  # a single multiply-add
+    ("(8,8):(8,1)", "(8,8):(8,1)", "(8,8):(8,1)"),                  # far below one tile
+    ("((1,130),(1,72)):((5,72),(7,1))", "(65,72):(72,1)", "(130,(65,1)):(65,(1,9))"),   # extent-1 leaves inside the modes
+    ("(257,72):(72,1)", "(513,72):(72,1)", "(257,513):(520,1)"),    # one row / column past a tile boundary
+])
+def test_gemm_degenerate_and_ragged_extents(shape):
+    """Degenerate extents (single rows / columns, K = 1, extent-1 leaves) and shapes one past a tile boundary, on whatever
+    plan the planner picks, in both value types: exact on the integer fills, within tolerance on random data."""
+    _bf16_case(*shape, kat=True)
+    _bf16_case(*shape, kat=False, seed=61)
+    _bf16_case(*shape, kat=False, seed=67, f16=True)
+    _bf16_case(*shape, kat=True, path=1)                             # and on the SIMT plan
