@@ -497,15 +497,15 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
                 p.force_wide = tm == 512 ? 1 : -1;
                 if (!p.full_range) return fail(TLB_ERR_CONTRACT, "tlb_gemm_*_tiled: whole problems only");
             }
-            const bool mn_major = p.a_mn || p.b_mn;
-            if ((!mn_major && !p.c_16) || umma_wide_applies(p)) {
+            // MN-major operands run on both tcgen05 plans; a 2-byte C needs the wide plan's epilogue
+            if (!p.c_16 || umma_wide_applies(p)) {
                 if (p.cta_group == 2 && !even)
                     return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
                 return umma_gemm_launch(p, stream);
             }
-            // MN-major operands and 2-byte C are handled by the wide plan only; anything it does not cover runs on the SIMT plan
+            // a 2-byte C is handled by the wide plan only; what it does not cover runs on the packed or the SIMT plan
             if (g_gemm_path == 2 || g_gemm_path == 3)
-                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: MN-major operands need the wide tcgen05 plan (whole pair tiles, n-contiguous C)");
+                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: a 2-byte C needs the wide tcgen05 plan (whole pair tiles, n-contiguous C)");
         } else if (g_gemm_path == 2 || g_gemm_path == 3) {
             return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: the forced tcgen05 path does not apply to these layouts");
         }

@@ -28,6 +28,8 @@
 #include <cstring>
 #include <vector>
 
+#include <type_traits>
+
 #include <cuda.h>
 
 #include "tlb_internal.h"
@@ -93,6 +95,8 @@ struct UmmaArgs {
                                    // 4 = no staging stores, 8 = no TMA store
     long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
     uint32_t ab_f16;               // operands are fp16 (A / B format fields of the instruction descriptor = 0)
+    uint32_t a_mn, b_mn;           // operand is MN-major: staged as 64-row chunks of [64 k][128 B] (the map's dimension 0 is the
+                                   // row index), MN-major UMMA descriptors (LBO = 8 KiB between chunks, idesc bits 15 / 16)
     long long* clk;                // optional (TLB_GEMM_CLOCK=1): CTA 0 stamps {clock64, globaltimer} at entry and exit
     // how a tile's (row, k | column, batch) start turns into the coordinates of the layout-derived tensor maps
     int32_t rank_a, rank_b, rank_c;
@@ -230,8 +234,24 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             if (lane == 0) TLB_TRACE(8 + item * 10 + 0);
             // row / batch coordinates of this tile's operand boxes: once per tile, k refreshed per k-block
             int ta[5], tb[5];
-            tile_coords_t<PLAIN>(args.ca, rank_a, false, m0, 0, batch, ta);
-            tile_coords_t<PLAIN>(args.cb, rank_b, false, n0, 0, batch, tb);
+            if (!args.a_mn) tile_coords_t<PLAIN>(args.ca, rank_a, false, m0, 0, batch, ta);
+            if (!args.b_mn) tile_coords_t<PLAIN>(args.cb, rank_b, false, n0, 0, batch, tb);
+            // one operand tile of this k-block: a single box (K-major) or 64-row chunks of [64 k][64 rows] (MN-major)
+            auto load_operand = [&](auto cg2, bool mn, const void* map, const TmaCoord* tcd, int rk, uint32_t dst, uint32_t bar,
+                                    int row0, int rows, int kb, int* tk, bool hint) {
+                constexpr bool CG2 = decltype(cg2)::value;
+                if (!mn) {
+                    tile_coords_k<PLAIN>(tcd, rk, kb * BK, tk);
+                    if (hint) tma_load_tile_hint<CG2>(dst, map, bar, rk, tk, pol_ab);
+                    else tma_load_tile<CG2>(dst, map, bar, rk, tk);
+                } else {
+                    int tc[5];
+                    for (int c = 0; c < rows / 64; ++c) {
+                        tile_coords_t<PLAIN>(tcd, rk, true, row0 + c * 64, kb * BK, batch, tc);
+                        tma_load_tile<CG2>(dst + c * 8192, map, bar, rk, tc);
+                    }
+                }
+            };
             for (int kb = kb0; kb < kb1; ++kb) {
                 // Stages are released in pairs (one commit per 8 MMAs). The MMA thread commits on the LEADER's
                 // barrier only; the leader's producer relays each release to the peer CTA's barrier.
@@ -244,29 +264,15 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         if (leader) mbar_arrive(full_bar(stage)); // timing experiment: stale smem, no TMA traffic
                     } else if constexpr (CG == 1) {
                         mbar_expect_tx(full_bar(stage), C::kStageBytes);
-                        tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, ta);
-                        tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tb);
-                        if (hint_ab) {
-                            tma_load_tile_hint<false>(a_stage(stage), &map_a, full_bar(stage), rank_a, ta, pol_ab);
-                            tma_load_tile_hint<false>(b_stage(stage), &map_b, full_bar(stage), rank_b, tb, pol_ab);
-                        } else {
-                            tma_load_tile<false>(a_stage(stage), &map_a, full_bar(stage), rank_a, ta);
-                            tma_load_tile<false>(b_stage(stage), &map_b, full_bar(stage), rank_b, tb);
-                        }
+                        load_operand(std::false_type{}, args.a_mn != 0, &map_a, args.ca, rank_a, a_stage(stage), full_bar(stage), m0, BM, kb, ta, hint_ab);
+                        load_operand(std::false_type{}, args.b_mn != 0, &map_b, args.cb, rank_b, b_stage(stage), full_bar(stage), n0, C::kBRows, kb, tb, hint_ab);
                     } else {
                         // The leader's barrier expects the bytes of BOTH CTAs; the peer's TMA may complete before
                         // this expect_tx is issued (tx-count goes transiently negative, as with multicast).
                         const uint32_t lbar = lbar0 + 8u * stage;
-                        tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, ta);
-                        tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tb);
                         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kStageBytes);
-                        if (hint_ab) {
-                            tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, rank_a, ta, pol_ab);
-                            tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, rank_b, tb, pol_ab);
-                        } else {
-                            tma_load_tile<true>(a_stage(stage), &map_a, lbar, rank_a, ta);
-                            tma_load_tile<true>(b_stage(stage), &map_b, lbar, rank_b, tb);
-                        }
+                        load_operand(std::true_type{}, args.a_mn != 0, &map_a, args.ca, rank_a, a_stage(stage), lbar, m0, BM, kb, ta, hint_ab);
+                        load_operand(std::true_type{}, args.b_mn != 0, &map_b, args.cb, rank_b, b_stage(stage), lbar, n0, C::kBRows, kb, tb, hint_ab);
                     }
                 }
                 __syncwarp();
@@ -280,8 +286,15 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         // lane issues the MMAs and the commits (tcgen05.commit tracks the MMAs of the issuing thread). =====
         if (leader) {
             // A / B format fields (bits 7-9, 10-12): 1 = bf16, 0 = fp16
-            const uint32_t idesc = args.ab_f16 ? (make_idesc<CG, BN>() & ~((1u << 7) | (1u << 10))) : make_idesc<CG, BN>();
-            const uint32_t a_lo0 = desc_lo(a_stage(0)), b_lo0 = desc_lo(b_stage(0));
+            // K-major tiles: rows of 128 B, 8-row groups 1024 B apart (SBO), a k-step of 16 advances the start by 32 B; MN-major
+            // tiles: 64-row chunks of [64 k][128 B], 8-k groups 1024 B apart (SBO), chunks 8192 B apart (LBO), a k-step of 16
+            // advances the start by 2 KiB; idesc bits 15 / 16 select MN-major A / B
+            const uint32_t idesc = (args.ab_f16 ? (make_idesc<CG, BN>() & ~((1u << 7) | (1u << 10))) : make_idesc<CG, BN>()) |
+                                   (args.a_mn ? (1u << 15) : 0u) | (args.b_mn ? (1u << 16) : 0u);
+            const uint32_t mn_lbo = (8192u >> 4) << 16;
+            const uint32_t a_lo0 = args.a_mn ? (((a_stage(0) >> 4) & 0x3fffu) | mn_lbo) : desc_lo(a_stage(0));
+            const uint32_t b_lo0 = args.b_mn ? (((b_stage(0) >> 4) & 0x3fffu) | mn_lbo) : desc_lo(b_stage(0));
+            const uint32_t a_kstep = args.a_mn ? (2048u >> 4) : 2u, b_kstep = args.b_mn ? (2048u >> 4) : 2u;
             int stage = 0;
             uint32_t phase = 0, acc = 0, acc_phase = 0;
             for (uint32_t w = args.unit_begin + worker; w < args.work_end; w += n_workers) {
@@ -307,7 +320,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                         const uint32_t b_lo = b_lo0 + stage * (C::kStageBytes >> 4);
 #pragma unroll
                         for (int k = 0; k < BK / UMMA_K; ++k)
-                            umma_bf16<CG>(d_tmem, make_desc(a_lo + 2 * k), make_desc(b_lo + 2 * k), idesc,
+                            umma_bf16<CG>(d_tmem, make_desc(a_lo + a_kstep * k), make_desc(b_lo + b_kstep * k), idesc,
                                           (kb != kb0 || k != 0) ? 1u : 0u);
                         if (stage & 1) umma_commit_local<CG>(empty_bar(stage >> 1)); // both stages of the pair are consumed
                         if (kb == kb1 - 1) umma_commit<CG>(tfull_bar(acc)); // accumulator complete -> epilogue (both CTAs)
@@ -587,6 +600,8 @@ template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t
     a.N = p.N;
     a.K = p.K;
     a.ab_f16 = p.ab_f16 ? 1u : 0u;
+    a.a_mn = p.a_mn ? 1u : 0u;
+    a.b_mn = p.b_mn ? 1u : 0u;
     a.mb = (p.M + 255) / 256;
     a.nb = (p.N + BN - 1) / BN;
     a.rank_a = ma.rank;
@@ -665,7 +680,7 @@ template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t
         TLB_CUDA(cudaMemset(a.trace, 0, trace_bytes));
     }
     // plain (unfolded) operands and C: the coordinates of every map are the kernel's loop variables (tile_coords_t)
-    const bool plain = tma_map_is_plain(ma, false) && tma_map_is_plain(mb, false) && (EPI == EPI_REGS || tma_map_is_plain(mc, false));
+    const bool plain = tma_map_is_plain(ma, p.a_mn != 0) && tma_map_is_plain(mb, p.b_mn != 0) && (EPI == EPI_REGS || tma_map_is_plain(mc, false));
     TLB_CUDA((cudaLaunchKernelEx(&cfg, plain ? kern_plain : kern_any, tma, tmb, tmc, a)));
     count_launch();
     static const char* const names[2][2][2] = {{{"umma_1sm_regs", "umma_1sm"}, {"umma_2sm_regs", "umma_2sm"}},

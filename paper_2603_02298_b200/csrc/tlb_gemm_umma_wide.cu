@@ -667,8 +667,8 @@ bool umma_wide_applies(const UmmaProblem& p) {
     const uint32_t mb = static_cast<uint32_t>((p.M + 255) / 256);
     if (!p.full_range && (mb % 2 != 0 || p.tile_begin % 4 != 0 || p.tile_end % 4 != 0)) return false;
     // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue; measured better up to 2048^3, worse from
-    // 3072^3) unless an operand is MN-major or the wide plan is forced (TLB_GEMM_WIDE=1)
-    if (!(p.a_mn || p.b_mn || p.c_16)) {
+    // 3072^3) unless C is 2-byte (wide plan only) or the wide plan is forced (TLB_GEMM_WIDE=1)
+    if (!p.c_16) {
         const uint64_t nb = static_cast<uint64_t>((p.N + 255) / 256);
         const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
                                                  : (p.tile_end - p.tile_begin) / 4;

@@ -134,18 +134,23 @@ def _tile_count(la, lb, lc):
 
 
 def test_gemm_simt_fallback_keeps_the_transposed_tile_ids():
-    """MN-major A, m-contiguous C whose leading dimension TMA cannot address (ldc % 4 != 0), and unequal block counts
-    along m and n: the tcgen05 fit runs the problem transposed, the call falls through to SIMT, and the SIMT kernel must
-    index the tile grid the same way (columns n >= 256 were skipped). Whole range, then an odd partition."""
+    """A fit that runs the problem transposed (m-contiguous C) but whose call falls through to SIMT: a 2-byte C whose
+    leading dimension the wide plan's TMA epilogue cannot address, with unequal block counts along m and n. The SIMT
+    kernel must index the tile grid the way the tcgen05 fit counted it (columns n >= 256 were skipped). Whole
+    range, then an odd partition of the tile ids. (fp32-C problems of this kind now run on the 256 x 256 plan's register
+    epilogue: second half.)"""
     shape = ("(200,136):(1,208)", "(300,136):(1,304)", "(200,300):(1,201)")
-    assert _bf16_case(*shape, kat=True).startswith("simt")
-    assert _bf16_case(*shape, kat=False, seed=3).startswith("simt")
+    assert _c16_case(shape, False).startswith("simt")
     tiles = _tile_count(*shape)
     assert tiles == 4
-    assert _bf16_case(*shape, kat=True, tile_ranges=[(0, 1), (1, 3), (3, tiles)]).startswith("simt")
+    assert _c16_case(shape, False, tile_ranges=[(0, 1), (1, 3), (3, tiles)]).startswith("simt")
     big = ("(600,72):(1,608)", "(300,72):(1,304)", "(600,300):(1,601)")
     tiles = _tile_count(*big)
-    assert _bf16_case(*big, kat=True, tile_ranges=[(0, 3), (3, 4), (4, tiles)]).startswith("simt")
+    assert _c16_case(big, True, tile_ranges=[(0, 3), (3, 4), (4, tiles)]).startswith("simt")
+    # the same layouts with an fp32 C: MN-major operands on the 256 x 256 plan, any C strides through the register epilogue
+    assert _bf16_case(*shape, kat=True) == "umma_2sm_regs"
+    assert _bf16_case(*shape, kat=False, seed=3) == "umma_2sm_regs"
+    assert _bf16_case(*big, kat=True, tile_ranges=[(0, 4), (4, _tile_count(*big))]).startswith("umma_")
 
 
 UMMA_SHAPES = [
@@ -262,14 +267,21 @@ MN_MAJOR_SHAPES = [
 
 
 @pytest.mark.parametrize("shape", MN_MAJOR_SHAPES)
-def test_gemm_bf16_mn_major_operands_on_tensor_cores_kat_exact(shape):
-    """NT / NTT families on tcgen05: MN-major tiles staged as 64-row chunks, MN-major UMMA descriptors (idesc bits 15/16)."""
+def test_gemm_bf16_mn_major_operands_on_tensor_cores_kat_exact(shape, tlb_config):
+    """NT / NTT families on tcgen05: MN-major tiles staged as 64-row chunks, MN-major UMMA descriptors (idesc bits 15/16),
+    on every tensor-core plan: the planner's choice (256 x 256 for these short k-loops), one CTA per tile, and the wide plan."""
+    assert _bf16_case(*shape, kat=True).startswith("umma_2sm")
+    assert _bf16_case(*shape, kat=True, path=2).startswith("umma_1sm")
+    tlb_config("GEMM_WIDE", "1")
     assert _bf16_case(*shape, kat=True) == "umma_2sm_wide"
 
 
 @pytest.mark.parametrize("shape", MN_MAJOR_SHAPES[:2] + MN_MAJOR_SHAPES[4:])
-def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape):
-    assert _bf16_case(*shape, kat=False, seed=13) == "umma_2sm_wide"
+def test_gemm_bf16_mn_major_operands_random_within_tolerance(shape, tlb_config):
+    assert _bf16_case(*shape, kat=False, seed=13).startswith("umma_2sm")
+    assert _bf16_case(*shape, kat=False, seed=15, f16=True, path=2).startswith("umma_1sm")
+    tlb_config("GEMM_WIDE", "1")
+    assert _bf16_case(*shape, kat=False, seed=17) == "umma_2sm_wide"
 
 
 @pytest.mark.parametrize("shape,path,plan", [
@@ -298,6 +310,11 @@ def test_gemm_c_in_the_operand_type(shape, f16):
     """C with the operands' 2-byte type (the reference's tensors share one value type): fp32 accumulation in TMEM, one
     rounding to bf16 / fp16, added to C in that type (L2 reduction on the wide plan, in registers on the SIMT plan).
     Tolerance: one unit in the last place of the result type on |C| + sum |a b| (2^-7 bf16, 2^-10 fp16)."""
+    plan = _c16_case(shape, f16)
+    assert plan == ("simt_f16" if f16 else "simt_bf16") if shape[0].startswith("(4,8)") else plan == "umma_2sm_wide"
+
+
+def _c16_case(shape, f16, tile_ranges=None):
     la, lb, lc = shape
     M, N, K = _dims(la, lb)
     rng = np.random.default_rng(31)
@@ -324,14 +341,19 @@ def test_gemm_c_in_the_operand_type(shape, f16):
     ta, ka = host.tensor_of(la, ta_, ranked=True)
     tb, kb = host.tensor_of(lb, tb_, ranked=True)
     tc, kc = host.tensor_of(lc, tc_, ranked=True)
-    plan = (host.gemm_f16 if f16 else host.gemm_bf16)((ta, ka), (tb, kb), (tc, kc))
+    fn = host.gemm_f16 if f16 else host.gemm_bf16
+    if tile_ranges is None:
+        plan = fn((ta, ka), (tb, kb), (tc, kc))
+    else:
+        for (t0, t1) in tile_ranges:
+            plan = fn((ta, ka), (tb, kb), (tc, kc), t0, t1)
     torch.cuda.synchronize()
-    assert plan == ("simt_f16" if f16 else "simt_bf16") if la.startswith("(4,8)") else plan == "umma_2sm_wide"
     got = back(tc_.cpu().numpy().view(np.uint16))
     scale = np.abs(back(cb)) + sabs
     touched = sabs > 0
     assert (np.abs(got - want)[touched] <= 2 * ulp * scale[touched] + 1e-6).all()
     assert (got[~touched] == back(cb)[~touched]).all()                   # cells the layout does not address stay untouched
+    return plan
 
 
 def test_gemm_wide_plan_whole_tiles_then_k_ranges():
@@ -896,11 +918,13 @@ _FUZZ_PLANS = set()
 
 
 @pytest.mark.parametrize("seed", range(20))
-def test_gemm_fuzz_layout_families_against_the_oracle(seed):
+def test_gemm_fuzz_layout_families_against_the_oracle(seed, tlb_config):
     """Differential fuzz through every GEMM plan the planner may pick (tcgen05 1-CTA / 2-CTA / wide, register and TMA
     epilogues, rank-4/5 tensor maps, packed, SIMT): 8 random problems per seed against the sequential-k restatement,
     bf16 and fp16, exact where the plan keeps the reference's order, within the stated tolerance elsewhere."""
     rng = np.random.default_rng(1000 + seed)
+    if seed % 2:
+        tlb_config("GEMM_WIDE", "1")   # odd seeds: the wide plan wherever it applies (the planner keeps it for K >= 4096)
     plans = set()
     for _ in range(8):
         la, lb, lc = _fuzz_gemm_case(rng)

@@ -1,10 +1,29 @@
 #!/bin/bash
-for rep in 1 2; do
-for o in 0 1; do
-  echo "== SK_ORDER=$o"
-  TLB_GEMM_SK_ORDER=$o timeout 120 python tools/gemm_probe.py 4096 4096 4096 50 2>&1 | tail -1
-  TLB_GEMM_SK_ORDER=$o timeout 120 python tools/gemm_probe.py 8192 8192 8192 20 2>&1 | tail -1
-  TLB_GEMM_SK_ORDER=$o timeout 120 python tools/gemm_probe.py 4096 4096 4096 3000 2>&1 | tail -1
-done
-done
-TLB_GEMM_SK_ORDER=1 timeout 600 python -m pytest tests/test_gemm_gpu.py -m gpu -q -x -k "wide_plan_kat or c2 or chunked or fuzz" 2>&1 | tail -3
+timeout 1200 python -m pytest tests/test_gemm_gpu.py tests/test_dropin_gpu.py -m gpu -q -x 2>&1 | tail -12
+python - <<'PY'
+# NT (MN-major operands) at a short k-loop: 256 x 256 plan vs the wide plan
+import sys, os, torch
+sys.path.insert(0, '.')
+from paper_2603_02298_b200 import abi, host
+lib = abi.load()
+M = N = 4096
+for K in (2048, 4096):
+    for wide in ("0", "1"):
+        host.config("GEMM_WIDE", wide)
+        sets = []
+        for s in range(3):
+            a = torch.empty(M * K, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+            b = torch.empty(N * K, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+            c = torch.zeros(M * N, dtype=torch.float32, device="cuda")
+            sets.append((host.tensor_of(f"({M},{K}):(1,{M})", a.view(torch.int16), ranked=True),
+                         host.tensor_of(f"({N},{K}):(1,{N})", b.view(torch.int16), ranked=True),
+                         host.tensor_of(f"({M},{N}):({N},1)", c, ranked=True)))
+        for i in range(3): host.gemm_bf16(*sets[i % 3])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(50): host.gemm_bf16(*sets[i % 3])
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 50
+        print(f"NT {M}x{N}x{K} GEMM_WIDE={wide} plan {lib.tlb_last_plan().decode()}: {ms*1e3:.1f} us {2*M*N*K/ms/1e9:.1f} TFLOP/s")
+PY
