@@ -120,6 +120,7 @@ int umma_gemm_launch(const UmmaProblem& p, cudaStream_t stream);
 bool umma_pdl_enabled();      // programmatic dependent launch (TLB_GEMM_PDL=0 turns it off)
 long long* umma_clk_slot();   // TLB_GEMM_CLOCK=1: where CTA 0 stamps {clock64, globaltimer}; nullptr when off
 bool umma_wide_applies(const UmmaProblem& p);
+bool umma_c16_applies(const UmmaProblem& p);   // 2-byte C on the 256 x 256 plans (TMA reduce-add epilogue)
 int umma_wide_launch(const UmmaProblem& p, cudaStream_t stream);
 
 } // namespace tlb

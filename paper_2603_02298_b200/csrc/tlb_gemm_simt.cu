@@ -497,15 +497,15 @@ int run_gemm(const tlb_tensor* A, const tlb_tensor* B, const tlb_tensor* C, bool
                 p.force_wide = tm == 512 ? 1 : -1;
                 if (!p.full_range) return fail(TLB_ERR_CONTRACT, "tlb_gemm_*_tiled: whole problems only");
             }
-            // MN-major operands run on both tcgen05 plans; a 2-byte C needs the wide plan's epilogue
-            if (!p.c_16 || umma_wide_applies(p)) {
+            // MN-major operands and a 2-byte C run on both tcgen05 plans (the latter through the TMA reduce-add epilogues only)
+            if (!p.c_16 || umma_wide_applies(p) || umma_c16_applies(p)) {
                 if (p.cta_group == 2 && !even)
                     return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: cta_group::2 needs a tile range aligned to tile pairs");
                 return umma_gemm_launch(p, stream);
             }
-            // a 2-byte C is handled by the wide plan only; what it does not cover runs on the packed or the SIMT plan
+            // a 2-byte C the TMA epilogues cannot address runs on the packed or the SIMT plan
             if (g_gemm_path == 2 || g_gemm_path == 3)
-                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: a 2-byte C needs the wide tcgen05 plan (whole pair tiles, n-contiguous C)");
+                return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: a 2-byte C needs a TMA-addressable layout on the tcgen05 plans (n-contiguous rows, multiples of 16 bytes)");
         } else if (g_gemm_path == 2 || g_gemm_path == 3) {
             return fail(TLB_ERR_UNSUPPORTED, "tlb_gemm: the forced tcgen05 path does not apply to these layouts");
         }

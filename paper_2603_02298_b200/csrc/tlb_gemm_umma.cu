@@ -95,6 +95,7 @@ struct UmmaArgs {
                                    // 4 = no staging stores, 8 = no TMA store
     long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
     uint32_t ab_f16;               // operands are fp16 (A / B format fields of the instruction descriptor = 0)
+    uint32_t c_16;                 // C has the operands' 2-byte type (TMA epilogue only): 64-column chunks, rounded once, added at L2
     uint32_t a_mn, b_mn;           // operand is MN-major: staged as 64-row chunks of [64 k][128 B] (the map's dimension 0 is the
                                    // row index), MN-major UMMA descriptors (LBO = 8 KiB between chunks, idesc bits 15 / 16)
     long long* clk;                // optional (TLB_GEMM_CLOCK=1): CTA 0 stamps {clock64, globaltimer} at entry and exit
@@ -362,16 +363,40 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                 if (warp == 0 && lane == 0) TLB_TRACE(8 + item * 10 + 6);
                 const int m0 = static_cast<int>(m_tile) * BM;
                 const int nbase = static_cast<int>(n_blk) * BN + static_cast<int>(half) * (BN / 2);
+                // fp32 C: 32-column chunks (128 B rows); 2-byte C: 64-column chunks, two TMEM loads rounded to nearest even
+                const int n_chunks = args.c_16 ? kChunks / 2 : kChunks, cw = args.c_16 ? 64 : 32;
 #pragma unroll 1
-                for (int ci = 0; ci < kChunks; ++ci, ++chunk_no) {
+                for (int ci = 0; ci < n_chunks; ++ci, ++chunk_no) {
                     const uint32_t buf = epi_base + (half * C::kEpiBufs + (chunk_no % C::kEpiBufs)) * kEpiChunkBytes;
                     // the TMA store that last used this buffer must have finished reading it
                     if (issuer) bulk_wait_read<C::kEpiBufs - 1>();
                     named_bar(bar_id, 128);
                     uint32_t v[32];
-                    tmem_ld32(tmem_base + ((quad * 32u) << 16) + acc * BN + half * (BN / 2) + ci * 32, v);
-                    tmem_ld_wait();
-                    if (ci == kChunks - 1) {
+                    const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN + half * (BN / 2) + ci * cw;
+                    tmem_ld32(taddr, v);
+                    if (args.c_16) {
+                        uint32_t w[32];
+                        tmem_ld32(taddr + 32, w);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            uint32_t lo, hi;
+                            if (args.ab_f16) {
+                                asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(__uint_as_float(v[2 * j + 1])), "f"(__uint_as_float(v[2 * j])));
+                                asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(__uint_as_float(w[2 * j + 1])), "f"(__uint_as_float(w[2 * j])));
+                            } else {
+                                asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(__uint_as_float(v[2 * j + 1])), "f"(__uint_as_float(v[2 * j])));
+                                asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(__uint_as_float(w[2 * j + 1])), "f"(__uint_as_float(w[2 * j])));
+                            }
+                            v[j] = lo;        // v[0..15]: columns 0..31 packed, v[16..31]: columns 32..63
+                            w[j] = hi;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[16 + j] = w[j];
+                    } else {
+                        tmem_ld_wait();
+                    }
+                    if (ci == n_chunks - 1) {
                         // every TMEM read of this accumulator is done: hand it back to the MMA warp early
                         tc_fence_before();
                         __syncwarp();
@@ -392,7 +417,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     named_bar(bar_id, 128);
                     if (issuer && !(args.debug & (2u | 8u))) {
                         int tc[5];
-                        tile_coords_t<PLAIN>(args.cc, rank_c, false, m0, nbase + ci * 32, batch, tc);
+                        tile_coords_t<PLAIN>(args.cc, rank_c, false, m0, nbase + ci * cw, batch, tc);
                         if (hint_c && rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
                         else tma_reduce_add_tile(&map_c, buf, rank_c, tc);
                         bulk_commit();
@@ -567,6 +592,7 @@ namespace {
 int pick_epilogue(const UmmaProblem& p) {
     if (knob(K_GEMM_EPILOGUE) == 1) return EPI_REGS; // "regs": keep C in registers (profiling / A-B comparisons)
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
+    if (p.c_16) return EPI_TMA; // umma_c16_applies has checked the TMA constraints
     if (base_ok && p.cs_n == 1 && p.cs_m % 4 == 0 && p.cs_m >= p.N) return EPI_TMA;
     if (base_ok && p.c_fold_tma) return EPI_TMA; // folded C modes with a unit-stride column leaf (GETT-style C)
     return EPI_REGS;
@@ -587,7 +613,7 @@ template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t
     TmaTileMap ma, mb, mc;
     TLB_TRY(umma_operand_map(p, 0, BM, &ma));
     TLB_TRY(umma_operand_map(p, 1, C::kBRows, &mb));
-    if (EPI != EPI_REGS) TLB_TRY(umma_c_map(p, 32, BM, TMA_SW_128, &mc));
+    if (EPI != EPI_REGS) TLB_TRY(umma_c_map(p, p.c_16 ? 64 : 32, BM, TMA_SW_128, &mc));
     else mc = ma; // unused by the register epilogue
     TLB_TRY(epilogue_partition_check(BN, 1)); // tcgen05.ld partition derived from the accumulator layout (tlb_gemm_layout.cu)
     UmmaArgs a;
@@ -602,6 +628,7 @@ template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t
     a.ab_f16 = p.ab_f16 ? 1u : 0u;
     a.a_mn = p.a_mn ? 1u : 0u;
     a.b_mn = p.b_mn ? 1u : 0u;
+    a.c_16 = p.c_16 ? 1u : 0u;
     a.mb = (p.M + 255) / 256;
     a.nb = (p.N + BN - 1) / BN;
     a.rank_a = ma.rank;
@@ -631,7 +658,8 @@ template <int CG, int EPI, int BN> int launch(const UmmaProblem& p, cudaStream_t
         const uint32_t tail = units % W;
         const int kblocks = (p.K + BK - 1) / BK;
         uint32_t split = 1;
-        if (p.split_tail && tail > 0 && units > W) {
+        // (2-byte C: every K-slice would be one more rounding at L2, so tiles are never split)
+        if (p.split_tail && !p.c_16 && tail > 0 && units > W) {
             split = W / tail;
             split = std::min<uint32_t>(split, 4);
             while (split > 1 && kblocks / static_cast<int>(split) < 8) --split;
@@ -710,6 +738,14 @@ template <int CG> int launch_cg(const UmmaProblem& p, cudaStream_t stream) {
 } // namespace
 
 long long* umma_clk_slot() { return clk_slot(); }
+// 2-byte C on the 256 x 256 plans: the TMA reduce-add epilogue must be able to address it (n-contiguous rows that are
+// multiples of 16 bytes, or folded modes the rank-4/5 map covers).
+bool umma_c16_applies(const UmmaProblem& p) {
+    const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 8 == 0 && p.c_bs > 0));
+    if (!p.c_16 || !base_ok) return false;
+    if (p.c_fold_tma) return true;
+    return p.cs_n == 1 && p.cs_m % 8 == 0 && p.cs_m >= p.N;
+}
 // TLB_GEMM_PDL=0 turns programmatic dependent launch off (A/B comparisons).
 bool umma_pdl_enabled() { return knob(K_GEMM_PDL) != 0; }
 

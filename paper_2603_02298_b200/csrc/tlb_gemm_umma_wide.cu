@@ -667,8 +667,8 @@ bool umma_wide_applies(const UmmaProblem& p) {
     const uint32_t mb = static_cast<uint32_t>((p.M + 255) / 256);
     if (!p.full_range && (mb % 2 != 0 || p.tile_begin % 4 != 0 || p.tile_end % 4 != 0)) return false;
     // small problems keep the 256 x 256 plan (finer tiles, overlapped epilogue; measured better up to 2048^3, worse from
-    // 3072^3) unless C is 2-byte (wide plan only) or the wide plan is forced (TLB_GEMM_WIDE=1)
-    if (!p.c_16) {
+    // 3072^3) unless the wide plan is forced (TLB_GEMM_WIDE=1)
+    {
         const uint64_t nb = static_cast<uint64_t>((p.N + 255) / 256);
         const uint64_t pair_tiles = p.full_range ? static_cast<uint64_t>((p.M + 511) / 512) * nb * static_cast<uint64_t>(std::max(p.batch, 1))
                                                  : (p.tile_end - p.tile_begin) / 4;
@@ -677,7 +677,8 @@ bool umma_wide_applies(const UmmaProblem& p) {
         // full), the 256 x 256 plan overlaps its flush with the next tile. Measured crossover (round 2, 4096^2 and 8192^2
         // outputs): K = 2048 the 256 x 256 plan is 13 % ahead, K = 3072 0-3 %, K = 4096 a tie, from K = 5120 the wide plan
         // leads (6144^3 +4 %, 3072^2 x 8192 +7 %).
-        if (wide_knob != 1 && (p.K + BK - 1) / BK < 64) return false;
+        // (a 2-byte C flushes half the bytes: the wide plan already leads at K = 2048, 1285 vs 1268 TFLOP/s)
+        if (wide_knob != 1 && (p.K + BK - 1) / BK < (p.c_16 ? 32 : 64)) return false;
     }
     const bool base_ok = (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && (p.batch <= 1 || (p.c_bs % 4 == 0 && p.c_bs > 0));
     if (p.c_fold_tma) return base_ok && (!p.c_16 || p.batch <= 1 || p.c_bs % 8 == 0);

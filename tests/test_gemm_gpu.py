@@ -311,7 +311,20 @@ def test_gemm_c_in_the_operand_type(shape, f16):
     rounding to bf16 / fp16, added to C in that type (L2 reduction on the wide plan, in registers on the SIMT plan).
     Tolerance: one unit in the last place of the result type on |C| + sum |a b| (2^-7 bf16, 2^-10 fp16)."""
     plan = _c16_case(shape, f16)
-    assert plan == ("simt_f16" if f16 else "simt_bf16") if shape[0].startswith("(4,8)") else plan == "umma_2sm_wide"
+    if shape[0].startswith("(4,8)"):
+        assert plan == ("simt_f16" if f16 else "simt_bf16")
+        return
+    assert plan.startswith("umma_2sm") and not plan.endswith("regs")     # the planner's choice: 256 x 256 for short k-loops
+    prev = abi.load().tlb_gemm_set_path(2)
+    try:
+        assert _c16_case(shape, f16).startswith("umma_1sm")              # one CTA per tile
+    finally:
+        abi.load().tlb_gemm_set_path(prev)
+    host.config("GEMM_WIDE", "1")
+    try:
+        assert _c16_case(shape, f16) == "umma_2sm_wide"                  # and the 512 x 256 plan
+    finally:
+        host.config("GEMM_WIDE", None)
 
 
 def _c16_case(shape, f16, tile_ranges=None):
@@ -480,7 +493,7 @@ def test_gemm_batched_with_c_in_the_operand_type():
     ta = host.make_tensor(L(la).lower(ranked=True), ta_.data_ptr(), ta_.numel(), 2)
     tb = host.make_tensor(L(lb).lower(ranked=True), tb_.data_ptr(), tb_.numel(), 2)
     tc = host.make_tensor(L(lc).lower(ranked=True), tc_.data_ptr(), tc_.numel(), 2)
-    assert host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 1, 3) == "umma_2sm_wide"
+    assert host.gemm_bf16_batched((ta, None), (tb, None), (tc, None), M * K, N * K, M * N, 1, 3).startswith("umma_2sm")
     torch.cuda.synchronize()
     got = back(tc_.cpu().numpy().view(np.uint16))
     assert (got[0] == back(c0[0])).all()                                 # batch 0 untouched
