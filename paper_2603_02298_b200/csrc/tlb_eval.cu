@@ -242,7 +242,34 @@ __device__ __forceinline__ void block_count(unsigned long long bad, unsigned lon
     }
 }
 
+// The peel for Int layouts whose extents are all powers of two, on an index below 2^32: masks and shifts in 32 bits (the
+// checkers are compute bound: the generic peel spends most of its instructions on 64-bit division by multiplication).
+// NL: an upper bound on the leaf count the loop is unrolled for (4: the C5 layouts; the masks, shifts and strides then
+// stay in registers across a thread's grid-stride iterations), TLB_MAX_MODES: any count.
+template <int NL> __device__ __forceinline__ int64_t dev_eval_p2(const tlb_layout_desc& L, uint32_t i) {
+    int64_t acc = 0;
+    const int n = L.n_modes;
+#pragma unroll
+    for (int r = 0; r < NL; ++r) {
+        if (r < n) {
+            const uint32_t c = (r + 1 < n) ? (i & (static_cast<uint32_t>(L.extent[r]) - 1u)) : i;
+            i = (r + 1 < n) ? (i >> L.log2e[r]) : 0u;
+            acc += static_cast<int64_t>(c) * L.stride[r];
+        }
+    }
+    return acc;
+}
+// FAST > 0: every layout is Int with power-of-two extents (each below 2^32), at most FAST leaves, and the index range
+// ends below 2^32; an intermediate offset at or above 2^32 (or negative) takes the generic peel.
+template <int FAST> __device__ __forceinline__ int64_t dev_eval_sel(const tlb_layout_desc& L, uint64_t i) {
+    if constexpr (FAST > 0) {
+        if ((i >> 32) == 0) return dev_eval_p2<FAST>(L, static_cast<uint32_t>(i));
+    }
+    return dev_eval(L, i);
+}
+
 // Counts k with L(R(k)) != k.
+template <int FAST>
 __global__ void __launch_bounds__(kThreads) rinv_check_kernel(const __grid_constant__ tlb_layout_desc L,
                                                               const __grid_constant__ tlb_layout_desc R, uint64_t k0,
                                                               uint64_t n, unsigned long long* d_mismatch) {
@@ -250,14 +277,15 @@ __global__ void __launch_bounds__(kThreads) rinv_check_kernel(const __grid_const
     unsigned long long bad = 0;
     for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
         const uint64_t k = k0 + j;
-        const int64_t rk = dev_eval(R, k);
-        const int64_t back = rk < 0 ? -1 : dev_eval(L, static_cast<uint64_t>(rk));
+        const int64_t rk = dev_eval_sel<FAST>(R, k);
+        const int64_t back = rk < 0 ? -1 : dev_eval_sel<FAST>(L, static_cast<uint64_t>(rk));
         bad += (back != static_cast<int64_t>(k));
     }
     block_count(bad, d_mismatch);
 }
 
 // Counts i with A(B(i)) != Rr(i).
+template <int FAST>
 __global__ void __launch_bounds__(kThreads) compose_check_kernel(const __grid_constant__ tlb_layout_desc A,
                                                                  const __grid_constant__ tlb_layout_desc B,
                                                                  const __grid_constant__ tlb_layout_desc Rr,
@@ -267,9 +295,9 @@ __global__ void __launch_bounds__(kThreads) compose_check_kernel(const __grid_co
     unsigned long long bad = 0;
     for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
         const uint64_t i = i0 + j;
-        const int64_t b = dev_eval(B, i);
-        const int64_t want = b < 0 ? INT64_MIN : dev_eval(A, static_cast<uint64_t>(b));
-        bad += (want != dev_eval(Rr, i));
+        const int64_t b = dev_eval_sel<FAST>(B, i);
+        const int64_t want = b < 0 ? INT64_MIN : dev_eval_sel<FAST>(A, static_cast<uint64_t>(b));
+        bad += (want != dev_eval_sel<FAST>(Rr, i));
     }
     block_count(bad, d_mismatch);
 }
@@ -491,6 +519,16 @@ int tlb_crd2idx_range(const tlb_layout_desc* shape, const int64_t* d_crd, uint64
     return tlb_crd2idx_range_checked(shape, d_crd, n, d_out, nullptr, stream);
 }
 
+namespace {
+// Int layout, every extent a power of two below 2^32 (the last leaf's coordinate is unbounded: it is never masked).
+bool pow2_fast(const tlb_layout_desc& L) {
+    if (L.kind != TLB_KIND_INT || !(L.flags & TLB_LF_ALL_POW2)) return false;
+    for (int r = 0; r < L.n_modes; ++r)
+        if (L.extent[r] >= (1ll << 32)) return false;
+    return true;
+}
+} // namespace
+
 int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uint64_t k0, uint64_t n,
                          unsigned long long* d_mismatch, void* stream) {
     TLB_TRY(check_int_or_xor(L, "tlb_rinv_check_range"));
@@ -502,7 +540,13 @@ int tlb_rinv_check_range(const tlb_layout_desc* L, const tlb_layout_desc* R, uin
     TLB_TRY(overflow_preflight(*R, 0, k0 + n - 1));
     // L is evaluated at R(k), and k may lie in R's extended domain: bound |R(k)| over [0, k0 + n)
     TLB_TRY(overflow_preflight(*L, 0, max_abs_offset(*R, k0 + n - 1)));
-    rinv_check_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*L, *R, k0, n, d_mismatch);
+    const bool fast = pow2_fast(*L) && pow2_fast(*R) && k0 + n <= (1ull << 32);
+    if (fast && L->n_modes <= 4 && R->n_modes <= 4)
+        rinv_check_kernel<4><<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*L, *R, k0, n, d_mismatch);
+    else if (fast)
+        rinv_check_kernel<TLB_MAX_MODES><<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*L, *R, k0, n, d_mismatch);
+    else
+        rinv_check_kernel<0><<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*L, *R, k0, n, d_mismatch);
     count_launch();
     TLB_CUDA(cudaGetLastError());
     return TLB_OK;
@@ -521,7 +565,13 @@ int tlb_compose_check_range(const tlb_layout_desc* A, const tlb_layout_desc* B, 
     TLB_TRY(overflow_preflight(*B, 0, i0 + n - 1));
     TLB_TRY(overflow_preflight(*R, 0, i0 + n - 1));
     TLB_TRY(overflow_preflight(*A, 0, max_abs_offset(*B, i0 + n - 1)));
-    compose_check_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*A, *B, *R, i0, n, d_mismatch);
+    const bool fast = pow2_fast(*A) && pow2_fast(*B) && pow2_fast(*R) && i0 + n <= (1ull << 32);
+    if (fast && A->n_modes <= 4 && B->n_modes <= 4 && R->n_modes <= 4)
+        compose_check_kernel<4><<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*A, *B, *R, i0, n, d_mismatch);
+    else if (fast)
+        compose_check_kernel<TLB_MAX_MODES><<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*A, *B, *R, i0, n, d_mismatch);
+    else
+        compose_check_kernel<0><<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(*A, *B, *R, i0, n, d_mismatch);
     count_launch();
     TLB_CUDA(cudaGetLastError());
     return TLB_OK;
