@@ -40,6 +40,8 @@ struct TmaCoord {
     uint32_t src;          // which tile coordinate feeds this dimension: 0 = row index, 1 = k (or column) index, 2 = batch
     uint32_t div_m, div_s; // q = (value * div_m) >> div_s                 == value / div
     uint32_t mod, mod_m, mod_s; // coordinate = q - ((q * mod_m) >> mod_s) * mod  == q % mod; mod == 0: no remainder
+    uint32_t kinc;         // k-fed dimensions: what one k-block (64 elements of k) adds to the coordinate, before carries
+                           // (tile_coords_step: the producer's k-loop advances coordinates instead of recomputing them)
 };
 inline void magic_u31(uint32_t d, uint32_t* m, uint32_t* s) { // floor(v / d) == (uint64(v) * m) >> s for every v < 2^31
     uint32_t l = 0;
@@ -48,9 +50,11 @@ inline void magic_u31(uint32_t d, uint32_t* m, uint32_t* s) { // floor(v / d) ==
     *m = static_cast<uint32_t>(((1ull << *s) + d - 1) / d);
 }
 inline TmaCoord tma_coord(uint32_t src, uint32_t div, uint32_t mod) {
-    TmaCoord c = {src, 0u, 0u, mod, 0u, 0u};
+    TmaCoord c = {src, 0u, 0u, mod, 0u, 0u, 0u};
     magic_u31(div ? div : 1u, &c.div_m, &c.div_s);
     if (mod) magic_u31(mod, &c.mod_m, &c.mod_s);
+    const uint32_t d = div ? div : 1u;
+    if (src == 1u && d <= 64u && 64u % d == 0u) c.kinc = mod ? (64u / d) % mod : 64u / d;
     return c;
 }
 struct TmaTileMap {

@@ -242,7 +242,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                                     int row0, int rows, int kb, int* tk, bool hint) {
                 constexpr bool CG2 = decltype(cg2)::value;
                 if (!mn) {
-                    tile_coords_k<PLAIN>(tcd, rk, kb * BK, tk);
+                    if (kb == kb0 || (args.debug & 64u)) tile_coords_k<PLAIN>(tcd, rk, kb * BK, tk);
+                    else tile_coords_step<PLAIN>(tcd, rk, tk);
                     if (hint) tma_load_tile_hint<CG2>(dst, map, bar, rk, tk, pol_ab);
                     else tma_load_tile<CG2>(dst, map, bar, rk, tk);
                 } else {

@@ -302,7 +302,8 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                                                static_cast<int>(batch), a_mask);
                         } else if (!args.a_mn) {
                             // K-major A: one box of 256 rows x 64 k (rows of 128 B)
-                            tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, tca);
+                            if (kb == it.kb0 || (args.debug & 64u)) tile_coords_k<PLAIN>(args.ca, rank_a, kb * BK, tca);
+                            else tile_coords_step<PLAIN>(args.ca, rank_a, tca);
                             if (args.hints & 1u) tma_load_tile_hint<true>(a_stage(stage), &map_a, lbar, rank_a, tca, pol_ab);
                             else tma_load_tile<true>(a_stage(stage), &map_a, lbar, rank_a, tca);
                         } else {
@@ -314,7 +315,8 @@ umma_wide_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                             }
                         }
                         if (!args.b_mn) {
-                            tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tcb);
+                            if (kb == it.kb0 || (args.debug & 64u)) tile_coords_k<PLAIN>(args.cb, rank_b, kb * BK, tcb);
+                            else tile_coords_step<PLAIN>(args.cb, rank_b, tcb);
                             if (args.hints & 1u) tma_load_tile_hint<true>(b_stage(stage), &map_b, lbar, rank_b, tcb, pol_ab);
                             else tma_load_tile<true>(b_stage(stage), &map_b, lbar, rank_b, tcb);
                         } else {

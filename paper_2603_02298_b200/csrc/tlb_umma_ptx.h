@@ -259,6 +259,30 @@ __device__ __forceinline__ void tile_coords_k(const TmaCoord* tc, int rank, uint
         }
     }
 }
+// One k-block further: every k-fed dimension advances by its kinc; a dimension that reaches its extent wraps and carries
+// one into the next k-fed dimension (their divisors are the running products of the extents before them, so the carry is
+// exactly one). Valid when the tile starts at a multiple of 64 in k and the divisors divide 64 or are multiples of it,
+// which tile_dims_derive guarantees for 64-element k boxes. Adds and compares only.
+template <bool PLAIN>
+__device__ __forceinline__ void tile_coords_step(const TmaCoord* tc, int rank, int* c) {
+    if constexpr (PLAIN) {
+        c[0] += 64;
+    } else {
+        uint32_t carry = 0;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            if (d < rank && tc[d].src == 1u) {
+                uint32_t v = static_cast<uint32_t>(c[d]) + tc[d].kinc + carry;
+                carry = 0;
+                if (tc[d].mod && v >= tc[d].mod) {
+                    v -= tc[d].mod;
+                    carry = 1;
+                }
+                c[d] = static_cast<int>(v);
+            }
+        }
+    }
+}
 // cp.async.bulk.tensor of rank 3..5; CG2: cta_group::2 form (transaction bytes complete on the leader's barrier).
 template <bool CG2>
 __device__ __forceinline__ void tma_load_tile(uint32_t dst, const void* map, uint32_t bar, int rank, const int* c) {
