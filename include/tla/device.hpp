@@ -117,6 +117,16 @@ inline void copy(const DeviceTensor& src, const DeviceTensor& dst, Int i_begin =
                                     i_end < 0 ? UINT64_MAX : static_cast<uint64_t>(i_end), dst.stream));
 }
 
+// Thread-value partitioned copy: `tv` is a rank-2 layout (thread, value) -> integral coordinate, built with the
+// reference's own products (raked_product / blocked_product, algebra.hpp:629-635; the thread-value maps of
+// proj/demo/partition_demo.cpp:26-40). Logical thread t moves dst(tv(t, v)) = src(tv(t, v)) for every value v.
+inline void copy(const DeviceTensor& src, const DeviceTensor& dst, const Layout& tv) {
+    tlb_layout_desc ds = device_detail::lower(src.layout(), false), dd = device_detail::lower(dst.layout(), false),
+                    dt = device_detail::lower(tv, true);
+    tlb_tensor s = device_detail::view(ds, src), d = device_detail::view(dd, dst);
+    device_detail::rethrow(tlb_copy_tv(&s, &d, &dt, dst.stream));
+}
+
 // A counting source (Accessor::counting(base), tensor.hpp:22): dst(i) = base + src_layout(i).
 inline void copy_counting(const Layout& src_layout, Int base, const DeviceTensor& dst) {
     tlb_layout_desc ds = device_detail::lower(src_layout, false), dd = device_detail::lower(dst.layout(), false);

@@ -199,6 +199,20 @@ int tlb_copy_plan(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin
  * refinement the copy planner works on (it is what bounds the "vec" plan's vector width); layouts the reference cannot
  * right-invert give the scalar answer 1, as there. */
 int tlb_max_common_vector(const tlb_layout_desc* a, const tlb_layout_desc* b, int64_t* k);
+/* Thread-value partitioned copy: the caller chooses WHICH thread moves WHICH elements with a layout, the way the paper
+ * partitions work (local_partition; the thread-value maps of proj/demo/partition_demo.cpp:26-40, built
+ * with blocked_product / raked_product, algebra.hpp:629-635). `tv` is a rank-2 layout (thread, value) -> integral
+ * coordinate of src and dst (from tlb_layout_lower_ranked): logical thread t copies dst(tv(t, v)) = src(tv(t, v)) for every
+ * value v; coordinates at or beyond size(src) are skipped, so a TV layout may over-cover a ragged tensor. tv and dst must
+ * be injective (one writer per cell), strides non-negative integers. Runs of the value mode that tv, src and dst all keep
+ * contiguous and aligned move as <= 16-byte vectors. Plans "tv_vec" / "tv". */
+int tlb_copy_tv(const tlb_tensor* src, const tlb_tensor* dst, const tlb_layout_desc* tv, void* stream);
+/* The thread-value layout the library derives for (src, dst) itself: V = the widest power-of-two vector that
+ * tla::max_common_vector(src, dst) (analysis.hpp:18-28) and 16 bytes allow, one tile = raked_product((V):(1), (T):(1)) =
+ * (T, V):(V, 1) (algebra.hpp:633), tiles repeated in the value mode: ((T), (V, R)):((V), (1, T V)). Writes 3 flat modes and
+ * top_leaves2 = {1, 2} for tlb_layout_lower_ranked. Host only. */
+int tlb_copy_tv_auto(const tlb_layout_desc* src, const tlb_layout_desc* dst, int elem_bytes, int threads, tlb_mode* tv_modes,
+                     int32_t* n_modes, int32_t* top_leaves2);
 /* Planner knobs for tlb_copy on the calling thread: force one path (testing / profiling).
  * 0 = auto, 1 = gather only, 2 = tiled (LDG-fed), 3 = tiled TMA-fed. Returns the previous value. */
 int tlb_copy_set_path(int path);

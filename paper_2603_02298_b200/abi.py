@@ -82,6 +82,8 @@ SYMBOLS = {
     "tlb_locate_offsets": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), _P(tlb_mode), _P(C.c_int32), C.c_void_p]),
     "tlb_tensormap_cache_stats": (C.c_int, [_P(C.c_uint64), _P(C.c_uint64)]),
     "tlb_workspace_trim": (C.c_int, [C.c_uint64]),
+    "tlb_copy_tv": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_layout_desc), C.c_void_p]),
+    "tlb_copy_tv_auto": (C.c_int, [_P(tlb_layout_desc), _P(tlb_layout_desc), C.c_int, C.c_int, _P(tlb_mode), _P(C.c_int32), _P(C.c_int32)]),
     "tlb_gemm_tile_count": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), _P(C.c_uint32)]),
     "tlb_gemm_bf16_batched": (C.c_int, [_P(tlb_tensor), _P(tlb_tensor), _P(tlb_tensor), C.c_int64, C.c_int64, C.c_int64,
                                         C.c_int32, C.c_int32, C.c_void_p]),

@@ -114,6 +114,29 @@ gather_vec_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_consta
     }
 }
 
+// Thread-value partitioned copy (local_partition; partition_demo.cpp:26-40): TV is a rank-2 layout
+// (thread, value) -> integral coordinate. GPU thread t is logical thread t; it walks its values in chunks of `vec` cells
+// that the host has proven contiguous and aligned in TV, source and destination (vec = 1: cell by cell).
+template <int VB>
+__global__ void __launch_bounds__(kThreads)
+copy_tv_kernel(const __grid_constant__ tlb_layout_desc TV, const __grid_constant__ tlb_layout_desc S,
+               const __grid_constant__ tlb_layout_desc D, const char* __restrict__ src, char* __restrict__ dst,
+               int64_t s_origin, int64_t d_origin, uint64_t n_threads, uint64_t n_values, uint64_t size, int vec, int elem_bytes) {
+    using T = typename Cell<VB>::type;
+    pdl_wait();
+    const uint64_t n_chunks = n_values / static_cast<uint64_t>(vec);
+    const uint64_t total = n_threads * n_chunks, stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    // consecutive GPU threads are consecutive logical threads of one value chunk (the coalescing a raked TV layout is built for)
+    for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < total; w += stride) {
+        const uint64_t t = w % n_threads, c = w / n_threads;
+        const int64_t i = dev_eval_top(TV, 0, t) + dev_eval_top(TV, 1, c * static_cast<uint64_t>(vec));
+        if (i < 0 || static_cast<uint64_t>(i) >= size) continue; // a TV layout may over-cover the tensor (predicated tail)
+        const int64_t sp = dev_position(S, s_origin, dev_eval(S, static_cast<uint64_t>(i)));
+        const int64_t dp = dev_position(D, d_origin, dev_eval(D, static_cast<uint64_t>(i)));
+        *reinterpret_cast<T*>(dst + dp * elem_bytes) = *reinterpret_cast<const T*>(src + sp * elem_bytes);
+    }
+}
+
 // gather over the common refinement: one peel yields both offsets (half the index arithmetic of two evaluations), and,
 // the destination being injective, the refined modes may be walked in any order: the host sorts them by destination
 // stride so that consecutive threads store to neighbouring cells.
@@ -1420,6 +1443,107 @@ int tlb_copy_plan(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin
     const int st = tlb::copy_impl(src, dst, i_begin, i_end, nullptr);
     tlb::g_dry_run = false;
     return st;
+}
+
+/* ---- thread-value partitioned copy ----------------------------------------------------------------------------- */
+int tlb_copy_tv(const tlb_tensor* src, const tlb_tensor* dst, const tlb_layout_desc* tv, void* stream) {
+    using namespace tlb;
+    if (!tv) return fail(TLB_ERR_CONTRACT, "tlb_copy_tv: null thread-value layout");
+    TLB_TRY(check_tensor(src, "tlb_copy_tv source", false));
+    TLB_TRY(check_tensor(dst, "tlb_copy_tv destination", true));
+    const tlb_layout_desc& S = *src->layout;
+    const tlb_layout_desc& D = *dst->layout;
+    if (S.size != D.size) return fail(TLB_ERR_CONTRACT, "copy requires equal sizes");
+    if (src->elem_bytes != dst->elem_bytes) return fail(TLB_ERR_CONTRACT, "tlb_copy_tv: element sizes differ");
+    if (src->accessor != TLB_ACC_BUFFER) return fail(TLB_ERR_UNSUPPORTED, "tlb_copy_tv: the source must be a buffer tensor");
+    if (tv->n_top != 2) return fail(TLB_ERR_CONTRACT, "tlb_copy_tv: the thread-value layout must have rank 2 (thread, value)");
+    if (tv->kind != TLB_KIND_INT || (tv->flags & TLB_LF_HAS_NEG))
+        return fail(TLB_ERR_SEMIMODULE, "tlb_copy_tv: the thread-value layout must have non-negative integer strides");
+    // every cell must have ONE writer: the destination injective, and no two (thread, value) pairs on one coordinate
+    if (!(D.flags & TLB_LF_INJECTIVE) || !(tv->flags & TLB_LF_INJECTIVE))
+        return fail(TLB_ERR_UNSUPPORTED, "tlb_copy_tv: the destination and the thread-value layout must be injective");
+    const uint64_t size = static_cast<uint64_t>(S.size);
+    if (size == 0 || tv->size == 0) {
+        set_plan("empty");
+        return TLB_OK;
+    }
+    TLB_TRY(require_device());
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    TLB_TRY(overflow_preflight(S, src->origin, size - 1));
+    TLB_TRY(overflow_preflight(D, dst->origin, size - 1));
+    TLB_TRY(overflow_preflight(*tv, 0, static_cast<uint64_t>(tv->size) - 1));
+    Span sspan, dspan;
+    TLB_TRY(bounds_preflight(*src, 0, size, "source", cs, &sspan));
+    TLB_TRY(bounds_preflight(*dst, 0, size, "destination", cs, &dspan));
+    {
+        const uintptr_t eb = static_cast<uintptr_t>(dst->elem_bytes);
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(src->data) + static_cast<uintptr_t>(sspan.lo) * eb;
+        const uintptr_t s1 = reinterpret_cast<uintptr_t>(src->data) + (static_cast<uintptr_t>(sspan.hi) + 1) * eb;
+        const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst->data) + static_cast<uintptr_t>(dspan.lo) * eb;
+        const uintptr_t d1 = reinterpret_cast<uintptr_t>(dst->data) + (static_cast<uintptr_t>(dspan.hi) + 1) * eb;
+        if (s0 < d1 && d0 < s1) return fail(TLB_ERR_UNSUPPORTED, "tlb_copy_tv: source and destination overlap in memory (use tlb_copy)");
+    }
+    uint64_t n_threads = 1, n_values = 1;
+    for (int r = tv->top_start[0]; r < tv->top_start[1]; ++r) n_threads *= static_cast<uint64_t>(tv->extent[r]);
+    for (int r = tv->top_start[1]; r < tv->top_start[2]; ++r) n_values *= static_cast<uint64_t>(tv->extent[r]);
+    // Vector width: the value mode starts with a unit-stride leaf of extent >= V, nothing else in TV reaches below V, and
+    // both tensors keep V-aligned runs of V coordinates contiguous (low_run: Int and Xor layouts).
+    const int eb = dst->elem_bytes;
+    int V = 1;
+    {
+        int lead = tv->top_start[1];
+        while (lead < tv->top_start[2] && tv->extent[lead] == 1) ++lead;
+        if (eb < 16 && lead < tv->top_start[2] && tv->stride[lead] == 1) {
+            V = std::min(low_run(*src, 16 / eb), low_run(*dst, 16 / eb));
+            while (V > 1) {
+                bool ok = tv->extent[lead] % V == 0 && size % static_cast<uint64_t>(V) == 0;
+                for (int r = 0; ok && r < tv->n_modes; ++r)
+                    if (r != lead && tv->extent[r] > 1) ok = tv->stride[r] % V == 0;
+                if (ok) break;
+                V >>= 1;
+            }
+        }
+    }
+    const uint64_t total = n_threads * (n_values / static_cast<uint64_t>(V));
+    const int grid = launch_grid(total, kThreads, 8);
+    const char* sb = static_cast<const char*>(src->data);
+    char* db = static_cast<char*>(dst->data);
+#define TLB_CTV(VB) TLB_CUDA(launch_pdl(copy_tv_kernel<VB>, dim3(grid), dim3(kThreads), 0, cs, *tv, S, D, sb, db, src->origin, dst->origin, n_threads, n_values, size, V, eb))
+    switch (V * eb) {
+    case 1: TLB_CTV(1); break;
+    case 2: TLB_CTV(2); break;
+    case 4: TLB_CTV(4); break;
+    case 8: TLB_CTV(8); break;
+    default: TLB_CTV(16); break;
+    }
+#undef TLB_CTV
+    count_launch();
+    set_plan(V > 1 ? "tv_vec" : "tv");
+    return TLB_OK;
+}
+
+int tlb_copy_tv_auto(const tlb_layout_desc* src, const tlb_layout_desc* dst, int elem_bytes, int threads, tlb_mode* tv_modes,
+                     int32_t* n_modes, int32_t* top_leaves2) {
+    using namespace tlb;
+    if (!src || !dst || !tv_modes || !n_modes || !top_leaves2) return fail(TLB_ERR_CONTRACT, "tlb_copy_tv_auto: null argument");
+    if (src->size != dst->size) return fail(TLB_ERR_CONTRACT, "copy requires equal sizes");
+    if (threads < 1 || (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16))
+        return fail(TLB_ERR_CONTRACT, "tlb_copy_tv_auto: bad thread count or element size");
+    int64_t mcv = 1;
+    TLB_TRY(tlb_max_common_vector(src, dst, &mcv));
+    int64_t V = 1;
+    while (V * 2 <= 16 / elem_bytes && V * 2 <= mcv && mcv % (V * 2) == 0) V *= 2;
+    const int64_t T = threads, tile = T * V;
+    const int64_t R = (src->size + tile - 1) / tile;
+    // raked_product((V):(1), (T):(1)) = (T, V):(V, 1) (algebra.hpp:633) is one tile of T vectors; the tiles follow in the
+    // value mode, so thread t owns vector t of every tile: ((T), (V, R)) : ((V), (1, T V))
+    tv_modes[0] = {T, V, TLB_KIND_INT, 0};
+    tv_modes[1] = {V, 1, TLB_KIND_INT, 0};
+    tv_modes[2] = {R, tile, TLB_KIND_INT, 0};
+    *n_modes = 3;
+    top_leaves2[0] = 1;
+    top_leaves2[1] = 2;
+    return TLB_OK;
 }
 
 int tlb_copy_set_path(int path) {

@@ -239,6 +239,27 @@ def max_common_vector(a: Layout | str, b: Layout | str) -> int:
     return k.value
 
 
+def copy_tv(src, dst, tv: Layout | str, stream=None) -> str:
+    """tlb_copy_tv: thread-value partitioned copy; tv is a rank-2 layout (thread, value) -> integral coordinate."""
+    lib = abi.load()
+    d = (L(tv) if isinstance(tv, str) else tv).lower(ranked=True)
+    abi.check(lib.tlb_copy_tv(C.byref(src[0]), C.byref(dst[0]), C.byref(d), _stream_ptr(stream)))
+    return lib.tlb_last_plan().decode()
+
+
+def copy_tv_auto(src_layout: Layout | str, dst_layout: Layout | str, elem_bytes: int, threads: int = 256) -> str:
+    """The thread-value layout the library derives for a copy, in the reference's text syntax."""
+    ds = (L(src_layout) if isinstance(src_layout, str) else src_layout).lower()
+    dd = (L(dst_layout) if isinstance(dst_layout, str) else dst_layout).lower()
+    modes = (abi.tlb_mode * 16)()
+    n = C.c_int32(0)
+    tops = (C.c_int32 * 2)()
+    abi.check(abi.load().tlb_copy_tv_auto(C.byref(ds), C.byref(dd), elem_bytes, threads, modes, C.byref(n), tops))
+    assert n.value == 3 and list(tops) == [1, 2]
+    (t, v, r) = [(int(modes[k].extent), int(modes[k].stride)) for k in range(3)]
+    return f"({t[0]},({v[0]},{r[0]})):({t[1]},({v[1]},{r[1]}))"
+
+
 def copy_host(src, dst) -> None:
     abi.check(abi.load().tlb_copy_host(C.byref(src[0]), C.byref(dst[0])))
 

@@ -144,6 +144,34 @@ static void local_tile_copy() {
     CHECK(ddst.get() == *out);
 }
 
+// Thread-value partitioned copy: the TV layout is the reference's raked_product of a value layout and a thread layout
+// (algebra.hpp:633) extended over the tiles, and partition_demo.cpp's ((4,8),2):((16,1),8) over an 8 x 8 tile; the device
+// copy driven by it must equal tla::copy.
+static void tv_partitioned_copy() {
+    Layout src = L("(64,32):(32,1)"), dst = L("(64,32):(1,64)");
+    auto store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(src)));
+    std::iota(store->begin(), store->end(), 11);
+    auto out = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(dst)), -1);
+    copy(Tensor(Accessor::buffer(store), src), Tensor(Accessor::buffer(out), dst));                    // reference
+    // one tile = raked_product((2):(1), (64):(1)) = (64,2):(2,1); 16 tiles in the value mode
+    Layout tile = raked_product(L("2:1"), L("64:1"));
+    CHECK(format_layout(tile) == "(64,2):(2,1)");
+    Layout tv = L("(64,(2,16)):(2,(1,128))");
+    DevBuf<Int> dsrc(*store), ddst(std::vector<Int>(static_cast<size_t>(cosize(dst)), -1));
+    copy(DeviceTensor(dsrc.p, Int(dsrc.n), 8, src), DeviceTensor(ddst.p, Int(ddst.n), 8, dst), tv);    // device
+    cudaDeviceSynchronize();
+    CHECK(ddst.get() == *out);
+    Layout s8 = L("(8,8):(1,8)"), d8 = L("(8,8):(8,1)");
+    auto st8 = std::make_shared<std::vector<Int>>(64);
+    std::iota(st8->begin(), st8->end(), 3);
+    auto out8 = std::make_shared<std::vector<Int>>(64, -1);
+    copy(Tensor(Accessor::buffer(st8), s8), Tensor(Accessor::buffer(out8), d8));
+    DevBuf<Int> a8(*st8), b8(std::vector<Int>(64, -1));
+    copy(DeviceTensor(a8.p, 64, 8, s8), DeviceTensor(b8.p, 64, 8, d8), L("((4,8),2):((16,1),8)"));
+    cudaDeviceSynchronize();
+    CHECK(b8.get() == *out8);
+}
+
 // GEMM on local_tile-sliced operands: C_tile(128 x 256) += A_tile(128 x 64) * B_tile(256 x 64)^T where the three tiles are
 // local_tile views of larger matrices (tile (1,2) of A, (0,2) of B, (1,0) of C); checked against tla::gemm on the same
 // slices of host tensors, cell by cell, for the checked-int64 path and for bf16 on tcgen05 (and with a caller-chosen tiler).
@@ -324,6 +352,7 @@ int main() {
     copy_pairs();
     fig7_slices_on_device();
     local_tile_copy();
+    tv_partitioned_copy();
     gemm_families();
     gemm_on_local_tiles();
     locate_offsets_on_device();

@@ -509,3 +509,62 @@ def test_tma_coordinates_come_from_the_tiled_coordinate_identity():
         torch.cuda.synchronize()
         want = hbuf[row0 * 192 + col0 + tile_off].T
         assert (got.cpu().numpy().view(np.int32).reshape(32, 32) == want).all(), t
+
+
+def _copy_tv_case(s, d, eb, tv, seed=0, expect_all=True):
+    """tlb_copy_tv against the oracle: with a thread-value layout that covers every coordinate once the result is
+    tla::copy's; cells no (thread, value) pair maps to must keep their pre-fill."""
+    ns, nd = ou.cosize_of(s), ou.cosize_of(d)
+    src, dst0 = cells(ns, eb, seed), cells(nd, eb, fill=-1 if eb != 1 else 255)
+    want = dst0.copy()
+    n = L(s).size
+    covered = np.unique(ou.orc_eval_range(tv, 0, L(tv).size))
+    covered = covered[covered < n]
+    if expect_all:
+        assert covered.size == n
+        assert ou.orc_copy(s, src, d, want) == 0
+    else:
+        so, do = ou.orc_eval_range(s, 0, n), ou.orc_eval_range(d, 0, n)
+        want[do[covered]] = src[so[covered]]
+    tsrc, tdst = dev(src), dev(dst0)
+    a = host.make_tensor(L(s).lower(), tsrc.data_ptr(), ns, eb)
+    b = host.make_tensor(L(d).lower(), tdst.data_ptr(), nd, eb)
+    plan = host.copy_tv((a, None), (b, None), tv)
+    torch.cuda.synchronize()
+    got = tdst.cpu().numpy()
+    assert (got == want).all(), f"copy_tv {s} -> {d} tv={tv}: {int((got != want).sum())} cells differ"
+    return plan
+
+
+@pytest.mark.parametrize("eb", [1, 2, 4, 8])
+def test_copy_partitioned_by_thread_value_layouts(eb):
+    """local_partition-style copies (partition_demo.cpp:26-40): the library-derived raked TV layout on
+    contiguous, transposed, strided and swizzled pairs (vectors where max_common_vector allows), thread-value maps built
+    with the reference's products, and a TV layout that covers only part of the tensor."""
+    pairs = [("4096:1", "4096:1"), ("(64,64):(64,1)", "(64,64):(1,64)"), ("(8,16,8):(1,8,128)", "(8,16,8):(1,64,8)"),
+             ("(128,8,4):(1,128,1024)", "(128,8,4):(f1,f144,f1024)"), ("1000:1", "1000:1"), ("(30,20):(3,91)", "(30,20):(20,1)")]
+    plans = set()
+    for k, (s, d) in enumerate(pairs):
+        tv = host.copy_tv_auto(s, d, eb, threads=64)
+        plans.add(_copy_tv_case(s, d, eb, tv, seed=k))
+    assert plans == {"tv", "tv_vec"} if eb < 8 else plans <= {"tv", "tv_vec"}
+    # partition_demo.cpp: 32 threads in a (4,8) arrangement, 2 values each, over an 8 x 8 tile stored column-major
+    _copy_tv_case("(8,8):(1,8)", "(8,8):(8,1)", eb, "((4,8),2):((16,1),8)", seed=7)
+    # blocked_product((2,2):(1,2), (4,4):(1,4)) as a TV layout: each of 16 threads owns a 2 x 2 block of a 8 x 8 tile
+    _copy_tv_case("(8,8):(1,8)", "(8,8):(1,8)", eb, "((4,4),(2,2)):((2,16),(1,8))", seed=8)
+    # half of the threads only: the other cells keep their pre-fill
+    _copy_tv_case("(8,8):(1,8)", "(8,8):(8,1)", eb, "((4,4),2):((16,1),8)", seed=9, expect_all=False)
+
+
+def test_copy_tv_contracts():
+    src, dst = dev(cells(64, 8, 1)), dev(cells(64, 8, fill=-1))
+    a = host.make_tensor(L("(8,8):(1,8)").lower(), src.data_ptr(), 64, 8)
+    b = host.make_tensor(L("(8,8):(8,1)").lower(), dst.data_ptr(), 64, 8)
+    for tv, status in [("64:1", abi.TLB_ERR_CONTRACT),                       # rank 1: no (thread, value) structure
+                       ("((4,8),2):((16,1),1)", abi.TLB_ERR_UNSUPPORTED),    # two (thread, value) pairs on one coordinate
+                       ("(32,2):(f1,f32)", abi.TLB_ERR_SEMIMODULE)]:
+        with pytest.raises(TlbError) as e:
+            host.copy_tv((a, None), (b, None), tv)
+        assert e.value.status == status, tv
+    torch.cuda.synchronize()
+    assert (dst.cpu().numpy() == -1).all()                                   # nothing was written

@@ -114,3 +114,26 @@ def test_vec_plan_width_is_bounded_by_the_common_vector():
     assert host.max_common_vector("(64,32):(1,64)", "(64,32):(1,128)") == 64
     assert host.copy_plan("(64,32):(1,64)", "(64,32):(1,128)", 4) == "vec"
     assert host.max_common_vector("(63,5):(1,63)", "(63,5):(1,64)") == 63
+
+
+def test_tv_layout_derived_by_raked_product():
+    """tlb_copy_tv_auto: V from max_common_vector (analysis.hpp:18-28) capped at 16 bytes, one tile of T vectors =
+    raked_product((V):(1), (T):(1)) (algebra.hpp:633: the reference returns (T,V):(V,1)), tiles repeated in the value mode."""
+    import oracle_util as ou
+    # contiguous on both sides: 16-byte vectors
+    assert host.copy_tv_auto("4096:1", "4096:1", 4, 256) == "(256,(4,4)):(4,(1,1024))"
+    assert host.copy_tv_auto("4096:1", "4096:1", 2, 128) == "(128,(8,4)):(8,(1,1024))"
+    # a transpose has no common vector: scalar values, the tile is T cells
+    assert host.max_common_vector("(64,64):(64,1)", "(64,64):(1,64)") == 1
+    assert host.copy_tv_auto("(64,64):(64,1)", "(64,64):(1,64)", 4, 256) == "(256,(1,16)):(1,(1,256))"
+    # a common run of 8 fp32: capped at 4 per vector
+    assert host.max_common_vector("(8,16):(1,8)", "(8,16):(1,16)") == 8
+    assert host.copy_tv_auto("(8,16):(1,8)", "(8,16):(1,16)", 4, 32) == "(32,(4,1)):(4,(1,128))"
+    if ou.have_ref():
+        # the (T, V) tile IS the reference's raked_product of the value and the thread layout
+        assert ou.ref_op("raked_product", "4:1", "256:1") == (0, "(256,4):(4,1)")
+        assert ou.ref_op("raked_product", "8:1", "128:1") == (0, "(128,8):(8,1)")
+    # every coordinate of the tensor is covered exactly once (ragged sizes over-cover: predicated tail)
+    tv = host.copy_tv_auto("1000:1", "1000:1", 4, 64)
+    idx = ou.orc_eval_range(tv, 0, host.L(tv).size)
+    assert sorted(idx.tolist()) == list(range(host.L(tv).size)) and host.L(tv).size >= 1000
