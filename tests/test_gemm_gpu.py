@@ -964,3 +964,12 @@ def test_gemm_degenerate_and_ragged_extents(shape):
     _bf16_case(*shape, kat=False, seed=61)
     _bf16_case(*shape, kat=False, seed=67, f16=True)
     _bf16_case(*shape, kat=True, path=1)                             # and on the SIMT plan
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_gemm_packed_plan_with_c_in_the_operand_type(f16, tlb_config):
+    """The packed plan with a 2-byte C: C is gathered into an n-contiguous 2-byte tile buffer, the tcgen05 plan adds into it
+    in that type (one rounding), and the copy scatters it back through C's strided layout."""
+    tlb_config("GEMM_PACK_MIN", "0")
+    assert _c16_case(("(512,256):(3,1549)", "(384,256):(2,771)", "(512,384):(5,2563)"), f16).startswith("packed+umma")
+    assert _c16_case(("(300,200):(f1,f512)", "(100,200):(200,1)", "(300,100):(1,301)"), f16).startswith("packed+umma")
