@@ -414,6 +414,19 @@ def run_ours(args):
         csec = timed(torch, dist, 1, lambda i: y_.copy_(x_), K, W)
         library = {"cublas_bf16_4096_tflops": flops * K / lsec / 1e12, "torch_copy_512MiB_gbs": 2 * x_.numel() * 4 * K / csec / 1e9,
                    "note": "torch.matmul bf16->bf16 / torch copy_ timed in this process with the same recipe"}
+        # the like-for-like of the headline: the library's bf16 x bf16 GEMM with an fp32 output (beta = 0: C written, not
+        # read) and with fp32 C accumulated in place (beta = 1: C += A B^T, the reference's contract, tensor.hpp:226)
+        try:
+            c32 = [torch.zeros(M, N, dtype=torch.float32, device="cuda") for _ in range(nsets)]
+            fsec = timed(torch, dist, 1, lambda i: torch.mm(lsets[i % nsets][0], lsets[i % nsets][1].t(), out_dtype=torch.float32,
+                                                             out=c32[i % nsets]), K, W)
+            library["cublas_bf16_fp32_out_4096_tflops"] = flops * K / fsec / 1e12
+            asec = timed(torch, dist, 1, lambda i: torch.addmm(c32[i % nsets], lsets[i % nsets][0], lsets[i % nsets][1].t(),
+                                                                out_dtype=torch.float32, out=c32[i % nsets]), K, W)
+            library["cublas_bf16_fp32_c_accumulate_4096_tflops"] = flops * K / asec / 1e12
+            del c32
+        except Exception as ex:  # an older torch without out_dtype: the bf16 -> bf16 figure stands alone
+            library["fp32_out_note"] = f"torch.mm(out_dtype=float32) unavailable: {type(ex).__name__}"
         del lsets, x_, y_
     del ha, hb, hc, sets
     torch.cuda.empty_cache()

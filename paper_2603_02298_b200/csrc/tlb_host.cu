@@ -107,8 +107,23 @@ bool gemm_host_pipelined(const tlb_tensor* A, const tlb_tensor* B, const tlb_ten
     // measured on C2: 3.03 ms with 1024-row panels (the default), 3.09 with 512, 3.22 with 2048, 3.76 unpipelined
     const int64_t panel = std::max(512, knob(K_HOST_PANEL) / 512 * 512);
     const int64_t rows = slice_n ? f.N : f.M;
-    const int64_t n_panels = (rows + panel - 1) / panel;
-    if (n_panels < 2 || n_panels > kMaxPanels) return false;
+    if ((rows + panel - 1) / panel < 2 || (rows + panel - 1) / panel > kMaxPanels - 3) return false;
+    // Panel boundaries: full panels, then the last one tapers (1/2, 1/4, 1/4 of a panel, never below 256 rows). What is
+    // left after the last upload is that panel's GEMM and download, so the tail should be small: 4 MiB instead of 16 MiB
+    // of C on the C2 shape (HOST_TAPER=0 keeps uniform panels).
+    int64_t cut[kMaxPanels + 1];
+    int n_panels = 0;
+    cut[0] = 0;
+    {
+        int64_t r = 0;
+        while (rows - r > panel) cut[++n_panels] = (r += panel);
+        const int64_t last = rows - r;
+        if (knob(K_HOST_TAPER) != 0 && last >= 1024 && last % 4 == 0) {
+            cut[++n_panels] = (r += last / 2);
+            cut[++n_panels] = (r += last / 4);
+        }
+        cut[++n_panels] = rows;
+    }
     // the whole buffers are mirrored at the same offsets on the device; a panel is the same layout with fewer rows
     const tlb_tensor& whole_h = slice_n ? *A : *B;                 // uploaded first, in full
     const tlb_tensor& sliced_h = slice_n ? *B : *A;
@@ -141,8 +156,8 @@ bool gemm_host_pipelined(const tlb_tensor* A, const tlb_tensor* B, const tlb_ten
     TLB_PC(cudaMemcpyAsync(d_whole, whole_h.data, static_cast<size_t>(whole_h.capacity) * 2, cudaMemcpyHostToDevice, ctx.s));
     tlb_tensor dw = whole_h;
     dw.data = d_whole;
-    for (int64_t p = 0; p < n_panels; ++p) {
-        const int64_t r0 = p * panel, nr = std::min(panel, rows - r0);
+    for (int p = 0; p < n_panels; ++p) {
+        const int64_t r0 = cut[p], nr = cut[p + 1] - r0;
         // element ranges of the panel inside the two sliced buffers (rows r0 .. r0 + nr, padding included)
         const int64_t s_off = sliced_h.origin + r0 * ld_s, s_len = (nr - 1) * ld_s + f.K;
         const int64_t c_off = C->origin + r0 * ld_c, c_len = (nr - 1) * ld_c + (slice_n ? f.M : f.N);
