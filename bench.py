@@ -686,9 +686,12 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
             sec = timed(torch, dist, world, lambda i: host.gemm_bf16(*fsets[i % 2]), steps, 3)
             fl = 2.0 * M_ * N_ * K_
             per = fl / (sec / steps) / 1e12
+            plan_ = lib.tlb_last_plan().decode()
+            if not plan_.startswith("packed"):   # name the kernel the planner actually chose
+                kernel = "umma_wide_kernel" if plan_.endswith("wide") else "umma_gemm_kernel"
             out.append({"name": name, "metric": "gemm_tflops", "value": fl * steps * world / sec / 1e12, "unit": "TFLOP/s", "n_gpus": world,
                         "scaling": "weak", "steps": steps, "ms_per_step": sec / steps * 1e3,
-                        "config": {"workload": workload, "A": la, "B": lb, "C": lc, "plan": lib.tlb_last_plan().decode()},
+                        "config": {"workload": workload, "A": la, "B": lb, "C": lc, "plan": plan_},
                         "roofline": {"bound": "tensor", "achieved": per, "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": per / pk["bf16_tflops"],
                                      "traffic": None, "kernel": kernel, "peak_source": f"{pk['_source']} burst cuBLAS bf16",
                                      "frac_of_nominal_2250": per / 2250.0, "algorithmic_flop_per_launch": fl}})

@@ -108,7 +108,9 @@ def load() -> C.CDLL:
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2603_02298_b200.build` "
                                "(the CUDA library is the product; there is no CPU fallback)")
-        lib = C.CDLL(str(LIB_PATH))
+        import os
+        # TLB_LIB: a differently built libtlb.so (kernel experiments of tools/, never set by the tests or the bench)
+        lib = C.CDLL(os.environ.get("TLB_LIB") or str(LIB_PATH))
         for name, (res, args) in SYMBOLS.items():
             fn = getattr(lib, name)  # AttributeError if the header and the library disagree
             fn.restype = res

@@ -30,6 +30,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-Wall,-Wno-unused-function",
     "--expt-relaxed-constexpr",
     "-I", str(ROOT / "include"), "-I", str(CSRC),
+    *os.environ.get("TLB_NVCC_EXTRA", "").split(),   # experiments only (e.g. -DTLB_UMMA_STAGES=4)
 ]
 
 

@@ -57,9 +57,15 @@ constexpr uint32_t kTmemCols = 512; // two 256-column fp32 accumulators
 enum { EPI_REGS = 0, EPI_TMA = 1 };
 constexpr uint32_t kEpiChunkBytes = BM * 32 * 4; // 16 KiB
 
+#ifndef TLB_UMMA_STAGES
+#define TLB_UMMA_STAGES 6
+#endif
+#ifndef TLB_UMMA_EPIBUFS
+#define TLB_UMMA_EPIBUFS 1
+#endif
 template <int CG, int EPI, int BN> struct Cfg {
-    static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : 1; // staging buffers per column half
-    static constexpr int kStages = CG == 1 ? 4 : 6; // even: smem stages are released in pairs
+    static constexpr int kEpiBufs = EPI == EPI_REGS ? 0 : (CG == 2 ? TLB_UMMA_EPIBUFS : 1); // staging buffers per column half
+    static constexpr int kStages = CG == 1 ? 4 : TLB_UMMA_STAGES; // even: smem stages are released in pairs
     static constexpr int kPairs = kStages / 2;
     static constexpr int kBRows = CG == 1 ? BN : BN / 2; // rows of B this CTA stages
     static constexpr uint32_t kABytes = BM * BK * 2;
@@ -92,7 +98,7 @@ struct UmmaArgs {
     uint32_t hints;                // L2 cache hints: 1 = operand loads evict_last, 2 = C reductions evict_first
     uint32_t debug;                // TLB_GEMM_DEBUG timing experiments (results are garbage): 1 = no TMA loads after
                                    // the ring is filled once, 2 = epilogue without smem / global traffic,
-                                   // 4 = no staging stores, 8 = no TMA store
+                                   // 4 = no staging stores, 8 = no TMA store, 16 = plain TMA store instead of reduce-add
     long long* trace;              // optional per-CTA timeline (TLB_GEMM_TRACE=<file>), kTraceSlots int64 per CTA
     uint32_t ab_f16;               // operands are fp16 (A / B format fields of the instruction descriptor = 0)
     uint32_t c_16;                 // C has the operands' 2-byte type (TMA epilogue only): 64-column chunks, rounded once, added at L2
@@ -419,7 +425,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
                     if (issuer && !(args.debug & (2u | 8u))) {
                         int tc[5];
                         tile_coords_t<PLAIN>(args.cc, rank_c, false, m0, nbase + ci * cw, batch, tc);
-                        if (hint_c && rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
+                        if ((args.debug & 16u) && rank_c == 3)  // timing experiment: plain store instead of the L2 reduction
+                            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&map_c),
+                                         "r"(buf), "r"(tc[0]), "r"(tc[1]), "r"(tc[2]) : "memory");
+                        else if (hint_c && rank_c == 3) tma_reduce_add_3d_hint(&map_c, buf, tc[0], tc[1], tc[2], pol_c);
                         else tma_reduce_add_tile(&map_c, buf, rank_c, tc);
                         bulk_commit();
                     }
