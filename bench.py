@@ -520,14 +520,18 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
             e.update(extra)
         return e
 
-    def copy_config(name, s, d, eb, workload, kernel, steps, warm, cpu_sample=None, e2e_steps=0, dtype=torch.int32):
+    def copy_config(name, s, d, eb, workload, kernel, steps, warm, cpu_sample=None, e2e_steps=0, dtype=torch.int32, tv_threads=0):
         n = host.L(s).size
         src = torch.arange(host.L(s).lower().max_offset + 1, dtype=dtype, device="cuda")   # element-index bit patterns
         dst = torch.empty(host.L(d).lower().max_offset + 1, dtype=dtype, device="cuda")
         a = host.tensor_of(s, src)
         b = host.tensor_of(d, dst)
         i0, i1 = shard.copy_range(s, world, rank) if world > 1 else (0, 2**64 - 1)
-        sec = timed(torch, dist, world, lambda i: host.copy(a, b, i0, i1), steps, warm)
+        if tv_threads:   # the copy partitioned by the library-derived thread-value layout (every rank the whole problem)
+            tv = host.copy_tv_auto(s, d, eb, tv_threads)
+            sec = timed(torch, dist, world, lambda i: host.copy_tv(a, b, tv), steps, warm)
+        else:
+            sec = timed(torch, dist, world, lambda i: host.copy(a, b, i0, i1), steps, warm)
         plan = lib.tlb_last_plan().decode()
         extra = {}
         if world > 1:
@@ -574,6 +578,13 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
         copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,8191)", 4,
                     "2^25 fp32 elements into a destination whose columns overlap by one cell (stride 8191 < 8192: last writer wins, tensor.hpp:198)",
                     "winner_kernel + ordered_kernel", max(3, K // 8), 2)
+        # the paper's own way of partitioning a copy (local_partition by a thread-value layout): the C1 layouts
+        # through tlb_copy_tv with the TV layout the library derives (max_common_vector + raked_product); the digit-permutation
+        # TV layout composes with both tensors and the call runs the planner's staged plan in TV's order
+        if world == 1:
+            copy_config("Cx_tv_partitioned", "(8192,8192):(8192,1)", "(8192,8192):(1,8192)", 4,
+                        "C1's transpose partitioned by the derived thread-value layout (256 threads): tlb_copy_tv = tlb_copy between src o TV and dst o TV",
+                        "tiled_kernel", max(3, K // 2), 3, tv_threads=256)
         # a stride-0 (broadcast) destination mode: only the slice at its last coordinate survives, so the call is an 8192-element
         # copy; reported as elements of the reference's loop retired per second, not as bandwidth
         n_b = 8192 * 4096

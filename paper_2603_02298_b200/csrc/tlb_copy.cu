@@ -1405,6 +1405,77 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
 
 } // namespace tlb
 
+
+namespace tlb {
+namespace {
+// Partitioning IS composition: the tensors a thread-value layout partitions are src o TV and dst o TV,
+// layouts over the (thread, value) domain. When TV is a bijection onto [0, size) whose leaves are DIGITS of the integral
+// coordinate (sorted by stride they nest: d_0 = 1, d_{k+1} = d_k e_k, what blocked / raked products of compact layouts
+// give), A o TV is exact leaf by leaf with no carries between leaves, and each TV leaf splits into sub-digits that lie
+// inside one leaf of the source and one leaf of the destination (compose, algebra.hpp:235, without the O(|B|)
+// verify_distributed loop: the nesting test is the proof). The copy is then the plain layout-driven copy between the
+// two compositions, walked in TV's own order, and takes the planner's staged / vectorised plans. Returns false when TV
+// is not such a digit permutation, a sub-digit would straddle a leaf, or the result needs more than TLB_MAX_MODES leaves.
+bool tv_compose(const tlb_layout_desc& S, const tlb_layout_desc& D, const tlb_layout_desc& TV, tlb_layout_desc* st, tlb_layout_desc* dt) {
+    if (S.kind != TLB_KIND_INT || D.kind != TLB_KIND_INT || TV.kind != TLB_KIND_INT) return false;
+    if (TV.size != S.size || S.size != D.size || S.size < 1) return false;
+    // TV's leaves as digits of i
+    int order[TLB_MAX_MODES], m = 0;
+    for (int r = 0; r < TV.n_modes; ++r)
+        if (TV.extent[r] > 1) {
+            if (TV.stride[r] <= 0) return false;
+            order[m++] = r;
+        }
+    std::sort(order, order + m, [&](int a, int b) { return TV.stride[a] < TV.stride[b]; });
+    int64_t next = 1;
+    for (int k = 0; k < m; ++k) {
+        if (TV.stride[order[k]] != next) return false;
+        next *= TV.extent[order[k]];
+    }
+    if (next != S.size) return false;
+    // sub-digit (x, q): extent x at index stride q. Inside leaf r of A (prefix product P_r <= q, q % P_r == 0, (q / P_r) x
+    // divides E_r, the last leaf unbounded) it contributes stride_r * (q / P_r) per step.
+    auto locate = [](const tlb_layout_desc& A, int64_t q, int64_t* avail, int64_t* stride) {
+        int64_t P = 1;
+        for (int r = 0; r < A.n_modes; ++r) {
+            const bool last = r + 1 == A.n_modes;
+            if (!last && q >= P * A.extent[r]) {
+                P *= A.extent[r];
+                continue;
+            }
+            if (q % P != 0) return false;
+            const int64_t sub = q / P;
+            if (!last && A.extent[r] % sub != 0) return false;
+            *avail = last ? INT64_MAX : A.extent[r] / sub;
+            if (A.stride[r] != 0 && (sub > INT64_MAX / std::max<int64_t>(1, std::llabs(A.stride[r])))) return false;
+            *stride = A.stride[r] * sub;
+            return true;
+        }
+        return false;
+    };
+    tlb_mode ms[TLB_MAX_MODES], md[TLB_MAX_MODES];
+    int n = 0;
+    for (int r = 0; r < TV.n_modes; ++r) {          // TV's own (colex) leaf order = the order of the composed domain
+        int64_t e = TV.extent[r], q = TV.stride[r];
+        if (e == 1) continue;
+        while (e > 1) {
+            int64_t as, ad, ss, ds;
+            if (!locate(S, q, &as, &ss) || !locate(D, q, &ad, &ds)) return false;
+            const int64_t x = std::min(e, std::min(as, ad));
+            if (x < 2 || e % x != 0 || n == TLB_MAX_MODES) return false;
+            ms[n] = {x, ss, TLB_KIND_INT, 0};
+            md[n] = {x, ds, TLB_KIND_INT, 0};
+            ++n;
+            e /= x;
+            q *= x;
+        }
+    }
+    if (n == 0) return false;
+    return tlb_layout_lower(ms, n, st) == TLB_OK && tlb_layout_lower(md, n, dt) == TLB_OK;
+}
+} // namespace
+} // namespace tlb
+
 extern "C" {
 
 // tla::max_common_vector (analysis.hpp:18-28) from the common refinement: the reference takes the stride-1 identity prefix
@@ -1482,6 +1553,22 @@ int tlb_copy_tv(const tlb_tensor* src, const tlb_tensor* dst, const tlb_layout_d
         const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst->data) + static_cast<uintptr_t>(dspan.lo) * eb;
         const uintptr_t d1 = reinterpret_cast<uintptr_t>(dst->data) + (static_cast<uintptr_t>(dspan.hi) + 1) * eb;
         if (s0 < d1 && d0 < s1) return fail(TLB_ERR_UNSUPPORTED, "tlb_copy_tv: source and destination overlap in memory (use tlb_copy)");
+    }
+    // the partitioned tensors as compositions src o TV / dst o TV: the planner's own plans (vec, tiled, ...) in TV's order
+    if (knob(K_COPY_TV_COMPOSE) != 0) {
+        tlb_layout_desc st, dt;
+        if (tv_compose(S, D, *tv, &st, &dt)) {
+            tlb_tensor cs_t = *src, cd_t = *dst;
+            cs_t.layout = &st;
+            cd_t.layout = &dt;
+            const int rc = copy_impl(&cs_t, &cd_t, 0, UINT64_MAX, cs);
+            if (rc == TLB_OK) {
+                static thread_local char plan_name[64];
+                std::snprintf(plan_name, sizeof(plan_name), "tv:%s", tlb_last_plan());
+                set_plan(plan_name);
+            }
+            return rc;
+        }
     }
     uint64_t n_threads = 1, n_values = 1;
     for (int r = tv->top_start[0]; r < tv->top_start[1]; ++r) n_threads *= static_cast<uint64_t>(tv->extent[r]);

@@ -547,13 +547,44 @@ def test_copy_partitioned_by_thread_value_layouts(eb):
     for k, (s, d) in enumerate(pairs):
         tv = host.copy_tv_auto(s, d, eb, threads=64)
         plans.add(_copy_tv_case(s, d, eb, tv, seed=k))
-    assert plans == {"tv", "tv_vec"} if eb < 8 else plans <= {"tv", "tv_vec"}
+    # digit-permutation TV layouts run as the copy between src o TV and dst o TV ("tv:<plan>"); 1000 = 2^3 5^3 elements with
+    # 64 threads is over-covered by its TV layout and keeps the per-thread kernel, as do the Xor destination's pairs
+    assert plans & {"tv", "tv_vec"} and any(p.startswith("tv:") for p in plans), plans
+    assert all(p in ("tv", "tv_vec") or p.startswith("tv:") for p in plans), plans
     # partition_demo.cpp: 32 threads in a (4,8) arrangement, 2 values each, over an 8 x 8 tile stored column-major
     _copy_tv_case("(8,8):(1,8)", "(8,8):(8,1)", eb, "((4,8),2):((16,1),8)", seed=7)
     # blocked_product((2,2):(1,2), (4,4):(1,4)) as a TV layout: each of 16 threads owns a 2 x 2 block of a 8 x 8 tile
     _copy_tv_case("(8,8):(1,8)", "(8,8):(1,8)", eb, "((4,4),(2,2)):((2,16),(1,8))", seed=8)
     # half of the threads only: the other cells keep their pre-fill
     _copy_tv_case("(8,8):(1,8)", "(8,8):(8,1)", eb, "((4,4),2):((16,1),8)", seed=9, expect_all=False)
+
+
+@pytest.mark.parametrize("eb", [2, 4])
+def test_copy_tv_runs_as_the_copy_between_the_compositions(eb):
+    """Partitioning is composition (compose, algebra.hpp:235): a TV layout that permutes the digits of the
+    integral coordinate turns tlb_copy_tv into tlb_copy between src o TV and dst o TV, so the planner's staged and
+    vectorised plans apply. Same cells as the per-thread kernel (COPY_TV_COMPOSE=0) and as tla::copy."""
+    cases = [("(256,256):(1,256)", "(256,256):(1,256)", None, "tv:vec"),                      # contiguous: vectors
+             ("(256,256):(256,1)", "(256,256):(1,256)", None, "tv:tiled"),                    # transpose: staged tile
+             ("(8,128,64):(1,512,8)", "(8,128,64):(128,1,1024)", None, "tv:"),                # hierarchical permute
+             ("(64,64):(1,64)", "(64,64):(64,1)", "((4,8,2),(2,32)):((16,1,8),(64,128))", "tv:"),  # a hand-built digit permutation
+             ("(96,40):(1,96)", "(96,40):(40,1)", "((32,3),40):((1,32),96)", "tv:")]          # non-power-of-two digits
+    for k, (sl, dl, tv, want) in enumerate(cases):
+        tv = tv or host.copy_tv_auto(sl, dl, eb, threads=256)
+        plan = _copy_tv_case(sl, dl, eb, tv, seed=20 + k)
+        assert plan.startswith(want), (sl, dl, tv, plan)
+        host.config("COPY_TV_COMPOSE", "0")
+        try:
+            assert _copy_tv_case(sl, dl, eb, tv, seed=20 + k) in ("tv", "tv_vec")
+        finally:
+            host.config("COPY_TV_COMPOSE", None)
+    # digits of extent 3, 2, 2 in two different thread / value arrangements over a 12-cell tensor whose destination splits 3 x 4
+    assert _copy_tv_case("12:1", "(3,4):(4,1)", eb, "(3,(2,2)):(1,(3,6))", seed=31).startswith("tv:")
+    assert _copy_tv_case("12:1", "(3,4):(4,1)", eb, "(2,(3,2)):(3,(1,6))", seed=32).startswith("tv:")
+    # a digit of extent 4 splits across the source's leaves 6 and 2 (stride-3 half, then the second leaf)
+    assert _copy_tv_case("(6,2):(1,6)", "(6,2):(2,1)", eb, "(4,3):(3,1)", seed=33).startswith("tv:")
+    # a digit that would straddle a leaf (i = c0 + 4 c1 against a leaf of extent 6): not a composition, per-thread kernel
+    assert _copy_tv_case("(6,2):(1,6)", "(6,2):(2,1)", eb, "(4,3):(1,4)", seed=34) in ("tv", "tv_vec")
 
 
 def test_copy_tv_contracts():
