@@ -205,7 +205,13 @@ int tlb_max_common_vector(const tlb_layout_desc* a, const tlb_layout_desc* b, in
  * coordinate of src and dst (from tlb_layout_lower_ranked): logical thread t copies dst(tv(t, v)) = src(tv(t, v)) for every
  * value v; coordinates at or beyond size(src) are skipped, so a TV layout may over-cover a ragged tensor. tv and dst must
  * be injective (one writer per cell), strides non-negative integers. Runs of the value mode that tv, src and dst all keep
- * contiguous and aligned move as <= 16-byte vectors. Plans "tv_vec" / "tv". */
+ * contiguous and aligned move as <= 16-byte vectors. Plans "tv_vec" / "tv".
+ * Partitioning is composition: when tv is a bijection onto [0, size) whose leaves are digits of the integral coordinate
+ * (sorted by stride they nest; what blocked_product / raked_product of compact layouts give) and every digit falls inside
+ * one leaf of src and of dst, the partitioned tensors src o tv and dst o tv are layouts (compose, algebra.hpp:235; the
+ * nesting test replaces its O(|B|) verify_distributed loop) and the call IS tlb_copy between them, walked in tv's order:
+ * plans "tv:vec", "tv:tiled", ... at the planner's speed (C1 through the derived TV layout: 0.87 -> 6.0 TB/s). Other TV
+ * layouts keep the per-thread kernel; knob COPY_TV_COMPOSE=0 forces it. */
 int tlb_copy_tv(const tlb_tensor* src, const tlb_tensor* dst, const tlb_layout_desc* tv, void* stream);
 /* The thread-value layout the library derives for (src, dst) itself: V = the widest power-of-two vector that
  * tla::max_common_vector(src, dst) (analysis.hpp:18-28) and 16 bytes allow, one tile = raked_product((V):(1), (T):(1)) =
