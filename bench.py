@@ -465,7 +465,7 @@ def run_ours(args):
         del psets
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:   # N = 1 only: at N > 1 the other ranks would idle at the next barrier
         threads = os.cpu_count() or 1
         dt, macs, kind = cpu_gemm_sample(2, 16, 4096, threads)
         per_mac = dt * threads / macs
@@ -502,7 +502,7 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
     out = []
     hbm = pk["hbm_gbs"]
     want = lambda name: only is None or name in only
-    cpu_ok = rank == 0 and not args.no_cpu
+    cpu_ok = rank == 0 and world == 1 and not args.no_cpu   # the CPU legs run at N = 1 only
 
     def entry(name, metric, workload, bytes_per_step, sec, steps, plan, kernel, extra=None):
         # bytes_per_step is the WHOLE problem's algorithmic bytes; at N > 1 each rank moved 1/N of them per step
@@ -573,7 +573,7 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
     # fallback plans: an Xor (swizzled) destination and a non-injective destination
     if want("Cx"):
         copy_config("Cx_xor_dst", "(128,8,65536):(1,128,1024)", "(128,8,65536):(f1,f144,f1024)", 4,
-                    "2^26 fp32 elements into a Swizzle<3,4,3>-per-KiB destination (128,8,65536):(f1,f144,f1024)", "gather_vec_kernel (Xor strides, 16-byte vectors)",
+                    "2^26 fp32 elements into a Swizzle<3,4,3>-per-KiB destination (128,8,65536):(f1,f144,f1024)", "gather_run_kernel (Xor strides, one evaluation per 64-byte run, 256-bit accesses)",
                     max(3, K // 4), 3)
         copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,8191)", 4,
                     "2^25 fp32 elements into a destination whose columns overlap by one cell (stride 8191 < 8192: last writer wins, tensor.hpp:198)",

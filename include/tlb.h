@@ -185,7 +185,8 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
  *                   "tiled_u" with cell-sized accesses for unaligned bases / leading dimensions, "tiled_s" along the
  *                   smallest-stride modes of layouts WITHOUT a unit stride, "tiled_tma" the TMA-fed persistent variant
  *   "gather_vec"    anything else whose low run (max_common_vector, also for Xor layouts) is >= 2 cells: one evaluation
- *                   of both layouts per <= 16-byte vector;  "gather": one cell per thread
+ *                   of both layouts per <= 16-byte vector;  "gather_run": per 32 / 64-byte run both layouts keep, 256-bit
+ *                   accesses;  "gather": one cell per thread
  *   "last_writer+P" non-injective destination whose aliasing is only stride-0 (broadcast) modes: the injective copy
  *                   (plan P) of the slice at their last coordinates;  "ordered": overlapping strides, winner election
  *   "aliased" / "serial"  source and destination overlap in memory (see Aliasing above). */

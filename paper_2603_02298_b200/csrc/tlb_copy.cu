@@ -114,6 +114,34 @@ gather_vec_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_consta
     }
 }
 
+// Same fallback when both layouts keep LONGER runs: a thread moves one run of RB = 32 or 64 bytes per evaluation of the
+// two layouts, as 256-bit accesses (LDG.E.256 / STG.E.256: every request covers whole 32-byte sectors; 16-byte lanes 64
+// bytes apart would ask for every sector twice).
+template <int RB>
+__global__ void __launch_bounds__(kThreads)
+gather_run_kernel(const __grid_constant__ tlb_layout_desc S, const __grid_constant__ tlb_layout_desc D,
+                  const char* __restrict__ src, char* __restrict__ dst, int64_t s_origin, int64_t d_origin, uint64_t i0,
+                  uint64_t n_runs, int run_elems, int elem_bytes) {
+    pdl_wait();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n_runs; k += stride) {
+        const uint64_t i = i0 + k * static_cast<uint64_t>(run_elems);
+        const char* sp = src + dev_position(S, s_origin, dev_eval(S, i)) * elem_bytes;
+        char* dp = dst + dev_position(D, d_origin, dev_eval(D, i)) * elem_bytes;
+        uint64_t v[RB / 8];
+#pragma unroll
+        for (int j = 0; j < RB / 32; ++j)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.b64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(v[4 * j]), "=l"(v[4 * j + 1]), "=l"(v[4 * j + 2]), "=l"(v[4 * j + 3])
+                         : "l"(sp + 32 * j));
+#pragma unroll
+        for (int j = 0; j < RB / 32; ++j)
+            asm volatile("st.global.L1::no_allocate.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dp + 32 * j), "l"(v[4 * j]), "l"(v[4 * j + 1]),
+                         "l"(v[4 * j + 2]), "l"(v[4 * j + 3])
+                         : "memory");
+    }
+}
+
 // Thread-value partitioned copy (local_partition; partition_demo.cpp:26-40): TV is a rank-2 layout
 // (thread, value) -> integral coordinate. GPU thread t is logical thread t; it walks its values in chunks of `vec` cells
 // that the host has proven contiguous and aligned in TV, source and destination (vec = 1: cell by cell).
@@ -754,8 +782,28 @@ int launch_gather(const CopyCall& c) {
         V = std::min(low_run(*c.src, 16 / eb), low_run(*c.dst, 16 / eb));
         while (V > 1 && (c.i0 % V != 0 || c.n % V != 0)) V >>= 1;
     }
+    // runs of 32 or 64 bytes that both layouts keep contiguous and aligned: one evaluation per run, 256-bit accesses
+    int R = 1;
+    if (V * eb == 16 && knob(K_COPY_GATHER_RUN) != 0) {
+        R = std::min(low_run(*c.src, 64 / eb), low_run(*c.dst, 64 / eb));
+        while (R * eb > 16 && (c.i0 % R != 0 || c.n % R != 0)) R >>= 1;
+        if (R * eb < 32) R = 1;
+    }
     if (g_dry_run) {
-        set_plan(V > 1 ? "gather_vec" : "gather");
+        set_plan(R > 1 ? "gather_run" : V > 1 ? "gather_vec" : "gather");
+        return TLB_OK;
+    }
+    if (R > 1) {
+        const uint64_t n_runs = c.n / R;
+        const int gridr = launch_grid(n_runs, kThreads, 8);
+        const char* sb = static_cast<const char*>(c.src->data);
+        char* db = static_cast<char*>(c.dst->data);
+        if (R * eb == 64)
+            TLB_CUDA(launch_pdl(gather_run_kernel<64>, dim3(gridr), dim3(kThreads), 0, c.stream, S, D, sb, db, c.src->origin, c.dst->origin, c.i0, n_runs, R, eb));
+        else
+            TLB_CUDA(launch_pdl(gather_run_kernel<32>, dim3(gridr), dim3(kThreads), 0, c.stream, S, D, sb, db, c.src->origin, c.dst->origin, c.i0, n_runs, R, eb));
+        count_launch();
+        set_plan("gather_run");
         return TLB_OK;
     }
     if (V > 1) {

@@ -66,6 +66,7 @@ enum KnobId {
     K_GEMM_PACK,        // 1: operands / C that no tensor map can address are packed and run on tcgen05 (default), 0: SIMT plan
     K_GEMM_PACK_MIN,    // log2 of the smallest M*N*K that takes the packed plan
     K_COPY_TV_COMPOSE,  // tlb_copy_tv: run digit-permutation TV layouts as the copy between src o TV and dst o TV (1), or always the per-thread kernel (0)
+    K_COPY_GATHER_RUN,  // gather fallback: 32 / 64-byte runs per evaluation with 256-bit accesses (1), or 16-byte vectors only (0)
     K_HOST_TAPER,       // pipelined host GEMM: the last panel is cut into 1/2, 1/4, 1/4 so that little is left after the last upload
     K_COUNT
 };

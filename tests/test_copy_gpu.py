@@ -222,7 +222,7 @@ def test_copy_structured_fuzz_reaches_every_plan():
         s, d, so, do, slack = _structured_pair(rng)
         plans.add(run_copy_case(s, d, int(rng.choice([1, 2, 4, 8, 16])), src_origin=so, dst_origin=do, slack=slack, seed=case))
     kinds = {p.split("+")[0] for p in plans}
-    assert {"vec", "tiled", "gather", "gather_vec", "last_writer"} <= kinds and kinds & {"tiled_u", "tiled_s"}, plans
+    assert {"vec", "tiled", "gather", "last_writer"} <= kinds and kinds & {"tiled_u", "tiled_s"} and kinds & {"gather_vec", "gather_run"}, plans
 
 
 def test_copy_xor_layouts():
@@ -242,10 +242,11 @@ def test_copy_xor_layouts():
     assert (tdst.cpu().numpy() == want).all()
 
 
-@pytest.mark.parametrize("eb,plan", [(1, "gather_vec"), (2, "gather_vec"), (4, "gather_vec"), (8, "gather_vec"), (16, "gather")])
+@pytest.mark.parametrize("eb,plan", [(1, "gather_vec"), (2, "gather_run"), (4, "gather_run"), (8, "gather_run"), (16, "gather_run")])
 def test_copy_xor_layouts_vectorised(eb, plan):
     """Swizzled (Xor) layouts keep the low coordinate bits contiguous (leaf 0 is f1, the other masks start at bit 4): the
-    gather evaluates both layouts once per 16-byte vector (max_common_vector, analysis.hpp:18-28, extended to Xor leaves).
+    gather evaluates both layouts once per 16-byte vector (max_common_vector, analysis.hpp:18-28, extended to Xor leaves),
+    or once per 32 / 64-byte run moved with 256-bit accesses when both layouts keep that much contiguous ("gather_run").
     Both directions, an Xor layout on both sides, origins (Xor acts on the absolute position, tensor.hpp:57) and a range
     that is not a whole number of vectors (falls back to one cell per thread)."""
     sw, flat = "(128,8,32):(f1,f144,f1024)", "(128,8,32):(1,128,1024)"
@@ -254,6 +255,11 @@ def test_copy_xor_layouts_vectorised(eb, plan):
     assert run_copy_case(sw, "(128,8,32):(f1,f160,f1024)", eb, seed=2) == plan   # two different swizzles
     assert run_copy_case(flat, sw, eb, src_origin=16, dst_origin=32768, seed=3) == plan
     assert run_copy_case(flat, sw, eb, src_origin=1, dst_origin=32768, seed=4) in ("gather", "gather_vec")   # unaligned source
+    host.config("COPY_GATHER_RUN", "0")
+    try:
+        assert run_copy_case(flat, sw, eb, seed=5) == ("gather" if eb == 16 else "gather_vec")
+    finally:
+        host.config("COPY_GATHER_RUN", None)
 
 
 @pytest.mark.parametrize("eb", [2, 4, 8])

@@ -22,9 +22,11 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(8,3):(1,8)", "(8,3):(3,1)", 8, "gather"),
     # Xor strides, interleaved runs, ragged rows, aliasing destinations
     ("(8,8):(f1,f9)", "64:1", 8, "gather"),
-    # ... but a swizzle that leaves the low bits alone moves whole 16-byte vectors per evaluation
-    ("(128,8,64):(1,128,1024)", "(128,8,64):(f1,f144,f1024)", 4, "gather_vec"),
-    ("(128,8,64):(f1,f144,f1024)", "(128,8,64):(1,128,1024)", 2, "gather_vec"),
+    # ... but a swizzle that leaves the low bits alone moves whole 16-byte vectors per evaluation, 32 / 64-byte runs when
+    # both layouts keep them (Swizzle<3,4,3> on fp32 cells: 16 cells), with 256-bit accesses
+    ("(128,8,64):(1,128,1024)", "(128,8,64):(f1,f144,f1024)", 4, "gather_run"),
+    ("(128,8,64):(f1,f144,f1024)", "(128,8,64):(1,128,1024)", 2, "gather_run"),
+    ("(128,8,64):(f1,f144,f1024)", "(128,8,64):(1,128,1024)", 1, "gather_vec"),
     ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, "gather"),
     ("(96,160):(160,1)", "(96,160):(1,96)", 2, "gather"),
     # no unit stride on the source: the staged plan runs along the smallest-stride mode
