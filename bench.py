@@ -575,6 +575,9 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
         copy_config("Cx_xor_dst", "(128,8,65536):(1,128,1024)", "(128,8,65536):(f1,f144,f1024)", 4,
                     "2^26 fp32 elements into a Swizzle<3,4,3>-per-KiB destination (128,8,65536):(f1,f144,f1024)", "gather_run_kernel (Xor strides, one evaluation per 64-byte run, 256-bit accesses)",
                     max(3, K // 4), 3)
+        copy_config("Cx_ragged_transpose", "(8000,6000):(6000,1)", "(8000,6000):(1,8000)", 4,
+                    "fp32 8000x6000 transpose: rows are not whole 128-byte pieces nor whole tiles (whole-tile body on the staged plan + edge strips)",
+                    "tiled_kernel (body) + gather_joint_kernel (edge strips)", max(3, K // 4), 3)
         copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,8191)", 4,
                     "2^25 fp32 elements into a destination whose columns overlap by one cell (stride 8191 < 8192: last writer wins, tensor.hpp:198)",
                     "winner_kernel + ordered_kernel", max(3, K // 8), 2)

@@ -1401,6 +1401,80 @@ int try_last_writer_slice(const CopyCall& c, bool* done) {
     return st;
 }
 
+// Ragged extents (a 4000 x 3000 transpose: rows of 3000 cells are not whole 128-byte pieces, 4000 rows not whole tiles).
+// The staged plan needs whole tiles, so the call is cut, on the refined modes, into a BODY whose two run modes are rounded
+// down to tile multiples and at most two edge strips: the tail of the A run over every b, and the tail of the B run over the
+// body's a. The destination is injective and the pieces are disjoint boxes of the coordinate space, so each piece is an
+// independent copy and the union is tla::copy's result. Pieces recurse (a 160-row tail is a 128-row body plus 32 rows).
+thread_local int g_ragged_depth = 0;
+thread_local std::string g_ragged_plan;
+int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
+    *done = false;
+    if (g_copy_path != 0 || g_ragged_depth >= 3 || knob(K_COPY_RAGGED) == 0 || !R.ok) return TLB_OK;
+    const int eb = c.dst->elem_bytes;
+    if (eb != 1 && eb != 2 && eb != 4 && eb != 8 && eb != 16) return TLB_OK;
+    const std::vector<JM>& modes = R.modes;
+    if (modes.size() > TLB_MAX_MODES) return TLB_OK;
+    int ia = -1, ib = -1;
+    for (size_t r = 0; r < modes.size(); ++r) {
+        if (modes[r].ss == 1 && ia < 0) ia = static_cast<int>(r);
+        if (modes[r].ds == 1 && ib < 0) ib = static_cast<int>(r);
+    }
+    if (ia < 0 || ib < 0 || ia == ib) return TLB_OK;
+    const int64_t La = 128 / eb, eA = modes[ia].e, eB = modes[ib].e;
+    // small copies: one gather launch beats a handful of launches (1000 x 1000 fp32: 13 us as one gather). The knob is the
+    // log2 of the smallest element count that is cut (default 22).
+    if (c.n < (1ull << std::min(40, knob(K_COPY_RAGGED)))) return TLB_OK;
+    // the tallest tile that fits (the leftover rows recurse into shorter tiles: measured better than starting with short
+    // tiles, 300^3 reversal 65 us against 78 us)
+    int64_t Lb = 0;
+    for (int64_t cand : {256, 128, 64, 32}) {
+        if ((cand == 256 && !lb256_enabled()) || (eb == 1 && cand < 128) || cand > eB) continue;
+        Lb = cand;
+        break;
+    }
+    if (Lb == 0 || eA < La) return TLB_OK;
+    const int64_t bodyA = eA / La * La, bodyB = eB / Lb * Lb;
+    if (bodyA == eA && bodyB == eB) return TLB_OK; // whole tiles already: the staged plan was refused for another reason
+    // one piece: A coordinates [a0, a0 + ea), B coordinates [b0, b0 + ebx), every other mode whole
+    auto piece = [&](int64_t a0, int64_t ea, int64_t b0, int64_t ebx) -> int {
+        tlb_mode sm[TLB_MAX_MODES], dm[TLB_MAX_MODES];
+        for (size_t r = 0; r < modes.size(); ++r) {
+            const int64_t e = static_cast<int>(r) == ia ? ea : static_cast<int>(r) == ib ? ebx : modes[r].e;
+            sm[r] = {e, modes[r].ss, TLB_KIND_INT, 0};
+            dm[r] = {e, modes[r].ds, TLB_KIND_INT, 0};
+        }
+        tlb_layout_desc ls, ld;
+        TLB_TRY(tlb_layout_lower(sm, static_cast<int>(modes.size()), &ls));
+        TLB_TRY(tlb_layout_lower(dm, static_cast<int>(modes.size()), &ld));
+        tlb_tensor s2 = *c.src, d2 = *c.dst;
+        s2.layout = &ls;
+        d2.layout = &ld;
+        s2.origin = R.base_s + a0 * modes[ia].ss + b0 * modes[ib].ss;
+        d2.origin = R.base_d + a0 * modes[ia].ds + b0 * modes[ib].ds;
+        ++g_ragged_depth;
+        const int st = copy_impl(&s2, &d2, 0, static_cast<uint64_t>(ls.size), c.stream);
+        --g_ragged_depth;
+        return st;
+    };
+    // the cut pays only if the body takes a staged plan: ask the planner first
+    const bool was_dry = g_dry_run;
+    g_dry_run = true;
+    const int probe = piece(0, bodyA, 0, bodyB);
+    g_dry_run = was_dry;
+    const std::string body_plan = tlb_last_plan();
+    if (probe != TLB_OK || body_plan.compare(0, 5, "tiled") != 0) return TLB_OK;
+    g_ragged_plan = "ragged:" + body_plan;
+    if (!g_dry_run) {
+        TLB_TRY(piece(0, bodyA, 0, bodyB));
+        if (bodyA < eA) TLB_TRY(piece(bodyA, eA - bodyA, 0, eB));
+        if (bodyB < eB) TLB_TRY(piece(0, bodyA, bodyB, eB - bodyB));
+    }
+    set_plan(g_ragged_plan.c_str());
+    *done = true;
+    return TLB_OK;
+}
+
 int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, uint64_t i_end, cudaStream_t stream) {
     TLB_TRY(check_tensor(src, "tlb_copy source", false));
     TLB_TRY(check_tensor(dst, "tlb_copy destination", true));
@@ -1446,6 +1520,10 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
         if (done) return TLB_OK;
         if (g_copy_path == 2 || g_copy_path == 3)
             return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the forced tiled path does not apply to these layouts");
+        if (refined.ok) {
+            TLB_TRY(try_ragged(c, refined, &done));
+            if (done) return TLB_OK;
+        }
         if (refined.ok && refined.modes.size() <= TLB_MAX_MODES) return launch_gather_joint(c, refined);
     }
     return launch_gather(c);

@@ -24,7 +24,7 @@ def cells(n: int, eb: int, seed: int = 0, fill=None) -> np.ndarray:
     return rng.integers(info.min, info.max, m, dtype=dt, endpoint=True)
 
 
-def run_copy_case(s: str, d: str, eb: int = 8, src_origin=0, dst_origin=0, path=0, slack=0, seed=0):
+def run_copy_case(s: str, d: str, eb: int = 8, src_origin=0, dst_origin=0, path=0, slack=0, seed=0, i_begin=0, i_end=2**64 - 1):
     """GPU tlb_copy vs the C restatement on the same seeded cells; returns the plan name."""
     from paper_2603_02298_b200 import abi
     ns, nd = ou.cosize_of(s) + src_origin + slack, ou.cosize_of(d) + dst_origin + slack
@@ -33,9 +33,9 @@ def run_copy_case(s: str, d: str, eb: int = 8, src_origin=0, dst_origin=0, path=
     want = dst0.copy()
     if eb == 16:
         sv, wv = src.view([("a", np.int64), ("b", np.int64)]), want.view([("a", np.int64), ("b", np.int64)])
-        st = ou.orc_copy(s, sv, d, wv, src_origin, dst_origin)
+        st = ou.orc_copy(s, sv, d, wv, src_origin, dst_origin, i_begin=i_begin, i_end=min(i_end, L(s).size))
     else:
-        st = ou.orc_copy(s, src, d, want, src_origin, dst_origin)
+        st = ou.orc_copy(s, src, d, want, src_origin, dst_origin, i_begin=i_begin, i_end=min(i_end, L(s).size))
     assert st == 0
     tsrc, tdst = dev(src), dev(dst0)
     ls, ld = L(s), L(d)
@@ -44,7 +44,7 @@ def run_copy_case(s: str, d: str, eb: int = 8, src_origin=0, dst_origin=0, path=
     b = host.make_tensor(dd, tdst.data_ptr(), nd, eb, dst_origin)
     prev = abi.load().tlb_copy_set_path(path)
     try:
-        plan = host.copy((a, None), (b, None))
+        plan = host.copy((a, None), (b, None), i_begin, i_end)
     finally:
         abi.load().tlb_copy_set_path(prev)
     torch.cuda.synchronize()

@@ -225,6 +225,31 @@ def test_copy_structured_fuzz_reaches_every_plan():
     assert {"vec", "tiled", "gather", "last_writer"} <= kinds and kinds & {"tiled_u", "tiled_s"} and kinds & {"gather_vec", "gather_run"}, plans
 
 
+@pytest.mark.parametrize("eb", [2, 4, 8, 16])
+def test_copy_ragged_extents_take_the_staged_plan(eb):
+    """Extents that are not whole tiles (a 403 x 301 transpose, a ragged hierarchical permute, padded rows, origins, a
+    sub-range of whole outer slices): the call is cut into a whole-tile body on the staged plan and edge strips; every cell
+    of the destination, pre-fill included, equals tla::copy's (tensor.hpp:195-199). The cut starts at 2^22 elements by
+    default (smaller copies are one gather launch); the small cases lower that bound through the knob."""
+    assert run_copy_case("(2403,1801):(1801,1)", "(2403,1801):(1,2403)", eb).startswith("ragged:tiled")     # default threshold
+    assert run_copy_case("(403,301):(301,1)", "(403,301):(1,403)", eb, seed=7) == "gather"
+    host.config("COPY_RAGGED", "14")
+    try:
+        assert run_copy_case("(403,301):(301,1)", "(403,301):(1,403)", eb).startswith("ragged:tiled")
+        assert run_copy_case("(403,301):(1,403)", "(403,301):(301,1)", eb, seed=1).startswith("ragged:tiled")
+        assert run_copy_case("(520,300):(304,1)", "(520,300):(1,528)", eb, slack=40, seed=2).startswith("ragged:tiled")   # padded leading dimensions
+        assert run_copy_case("(70,50,40):(1,70,3500)", "(70,50,40):(2000,40,1)", eb, seed=3).startswith("ragged:")        # rank-3 reversal
+        assert run_copy_case("(403,301):(301,1)", "(403,301):(1,403)", eb, src_origin=3, dst_origin=5, seed=4).startswith("ragged:")
+        if eb == 4:
+            # a sub-range of whole outer slices of a ragged rank-3 permute
+            s, d = "(300,70,8):(70,1,21000)", "(300,70,8):(1,300,21000)"
+            assert run_copy_case(s, d, eb, i_begin=2 * 21000, i_end=7 * 21000, seed=5).startswith("ragged:")
+        host.config("COPY_RAGGED", "0")
+        assert run_copy_case("(2403,1801):(1801,1)", "(2403,1801):(1,2403)", eb, seed=6) == "gather"
+    finally:
+        host.config("COPY_RAGGED", None)
+
+
 def test_copy_xor_layouts():
     run_copy_case("(8,8):(f1,f9)", "64:1", 8)
     run_copy_case("64:1", "(8,8):(f1,f9)", 4)

@@ -29,6 +29,13 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(128,8,64):(f1,f144,f1024)", "(128,8,64):(1,128,1024)", 1, "gather_vec"),
     ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, "gather"),
     ("(96,160):(160,1)", "(96,160):(1,96)", 2, "gather"),
+    # ragged extents (rows that are not whole 128-byte pieces / whole tiles): a whole-tile body on the staged plan plus
+    # edge strips, from 2^22 elements (smaller copies are one gather launch)
+    ("(4000,3000):(3000,1)", "(4000,3000):(1,4000)", 4, "ragged:tiled"),
+    ("(4001,3001):(3001,1)", "(4001,3001):(1,4001)", 4, "ragged:tiled_u"),
+    ("(300,300,300):(1,300,90000)", "(300,300,300):(90000,300,1)", 4, "ragged:tiled"),
+    ("(1000,1000):(1000,1)", "(1000,1000):(1,1000)", 4, "gather"),
+    ("(33,33):(33,1)", "(33,33):(1,33)", 4, "gather"),
     # no unit stride on the source: the staged plan runs along the smallest-stride mode
     ("(2048,2048):(3,6151)", "(2048,2048):(2048,1)", 2, "tiled_s"),
     ("(2048,2048):(2048,1)", "(2048,2048):(5,10243)", 4, "tiled_s"),
