@@ -38,6 +38,8 @@ namespace {
 
 thread_local int g_copy_path = 0; // 0 auto, 1 gather, 2 tiled (LDG), 3 tiled TMA
 thread_local bool g_dry_run = false; // tlb_copy_plan: run the planner, launch nothing
+thread_local int g_ragged_depth = 0;   // recursion depth of the ragged cut (try_ragged)
+thread_local std::string g_ragged_plan;
 
 // TLB_COPY_TMA=1 makes the TMA-fed tiled kernel the default for layouts that admit a tensor map.
 bool tma_default() { return knob(K_COPY_TMA) == 1; }
@@ -1065,6 +1067,15 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         };
         while (vb > eb && !fits(vb)) vb >>= 1;
         if (eb == 16) vb = fits(16) ? 16 : 0;
+        // A run whose extent alone keeps the vectors narrow (an odd number of cells): large copies are cut into whole
+        // 16-byte vectors plus the last cells of the run (try_ragged) instead of moving everything cell by cell.
+        if (vb < 16 && eb < 16 && g_copy_path == 0 && g_ragged_depth == 0 && knob(K_COPY_RAGGED) != 0 &&
+            c.n >= (1ull << std::min(40, knob(K_COPY_RAGGED))) && modes[ia].e >= 16 / eb) {
+            bool wide = aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
+            for (size_t r = 0; wide && r < modes.size(); ++r)
+                if (static_cast<int>(r) != ia) wide = modes[r].ss % (16 / eb) == 0 && modes[r].ds % (16 / eb) == 0;
+            if (wide) return TLB_OK;
+        }
         if (vb < eb || vb == 1 || !fits(vb)) return TLB_OK;
         const int64_t v = vb / eb;
         std::vector<JM> order;
@@ -1406,8 +1417,6 @@ int try_last_writer_slice(const CopyCall& c, bool* done) {
 // down to tile multiples and at most two edge strips: the tail of the A run over every b, and the tail of the B run over the
 // body's a. The destination is injective and the pieces are disjoint boxes of the coordinate space, so each piece is an
 // independent copy and the union is tla::copy's result. Pieces recurse (a 160-row tail is a 128-row body plus 32 rows).
-thread_local int g_ragged_depth = 0;
-thread_local std::string g_ragged_plan;
 int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
     *done = false;
     if (g_copy_path != 0 || g_ragged_depth >= 3 || knob(K_COPY_RAGGED) == 0 || !R.ok) return TLB_OK;
@@ -1420,7 +1429,48 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
         if (modes[r].ss == 1 && ia < 0) ia = static_cast<int>(r);
         if (modes[r].ds == 1 && ib < 0) ib = static_cast<int>(r);
     }
-    if (ia < 0 || ib < 0 || ia == ib) return TLB_OK;
+    if (ia < 0 || ib < 0) return TLB_OK;
+    if (c.n < (1ull << std::min(40, knob(K_COPY_RAGGED)))) return TLB_OK;
+    if (ia == ib) {
+        // one mode contiguous on both sides whose extent is not a whole number of 16-byte vectors (an odd number of bytes):
+        // whole vectors on the vec plan, the last cells of the run through the gather
+        const int64_t V = 16 / eb, e = modes[ia].e, body = e / V * V;
+        if (eb >= 16 || body == e || body == 0) return TLB_OK;
+        auto part = [&](int64_t a0, int64_t ea) -> int {
+            tlb_mode sm[TLB_MAX_MODES], dm[TLB_MAX_MODES];
+            for (size_t r = 0; r < modes.size(); ++r) {
+                const int64_t ex = static_cast<int>(r) == ia ? ea : modes[r].e;
+                sm[r] = {ex, modes[r].ss, TLB_KIND_INT, 0};
+                dm[r] = {ex, modes[r].ds, TLB_KIND_INT, 0};
+            }
+            tlb_layout_desc ls, ld;
+            TLB_TRY(tlb_layout_lower(sm, static_cast<int>(modes.size()), &ls));
+            TLB_TRY(tlb_layout_lower(dm, static_cast<int>(modes.size()), &ld));
+            tlb_tensor s2 = *c.src, d2 = *c.dst;
+            s2.layout = &ls;
+            d2.layout = &ld;
+            s2.origin = R.base_s + a0 * modes[ia].ss;
+            d2.origin = R.base_d + a0 * modes[ia].ds;
+            ++g_ragged_depth;
+            const int st = copy_impl(&s2, &d2, 0, static_cast<uint64_t>(ls.size), c.stream);
+            --g_ragged_depth;
+            return st;
+        };
+        const bool was_dry = g_dry_run;
+        g_dry_run = true;
+        const int probe = part(0, body);
+        g_dry_run = was_dry;
+        const std::string body_plan = tlb_last_plan();
+        if (probe != TLB_OK || body_plan != "vec") return TLB_OK;
+        g_ragged_plan = "ragged:vec";
+        if (!g_dry_run) {
+            TLB_TRY(part(0, body));
+            TLB_TRY(part(body, e - body));
+        }
+        set_plan(g_ragged_plan.c_str());
+        *done = true;
+        return TLB_OK;
+    }
     const int64_t La = 128 / eb, eA = modes[ia].e, eB = modes[ib].e;
     // small copies: one gather launch beats a handful of launches (1000 x 1000 fp32: 13 us as one gather). The knob is the
     // log2 of the smallest element count that is cut (default 22).

@@ -244,6 +244,10 @@ def test_copy_ragged_extents_take_the_staged_plan(eb):
             # a sub-range of whole outer slices of a ragged rank-3 permute
             s, d = "(300,70,8):(70,1,21000)", "(300,70,8):(1,300,21000)"
             assert run_copy_case(s, d, eb, i_begin=2 * 21000, i_end=7 * 21000, seed=5).startswith("ragged:")
+        if eb < 16:
+            # one contiguous mode that is not a whole number of 16-byte vectors: whole vectors on the vec plan, the rest gathered
+            n_odd = 16 // eb * 1237 + 1
+            assert run_copy_case(f"({n_odd},29):(1,{n_odd})", f"({n_odd},29):(1,{n_odd})", eb, seed=8) == "ragged:vec"
         host.config("COPY_RAGGED", "0")
         assert run_copy_case("(2403,1801):(1801,1)", "(2403,1801):(1,2403)", eb, seed=6) == "gather"
     finally:

@@ -35,6 +35,7 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(4001,3001):(3001,1)", "(4001,3001):(1,4001)", 4, "ragged:tiled_u"),
     ("(300,300,300):(1,300,90000)", "(300,300,300):(90000,300,1)", 4, "ragged:tiled"),
     ("(1000,1000):(1000,1)", "(1000,1000):(1,1000)", 4, "gather"),
+    ("(5001,5003):(1,5001)", "(5001,5003):(1,5001)", 1, "ragged:vec"),     # an odd number of contiguous bytes
     ("(33,33):(33,1)", "(33,33):(1,33)", 4, "gather"),
     # no unit stride on the source: the staged plan runs along the smallest-stride mode
     ("(2048,2048):(3,6151)", "(2048,2048):(2048,1)", 2, "tiled_s"),
