@@ -578,6 +578,9 @@ def other_configs(torch, dist, world, rank, lib, host, shard, pk, K, W, args, on
         copy_config("Cx_ragged_transpose", "(8000,6000):(6000,1)", "(8000,6000):(1,8000)", 4,
                     "fp32 8000x6000 transpose: rows are not whole 128-byte pieces nor whole tiles (whole-tile body on the staged plan + edge strips)",
                     "tiled_kernel (body) + gather_joint_kernel (edge strips)", max(3, K // 4), 3)
+        copy_config("Cx_interleave", "(4,16777216):(1,4)", "(4,16777216):(16777216,1)", 4,
+                    "AoS -> SoA: 2^24 fp32 4-vectors de-interleaved into four planar rows (register-permuting interleave plan, 256-bit accesses)",
+                    "interleave_kernel<4, 4, true>", max(3, K // 4), 3)
         copy_config("Cx_non_injective_dst", "(8192,4096):(1,8192)", "(8192,4096):(1,8191)", 4,
                     "2^25 fp32 elements into a destination whose columns overlap by one cell (stride 8191 < 8192: last writer wins, tensor.hpp:198)",
                     "winner_kernel + ordered_kernel", max(3, K // 8), 2)

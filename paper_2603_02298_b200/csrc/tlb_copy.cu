@@ -347,6 +347,92 @@ vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, ch
 }
 
 // ---------------------------------------------------------------------------------------
+// interleave: AoS <-> SoA. A short mode c (2, 3, 4 or 8 cells: channels, the parts of a complex number) and a long mode j
+// where one side keeps (c, j) jointly contiguous (cell j * EC + c: interleaved) and the other keeps j contiguous for each
+// c (planar, rows `planar_stride` apart). The staged plan has no whole 128-byte A run that leaves a unit-stride B run here.
+// A lane owns NJ = G * 16 / EB consecutive j: on the interleaved side that is one contiguous piece of EC * G * 16 bytes, on
+// the planar side EC pieces of G * 16 bytes, and the permutation between them happens in registers. Consecutive lanes own
+// consecutive pieces, so every warp-level access covers whole sectors on both sides (256-bit accesses on the interleaved
+// side, where a lane's piece is a multiple of 32 bytes: G = 2 for odd EC); no shared memory, no barriers.
+// ---------------------------------------------------------------------------------------
+struct InterParams {
+    JointDesc rest;          // unit index / nJ -> base offsets (elements) of the other modes on both sides
+    int64_t nJ;              // units along j
+    int64_t planar_stride;   // elements between the rows of consecutive c on the planar side
+    uint64_t n_units;
+    int32_t wide_i, wide_p;  // 256-bit accesses allowed on the interleaved / planar side (32-byte alignment proven)
+};
+
+__device__ __forceinline__ void ld32(const char* p, uint4* lo, uint4* hi) {
+    uint64_t a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+    lo->x = static_cast<uint32_t>(a); lo->y = static_cast<uint32_t>(a >> 32); lo->z = static_cast<uint32_t>(b); lo->w = static_cast<uint32_t>(b >> 32);
+    hi->x = static_cast<uint32_t>(c); hi->y = static_cast<uint32_t>(c >> 32); hi->z = static_cast<uint32_t>(d); hi->w = static_cast<uint32_t>(d >> 32);
+}
+__device__ __forceinline__ void st32(char* p, const uint4& lo, const uint4& hi) {
+    const uint64_t a = lo.x | (static_cast<uint64_t>(lo.y) << 32), b = lo.z | (static_cast<uint64_t>(lo.w) << 32);
+    const uint64_t c = hi.x | (static_cast<uint64_t>(hi.y) << 32), d = hi.z | (static_cast<uint64_t>(hi.w) << 32);
+    asm volatile("st.global.L1::no_allocate.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
+template <int EB, int EC, bool DEINT>
+__global__ void __launch_bounds__(kThreads)
+interleave_kernel(const __grid_constant__ InterParams P, const char* __restrict__ src, char* __restrict__ dst) {
+    using T = typename Cell<EB>::type;
+    constexpr int V = 16 / EB, G = (EC % 2) ? 2 : 1, NJ = G * V, NE = EC * NJ, NV = EC * G; // NV 16-byte vectors per unit
+    pdl_wait();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < P.n_units; w += stride) {
+        const uint64_t t = w / static_cast<uint64_t>(P.nJ), u = w - t * static_cast<uint64_t>(P.nJ);
+        int64_t bs, bd;
+        dev_joint(P.rest, t, &bs, &bd);
+        union { uint4 v[NV]; T e[NE]; } inter;   // cell jj * EC + c
+        union { uint4 v[G]; T e[NJ]; } row;      // cells jj of one c
+        if constexpr (DEINT) {
+            const char* sp = src + (bs + static_cast<int64_t>(u) * NE) * EB;
+            if (P.wide_i) {
+#pragma unroll
+                for (int k = 0; k < NV; k += 2) ld32(sp + 16 * k, &inter.v[k], &inter.v[k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) inter.v[k] = ldg_stream(sp + 16 * k);
+            }
+#pragma unroll
+            for (int c = 0; c < EC; ++c) {
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) row.e[jj] = inter.e[jj * EC + c];
+                char* dp = dst + (bd + static_cast<int64_t>(u) * NJ + c * P.planar_stride) * EB;
+                if (G == 2 && P.wide_p) st32(dp, row.v[0], row.v[G - 1]);
+                else {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) stg_stream(dp + 16 * g, row.v[g]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < EC; ++c) {
+                const char* sp = src + (bs + static_cast<int64_t>(u) * NJ + c * P.planar_stride) * EB;
+                if (G == 2 && P.wide_p) ld32(sp, &row.v[0], &row.v[G - 1]);
+                else {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) row.v[g] = ldg_stream(sp + 16 * g);
+                }
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) inter.e[jj * EC + c] = row.e[jj];
+            }
+            char* dp = dst + (bd + static_cast<int64_t>(u) * NE) * EB;
+            if (P.wide_i) {
+#pragma unroll
+                for (int k = 0; k < NV; k += 2) st32(dp + 16 * k, inter.v[k], inter.v[k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) stg_stream(dp + 16 * k, inter.v[k]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // tiled: swizzled shared-memory staging between a source-contiguous run A and a
 // destination-contiguous run B.
 // ---------------------------------------------------------------------------------------
@@ -1111,6 +1197,63 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         return TLB_OK;
     }
     if (ia == ib) return TLB_OK;
+
+    // ---- interleave plan (AoS <-> SoA): a short mode c and a long mode j, (c, j) jointly contiguous on one side, j
+    // contiguous on the other
+    if (!strided_runs && g_copy_path == 0 && knob(K_COPY_INTERLEAVE) != 0 && (eb == 1 || eb == 2 || eb == 4 || eb == 8)) {
+        auto short_mode = [](int64_t e) { return e == 2 || e == 3 || e == 4 || e == 8; };
+        const bool deint = modes[ib].ss == modes[ia].e && short_mode(modes[ia].e);   // source interleaved: c = ia (ss 1), j = ib (ds 1, ss = |c|)
+        const bool inter = !deint && modes[ia].ds == modes[ib].e && short_mode(modes[ib].e); // destination interleaved: c = ib (ds 1), j = ia (ss 1, ds = |c|)
+        if (deint || inter) {
+            const int ic = deint ? ia : ib, ij = deint ? ib : ia;
+            const int64_t EC = modes[ic].e, V = 16 / eb, G = (EC % 2) ? 2 : 1, NJ = G * V;
+            const int64_t pstride = deint ? modes[ic].ds : modes[ic].ss;
+            bool ok = (EC == 2 || EC == 3 || EC == 4 || EC == 8) && modes[ij].e % NJ == 0 && pstride % V == 0 && pstride > 0 &&
+                      aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
+            bool wide = aligned_to(sp, base_s, eb, 32) && aligned_to(dp, base_d, eb, 32);
+            bool wide_p = wide && pstride % (2 * V) == 0;
+            std::vector<JM> rest;
+            for (size_t r = 0; ok && r < modes.size(); ++r) {
+                if (static_cast<int>(r) == ic || static_cast<int>(r) == ij || modes[r].e == 1) continue;
+                ok = modes[r].ss % V == 0 && modes[r].ds % V == 0;
+                wide = wide && modes[r].ss % (2 * V) == 0 && modes[r].ds % (2 * V) == 0;
+                rest.push_back(modes[r]);
+            }
+            if (ok) {
+                std::stable_sort(rest.begin(), rest.end(), [](const JM& a, const JM& b) {
+                    return std::min(std::llabs(a.ss), std::llabs(a.ds)) < std::min(std::llabs(b.ss), std::llabs(b.ds));
+                });
+                InterParams P;
+                std::memset(&P, 0, sizeof(P));
+                TLB_TRY(fill_joint(rest, &P.rest));
+                P.nJ = modes[ij].e / NJ;
+                P.planar_stride = pstride;
+                uint64_t units = static_cast<uint64_t>(P.nJ);
+                for (const JM& m : rest) units *= static_cast<uint64_t>(m.e);
+                P.n_units = units;
+                P.wide_i = wide ? 1 : 0;
+                P.wide_p = wide && wide_p ? 1 : 0;
+                if (g_dry_run) {
+                    set_plan("interleave");
+                    *done = true;
+                    return TLB_OK;
+                }
+                const int grid = launch_grid(units, kThreads, 8);
+                const char* sb = sp + base_s * eb;
+                char* db = dp + base_d * eb;
+#define TLB_IL2(EB, EC_) do { if (deint) TLB_CUDA(launch_pdl(interleave_kernel<EB, EC_, true>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); \
+                              else TLB_CUDA(launch_pdl(interleave_kernel<EB, EC_, false>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); } while (0)
+#define TLB_IL(EB) do { if (EC == 2) TLB_IL2(EB, 2); else if (EC == 3) TLB_IL2(EB, 3); else if (EC == 4) TLB_IL2(EB, 4); else TLB_IL2(EB, 8); } while (0)
+                if (eb == 1) TLB_IL(1); else if (eb == 2) TLB_IL(2); else if (eb == 4) TLB_IL(4); else TLB_IL(8);
+#undef TLB_IL
+#undef TLB_IL2
+                count_launch();
+                set_plan("interleave");
+                *done = true;
+                return TLB_OK;
+            }
+        }
+    }
 
     // ---- tiled plan
     if (eb != 1 && eb != 2 && eb != 4 && eb != 8 && eb != 16) return TLB_OK;

@@ -254,6 +254,38 @@ def test_copy_ragged_extents_take_the_staged_plan(eb):
         host.config("COPY_RAGGED", None)
 
 
+@pytest.mark.parametrize("eb", [1, 2, 4, 8])
+@pytest.mark.parametrize("ec", [2, 3, 4, 8])
+def test_copy_interleave_plan(eb, ec):
+    """AoS <-> SoA (a short mode of 2 / 3 / 4 / 8 cells against a long one): the register-permuting interleave plan, both
+    directions, with outer modes, padded planar rows, origins that break the 32-byte alignment of the 256-bit accesses,
+    a sub-range of whole outer slices, and a j extent that is not a whole number of lane pieces (gather)."""
+    nj = 16 // eb * (2 if ec % 2 else 1)          # j per lane
+    J = nj * 37
+    aos, soa = f"({ec},{J}):(1,{ec})", f"({ec},{J}):({J},1)"
+    assert run_copy_case(aos, soa, eb) == "interleave"
+    assert run_copy_case(soa, aos, eb, seed=1) == "interleave"
+    # three outer images, planar rows padded by 2 lane pieces, interleaved images padded too
+    pj = J + 2 * nj
+    aos3, soa3 = f"({ec},{J},3):(1,{ec},{ec * pj})", f"({ec},{J},3):({pj},1,{ec * pj})"
+    assert run_copy_case(aos3, soa3, eb, seed=2) == "interleave"
+    assert run_copy_case(soa3, aos3, eb, seed=3) == "interleave"
+    # origins of 16 bytes: 128-bit accesses only
+    assert run_copy_case(aos, soa, eb, src_origin=16 // eb, dst_origin=16 // eb, seed=4) == "interleave"
+    assert run_copy_case(soa3, aos3, eb, src_origin=16 // eb, dst_origin=48 // eb, seed=5) == "interleave"
+    # whole outer slices 1 .. 2 of the three images
+    n1 = ec * J
+    assert run_copy_case(aos3, soa3, eb, i_begin=n1, i_end=3 * n1, seed=6) == "interleave"
+    # not a whole number of lane pieces / an unaligned origin: the gather plans
+    assert run_copy_case(f"({ec},{J + 1}):(1,{ec})", f"({ec},{J + 1}):({J + 1},1)", eb, seed=7).startswith("gather")
+    assert run_copy_case(aos, soa, eb, src_origin=1, seed=8).startswith("gather")
+    host.config("COPY_INTERLEAVE", "0")
+    try:
+        assert run_copy_case(aos, soa, eb, seed=9).startswith("gather")
+    finally:
+        host.config("COPY_INTERLEAVE", None)
+
+
 def test_copy_xor_layouts():
     run_copy_case("(8,8):(f1,f9)", "64:1", 8)
     run_copy_case("64:1", "(8,8):(f1,f9)", 4)
