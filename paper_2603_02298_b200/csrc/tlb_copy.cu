@@ -347,7 +347,8 @@ vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, ch
 }
 
 // ---------------------------------------------------------------------------------------
-// interleave: AoS <-> SoA. A short mode c (2, 3, 4 or 8 cells: channels, the parts of a complex number) and a long mode j
+// interleave: AoS <-> SoA. A short mode c (2 .. 8, 12 or 16 cells: channels, the parts of a complex number, the short side of a
+// tall-skinny transpose) and a long mode j
 // where one side keeps (c, j) jointly contiguous (cell j * EC + c: interleaved) and the other keeps j contiguous for each
 // c (planar, rows `planar_stride` apart). The staged plan has no whole 128-byte A run that leaves a unit-stride B run here.
 // A lane owns NJ = G * 16 / EB consecutive j: on the interleaved side that is one contiguous piece of EC * G * 16 bytes, on
@@ -1201,14 +1202,14 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     // ---- interleave plan (AoS <-> SoA): a short mode c and a long mode j, (c, j) jointly contiguous on one side, j
     // contiguous on the other
     if (!strided_runs && g_copy_path == 0 && knob(K_COPY_INTERLEAVE) != 0 && (eb == 1 || eb == 2 || eb == 4 || eb == 8)) {
-        auto short_mode = [](int64_t e) { return e == 2 || e == 3 || e == 4 || e == 8; };
+        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 8) || e == 12 || e == 16; };
         const bool deint = modes[ib].ss == modes[ia].e && short_mode(modes[ia].e);   // source interleaved: c = ia (ss 1), j = ib (ds 1, ss = |c|)
         const bool inter = !deint && modes[ia].ds == modes[ib].e && short_mode(modes[ib].e); // destination interleaved: c = ib (ds 1), j = ia (ss 1, ds = |c|)
         if (deint || inter) {
             const int ic = deint ? ia : ib, ij = deint ? ib : ia;
             const int64_t EC = modes[ic].e, V = 16 / eb, G = (EC % 2) ? 2 : 1, NJ = G * V;
             const int64_t pstride = deint ? modes[ic].ds : modes[ic].ss;
-            bool ok = (EC == 2 || EC == 3 || EC == 4 || EC == 8) && modes[ij].e % NJ == 0 && pstride % V == 0 && pstride > 0 &&
+            bool ok = short_mode(EC) && modes[ij].e % NJ == 0 && pstride % V == 0 && pstride > 0 &&
                       aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
             bool wide = aligned_to(sp, base_s, eb, 32) && aligned_to(dp, base_d, eb, 32);
             bool wide_p = wide && pstride % (2 * V) == 0;
@@ -1243,7 +1244,9 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
                 char* db = dp + base_d * eb;
 #define TLB_IL2(EB, EC_) do { if (deint) TLB_CUDA(launch_pdl(interleave_kernel<EB, EC_, true>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); \
                               else TLB_CUDA(launch_pdl(interleave_kernel<EB, EC_, false>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); } while (0)
-#define TLB_IL(EB) do { if (EC == 2) TLB_IL2(EB, 2); else if (EC == 3) TLB_IL2(EB, 3); else if (EC == 4) TLB_IL2(EB, 4); else TLB_IL2(EB, 8); } while (0)
+#define TLB_IL(EB) do { switch (EC) { case 2: TLB_IL2(EB, 2); break; case 3: TLB_IL2(EB, 3); break; case 4: TLB_IL2(EB, 4); break; case 5: TLB_IL2(EB, 5); break; \
+                                      case 6: TLB_IL2(EB, 6); break; case 7: TLB_IL2(EB, 7); break; case 8: TLB_IL2(EB, 8); break; case 12: TLB_IL2(EB, 12); break; \
+                                      default: TLB_IL2(EB, 16); break; } } while (0)
                 if (eb == 1) TLB_IL(1); else if (eb == 2) TLB_IL(2); else if (eb == 4) TLB_IL(4); else TLB_IL(8);
 #undef TLB_IL
 #undef TLB_IL2

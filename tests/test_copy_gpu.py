@@ -255,9 +255,9 @@ def test_copy_ragged_extents_take_the_staged_plan(eb):
 
 
 @pytest.mark.parametrize("eb", [1, 2, 4, 8])
-@pytest.mark.parametrize("ec", [2, 3, 4, 8])
+@pytest.mark.parametrize("ec", [2, 3, 4, 5, 6, 7, 8, 12, 16])
 def test_copy_interleave_plan(eb, ec):
-    """AoS <-> SoA (a short mode of 2 / 3 / 4 / 8 cells against a long one): the register-permuting interleave plan, both
+    """AoS <-> SoA and tall-skinny transposes (a short mode of 2 .. 8, 12 or 16 cells against a long one): the register-permuting interleave plan, both
     directions, with outer modes, padded planar rows, origins that break the 32-byte alignment of the 256-bit accesses,
     a sub-range of whole outer slices, and a j extent that is not a whole number of lane pieces (gather)."""
     nj = 16 // eb * (2 if ec % 2 else 1)          # j per lane

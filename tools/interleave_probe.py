@@ -33,3 +33,13 @@ for sl, dl, eb, what in cases:
     a, b = host.tensor_of(sl, src), host.tensor_of(dl, dst)
     sec = t(lambda: host.copy(a, b))
     print(f"{what}: {lib.tlb_last_plan().decode()} {2 * n * eb / sec / 1e9:.0f} GB/s ({sec * 1e6:.0f} us)")
+M = 2 ** 22
+for nn, eb in ((16, 4), (12, 4), (6, 4), (16, 2), (5, 8)):
+    sl, dl = f"({M},{nn}):({nn},1)", f"({M},{nn}):(1,{M})"
+    n = M * nn
+    src = torch.arange(n, dtype=torch.int64, device="cuda").to({2: torch.int16, 4: torch.int32, 8: torch.int64}[eb])
+    dst = torch.zeros_like(src)
+    a, b = host.tensor_of(sl, src), host.tensor_of(dl, dst)
+    sec = t(lambda: host.copy(a, b))
+    ok = torch.equal(dst.view(nn, M), src.view(M, nn).t())
+    print(f"tall-skinny transpose {M} x {nn} eb={eb}: {lib.tlb_last_plan().decode()} {2 * n * eb / sec / 1e9:.0f} GB/s ({sec * 1e6:.0f} us) correct={ok}")
