@@ -24,6 +24,7 @@
 //
 // All contract / bounds / overflow checks happen on the host before any launch.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -1618,6 +1619,51 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
         return TLB_OK;
     }
     const int64_t La = 128 / eb, eA = modes[ia].e, eB = modes[ib].e;
+    // AoS <-> SoA whose long mode is not a whole number of lane pieces: whole pieces on the interleave plan, the last j gathered
+    if (eb < 16) {
+        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 8) || e == 12 || e == 16; };
+        const bool deint = modes[ib].ss == eA && short_mode(eA), inter = !deint && modes[ia].ds == eB && short_mode(eB);
+        if (deint || inter) {
+            const int64_t EC = deint ? eA : eB, eJ = deint ? eB : eA, NJ = (16 / eb) * ((EC % 2) ? 2 : 1), bodyJ = eJ / NJ * NJ;
+            if (bodyJ >= NJ && bodyJ != eJ) {
+                auto cut = [&](int64_t j0, int64_t ej) { return deint ? std::array<int64_t, 4>{0, eA, j0, ej} : std::array<int64_t, 4>{j0, ej, 0, eB}; };
+                auto run = [&](const std::array<int64_t, 4>& q) -> int {
+                    tlb_mode sm[TLB_MAX_MODES], dm[TLB_MAX_MODES];
+                    for (size_t r = 0; r < modes.size(); ++r) {
+                        const int64_t e = static_cast<int>(r) == ia ? q[1] : static_cast<int>(r) == ib ? q[3] : modes[r].e;
+                        sm[r] = {e, modes[r].ss, TLB_KIND_INT, 0};
+                        dm[r] = {e, modes[r].ds, TLB_KIND_INT, 0};
+                    }
+                    tlb_layout_desc ls, ld;
+                    TLB_TRY(tlb_layout_lower(sm, static_cast<int>(modes.size()), &ls));
+                    TLB_TRY(tlb_layout_lower(dm, static_cast<int>(modes.size()), &ld));
+                    tlb_tensor s2 = *c.src, d2 = *c.dst;
+                    s2.layout = &ls;
+                    d2.layout = &ld;
+                    s2.origin = R.base_s + q[0] * modes[ia].ss + q[2] * modes[ib].ss;
+                    d2.origin = R.base_d + q[0] * modes[ia].ds + q[2] * modes[ib].ds;
+                    ++g_ragged_depth;
+                    const int st = copy_impl(&s2, &d2, 0, static_cast<uint64_t>(ls.size), c.stream);
+                    --g_ragged_depth;
+                    return st;
+                };
+                const bool was_dry = g_dry_run;
+                g_dry_run = true;
+                const int probe = run(cut(0, bodyJ));
+                g_dry_run = was_dry;
+                if (probe == TLB_OK && std::string(tlb_last_plan()) == "interleave") {
+                    g_ragged_plan = "ragged:interleave";
+                    if (!g_dry_run) {
+                        TLB_TRY(run(cut(0, bodyJ)));
+                        TLB_TRY(run(cut(bodyJ, eJ - bodyJ)));
+                    }
+                    set_plan(g_ragged_plan.c_str());
+                    *done = true;
+                    return TLB_OK;
+                }
+            }
+        }
+    }
     // small copies: one gather launch beats a handful of launches (1000 x 1000 fp32: 13 us as one gather). The knob is the
     // log2 of the smallest element count that is cut (default 22).
     if (c.n < (1ull << std::min(40, knob(K_COPY_RAGGED)))) return TLB_OK;

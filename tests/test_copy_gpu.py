@@ -284,6 +284,14 @@ def test_copy_interleave_plan(eb, ec):
         assert run_copy_case(aos, soa, eb, seed=9).startswith("gather")
     finally:
         host.config("COPY_INTERLEAVE", None)
+    # a long mode that is not a whole number of lane pieces (planar rows still 16-byte aligned): whole pieces + the last j
+    host.config("COPY_RAGGED", "4")
+    try:
+        jr, pr = J + 1, J + nj
+        assert run_copy_case(f"({ec},{jr}):(1,{ec})", f"({ec},{jr}):({pr},1)", eb, seed=10) == "ragged:interleave"
+        assert run_copy_case(f"({ec},{jr}):({pr},1)", f"({ec},{jr}):(1,{ec})", eb, seed=11) == "ragged:interleave"
+    finally:
+        host.config("COPY_RAGGED", None)
 
 
 def test_copy_xor_layouts():
