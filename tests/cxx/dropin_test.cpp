@@ -59,7 +59,9 @@ static void copy_pairs() {
     for (Row row : {Row{"8:1", "8:1"}, Row{"(8,2,3):(1,16,32)", "(8,2,3):(1,16,32)"}, Row{"(2,3,2):(42,1,128)", "12:1"},
                     Row{"12:1", "(2,3,2):(42,1,128)"}, Row{"7:0", "7:1"}, Row{"7:0", "7:0"},
                     Row{"(8,3):(1,8)", "(8,3):(3,1)"}, Row{"(8,(3,5)):(1,(57,8))", "(8,15):(1,8)"},
-                    Row{"(256,128):(128,1)", "(256,128):(1,256)"}}) {
+                    Row{"(256,128):(128,1)", "(256,128):(1,256)"},
+                    // round-2 plans: AoS -> SoA and a tall-skinny transpose (interleave)
+                    Row{"(4,64):(1,4)", "(4,64):(64,1)"}, Row{"(64,6):(6,1)", "(64,6):(1,64)"}}) {
         Layout src_l = L(row.src), dst_l = L(row.dst);
         auto src_store = std::make_shared<std::vector<Int>>(static_cast<size_t>(cosize(src_l)));
         std::iota(src_store->begin(), src_store->end(), 0);
@@ -161,6 +163,13 @@ static void tv_partitioned_copy() {
     copy(DeviceTensor(dsrc.p, Int(dsrc.n), 8, src), DeviceTensor(ddst.p, Int(ddst.n), 8, dst), tv);    // device
     cudaDeviceSynchronize();
     CHECK(ddst.get() == *out);
+    // partitioning is composition: the reference's own compose gives the partitioned tensors src o tv and
+    // dst o tv, and the plain copy between them is the same copy (this is what tlb_copy_tv runs for digit-permutation TVs)
+    Layout st = compose(src, tv), dt = compose(dst, tv);
+    DevBuf<Int> ddst2(std::vector<Int>(static_cast<size_t>(cosize(dst)), -1));
+    copy(DeviceTensor(dsrc.p, Int(dsrc.n), 8, st), DeviceTensor(ddst2.p, Int(ddst2.n), 8, dt));
+    cudaDeviceSynchronize();
+    CHECK(ddst2.get() == *out);
     Layout s8 = L("(8,8):(1,8)"), d8 = L("(8,8):(8,1)");
     auto st8 = std::make_shared<std::vector<Int>>(64);
     std::iota(st8->begin(), st8->end(), 3);
