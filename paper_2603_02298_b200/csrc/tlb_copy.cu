@@ -646,13 +646,14 @@ tiled_cell_kernel(const __grid_constant__ TileParams P, const char* __restrict__
     __syncthreads();
     const T* s = reinterpret_cast<const T*>(src) + base_s;
     T* d = reinterpret_cast<T*>(dst) + base_d;
+    const int ua = P.ua, ub = P.ub;                    // > 1: "tiled_s", runs along the smallest-stride modes
     constexpr int STEP = (N % (kThreads * U) == 0) ? U : 1;
     for (int i0 = threadIdx.x; i0 < N; i0 += kThreads * STEP) {
         T v[STEP];
 #pragma unroll
         for (int u = 0; u < STEP; ++u) {
             const int i = i0 + u * kThreads, b = i / LA, a = i % LA;
-            v[u] = s[s_offB[b] + a];
+            v[u] = s[s_offB[b] + static_cast<int64_t>(a) * ua];
         }
 #pragma unroll
         for (int u = 0; u < STEP; ++u) {
@@ -665,7 +666,7 @@ tiled_cell_kernel(const __grid_constant__ TileParams P, const char* __restrict__
 #pragma unroll
         for (int u = 0; u < STEP; ++u) {
             const int i = i0 + u * kThreads, a = i / LB, b = i % LB;
-            d[s_offA[a] + b] = *reinterpret_cast<const T*>(tile + b * PITCH + a * EB);
+            d[s_offA[a] + static_cast<int64_t>(b) * ub] = *reinterpret_cast<const T*>(tile + b * PITCH + a * EB);
         }
     }
 }
@@ -1449,14 +1450,14 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
             return TLB_OK;
         }
         const unsigned grid = static_cast<unsigned>(tiles);
-        if (unaligned && !strided_runs && knob(K_COPY_CELL_TILES) != 0) {
-            // unit-stride runs, nothing 16-byte aligned: consecutive lanes on consecutive cells
+        if (unaligned && knob(K_COPY_CELL_TILES) != 0) {
+            // nothing 16-byte aligned, or runs without a unit stride: consecutive lanes on consecutive cells of the run
 #define TLB_TC(EB) do { if (Lb == 128) TLB_CUDA(launch_pdl(tiled_cell_kernel<EB, 128>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); \
                         else TLB_CUDA(launch_pdl(tiled_cell_kernel<EB, 32>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); } while (0)
             if (eb == 2) TLB_TC(2); else if (eb == 4) TLB_TC(4); else TLB_TC(8);
 #undef TLB_TC
             count_launch();
-            set_plan("tiled_u");
+            set_plan(strided_runs ? "tiled_s" : "tiled_u");
             *done = true;
             return TLB_OK;
         }
