@@ -1348,7 +1348,8 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
                 rest.push_back(m);
             }
         const bool unaligned = !ok;
-        if (unaligned && ((eb != 2 && eb != 4 && eb != 8) || (Lb != 128 && Lb != 32) || g_copy_path == 3)) continue;
+        const bool cell_tiles = knob(K_COPY_CELL_TILES) != 0;   // 1-byte cells only have the cell-granular kernel, 128-row tiles
+        if (unaligned && ((eb != 2 && eb != 4 && eb != 8 && !(eb == 1 && cell_tiles && Lb == 128)) || (Lb != 128 && Lb != 32) || g_copy_path == 3)) continue;
         // B must be contiguous on the destination (row b -> +b) and A on the source: by construction.
         TileParams P;
         std::memset(&P, 0, sizeof(P));
@@ -1454,7 +1455,8 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
             // nothing 16-byte aligned, or runs without a unit stride: consecutive lanes on consecutive cells of the run
 #define TLB_TC(EB) do { if (Lb == 128) TLB_CUDA(launch_pdl(tiled_cell_kernel<EB, 128>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); \
                         else TLB_CUDA(launch_pdl(tiled_cell_kernel<EB, 32>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); } while (0)
-            if (eb == 2) TLB_TC(2); else if (eb == 4) TLB_TC(4); else TLB_TC(8);
+            if (eb == 1) TLB_CUDA(launch_pdl(tiled_cell_kernel<1, 128>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db));
+            else if (eb == 2) TLB_TC(2); else if (eb == 4) TLB_TC(4); else TLB_TC(8);
 #undef TLB_TC
             count_launch();
             set_plan(strided_runs ? "tiled_s" : "tiled_u");

@@ -57,7 +57,7 @@ def test_copy_tiled_plan_one_byte_cells(s, d):
     assert run_copy_case("(96,160):(160,1)", "(96,160):(1,96)", 1) == "gather"   # no 128-row B run
 
 
-@pytest.mark.parametrize("eb", [2, 4, 8])
+@pytest.mark.parametrize("eb", [1, 2, 4, 8])
 @pytest.mark.parametrize("s,d,so,do", [
     ("(256,128):(129,1)", "(256,128):(1,256)", 0, 0),                     # padded source rows: not a multiple of 16 bytes
     ("(256,128):(128,1)", "(256,128):(1,257)", 0, 0),                     # padded destination columns
@@ -67,8 +67,8 @@ def test_copy_tiled_plan_one_byte_cells(s, d):
 def test_copy_tiled_plan_unaligned(s, d, so, do, eb):
     """Leading dimensions / origins that break 16-byte alignment keep the staged plan with cell-sized global accesses."""
     plan = run_copy_case(s, d, eb, src_origin=so, dst_origin=do)
-    if s.startswith("(96,160)") and eb == 2:
-        assert plan == "gather"            # 160 two-byte cells are not a whole number of 128-byte rows
+    if s.startswith("(96,160)") and eb <= 2:
+        assert plan == "gather"            # 160 one- or two-byte cells are not a whole number of 128-byte rows (1-byte: 128-row tiles only)
     else:
         assert plan == "tiled_u"
 
@@ -154,7 +154,7 @@ def test_copy_forced_gather_equals_tiled():
 def test_copy_misaligned_origins_fall_back_and_stay_exact():
     assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 4, src_origin=1, dst_origin=3) == "tiled_u"
     assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 2, src_origin=1, dst_origin=3) == "tiled_u"
-    assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 1, src_origin=1, dst_origin=3) == "gather"
+    assert run_copy_case("(256,128):(128,1)", "(256,128):(1,256)", 1, src_origin=1, dst_origin=3) == "tiled_u"   # 1-byte cells: the cell-granular staged kernel (round 2)
     assert run_copy_case("4096:1", "4096:1", 2, src_origin=1, dst_origin=1) in ("vec", "gather")
 
 

@@ -60,8 +60,9 @@ def test_plan_depends_on_alignment_and_range():
     s, d = "(256,128):(128,1)", "(256,128):(1,256)"
     assert host.copy_plan(s, d, 4) == "tiled"
     assert host.copy_plan(s, d, 4, src_align=4) == "tiled_u"           # 16-byte vectors need 16-byte bases: cell-sized accesses
-    assert host.copy_plan(s, d, 2, src_align=2) == "tiled_u"           # ... for 2-, 4- and 8-byte cells
-    assert host.copy_plan(s, d, 1, src_align=1) == "gather"
+    assert host.copy_plan(s, d, 2, src_align=2) == "tiled_u"           # ... for 1-, 2-, 4- and 8-byte cells
+    assert host.copy_plan(s, d, 1, src_align=1) == "tiled_u"           # (1-byte cells: 128-row tiles only)
+    assert host.copy_plan("(96,256):(256,1)", "(96,256):(1,96)", 1, src_align=1) == "gather"
     assert host.copy_plan(s, d, 4, 0, 256 * 64) == "tiled"             # whole slices of the outermost mode
     assert host.copy_plan(s, d, 4, 5, 777) == "gather"                 # ragged range
     assert host.copy_plan(s, d, 4, 10, 10) == "empty"
