@@ -186,6 +186,8 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
  *                   smallest-stride modes of layouts WITHOUT a unit stride, "tiled_tma" the TMA-fed persistent variant
  *   "interleave"    AoS <-> SoA (a short mode of 2 .. 8, 12 or 16 cells against a long one): register permutation, whole
  *                   sectors on both sides, no shared memory
+ *   "tiled_n"       a whole short mode as one of the runs (a 4M x 24 transpose, 9-field AoS): cell-granular staged tiles with
+ *                   run-time extents
  *   "ragged:P"      run extents that are not whole tiles, from 2^22 elements: a whole-tile body on staged plan P plus edge
  *                   strips (disjoint boxes of an injective destination, each an independent copy)
  *   "gather_vec"    anything else whose low run (max_common_vector, also for Xor layouts) is >= 2 cells: one evaluation

@@ -671,6 +671,98 @@ tiled_cell_kernel(const __grid_constant__ TileParams P, const char* __restrict__
     }
 }
 
+// tiled, narrow runs ("tiled_n"): one of the two runs is a whole SHORT mode that no 128-byte row / 32-row tile can be assembled
+// from: a source-contiguous mode of la < 128 / EB cells (a 4M x 24 transpose, AoS with 9 or 24 fields: what the register-
+// permuting interleave plan does not cover), or a destination-contiguous mode of lb < 32 cells (the opposite direction).
+// Same cell-granular scheme as tiled_cell_kernel with run-time tile extents: consecutive lanes walk the tile in (b, a)
+// order when loading and in (a, b) order when storing (for an interleaved side that is one contiguous stream); the staged
+// row pitch is an odd number of words, so the column-wise accesses are conflict free for every extent.
+constexpr int kNarrowTileBytes = 256 * 132, kNarrowMaxRun = 256;
+template <int EB>
+__global__ void __launch_bounds__(kThreads)
+tiled_narrow_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src, char* __restrict__ dst) {
+    using T = typename Cell<EB>::type;
+    __shared__ __align__(16) unsigned char tile[kNarrowTileBytes];
+    __shared__ int64_t s_offB[kNarrowMaxRun];
+    __shared__ int64_t s_offA[kNarrowMaxRun];
+    pdl_wait();
+    const int la = P.La, lb = P.Lb;
+    const int pitch = ((((la * EB + 3) >> 2) | 1) + (EB == 8 ? 1 : 0)) << 2;   // bytes; 8-byte cells keep 8-byte alignment (even word count)
+    int64_t base_s, base_d;
+    dev_joint(P.rest, blockIdx.x, &base_s, &base_d);
+    for (int t = threadIdx.x; t < lb + la; t += kThreads) {
+        const bool isB = t < lb;
+        uint32_t i = isB ? t : t - lb;
+        const int np = isB ? P.nB : P.nA;
+        int64_t acc = 0;
+        for (int p = 0; p < np; ++p) {
+            const uint32_t e = static_cast<uint32_t>(isB ? P.eB[p] : P.eA[p]);
+            const uint32_t c = (p + 1 < np) ? i % e : i;
+            i /= e;
+            acc += static_cast<int64_t>(c) * (isB ? P.sB[p] : P.dA[p]);
+        }
+        if (isB) s_offB[t] = acc;
+        else s_offA[t - lb] = acc;
+    }
+    __syncthreads();
+    const T* s = reinterpret_cast<const T*>(src) + base_s;
+    T* d = reinterpret_cast<T*>(dst) + base_d;
+    const int n = lb * la;
+    constexpr int U = 4;   // cells in flight per thread
+    {
+        // (b, a) of the thread's k-th cell advance by (256 / la, 256 % la) with one carry: no division in the loop
+        const int db = kThreads / la, da = kThreads % la;
+        int b = threadIdx.x / la, a = threadIdx.x % la;
+        int i = threadIdx.x;
+        for (; i + (U - 1) * kThreads < n; i += U * kThreads) {
+            T v[U];
+            int off[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = s[s_offB[b] + a];
+                off[u] = b * pitch + a * EB;
+                a += da;
+                b += db;
+                if (a >= la) { a -= la; ++b; }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) *reinterpret_cast<T*>(tile + off[u]) = v[u];
+        }
+        for (; i < n; i += kThreads) {
+            *reinterpret_cast<T*>(tile + b * pitch + a * EB) = s[s_offB[b] + a];
+            a += da;
+            b += db;
+            if (a >= la) { a -= la; ++b; }
+        }
+    }
+    __syncthreads();
+    {
+        const int da = kThreads / lb, db = kThreads % lb;
+        int a = threadIdx.x / lb, b = threadIdx.x % lb;
+        int i = threadIdx.x;
+        for (; i + (U - 1) * kThreads < n; i += U * kThreads) {
+            T v[U];
+            int64_t off[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = *reinterpret_cast<const T*>(tile + b * pitch + a * EB);
+                off[u] = s_offA[a] + b;
+                b += db;
+                a += da;
+                if (b >= lb) { b -= lb; ++a; }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) d[off[u]] = v[u];
+        }
+        for (; i < n; i += kThreads) {
+            d[s_offA[a] + b] = *reinterpret_cast<const T*>(tile + b * pitch + a * EB);
+            b += db;
+            a += da;
+            if (b >= lb) { b -= lb; ++a; }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // tiled, TMA-fed: phase 1 is a cp.async.bulk.tensor load through a tensor map derived from the source layout
 // (tlb_tensormap_describe: parent = the source's refined modes, tile = the A and B runs) with the hardware
@@ -1500,6 +1592,66 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         return TLB_OK;
     }
     if (g_copy_path == 3) return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the source layout has no TMA tensor map for any tiling");
+    // ---- narrow runs: one run is a whole short mode (fewer cells than a 128-byte row / a 32-row tile), the other as above
+    if (!strided_runs && g_copy_path == 0 && knob(K_COPY_CELL_TILES) != 0 && eb <= 8) {
+        const bool narrow_a = modes[ia].e >= 2 && modes[ia].e * eb < 128;
+        const bool narrow_b = !narrow_a && modes[ib].e >= 2 && modes[ib].e < (eb == 1 ? 128 : 32);   // (1-byte cells: the staged plan needs 128 rows)
+        // the long run's length: the staged tile (rows of an odd number of words) must fit 33 KiB
+        const int64_t short_e = narrow_a ? modes[ia].e : modes[ib].e;
+        for (int64_t Lr : {static_cast<int64_t>(256), static_cast<int64_t>(128), static_cast<int64_t>(64), static_cast<int64_t>(32)}) {
+            if (!narrow_a && !narrow_b) break;
+            const int64_t la = narrow_a ? short_e : Lr, lb = narrow_a ? Lr : short_e;
+            const int64_t pitch = ((((la * eb + 3) >> 2) | 1) + (eb == 8 ? 1 : 0)) << 2;
+            if (lb * pitch > kNarrowTileBytes || la > kNarrowMaxRun || lb > kNarrowMaxRun) continue;
+            std::vector<JM> work = modes, A, B;
+            if (narrow_a) {
+                A.push_back(work[ia]);
+                work[ia].e = 1;
+                if (!take_run(&work, false, lb, &B, 1)) continue;
+            } else {
+                B.push_back(work[ib]);
+                work[ib].e = 1;
+                if (!take_run(&work, true, la, &A, 1)) continue;
+            }
+            if (A.size() > kMaxPieces || B.size() > kMaxPieces) continue;
+            std::vector<JM> rest;
+            for (const JM& m : work)
+                if (m.e > 1) rest.push_back(m);
+            std::stable_sort(rest.begin(), rest.end(), [](const JM& a, const JM& b) {
+                return std::min(std::llabs(a.ss), std::llabs(a.ds)) < std::min(std::llabs(b.ss), std::llabs(b.ds));
+            });
+            TileParams P;
+            std::memset(&P, 0, sizeof(P));
+            TLB_TRY(fill_joint(rest, &P.rest));
+            P.nA = static_cast<int>(A.size());
+            P.nB = static_cast<int>(B.size());
+            for (size_t r = 0; r < A.size(); ++r) { P.eA[r] = A[r].e; P.dA[r] = A[r].ds; }
+            for (size_t r = 0; r < B.size(); ++r) { P.eB[r] = B[r].e; P.sB[r] = B[r].ss; }
+            P.La = static_cast<int>(la);
+            P.Lb = static_cast<int>(lb);
+            P.ua = P.ub = 1;
+            uint64_t tiles = 1;
+            for (const JM& m : rest) tiles *= static_cast<uint64_t>(m.e);
+            P.n_tiles = tiles;
+            if (tiles > 0x7fffffffull) return TLB_OK;
+            if (g_dry_run) {
+                set_plan("tiled_n");
+                *done = true;
+                return TLB_OK;
+            }
+            const unsigned grid = static_cast<unsigned>(tiles);
+            const char* sb = sp + base_s * eb;
+            char* db = dp + base_d * eb;
+            if (eb == 1) TLB_CUDA(launch_pdl(tiled_narrow_kernel<1>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db));
+            else if (eb == 2) TLB_CUDA(launch_pdl(tiled_narrow_kernel<2>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db));
+            else if (eb == 4) TLB_CUDA(launch_pdl(tiled_narrow_kernel<4>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db));
+            else TLB_CUDA(launch_pdl(tiled_narrow_kernel<8>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db));
+            count_launch();
+            set_plan("tiled_n");
+            *done = true;
+            return TLB_OK;
+        }
+    }
     return TLB_OK;
 }
 
@@ -1750,8 +1902,10 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
         Lb = cand;
         break;
     }
-    if (Lb == 0 || eA < La) return TLB_OK;
-    const int64_t bodyA = eA / La * La, bodyB = eB / Lb * Lb;
+    const bool narrow = eA < La;   // a short A mode: the narrow-run staged kernel takes it whole, only B is cut
+    const bool narrow_b = !narrow && Lb == 0 && eB >= 2 && eB < (eb == 1 ? 128 : 32) && eb <= 8 && eA >= 128;   // a short B mode: only A is cut (128-cell pieces)
+    if ((Lb == 0 && !narrow_b) || (narrow && (eA < 2 || eb > 8))) return TLB_OK;
+    const int64_t bodyA = narrow ? eA : narrow_b ? eA / 128 * 128 : eA / La * La, bodyB = narrow_b ? eB : eB / Lb * Lb;
     if (bodyA == eA && bodyB == eB) return TLB_OK; // whole tiles already: the staged plan was refused for another reason
     // one piece: A coordinates [a0, a0 + ea), B coordinates [b0, b0 + ebx), every other mode whole
     auto piece = [&](int64_t a0, int64_t ea, int64_t b0, int64_t ebx) -> int {

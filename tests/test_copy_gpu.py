@@ -54,7 +54,7 @@ def test_copy_table1_all_element_sizes(eb):
 def test_copy_tiled_plan_one_byte_cells(s, d):
     """1-byte cells (fp8-sized): 16 x 16 byte blocks per lane, rotated row reads + barrel rotation, full-line stores."""
     assert run_copy_case(s, d, 1) == "tiled"
-    assert run_copy_case("(96,160):(160,1)", "(96,160):(1,96)", 1) == "gather"   # no 128-row B run
+    assert run_copy_case("(96,160):(160,1)", "(96,160):(1,96)", 1) == "tiled_n"  # no 128-row B run: the 96-cell destination run whole, narrow-run tiles
 
 
 @pytest.mark.parametrize("eb", [1, 2, 4, 8])
@@ -67,8 +67,10 @@ def test_copy_tiled_plan_one_byte_cells(s, d):
 def test_copy_tiled_plan_unaligned(s, d, so, do, eb):
     """Leading dimensions / origins that break 16-byte alignment keep the staged plan with cell-sized global accesses."""
     plan = run_copy_case(s, d, eb, src_origin=so, dst_origin=do)
-    if s.startswith("(96,160)") and eb <= 2:
-        assert plan == "gather"            # 160 one- or two-byte cells are not a whole number of 128-byte rows (1-byte: 128-row tiles only)
+    if s.startswith("(96,160)") and eb == 2:
+        assert plan == "gather"            # 160 two-byte cells are not a whole number of 128-byte rows
+    elif s.startswith("(96,160)") and eb == 1:
+        assert plan == "tiled_n"           # 96 rows < the 128 a 1-byte tile needs: the destination run whole, narrow-run tiles
     else:
         assert plan == "tiled_u"
 
@@ -127,9 +129,15 @@ def test_copy_tiled_plan_with_reversed_modes(s, d):
     assert (tdst.cpu().numpy() == want).all()
 
 
-def test_copy_interleaved_runs_fall_back_to_gather():
-    """The destination-contiguous run continues inside the source-contiguous run: no clean A x B tile."""
-    assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4) == "gather"
+def test_copy_interleaved_runs_take_narrow_tiles():
+    """The destination-contiguous run continues inside the source-contiguous run: no clean 128-byte A x B tile; since round 2
+    the 4-cell source run is staged whole on the narrow-run kernel (the gather before)."""
+    assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4) == "tiled_n"
+    host.config("COPY_CELL_TILES", "0")
+    try:
+        assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, seed=1) == "gather"
+    finally:
+        host.config("COPY_CELL_TILES", None)
 
 
 @pytest.mark.parametrize("s,d,plan", [
@@ -276,12 +284,13 @@ def test_copy_interleave_plan(eb, ec):
     # whole outer slices 1 .. 2 of the three images
     n1 = ec * J
     assert run_copy_case(aos3, soa3, eb, i_begin=n1, i_end=3 * n1, seed=6) == "interleave"
-    # not a whole number of lane pieces / an unaligned origin: the gather plans
+    # not a whole number of lane pieces / an unaligned origin: the narrow-run staged tiles when the long mode has whole
+    # 32-cell pieces, else the gather plans
     assert run_copy_case(f"({ec},{J + 1}):(1,{ec})", f"({ec},{J + 1}):({J + 1},1)", eb, seed=7).startswith("gather")
-    assert run_copy_case(aos, soa, eb, src_origin=1, seed=8).startswith("gather")
+    assert run_copy_case(aos, soa, eb, src_origin=1, seed=8) in ("gather", "tiled_n")
     host.config("COPY_INTERLEAVE", "0")
     try:
-        assert run_copy_case(aos, soa, eb, seed=9).startswith("gather")
+        assert run_copy_case(aos, soa, eb, seed=9) in ("gather", "gather_vec", "tiled_n")
     finally:
         host.config("COPY_INTERLEAVE", None)
     # a long mode that is not a whole number of lane pieces (planar rows still 16-byte aligned): whole pieces + the last j
@@ -292,6 +301,35 @@ def test_copy_interleave_plan(eb, ec):
         assert run_copy_case(f"({ec},{jr}):({pr},1)", f"({ec},{jr}):(1,{ec})", eb, seed=11) == "ragged:interleave"
     finally:
         host.config("COPY_RAGGED", None)
+
+
+@pytest.mark.parametrize("eb", [1, 2, 4, 8])
+def test_copy_narrow_runs_take_the_cell_granular_tiles(eb):
+    """A whole short mode as the source-contiguous run (fewer cells than a 128-byte row) or as the destination-contiguous
+    run (fewer than 32 cells): run-time tile extents on the cell-granular staged kernel, both directions, outer modes,
+    origins, hierarchical short runs; extents of the long mode that are not whole tiles through the ragged cut."""
+    for k, nn in enumerate((5, 9, 24, 31)):
+        if nn * eb >= 128:
+            continue
+        fwd = run_copy_case(f"(512,{nn}):({nn},1)", f"(512,{nn}):(1,512)", eb, seed=k)
+        bwd = run_copy_case(f"(512,{nn}):(1,512)", f"(512,{nn}):({nn},1)", eb, seed=10 + k)
+        assert fwd in ("tiled_n", "interleave") and bwd in ("tiled_n", "interleave"), (nn, fwd, bwd)
+    assert run_copy_case("(9,256,3):(1,9,2400)", "(9,256,3):(300,1,2700)", eb, src_origin=1, dst_origin=2, seed=20) == "tiled_n"
+    assert run_copy_case("(9,256,3):(300,1,2700)", "(9,256,3):(1,9,2400)", eb, src_origin=3, dst_origin=1, seed=21) == "tiled_n"
+    if eb == 4:
+        assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", eb, seed=22) == "tiled_n"
+    host.config("COPY_RAGGED", "4")
+    try:
+        want = "ragged:tiled_n" if 24 * eb < 128 else "ragged:tiled_u"   # 24 eight-byte cells are more than a 128-byte row
+        assert run_copy_case("(421,24):(24,1)", "(421,24):(1,421)", eb, seed=23) == want
+        assert run_copy_case("(421,24):(1,421)", "(421,24):(24,1)", eb, seed=24) == "ragged:tiled_n"
+    finally:
+        host.config("COPY_RAGGED", None)
+    host.config("COPY_CELL_TILES", "0")
+    try:
+        assert run_copy_case("(512,24):(24,1)", "(512,24):(1,512)", eb, seed=25).startswith("gather")
+    finally:
+        host.config("COPY_CELL_TILES", None)
 
 
 def test_copy_xor_layouts():

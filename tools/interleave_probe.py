@@ -43,3 +43,19 @@ for nn, eb in ((16, 4), (12, 4), (6, 4), (16, 2), (5, 8)):
     sec = t(lambda: host.copy(a, b))
     ok = torch.equal(dst.view(nn, M), src.view(M, nn).t())
     print(f"tall-skinny transpose {M} x {nn} eb={eb}: {lib.tlb_last_plan().decode()} {2 * n * eb / sec / 1e9:.0f} GB/s ({sec * 1e6:.0f} us) correct={ok}")
+for nn, eb in ((24, 4), (9, 4), (32, 2), (100, 1), (24, 2)):
+    for rev in (False, True):
+        sl, dl = f"({M},{nn}):({nn},1)", f"({M},{nn}):(1,{M})"
+        if rev:
+            sl, dl = dl, sl
+        n = M * nn
+        src = torch.arange(n, dtype=torch.int64, device="cuda").to({1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[eb])
+        dst = torch.zeros_like(src)
+        a, b = host.tensor_of(sl, src), host.tensor_of(dl, dst)
+        out = []
+        for kk in ("0", "1"):
+            host.config("COPY_CELL_TILES", kk)
+            sec = t(lambda: host.copy(a, b))
+            out.append(f"{lib.tlb_last_plan().decode()} {2 * n * eb / sec / 1e9:.0f} GB/s")
+        host.config("COPY_CELL_TILES", None)
+        print(f"{M} x {nn} eb={eb} {'planar -> interleaved' if rev else 'interleaved -> planar'}: " + " | ".join(out))
