@@ -10,6 +10,6 @@ run() { # name tool pytest-args...
 run copy_mem memcheck tests/test_copy_gpu.py -k "not c1 and not c3 and not full and not 4096"
 run eval_mem memcheck tests/test_eval_gpu.py -k "not 2_32 and not full and not c5"
 run gemm_mem memcheck tests/test_gemm_gpu.py -k "multicast_plan_matches or packed_plan_runs or conv_im2col or gett_folded_modes_on_tensor or chunked"
-run copy_race racecheck tests/test_copy_gpu.py -k "tiled or strided_runs or xor_layouts_vectorised or last_writer or ragged or compositions"
+run copy_race racecheck tests/test_copy_gpu.py -k "tiled or strided_runs or xor_layouts_vectorised or last_writer or ragged or compositions or narrow or interleave"
 run gemm_mem2 memcheck tests/test_gemm_gpu.py -k "mn_major_operands_on_tensor_cores or c_in_the_operand_type or degenerate or simt_fallback"
 run gemm_sync synccheck tests/test_gemm_gpu.py -k "multicast_plan_matches or umma_kat_exact or mn_major_operands_on_tensor_cores"
