@@ -111,6 +111,73 @@ __global__ void __launch_bounds__(kThreads) eval_group_kernel(const __grid_const
     }
 }
 
+// Odometer evaluation: 8 consecutive indices per thread for Int layouts whose LEADING leaf is not a multiple of the group
+// sizes above (a leaf of 3, 5, 6 ... cells: every index there cost a full peel, 2 TB/s against 7 TB/s). One peel gives the
+// coordinates of leaves 0 and 1 and the offset of the rest; the next index advances c0 by one stride, carries into c1 when
+// c0 wraps, and only a wrap of c1 (once per e0 * e1 indices) peels the rest again. Same values as the flat peel of
+// oracle_eval (oracle.hpp:58-69), last leaf unbounded.
+template <bool kWide>
+__global__ void __launch_bounds__(kThreads) eval_odo_kernel(const __grid_constant__ tlb_layout_desc L, uint64_t i0,
+                                                            uint64_t n_groups, int64_t* __restrict__ out) {
+    constexpr int G = 8;
+    pdl_wait();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const int n = L.n_modes;
+    const uint64_t e0 = static_cast<uint64_t>(L.extent[0]), e1 = static_cast<uint64_t>(L.extent[1]);
+    const int64_t d0 = L.stride[0], d1 = L.stride[1], wrap0 = static_cast<int64_t>(e0) * d0;
+    const bool bounded1 = n > 2;   // leaf 1 is the last leaf: unbounded, it never wraps
+    // offset of the leaves 2.. at their integral coordinate q (last leaf unbounded)
+    auto rest_of = [&](uint64_t q) {
+        int64_t acc = 0;
+        for (int r = 2; r < n; ++r) {
+            uint64_t c;
+            if (r + 1 < n) {
+                const uint64_t qq = dev_div(L, r, q);
+                c = q - qq * static_cast<uint64_t>(L.extent[r]);
+                q = qq;
+            } else {
+                c = q;
+            }
+            acc += static_cast<int64_t>(c) * L.stride[r];
+        }
+        return acc;
+    };
+    for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n_groups; g += stride) {
+        const uint64_t i = i0 + g * G;
+        const uint64_t q0 = dev_div(L, 0, i);
+        uint64_t c0 = i - q0 * e0, c1 = q0, q1 = 0;
+        if (bounded1) {
+            q1 = dev_div(L, 1, q0);
+            c1 = q0 - q1 * e1;
+        }
+        int64_t rest = bounded1 ? rest_of(q1) : 0;
+        int64_t acc = rest + static_cast<int64_t>(c1) * d1 + static_cast<int64_t>(c0) * d0;
+        int64_t v[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            v[j] = acc;
+            acc += d0;
+            if (++c0 == e0) {
+                c0 = 0;
+                acc += d1 - wrap0;
+                if (++c1 == e1 && bounded1) {
+                    c1 = 0;
+                    rest = rest_of(++q1);
+                    acc = rest;
+                }
+            }
+        }
+        int64_t* o = out + g * G;
+        if constexpr (kWide) {
+            st_cs_v4(o, v[0], v[1], v[2], v[3]);
+            st_cs_v4(o + 4, v[4], v[5], v[6], v[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < G; ++j) o[j] = v[j];
+        }
+    }
+}
+
 // Warp-coalesced grouped evaluation: a warp owns 32 consecutive groups of G indices (32*G outputs, 256*G bytes).
 // Lane l peels group l ONCE; the bases then travel by shuffle so that store j of the warp covers the 128
 // consecutive outputs [j*128, j*128+128): lane l writes outputs j*128 + 4l .. +3 (one 32-byte sector per lane,
@@ -463,6 +530,21 @@ int tlb_eval_range(const tlb_layout_desc* layout, uint64_t i0, uint64_t n, int64
             count_launch();
             TLB_CUDA(cudaGetLastError());
         }
+        return TLB_OK;
+    }
+    if (layout->kind == TLB_KIND_INT && layout->n_modes >= 2 && n >= 8 && knob(K_EVAL_ODOMETER) != 0) {
+        // no group size divides the leading leaf: 8 indices per thread by odometer over leaves 0 and 1
+        const uint64_t groups = n / 8;
+        const bool wide = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
+        if (wide) TLB_CUDA(launch_pdl(eval_odo_kernel<true>, dim3(grid_for(groups)), dim3(kThreads), 0, s, *layout, i0, groups, d_out));
+        else TLB_CUDA(launch_pdl(eval_odo_kernel<false>, dim3(grid_for(groups)), dim3(kThreads), 0, s, *layout, i0, groups, d_out));
+        count_launch();
+        if (groups * 8 < n) {
+            eval_range_kernel<false><<<grid_for(n - groups * 8), kThreads, 0, s>>>(*layout, i0 + groups * 8, n - groups * 8, d_out + groups * 8);
+            count_launch();
+            TLB_CUDA(cudaGetLastError());
+        }
+        set_plan("eval_odo");
         return TLB_OK;
     }
     set_plan("eval_scalar");

@@ -79,12 +79,39 @@ def test_c5_windows_through_the_kernel_the_bench_times(i0):
 def test_c5_non_group_aligned_start_falls_back_and_stays_exact():
     ops = ou.golden("ops.json")
     n = 2**20 + 5
-    got = _eval(ops["C5_L"], 7 * 2**28 + 3, n)                # i0 % 2 != 0: the scalar kernel
-    assert abi.load().tlb_last_plan().decode() == "eval_scalar"
+    got = _eval(ops["C5_L"], 7 * 2**28 + 3, n)                # i0 % 2 != 0: no group size applies, the odometer kernel
+    assert abi.load().tlb_last_plan().decode() == "eval_odo"
     assert (got == ou.orc_eval_range(ops["C5_L"], 7 * 2**28 + 3, n)).all()
     got = _eval(ops["C5_L"], 7 * 2**28 + 16, n)               # i0 % 16 == 0: G = 16 warp kernel + group + scalar tails
     assert abi.load().tlb_last_plan().decode() == "eval_warp16"
     assert (got == ou.orc_eval_range(ops["C5_L"], 7 * 2**28 + 16, n)).all()
+
+
+@pytest.mark.parametrize("text", [
+    "(3,1048576,64):(1,3,3145728)",            # leading leaf of 3 cells
+    "(5,7,11,13,1000):(1,5,35,385,5005)",      # small odd leaves: leaf 1 wraps every 35 indices
+    "(3,2,1000,1000):(2000000,7,1,1000)",      # e0 * e1 = 6 < the 8 indices of a thread: several re-peels per thread
+    "(6,100000):(100000,1)",                   # two leaves: leaf 1 is the last leaf, unbounded
+    "(7,9,100):(-1,-7,63)",                    # negative strides
+    "(1,3,1,50,4000):(9,1,9,3,150)",           # extent-1 leaves in front
+])
+def test_eval_odometer_for_leading_leaves_no_group_size_divides(text):
+    """Layouts whose leading leaf is not a multiple of 2 (or whose range starts at an odd index) are walked 8 indices per
+    thread by an odometer over leaves 0 and 1 (round 2: the per-index peel before, 2 TB/s against 7 TB/s). Every value
+    against the oracle, ranges that start anywhere, the extended domain, and the per-index kernel as a cross-check."""
+    size = L(text).size
+    for i0, n in ((0, min(size, 300000)), (1, 4099), (12345, 65536 + 3), (max(0, size - 1000), 1000 + 77)):
+        got = _eval(text, i0, n)
+        assert (got == ou.orc_eval_range(text, i0, n)).all(), (text, i0, n, abi.load().tlb_last_plan().decode())
+    _eval(text, 1, 4099)                       # an odd start rules out every group size
+    assert abi.load().tlb_last_plan().decode() == "eval_odo"
+    host.config("EVAL_ODOMETER", "0")
+    try:
+        got = _eval(text, 1, 4099)
+        assert abi.load().tlb_last_plan().decode() == "eval_scalar"
+        assert (got == ou.orc_eval_range(text, 1, 4099)).all()
+    finally:
+        host.config("EVAL_ODOMETER", None)
 
 
 def test_c5_right_inverse_identity_on_device():
