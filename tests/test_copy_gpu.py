@@ -332,6 +332,43 @@ def test_copy_narrow_runs_take_the_cell_granular_tiles(eb):
         host.config("COPY_CELL_TILES", None)
 
 
+def test_copy_round2_plans_differential_fuzz():
+    """Random permutes of 2 - 4 modes with random extents (whole tiles or not), paddings and origins, every cell size, with the
+    ragged cut enabled from 16 elements: the run must reach the ragged / interleave / narrow / cell-granular plans, and every
+    cell of every destination (pre-fill included) must equal tla::copy's."""
+    rng = np.random.default_rng(2026)
+    plans = set()
+    host.config("COPY_RAGGED", "4")
+    try:
+        for case in range(260):
+            rank = int(rng.integers(2, 5))
+            if rank == 2:
+                ext = [int(rng.choice([3, 4, 5, 9, 16, 24, 33, 64, 100, 129, 200, 257, 300])) for _ in range(2)]
+            else:
+                ext = [int(rng.choice([2, 3, 4, 5, 7, 8, 12, 16, 31, 32, 40, 65])) for _ in range(rank)]
+            pad_s, pad_d = int(rng.choice([0, 0, 1, 4, 8])), int(rng.choice([0, 0, 1, 4, 8]))
+            def compact(order, pad):
+                strides, run = [0] * rank, 1
+                for k, m in enumerate(order):
+                    strides[m] = run
+                    run *= ext[m]
+                    if k == 0:
+                        run += pad        # padded leading dimension
+                return strides
+            so = list(rng.permutation(rank))
+            do = list(rng.permutation(rank))
+            ss, ds = compact(so, pad_s), compact(do, pad_d)
+            s = "(" + ",".join(map(str, ext)) + "):(" + ",".join(map(str, ss)) + ")"
+            d = "(" + ",".join(map(str, ext)) + "):(" + ",".join(map(str, ds)) + ")"
+            eb = int(rng.choice([1, 2, 4, 8, 16]))
+            o_s, o_d = (int(rng.choice([0, 0, 1, 4, 16])) for _ in range(2))
+            plans.add(run_copy_case(s, d, eb, src_origin=o_s, dst_origin=o_d, seed=case))
+    finally:
+        host.config("COPY_RAGGED", None)
+    kinds = {p.split(":")[0] for p in plans} | {p.split(":")[-1] for p in plans}
+    assert {"ragged", "interleave", "tiled_n", "tiled_u", "tiled", "vec"} <= kinds, plans
+
+
 def test_copy_xor_layouts():
     run_copy_case("(8,8):(f1,f9)", "64:1", 8)
     run_copy_case("64:1", "(8,8):(f1,f9)", 4)
