@@ -621,8 +621,13 @@ tiled_cell_kernel(const __grid_constant__ TileParams P, const char* __restrict__
     using T = typename Cell<EB>::type;
     constexpr int LA = 128 / EB;
     constexpr int PITCH = 128 + (EB > 4 ? EB : 4);     // bytes per staged row
-    constexpr int N = LB * LA, U = 8;                  // cells per tile, loads in flight per thread
-    static_assert(N % (kThreads * U) == 0 || N % kThreads == 0, "tile size");
+#ifndef TLB_CELL_U
+#define TLB_CELL_U 32
+#endif
+    constexpr int N = LB * LA;                         // cells per tile
+    constexpr int U = (N / kThreads) < TLB_CELL_U ? (N / kThreads) : TLB_CELL_U;   // loads in flight per thread: narrow cells need many
+                                                       // (2-byte cells, 8 in flight: 4 KiB per CTA, latency bound at 3.5 TB/s)
+    static_assert(N % (kThreads * U) == 0, "tile size");
     __shared__ __align__(16) unsigned char tile[LB * PITCH];
     __shared__ int64_t s_offB[LB];
     __shared__ int64_t s_offA[LA];
@@ -647,7 +652,7 @@ tiled_cell_kernel(const __grid_constant__ TileParams P, const char* __restrict__
     const T* s = reinterpret_cast<const T*>(src) + base_s;
     T* d = reinterpret_cast<T*>(dst) + base_d;
     const int ua = P.ua, ub = P.ub;                    // > 1: "tiled_s", runs along the smallest-stride modes
-    constexpr int STEP = (N % (kThreads * U) == 0) ? U : 1;
+    constexpr int STEP = U;
     for (int i0 = threadIdx.x; i0 < N; i0 += kThreads * STEP) {
         T v[STEP];
 #pragma unroll
@@ -708,7 +713,10 @@ tiled_narrow_kernel(const __grid_constant__ TileParams P, const char* __restrict
     const T* s = reinterpret_cast<const T*>(src) + base_s;
     T* d = reinterpret_cast<T*>(dst) + base_d;
     const int n = lb * la;
-    constexpr int U = 4;   // cells in flight per thread
+#ifndef TLB_NARROW_U
+#define TLB_NARROW_U 4
+#endif
+    constexpr int U = TLB_NARROW_U;   // cells in flight per thread
     {
         // (b, a) of the thread's k-th cell advance by (256 / la, 256 % la) with one carry: no division in the loop
         const int db = kThreads / la, da = kThreads % la;
