@@ -2,8 +2,13 @@
 //
 //   for i in [0, size) ascending:  dst(i) = src(i)
 //
-// Four kernels, chosen by a host planner that works on the COMMON REFINEMENT of the two
-// layouts (every refined mode has one extent, one source stride, one destination stride):
+// Kernels chosen by a host planner that works on the COMMON REFINEMENT of the two layouts (every refined mode has one
+// extent, one source stride, one destination stride). The first four are round 1's; round 2 added, for the ordinary
+// layout pairs that fell to the gather: tiled_u / tiled_s / tiled_n (cell-granular staged tiles: unaligned bases, strided
+// runs, a whole short mode as one of the runs), interleave (AoS <-> SoA by register permutation), gather_vec / gather_run
+// (one evaluation per vector / per 32-64-byte run: swizzled layouts), last_writer (broadcast destinations), ragged:<plan>
+// (extents that are not whole tiles: a whole-tile body plus edge strips, cut on the refined modes), and tv:<plan>
+// (tlb_copy_tv of a digit-permutation thread-value layout = this copy between src o TV and dst o TV). DESIGN.md 3.2.
 //
 //   vec     one refined mode is contiguous on both sides: 16-byte (or narrower) vectors along
 //           it, one joint peel per vector.                                  [memcpy, row permutes]
