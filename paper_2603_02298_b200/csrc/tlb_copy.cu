@@ -353,7 +353,7 @@ vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, ch
 }
 
 // ---------------------------------------------------------------------------------------
-// interleave: AoS <-> SoA. A short mode c (2 .. 8, 12 or 16 cells: channels, the parts of a complex number, the short side of a
+// interleave: AoS <-> SoA. A short mode c (2 .. 10, 12, 16, 24 or 32 cells: channels, the parts of a complex number, the short side of a
 // tall-skinny transpose) and a long mode j
 // where one side keeps (c, j) jointly contiguous (cell j * EC + c: interleaved) and the other keeps j contiguous for each
 // c (planar, rows `planar_stride` apart). The staged plan has no whole 128-byte A run that leaves a unit-stride B run here.
@@ -1370,7 +1370,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     // ---- interleave plan (AoS <-> SoA): a short mode c and a long mode j, (c, j) jointly contiguous on one side, j
     // contiguous on the other
     if (!strided_runs && g_copy_path == 0 && knob(K_COPY_INTERLEAVE) != 0 && (eb == 1 || eb == 2 || eb == 4 || eb == 8)) {
-        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 8) || e == 12 || e == 16; };
+        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 10) || e == 12 || e == 16 || e == 24 || e == 32; };
         const bool deint = modes[ib].ss == modes[ia].e && short_mode(modes[ia].e);   // source interleaved: c = ia (ss 1), j = ib (ds 1, ss = |c|)
         const bool inter = !deint && modes[ia].ds == modes[ib].e && short_mode(modes[ib].e); // destination interleaved: c = ib (ds 1), j = ia (ss 1, ds = |c|)
         if (deint || inter) {
@@ -1413,8 +1413,9 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
 #define TLB_IL2(EB, EC_) do { if (deint) TLB_CUDA(launch_pdl(interleave_kernel<EB, EC_, true>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); \
                               else TLB_CUDA(launch_pdl(interleave_kernel<EB, EC_, false>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db)); } while (0)
 #define TLB_IL(EB) do { switch (EC) { case 2: TLB_IL2(EB, 2); break; case 3: TLB_IL2(EB, 3); break; case 4: TLB_IL2(EB, 4); break; case 5: TLB_IL2(EB, 5); break; \
-                                      case 6: TLB_IL2(EB, 6); break; case 7: TLB_IL2(EB, 7); break; case 8: TLB_IL2(EB, 8); break; case 12: TLB_IL2(EB, 12); break; \
-                                      default: TLB_IL2(EB, 16); break; } } while (0)
+                                      case 6: TLB_IL2(EB, 6); break; case 7: TLB_IL2(EB, 7); break; case 8: TLB_IL2(EB, 8); break; case 9: TLB_IL2(EB, 9); break; \
+                                      case 10: TLB_IL2(EB, 10); break; case 12: TLB_IL2(EB, 12); break; case 16: TLB_IL2(EB, 16); break; \
+                                      case 24: TLB_IL2(EB, 24); break; default: TLB_IL2(EB, 32); break; } } while (0)
                 if (eb == 1) TLB_IL(1); else if (eb == 2) TLB_IL(2); else if (eb == 4) TLB_IL(4); else TLB_IL(8);
 #undef TLB_IL
 #undef TLB_IL2
@@ -1861,7 +1862,7 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
     const int64_t La = 128 / eb, eA = modes[ia].e, eB = modes[ib].e;
     // AoS <-> SoA whose long mode is not a whole number of lane pieces: whole pieces on the interleave plan, the last j gathered
     if (eb < 16) {
-        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 8) || e == 12 || e == 16; };
+        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 10) || e == 12 || e == 16 || e == 24 || e == 32; };
         const bool deint = modes[ib].ss == eA && short_mode(eA), inter = !deint && modes[ia].ds == eB && short_mode(eB);
         if (deint || inter) {
             const int64_t EC = deint ? eA : eB, eJ = deint ? eB : eA, NJ = (16 / eb) * ((EC % 2) ? 2 : 1), bodyJ = eJ / NJ * NJ;

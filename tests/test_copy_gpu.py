@@ -263,9 +263,9 @@ def test_copy_ragged_extents_take_the_staged_plan(eb):
 
 
 @pytest.mark.parametrize("eb", [1, 2, 4, 8])
-@pytest.mark.parametrize("ec", [2, 3, 4, 5, 6, 7, 8, 12, 16])
+@pytest.mark.parametrize("ec", [2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 16, 24, 32])
 def test_copy_interleave_plan(eb, ec):
-    """AoS <-> SoA and tall-skinny transposes (a short mode of 2 .. 8, 12 or 16 cells against a long one): the register-permuting interleave plan, both
+    """AoS <-> SoA and tall-skinny transposes (a short mode of 2 .. 10, 12, 16, 24 or 32 cells against a long one): the register-permuting interleave plan, both
     directions, with outer modes, padded planar rows, origins that break the 32-byte alignment of the 256-bit accesses,
     a sub-range of whole outer slices, and a j extent that is not a whole number of lane pieces (gather)."""
     nj = 16 // eb * (2 if ec % 2 else 1)          # j per lane
@@ -308,26 +308,26 @@ def test_copy_narrow_runs_take_the_cell_granular_tiles(eb):
     """A whole short mode as the source-contiguous run (fewer cells than a 128-byte row) or as the destination-contiguous
     run (fewer than 32 cells): run-time tile extents on the cell-granular staged kernel, both directions, outer modes,
     origins, hierarchical short runs; extents of the long mode that are not whole tiles through the ragged cut."""
-    for k, nn in enumerate((5, 9, 24, 31)):
+    for k, nn in enumerate((5, 11, 20, 31)):
         if nn * eb >= 128:
             continue
         fwd = run_copy_case(f"(512,{nn}):({nn},1)", f"(512,{nn}):(1,512)", eb, seed=k)
         bwd = run_copy_case(f"(512,{nn}):(1,512)", f"(512,{nn}):({nn},1)", eb, seed=10 + k)
         assert fwd in ("tiled_n", "interleave") and bwd in ("tiled_n", "interleave"), (nn, fwd, bwd)
-    assert run_copy_case("(9,256,3):(1,9,2400)", "(9,256,3):(300,1,2700)", eb, src_origin=1, dst_origin=2, seed=20) == "tiled_n"
-    assert run_copy_case("(9,256,3):(300,1,2700)", "(9,256,3):(1,9,2400)", eb, src_origin=3, dst_origin=1, seed=21) == "tiled_n"
+    assert run_copy_case("(11,256,3):(1,11,2900)", "(11,256,3):(300,1,3300)", eb, src_origin=1, dst_origin=2, seed=20) == "tiled_n"
+    assert run_copy_case("(11,256,3):(300,1,3300)", "(11,256,3):(1,11,2900)", eb, src_origin=3, dst_origin=1, seed=21) == "tiled_n"
     if eb == 4:
         assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", eb, seed=22) == "tiled_n"
     host.config("COPY_RAGGED", "4")
     try:
-        want = "ragged:tiled_n" if 24 * eb < 128 else "ragged:tiled_u"   # 24 eight-byte cells are more than a 128-byte row
-        assert run_copy_case("(421,24):(24,1)", "(421,24):(1,421)", eb, seed=23) == want
-        assert run_copy_case("(421,24):(1,421)", "(421,24):(24,1)", eb, seed=24) == "ragged:tiled_n"
+        want = "ragged:tiled_n" if 20 * eb < 128 else "ragged:tiled_u"   # 20 eight-byte cells are more than a 128-byte row
+        assert run_copy_case("(421,20):(20,1)", "(421,20):(1,421)", eb, seed=23) == want
+        assert run_copy_case("(421,20):(1,421)", "(421,20):(20,1)", eb, seed=24) == "ragged:tiled_n"
     finally:
         host.config("COPY_RAGGED", None)
     host.config("COPY_CELL_TILES", "0")
     try:
-        assert run_copy_case("(512,24):(24,1)", "(512,24):(1,512)", eb, seed=25).startswith("gather")
+        assert run_copy_case("(512,20):(20,1)", "(512,20):(1,512)", eb, seed=25).startswith("gather")
     finally:
         host.config("COPY_CELL_TILES", None)
 
