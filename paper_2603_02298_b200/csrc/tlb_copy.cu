@@ -456,6 +456,7 @@ struct TileParams {
     int32_t ua, ub;         // element stride of the A run on the source / of the B run on the destination (1: contiguous;
                             // > 1: "tiled_s", runs along the smallest-stride modes of layouts without a unit stride)
     uint64_t n_tiles;
+    int32_t tpc;            // tiles per CTA of the aligned staged kernel (1 .. tiles_per_cta(Lb)); 0 reads as 1
 };
 
 // byte offset of 16-byte chunk `c` of row `r` in the staged tile: 128 B rows, chunk index XORed
@@ -551,19 +552,23 @@ __device__ __forceinline__ void tile_phase2(const unsigned char* tile, const int
     }
 }
 
+// Tiles per CTA of the aligned staged kernel: short tiles (32 / 64 rows: a destination run of 32 .. 127 cells) are only 4 / 8
+// KiB, and one tile per CTA leaves the per-CTA work (offset tables, two barriers, the launch of 8 warps) unamortised: a
+// 4M x 96 fp32 planar -> interleaved transpose ran 3.65 TB/s. A CTA of such a plan walks 256 / LB consecutive tiles with the
+// tables computed once and the loads of tile k + 1 issued before the stores of tile k.
+__host__ __device__ constexpr int tiles_per_cta(int lb, bool aligned) { return (aligned && lb <= 64) ? 256 / lb : 1; }
+
 template <int EB, int LB, bool AL = true>
 __global__ void __launch_bounds__(kThreads)
 tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src, char* __restrict__ dst) {
     constexpr int V = 16 / EB;                         // elements per 16-byte vector
     constexpr int LA = 128 / EB;                       // elements of A per row
+    constexpr int TPC = tiles_per_cta(LB, AL);
     __shared__ __align__(1024) unsigned char tile[LB * 128];
     __shared__ int64_t s_offB[LB];                     // source offset of row b
     __shared__ int64_t s_offA[LA];                     // destination offset of column a
 
     pdl_wait();
-    int64_t base_s, base_d;
-    dev_joint(P.rest, blockIdx.x, &base_s, &base_d);
-
     for (int t = threadIdx.x; t < LB + LA; t += kThreads) {
         const bool isB = t < LB;
         uint32_t i = isB ? t : t - LB;
@@ -584,34 +589,63 @@ tiled_kernel(const __grid_constant__ TileParams P, const char* __restrict__ src,
     constexpr int NVEC = LB * 8;
     constexpr int PER = (NVEC + kThreads - 1) / kThreads;
     uint4 stage[PER];
+    auto load_tile = [&](uint64_t t, int64_t* base_d) {
+        int64_t base_s;
+        dev_joint(P.rest, t, &base_s, base_d);
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-        const int v = threadIdx.x + u * kThreads;
-        if (NVEC % kThreads == 0 || v < NVEC) {
-            const int c = v & 7, b = v >> 3;
-            if constexpr (AL) {
-                stage[u] = ldg_stream(src + (base_s + s_offB[b] + c * V) * EB);
-            } else {
-                using T = typename Cell<EB>::type;
-                const char* gp = src + (base_s + s_offB[b] + static_cast<int64_t>(c * V) * P.ua) * EB;
-                union { uint4 v; T e[V]; } t;
+        for (int u = 0; u < PER; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (NVEC % kThreads == 0 || v < NVEC) {
+                const int c = v & 7, b = v >> 3;
+                if constexpr (AL) {
+                    stage[u] = ldg_stream(src + (base_s + s_offB[b] + c * V) * EB);
+                } else {
+                    using T = typename Cell<EB>::type;
+                    const char* gp = src + (base_s + s_offB[b] + static_cast<int64_t>(c * V) * P.ua) * EB;
+                    union { uint4 v; T e[V]; } tt;
 #pragma unroll
-                for (int k = 0; k < V; ++k) t.e[k] = reinterpret_cast<const T*>(gp)[static_cast<int64_t>(k) * P.ua];
-                stage[u] = t.v;
+                    for (int k = 0; k < V; ++k) tt.e[k] = reinterpret_cast<const T*>(gp)[static_cast<int64_t>(k) * P.ua];
+                    stage[u] = tt.v;
+                }
             }
         }
-    }
+    };
+    const int tpc = TPC == 1 ? 1 : max(1, min(TPC, P.tpc));   // run time: few tiles stay one per CTA (parallelism first)
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * tpc;
+    int64_t base_d, next_d = 0;
+    load_tile(t0, &base_d);
+    if constexpr (TPC == 1) {   // one tile per CTA: straight-line code (C1, C3)
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-        const int v = threadIdx.x + u * kThreads;
-        if (NVEC % kThreads == 0 || v < NVEC) {
-            const int c = v & 7, b = v >> 3;
-            *reinterpret_cast<uint4*>(tile + swz(b, c)) = stage[u];
+        for (int u = 0; u < PER; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (NVEC % kThreads == 0 || v < NVEC) {
+                const int c = v & 7, b = v >> 3;
+                *reinterpret_cast<uint4*>(tile + swz(b, c)) = stage[u];
+            }
         }
+        __syncthreads();
+        tile_phase2<EB, LB, AL>(tile, s_offA, dst, base_d, AL ? 1 : P.ub);
+        return;
     }
-    __syncthreads();
-
-    tile_phase2<EB, LB, AL>(tile, s_offA, dst, base_d, AL ? 1 : P.ub);
+#pragma unroll 1
+    for (int k = 0; k < tpc; ++k) {
+        const uint64_t t = t0 + k;
+        if (t >= P.n_tiles) break;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (NVEC % kThreads == 0 || v < NVEC) {
+                const int c = v & 7, b = v >> 3;
+                *reinterpret_cast<uint4*>(tile + swz(b, c)) = stage[u];
+            }
+        }
+        __syncthreads();
+        const bool more = k + 1 < tpc && t + 1 < P.n_tiles;
+        if (more) load_tile(t + 1, &next_d);           // in flight while this tile is written out
+        tile_phase2<EB, LB, AL>(tile, s_offA, dst, base_d, AL ? 1 : P.ub);
+        __syncthreads();                               // the staged tile is free again
+        base_d = next_d;
+    }
 }
 
 // tiled, cell-sized accesses ("tiled_u": bases or leading dimensions that are not multiples of 16 bytes, so no 128-bit
@@ -1586,7 +1620,12 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
             *done = true;
             return TLB_OK;
         }
-#define TLB_TILED(EB, LB) TLB_CUDA(launch_pdl(tiled_kernel<EB, LB, true>, dim3(grid), dim3(kThreads), 0, c.stream, P, sb, db))
+        // short tiles: several per CTA once there are enough tiles to keep every SM busy with whole groups
+        {
+            const int tmax = tiles_per_cta(static_cast<int>(Lb), true);
+            P.tpc = (knob(K_COPY_TILES_PER_CTA) != 0 && tmax > 1 && tiles >= 16ull * static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(tmax)) ? tmax : 1;
+        }
+#define TLB_TILED(EB, LB) TLB_CUDA(launch_pdl(tiled_kernel<EB, LB, true>, dim3((grid + P.tpc - 1) / P.tpc), dim3(kThreads), 0, c.stream, P, sb, db))
         if (eb == 1) {
             if (Lb == 256) TLB_TILED(1, 256); else TLB_TILED(1, 128);
         } else if (eb == 16) {
@@ -1612,7 +1651,18 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         const bool narrow_b = !narrow_a && modes[ib].e >= 2 && modes[ib].e < (eb == 1 ? 128 : 32);   // (1-byte cells: the staged plan needs 128 rows)
         // the long run's length: the staged tile (rows of an odd number of words) must fit 33 KiB
         const int64_t short_e = narrow_a ? modes[ia].e : modes[ib].e;
-        for (int64_t Lr : {static_cast<int64_t>(256), static_cast<int64_t>(128), static_cast<int64_t>(64), static_cast<int64_t>(32)}) {
+        // long-run candidates: tall tiles when they still give every SM a few CTAs, else shorter ones (a 16-column edge strip
+        // of 8000 rows is 31 tiles of 256 rows: slower than the gather it replaces)
+        const int64_t long_e = narrow_a ? modes[ib].e : modes[ia].e;
+        uint64_t others = 1;
+        for (size_t r = 0; r < modes.size(); ++r)
+            if (static_cast<int>(r) != ia && static_cast<int>(r) != ib) others *= static_cast<uint64_t>(modes[r].e);
+        std::vector<int64_t> cands;
+        for (int64_t Lr : {256, 128, 64, 32})
+            if (others * static_cast<uint64_t>(long_e / Lr) >= 2ull * static_cast<uint64_t>(sm_count())) cands.push_back(Lr);
+        for (int64_t Lr : {32, 64, 128, 256})
+            if (std::find(cands.begin(), cands.end(), Lr) == cands.end()) cands.push_back(Lr);
+        for (int64_t Lr : cands) {
             if (!narrow_a && !narrow_b) break;
             const int64_t la = narrow_a ? short_e : Lr, lb = narrow_a ? Lr : short_e;
             const int64_t pitch = ((((la * eb + 3) >> 2) | 1) + (eb == 8 ? 1 : 0)) << 2;
