@@ -1469,9 +1469,14 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     // Bases or strides that are not multiples of 16 bytes (padded leading dimensions, odd origins) keep the tiled
     // plan with cell-sized global accesses ("tiled_u": 128- and 32-row tiles, 2-, 4- and 8-byte cells).
     const bool base_al = aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
-    static const int64_t kLb[] = {256, 128, 64, 32};
+    // Rows per tile = cells of the destination-contiguous run per tile. Powers of two, and since round 2 the other multiples
+    // of 32 up to 256 for 2-, 4- and 8-byte cells: a run of 96 / 160 / 192 / 224 cells is ONE tile (384 .. 896-byte destination
+    // segments) instead of 32-row tiles with 128-byte segments.
+    static const int64_t kLb[] = {256, 224, 192, 160, 128, 96, 64, 32};
     for (int64_t Lb : kLb) {
         if (Lb == 256 && !lb256_enabled()) continue;
+        const bool odd_lb = Lb == 224 || Lb == 192 || Lb == 160 || Lb == 96;
+        if (odd_lb && ((eb != 2 && eb != 4 && eb != 8) || g_copy_path == 3 || (g_copy_path == 0 && tma_default()) || knob(K_COPY_ODD_TILES) == 0)) continue;
         if (eb == 1 && (Lb < 128 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 1-byte cells: LDG-staged, 128+ rows
         if (eb == 16 && (Lb == 64 || g_copy_path == 3 || (g_copy_path == 0 && tma_default()))) continue; // 16-byte cells: LDG-staged, 256 / 128 / 32 rows
         std::vector<JM> work = modes, A, B;
@@ -1630,12 +1635,12 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
             if (Lb == 256) TLB_TILED(1, 256); else TLB_TILED(1, 128);
         } else if (eb == 16) {
             if (Lb == 256) TLB_TILED(16, 256); else if (Lb == 128) TLB_TILED(16, 128); else TLB_TILED(16, 32);
-        } else if (eb == 4) {
-            if (Lb == 256) TLB_TILED(4, 256); else if (Lb == 128) TLB_TILED(4, 128); else if (Lb == 64) TLB_TILED(4, 64); else TLB_TILED(4, 32);
-        } else if (eb == 8) {
-            if (Lb == 256) TLB_TILED(8, 256); else if (Lb == 128) TLB_TILED(8, 128); else if (Lb == 64) TLB_TILED(8, 64); else TLB_TILED(8, 32);
         } else {
-            if (Lb == 256) TLB_TILED(2, 256); else if (Lb == 128) TLB_TILED(2, 128); else if (Lb == 64) TLB_TILED(2, 64); else TLB_TILED(2, 32);
+#define TLB_TILED_LB(EB) do { switch (Lb) { case 256: TLB_TILED(EB, 256); break; case 224: TLB_TILED(EB, 224); break; case 192: TLB_TILED(EB, 192); break; \
+                                           case 160: TLB_TILED(EB, 160); break; case 128: TLB_TILED(EB, 128); break; case 96: TLB_TILED(EB, 96); break;   \
+                                           case 64: TLB_TILED(EB, 64); break; default: TLB_TILED(EB, 32); break; } } while (0)
+            if (eb == 4) TLB_TILED_LB(4); else if (eb == 8) TLB_TILED_LB(8); else TLB_TILED_LB(2);
+#undef TLB_TILED_LB
         }
 #undef TLB_TILED
         count_launch();

@@ -72,6 +72,7 @@ enum KnobId {
     K_COPY_CELL_TILES,  // tiled_u: consecutive lanes on consecutive cells, padded staging (1), or the vector-shaped lane assignment with cell-sized accesses (0)
     K_EVAL_ODOMETER,    // tlb_eval_range: leading leaves no group size divides are walked by odometer, 8 indices per thread (1), or peeled per index (0)
     K_COPY_TILES_PER_CTA, // aligned staged copy, 32 / 64-row tiles: 256 / rows tiles per CTA when there are many tiles (1), always one (0)
+    K_COPY_ODD_TILES,   // staged copy: 96 / 160 / 192 / 224-row tiles for destination runs of that many cells (1), powers of two only (0)
     K_HOST_TAPER,       // pipelined host GEMM: the last panel is cut into 1/2, 1/4, 1/4 so that little is left after the last upload
     K_COUNT
 };

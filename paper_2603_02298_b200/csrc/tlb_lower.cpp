@@ -45,7 +45,7 @@ const KnobDef kKnobDefs[K_COUNT] = {
     {"GEMM_C16_SK", 0}, {"GEMM_SK_PCT", 4}, {"GEMM_EPI_KB", 10}, {"GEMM_CLOCK", 0}, {"PDL", 1},
     {"COPY_TMA", 0}, {"COPY_LB256", 1}, {"COPY_PERSIST", 1}, {"EVAL_NO_WARP", 0}, {"HOST_PIPELINE", 1}, {"HOST_PANEL", 1024},
     {"COPY_TMA_STAGES", 3}, {"COPY_TMA_CTAS", 2}, {"GEMM_CHUNK_WAVES", 8}, {"GEMM_MCAST", 0}, {"GEMM_EARLY_RELEASE", 1}, {"GEMM_PACK", 1}, {"GEMM_PACK_MIN", 27},
-    {"COPY_TV_COMPOSE", 1}, {"COPY_GATHER_RUN", 1}, {"COPY_RAGGED", 22}, {"COPY_INTERLEAVE", 1}, {"COPY_CELL_TILES", 1}, {"EVAL_ODOMETER", 1}, {"COPY_TILES_PER_CTA", 1}, {"HOST_TAPER", 1},
+    {"COPY_TV_COMPOSE", 1}, {"COPY_GATHER_RUN", 1}, {"COPY_RAGGED", 22}, {"COPY_INTERLEAVE", 1}, {"COPY_CELL_TILES", 1}, {"EVAL_ODOMETER", 1}, {"COPY_TILES_PER_CTA", 1}, {"COPY_ODD_TILES", 1}, {"HOST_TAPER", 1},
 };
 std::atomic<int> g_knobs[K_COUNT];
 std::once_flag g_knobs_once;

@@ -332,6 +332,25 @@ def test_copy_narrow_runs_take_the_cell_granular_tiles(eb):
         host.config("COPY_CELL_TILES", None)
 
 
+@pytest.mark.parametrize("eb", [2, 4, 8])
+@pytest.mark.parametrize("rows", [96, 160, 192, 224])
+def test_copy_tiles_of_96_to_224_rows(eb, rows):
+    """A destination-contiguous run of 96 / 160 / 192 / 224 cells is one staged tile (384 .. 1792-byte destination segments)
+    instead of 32-row tiles: both directions, an outer mode, several tiles per CTA for the 96-row tiles; the power-of-two
+    tiles under COPY_ODD_TILES=0 give the same cells."""
+    cols = 128
+    s, d = f"({rows},{cols},3):({cols},1,{rows * cols})", f"({rows},{cols},3):(1,{rows},{rows * cols})"
+    assert run_copy_case(s, d, eb) == "tiled"
+    run_copy_case(d, s, eb, seed=1)            # the opposite direction (its source run is `rows` cells: staged only when that is whole 128-byte rows)
+    big_s, big_d = f"({rows},16384):(16384,1)", f"({rows},16384):(1,{rows})"       # enough tiles for several per CTA
+    assert run_copy_case(big_s, big_d, eb, seed=2) == "tiled"
+    host.config("COPY_ODD_TILES", "0")
+    try:
+        assert run_copy_case(s, d, eb, seed=3) == "tiled"
+    finally:
+        host.config("COPY_ODD_TILES", None)
+
+
 def test_copy_round2_plans_differential_fuzz():
     """Random permutes of 2 - 4 modes with random extents (whole tiles or not), paddings and origins, every cell size, with the
     ragged cut enabled from 16 elements: the run must reach the ragged / interleave / narrow / cell-granular plans, and every
