@@ -45,6 +45,7 @@ namespace {
 thread_local int g_copy_path = 0; // 0 auto, 1 gather, 2 tiled (LDG), 3 tiled TMA
 thread_local bool g_dry_run = false; // tlb_copy_plan: run the planner, launch nothing
 thread_local int g_ragged_depth = 0;   // recursion depth of the ragged cut (try_ragged)
+thread_local bool g_defer_narrow = false, g_narrow_deferred = false; // copy_impl: the ragged interleave cut goes before narrow tiles
 thread_local std::string g_ragged_plan;
 
 // TLB_COPY_TMA=1 makes the TMA-fed tiled kernel the default for layouts that admit a tensor map.
@@ -1658,8 +1659,18 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     if (g_copy_path == 3) return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the source layout has no TMA tensor map for any tiling");
     // ---- narrow runs: one run is a whole short mode (fewer cells than a 128-byte row / a 32-row tile), the other as above
     if (!strided_runs && g_copy_path == 0 && knob(K_COPY_CELL_TILES) != 0 && eb <= 8) {
+        if (g_defer_narrow && knob(K_COPY_RAGGED) != 0 && c.n >= (1ull << std::min(40, knob(K_COPY_RAGGED)))) {
+            // an AoS <-> SoA pattern whose long mode is not whole lane pieces: let the ragged cut try the (faster) interleave body first
+            auto short_mode = [](int64_t e) { return (e >= 2 && e <= 10) || e == 12 || e == 16 || e == 24 || e == 32; };
+            if ((modes[ib].ss == modes[ia].e && short_mode(modes[ia].e)) || (modes[ia].ds == modes[ib].e && short_mode(modes[ib].e))) {
+                g_narrow_deferred = true;
+                return TLB_OK;
+            }
+        }
         const bool narrow_a = modes[ia].e >= 2 && modes[ia].e * eb < 128;
-        const bool narrow_b = !narrow_a && modes[ib].e >= 2 && modes[ib].e < (eb == 1 ? 128 : 32);   // (1-byte cells: the staged plan needs 128 rows)
+        // (1-byte cells: the staged plan needs 128 rows; other cells: a destination run below 128 cells that is not a whole
+        // number of 32-row tiles, e.g. 48, is taken whole here instead of being cut into 32 + 16)
+        const bool narrow_b = !narrow_a && modes[ib].e >= 2 && (modes[ib].e < (eb == 1 ? 128 : 32) || (modes[ib].e < 128 && modes[ib].e % 32 != 0));
         // the long run's length: the staged tile (rows of an odd number of words) must fit 33 KiB
         const int64_t short_e = narrow_a ? modes[ia].e : modes[ib].e;
         // long-run candidates: tall tiles when they still give every SM a few CTAs, else shorter ones (a 16-column edge strip
@@ -2062,8 +2073,20 @@ int copy_impl(const tlb_tensor* src, const tlb_tensor* dst, uint64_t i_begin, ui
     if (g_copy_path != 1) {
         bool done = false;
         Refined refined;
-        TLB_TRY(try_planned(c, &done, &refined));
+        g_defer_narrow = true;
+        g_narrow_deferred = false;
+        const int st_planned = try_planned(c, &done, &refined);
+        g_defer_narrow = false;
+        TLB_TRY(st_planned);
         if (done) return TLB_OK;
+        if (g_narrow_deferred) {   // ragged interleave first; the narrow-run tiles if that cut does not apply
+            g_narrow_deferred = false;
+            TLB_TRY(try_ragged(c, refined, &done));
+            if (done) return TLB_OK;
+            Refined again;
+            TLB_TRY(try_planned(c, &done, &again));
+            if (done) return TLB_OK;
+        }
         if (g_copy_path == 2 || g_copy_path == 3)
             return fail(TLB_ERR_UNSUPPORTED, "tlb_copy: the forced tiled path does not apply to these layouts");
         if (refined.ok) {

@@ -286,7 +286,7 @@ def test_copy_interleave_plan(eb, ec):
     assert run_copy_case(aos3, soa3, eb, i_begin=n1, i_end=3 * n1, seed=6) == "interleave"
     # not a whole number of lane pieces / an unaligned origin: the narrow-run staged tiles when the long mode has whole
     # 32-cell pieces, else the gather plans
-    assert run_copy_case(f"({ec},{J + 1}):(1,{ec})", f"({ec},{J + 1}):({J + 1},1)", eb, seed=7).startswith("gather")
+    assert run_copy_case(f"({ec},{J + 1}):(1,{ec})", f"({ec},{J + 1}):({J + 1},1)", eb, seed=7) in ("gather", "gather_vec", "tiled_n")
     assert run_copy_case(aos, soa, eb, src_origin=1, seed=8) in ("gather", "tiled_n")
     host.config("COPY_INTERLEAVE", "0")
     try:
