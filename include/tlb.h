@@ -184,7 +184,7 @@ int tlb_eval_axes_range(const tlb_mode* modes, int n_modes, int n_axes, uint64_t
  *   "tiled"         transposes / permutes: 128-byte swizzle-staged tiles (Swizzle<3,4,3>), 128-bit accesses both ways;
  *                   "tiled_u" with cell-sized accesses for unaligned bases / leading dimensions, "tiled_s" along the
  *                   smallest-stride modes of layouts WITHOUT a unit stride, "tiled_tma" the TMA-fed persistent variant
- *   "interleave"    AoS <-> SoA (a short mode of 2 .. 10, 12, 16, 24 or 32 cells against a long one): register permutation, whole
+ *   "interleave"    AoS <-> SoA (a short mode of 2 .. 26, 28, 30 or 32 cells for 2- / 4-byte cells, the common extents for 1- / 8-byte cells, against a long one): register permutation, whole
  *                   sectors on both sides, no shared memory
  *   "tiled_n"       a whole short mode as one of the runs (a 4M x 24 transpose, 9-field AoS): cell-granular staged tiles with
  *                   run-time extents

@@ -56,6 +56,13 @@ constexpr int kThreads = 256;
 // The tiled plan prefers 256-row tiles (1 KiB destination segments, 32 KiB of smem per CTA; C1 5.90 -> 6.09 TB/s);
 // TLB_COPY_LB256=0 caps the tile at 128 rows (A/B comparisons).
 bool lb256_enabled() { return knob(K_COPY_LB256) != 0; }
+// Short-mode extents the register-permuting interleave plan is compiled for: 2 .. 26, 28, 30, 32 for 2- and 4-byte cells
+// (bf16 / fp32: tall-skinny transposes of any width up to 32), the common ones for 1- and 8-byte cells.
+bool interleave_size(int64_t e, int eb) {
+    if (e < 2 || e > 32) return false;
+    if (eb == 2 || eb == 4) return e % 2 == 0 || e <= 25;   // odd extents own two lane pieces (G = 2): 27, 29 and 31 cells would spill
+    return e <= 10 || e == 12 || e == 16 || e == 24 || e == 32;
+}
 
 // ---------------------------------------------------------------------------------------
 // device helpers
@@ -354,7 +361,7 @@ vec_kernel(const __grid_constant__ JointDesc J, const char* __restrict__ src, ch
 }
 
 // ---------------------------------------------------------------------------------------
-// interleave: AoS <-> SoA. A short mode c (2 .. 10, 12, 16, 24 or 32 cells: channels, the parts of a complex number, the short side of a
+// interleave: AoS <-> SoA. A short mode c (2 .. 26, 28, 30 or 32 cells for 2- / 4-byte cells, the common extents otherwise: channels, the parts of a complex number, the short side of a
 // tall-skinny transpose) and a long mode j
 // where one side keeps (c, j) jointly contiguous (cell j * EC + c: interleaved) and the other keeps j contiguous for each
 // c (planar, rows `planar_stride` apart). The staged plan has no whole 128-byte A run that leaves a unit-stride B run here.
@@ -1411,7 +1418,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     // ---- interleave plan (AoS <-> SoA): a short mode c and a long mode j, (c, j) jointly contiguous on one side, j
     // contiguous on the other
     if (!strided_runs && g_copy_path == 0 && knob(K_COPY_INTERLEAVE) != 0 && (eb == 1 || eb == 2 || eb == 4 || eb == 8)) {
-        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 10) || e == 12 || e == 16 || e == 24 || e == 32; };
+        auto short_mode = [eb](int64_t e) { return interleave_size(e, eb); };
         const bool deint = modes[ib].ss == modes[ia].e && short_mode(modes[ia].e);   // source interleaved: c = ia (ss 1), j = ib (ds 1, ss = |c|)
         const bool inter = !deint && modes[ia].ds == modes[ib].e && short_mode(modes[ib].e); // destination interleaved: c = ib (ds 1), j = ia (ss 1, ds = |c|)
         if (deint || inter) {
@@ -1457,7 +1464,13 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
                                       case 6: TLB_IL2(EB, 6); break; case 7: TLB_IL2(EB, 7); break; case 8: TLB_IL2(EB, 8); break; case 9: TLB_IL2(EB, 9); break; \
                                       case 10: TLB_IL2(EB, 10); break; case 12: TLB_IL2(EB, 12); break; case 16: TLB_IL2(EB, 16); break; \
                                       case 24: TLB_IL2(EB, 24); break; default: TLB_IL2(EB, 32); break; } } while (0)
-                if (eb == 1) TLB_IL(1); else if (eb == 2) TLB_IL(2); else if (eb == 4) TLB_IL(4); else TLB_IL(8);
+#define TLB_ILX(EB) do { switch (EC) { case 11: TLB_IL2(EB, 11); break; case 13: TLB_IL2(EB, 13); break; case 14: TLB_IL2(EB, 14); break; case 15: TLB_IL2(EB, 15); break; \
+                                       case 17: TLB_IL2(EB, 17); break; case 18: TLB_IL2(EB, 18); break; case 19: TLB_IL2(EB, 19); break; case 20: TLB_IL2(EB, 20); break; \
+                                       case 21: TLB_IL2(EB, 21); break; case 22: TLB_IL2(EB, 22); break; case 23: TLB_IL2(EB, 23); break; case 25: TLB_IL2(EB, 25); break; \
+                                       case 26: TLB_IL2(EB, 26); break; case 28: TLB_IL2(EB, 28); break; \
+                                       case 30: TLB_IL2(EB, 30); break; default: TLB_IL(EB); break; } } while (0)
+                if (eb == 1) TLB_IL(1); else if (eb == 2) TLB_ILX(2); else if (eb == 4) TLB_ILX(4); else TLB_IL(8);
+#undef TLB_ILX
 #undef TLB_IL
 #undef TLB_IL2
                 count_launch();
@@ -1661,7 +1674,7 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
     if (!strided_runs && g_copy_path == 0 && knob(K_COPY_CELL_TILES) != 0 && eb <= 8) {
         if (g_defer_narrow && knob(K_COPY_RAGGED) != 0 && c.n >= (1ull << std::min(40, knob(K_COPY_RAGGED)))) {
             // an AoS <-> SoA pattern whose long mode is not whole lane pieces: let the ragged cut try the (faster) interleave body first
-            auto short_mode = [](int64_t e) { return (e >= 2 && e <= 10) || e == 12 || e == 16 || e == 24 || e == 32; };
+            auto short_mode = [eb](int64_t e) { return interleave_size(e, eb); };
             if ((modes[ib].ss == modes[ia].e && short_mode(modes[ia].e)) || (modes[ia].ds == modes[ib].e && short_mode(modes[ib].e))) {
                 g_narrow_deferred = true;
                 return TLB_OK;
@@ -1934,7 +1947,7 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
     const int64_t La = 128 / eb, eA = modes[ia].e, eB = modes[ib].e;
     // AoS <-> SoA whose long mode is not a whole number of lane pieces: whole pieces on the interleave plan, the last j gathered
     if (eb < 16) {
-        auto short_mode = [](int64_t e) { return (e >= 2 && e <= 10) || e == 12 || e == 16 || e == 24 || e == 32; };
+        auto short_mode = [eb](int64_t e) { return interleave_size(e, eb); };
         const bool deint = modes[ib].ss == eA && short_mode(eA), inter = !deint && modes[ia].ds == eB && short_mode(eB);
         if (deint || inter) {
             const int64_t EC = deint ? eA : eB, eJ = deint ? eB : eA, NJ = (16 / eb) * ((EC % 2) ? 2 : 1), bodyJ = eJ / NJ * NJ;

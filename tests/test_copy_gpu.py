@@ -263,11 +263,13 @@ def test_copy_ragged_extents_take_the_staged_plan(eb):
 
 
 @pytest.mark.parametrize("eb", [1, 2, 4, 8])
-@pytest.mark.parametrize("ec", [2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 16, 24, 32])
+@pytest.mark.parametrize("ec", [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 28, 30, 32])
 def test_copy_interleave_plan(eb, ec):
-    """AoS <-> SoA and tall-skinny transposes (a short mode of 2 .. 10, 12, 16, 24 or 32 cells against a long one): the register-permuting interleave plan, both
+    """AoS <-> SoA and tall-skinny transposes (a short mode of 2 .. 26, 28, 30 or 32 cells for 2- and 4-byte cells, the common extents for 1- and 8-byte cells, against a long one): the register-permuting interleave plan, both
     directions, with outer modes, padded planar rows, origins that break the 32-byte alignment of the 256-bit accesses,
     a sub-range of whole outer slices, and a j extent that is not a whole number of lane pieces (gather)."""
+    if eb not in (2, 4) and ec not in (2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 16, 24, 32):
+        pytest.skip("1- and 8-byte cells: the common short-mode extents only")
     nj = 16 // eb * (2 if ec % 2 else 1)          # j per lane
     J = nj * 37
     aos, soa = f"({ec},{J}):(1,{ec})", f"({ec},{J}):({J},1)"
@@ -308,26 +310,27 @@ def test_copy_narrow_runs_take_the_cell_granular_tiles(eb):
     """A whole short mode as the source-contiguous run (fewer cells than a 128-byte row) or as the destination-contiguous
     run (fewer than 32 cells): run-time tile extents on the cell-granular staged kernel, both directions, outer modes,
     origins, hierarchical short runs; extents of the long mode that are not whole tiles through the ragged cut."""
-    for k, nn in enumerate((5, 11, 20, 31)):
+    for k, nn in enumerate((5, 27, 29, 31)):
         if nn * eb >= 128:
             continue
         fwd = run_copy_case(f"(512,{nn}):({nn},1)", f"(512,{nn}):(1,512)", eb, seed=k)
         bwd = run_copy_case(f"(512,{nn}):(1,512)", f"(512,{nn}):({nn},1)", eb, seed=10 + k)
         assert fwd in ("tiled_n", "interleave") and bwd in ("tiled_n", "interleave"), (nn, fwd, bwd)
-    assert run_copy_case("(11,256,3):(1,11,2900)", "(11,256,3):(300,1,3300)", eb, src_origin=1, dst_origin=2, seed=20) == "tiled_n"
-    assert run_copy_case("(11,256,3):(300,1,3300)", "(11,256,3):(1,11,2900)", eb, src_origin=3, dst_origin=1, seed=21) == "tiled_n"
+    nn = 27 if eb < 8 else 11     # a short mode below one 128-byte row that is not an interleave size for this cell size
+    assert run_copy_case(f"({nn},256,3):(1,{nn},7000)", f"({nn},256,3):(300,1,8100)", eb, src_origin=1, dst_origin=2, seed=20) == "tiled_n"
+    assert run_copy_case(f"({nn},256,3):(300,1,8100)", f"({nn},256,3):(1,{nn},7000)", eb, src_origin=3, dst_origin=1, seed=21) == "tiled_n"
     if eb == 4:
         assert run_copy_case("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", eb, seed=22) == "tiled_n"
     host.config("COPY_RAGGED", "4")
     try:
-        want = "ragged:tiled_n" if 20 * eb < 128 else "ragged:tiled_u"   # 20 eight-byte cells are more than a 128-byte row
-        assert run_copy_case("(421,20):(20,1)", "(421,20):(1,421)", eb, seed=23) == want
-        assert run_copy_case("(421,20):(1,421)", "(421,20):(20,1)", eb, seed=24) == "ragged:tiled_n"
+        want = "ragged:tiled_n" if 27 * eb < 128 else "ragged:tiled_u"   # 27 eight-byte cells are more than a 128-byte row
+        assert run_copy_case("(421,27):(27,1)", "(421,27):(1,421)", eb, seed=23) == want
+        assert run_copy_case("(421,27):(1,421)", "(421,27):(27,1)", eb, seed=24) == "ragged:tiled_n"
     finally:
         host.config("COPY_RAGGED", None)
     host.config("COPY_CELL_TILES", "0")
     try:
-        assert run_copy_case("(512,20):(20,1)", "(512,20):(1,512)", eb, seed=25).startswith("gather")
+        assert run_copy_case("(512,27):(27,1)", "(512,27):(1,512)", eb, seed=25).startswith("gather")
     finally:
         host.config("COPY_CELL_TILES", None)
 

@@ -30,10 +30,11 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("((4,16),(32,4)):((1,512),(4,128))", "((4,16),(32,4)):((2048,1),(16,512))", 4, "tiled_n"),   # 4-cell source runs: narrow staged tiles
     # narrow runs: a whole short mode on one side (a 4M x 24 transpose and back), cell-granular staged tiles
     ("(4194304,24):(24,1)", "(4194304,24):(1,4194304)", 4, "interleave"),     # 24 cells: an interleave size since the last pass
-    ("(4194304,20):(20,1)", "(4194304,20):(1,4194304)", 4, "tiled_n"),
-    ("(4194304,20):(1,4194304)", "(4194304,20):(20,1)", 4, "tiled_n"),
-    ("(4194309,20):(20,1)", "(4194309,20):(1,4194309)", 4, "ragged:tiled_n"),
-    ("(4194309,20):(1,4194309)", "(4194309,20):(20,1)", 4, "ragged:tiled_n"),
+    ("(4194304,20):(20,1)", "(4194304,20):(1,4194304)", 4, "interleave"),
+    ("(4194304,27):(27,1)", "(4194304,27):(1,4194304)", 4, "tiled_n"),
+    ("(4194304,27):(1,4194304)", "(4194304,27):(27,1)", 4, "tiled_n"),
+    ("(4194309,27):(27,1)", "(4194309,27):(1,4194309)", 4, "ragged:tiled_n"),
+    ("(4194309,27):(1,4194309)", "(4194309,27):(27,1)", 4, "ragged:tiled_n"),
     ("(4194304,100):(100,1)", "(4194304,100):(1,4194304)", 1, "tiled_n"),
     ("(96,160):(160,1)", "(96,160):(1,96)", 2, "gather"),
     # AoS <-> SoA: register-permuting interleave plan (short mode 2 .. 10, 12, 16, 24 or 32 cells, whole lane pieces, 16-byte alignment)
@@ -41,7 +42,8 @@ from paper_2603_02298_b200 import L, TlbError, abi, host
     ("(224,224,3,16):(3,672,1,150528)", "(224,224,3,16):(1,224,50176,150528)", 1, "interleave"),
     ("(5,1048576):(1,5)", "(5,1048576):(1048576,1)", 4, "interleave"),
     ("(1048576,16):(16,1)", "(1048576,16):(1,1048576)", 4, "interleave"),      # tall-skinny transpose
-    ("(11,1048576):(1,11)", "(11,1048576):(1048576,1)", 4, "tiled_n"),         # 11 cells: not an interleave size, narrow staged tiles
+    ("(27,1048576):(1,27)", "(27,1048576):(1048576,1)", 4, "tiled_n"),         # 27 cells: not an interleave size, narrow staged tiles
+    ("(11,1048576):(1,11)", "(11,1048576):(1048576,1)", 8, "tiled_n"),         # 8-byte cells: the common extents only
     ("(4,1048576):(1,4)", "(4,1048576):(1048577,1)", 4, "tiled_n"),            # planar rows not 16-byte aligned: narrow staged tiles
     # ragged extents (rows that are not whole 128-byte pieces / whole tiles): a whole-tile body on the staged plan plus
     # edge strips, from 2^22 elements (smaller copies are one gather launch)
