@@ -1374,7 +1374,9 @@ int try_planned(const CopyCall& c, bool* done, Refined* refined) {
         // 16-byte vectors plus the last cells of the run (try_ragged) instead of moving everything cell by cell.
         if (vb < 16 && eb < 16 && g_copy_path == 0 && g_ragged_depth == 0 && knob(K_COPY_RAGGED) != 0 &&
             c.n >= (1ull << std::min(40, knob(K_COPY_RAGGED))) && modes[ia].e >= 16 / eb) {
-            bool wide = aligned_to(sp, base_s, eb, 16) && aligned_to(dp, base_d, eb, 16);
+            // (bases off a 16-byte boundary by the SAME amount on both sides are cut as well: head cells, vectors, tail cells)
+            bool wide = ((reinterpret_cast<uintptr_t>(sp) + static_cast<uintptr_t>(base_s) * eb) & 15u) ==
+                        ((reinterpret_cast<uintptr_t>(dp) + static_cast<uintptr_t>(base_d) * eb) & 15u);
             for (size_t r = 0; wide && r < modes.size(); ++r)
                 if (static_cast<int>(r) != ia) wide = modes[r].ss % (16 / eb) == 0 && modes[r].ds % (16 / eb) == 0;
             if (wide) return TLB_OK;
@@ -1907,8 +1909,17 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
     if (ia == ib) {
         // one mode contiguous on both sides whose extent is not a whole number of 16-byte vectors (an odd number of bytes):
         // whole vectors on the vec plan, the last cells of the run through the gather
-        const int64_t V = 16 / eb, e = modes[ia].e, body = e / V * V;
-        if (eb >= 16 || body == e || body == 0) return TLB_OK;
+        // ... and a run that STARTS off a 16-byte boundary by the same amount on both sides (a[1:] -> b[1:]): the head cells up to
+        // the boundary are gathered as well
+        if (eb >= 16) return TLB_OK;
+        const int64_t V = 16 / eb, e = modes[ia].e;
+        const uintptr_t as = (reinterpret_cast<uintptr_t>(c.src->data) + static_cast<uintptr_t>(R.base_s) * eb) & 15u;
+        const uintptr_t ad = (reinterpret_cast<uintptr_t>(c.dst->data) + static_cast<uintptr_t>(R.base_d) * eb) & 15u;
+        if (as != ad || as % eb != 0) return TLB_OK;
+        const int64_t head = as ? static_cast<int64_t>((16 - as) / eb) : 0;
+        if (head >= e) return TLB_OK;
+        const int64_t body = (e - head) / V * V;
+        if ((body == e && head == 0) || body == 0) return TLB_OK;
         auto part = [&](int64_t a0, int64_t ea) -> int {
             tlb_mode sm[TLB_MAX_MODES], dm[TLB_MAX_MODES];
             for (size_t r = 0; r < modes.size(); ++r) {
@@ -1931,14 +1942,15 @@ int try_ragged(const CopyCall& c, const Refined& R, bool* done) {
         };
         const bool was_dry = g_dry_run;
         g_dry_run = true;
-        const int probe = part(0, body);
+        const int probe = part(head, body);
         g_dry_run = was_dry;
         const std::string body_plan = tlb_last_plan();
         if (probe != TLB_OK || body_plan != "vec") return TLB_OK;
         g_ragged_plan = "ragged:vec";
         if (!g_dry_run) {
-            TLB_TRY(part(0, body));
-            TLB_TRY(part(body, e - body));
+            TLB_TRY(part(head, body));
+            if (head) TLB_TRY(part(0, head));
+            if (head + body < e) TLB_TRY(part(head + body, e - head - body));
         }
         set_plan(g_ragged_plan.c_str());
         *done = true;

@@ -256,6 +256,12 @@ def test_copy_ragged_extents_take_the_staged_plan(eb):
             # one contiguous mode that is not a whole number of 16-byte vectors: whole vectors on the vec plan, the rest gathered
             n_odd = 16 // eb * 1237 + 1
             assert run_copy_case(f"({n_odd},29):(1,{n_odd})", f"({n_odd},29):(1,{n_odd})", eb, seed=8) == "ragged:vec"
+            # a run that starts off a 16-byte boundary by the same amount on both sides (a[1:] -> b[1 + 16 / eb:]): head cells too
+            v = 16 // eb
+            assert run_copy_case("40001:1", "40001:1", eb, src_origin=1, dst_origin=1 + v, seed=9) == "ragged:vec"
+            assert run_copy_case(f"({v * 640},33):(1,{v * 640})", f"({v * 640},33):(1,{v * 800})", eb, src_origin=v - 1, dst_origin=2 * v - 1, seed=10) == "ragged:vec"
+            # different misalignments: no common vector boundary, cell by cell
+            assert run_copy_case("40001:1", "40001:1", eb, src_origin=1, dst_origin=2, seed=11) in ("vec", "gather")
         host.config("COPY_RAGGED", "0")
         assert run_copy_case("(2403,1801):(1801,1)", "(2403,1801):(1,2403)", eb, seed=6) == "gather"
     finally:
